@@ -1,0 +1,932 @@
+// sf_capi.cpp — the C ABI (include/scatterfield_b200.h) and the native host
+// runtime behind it: handle ownership, host<->device staging, parameter layout
+// and initialisation, Gauss-Legendre nodes, stream-ordered scratch memory and
+// query chunking. Every entry point converts exceptions to a status code plus a
+// thread-local message (reference Errc semantics, inc/error.h:11-32).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "sf_internal.h"
+
+using sfb::fail;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guard(F&& fn) {
+    try {
+        fn();
+        return SF_OK;
+    } catch (const sfb::Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return SF_ERR_NUMERIC;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SF_ERR_INVALID_ARGUMENT;
+    }
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // clear: unregistered host memory
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Stream-ordered scratch buffer.
+template <typename T>
+struct Scratch {
+    T* p = nullptr;
+    cudaStream_t s = nullptr;
+    Scratch() = default;
+    Scratch(size_t n, cudaStream_t st) { alloc(n, st); }
+    void alloc(size_t n, cudaStream_t st) {
+        s = st;
+        if (n) SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st));
+    }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+};
+
+// Input array: device pointer passed through, host array staged to the device.
+template <typename T>
+struct In {
+    const T* d = nullptr;
+    Scratch<T> buf;
+    In(const T* src, size_t n, cudaStream_t s) {
+        if (!src || n == 0) return;
+        if (is_device_ptr(src)) {
+            d = src;
+            return;
+        }
+        buf.alloc(n, s);
+        SFB_CUDA(cudaMemcpyAsync(buf.p, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+        d = buf.p;
+    }
+};
+
+// Output array: device pointer written directly, host array copied back by finish().
+template <typename T>
+struct Out {
+    T* host = nullptr;
+    T* d = nullptr;
+    size_t n = 0;
+    Scratch<T> buf;
+    cudaStream_t s;
+    Out(T* dst, size_t count, cudaStream_t st) : n(count), s(st) {
+        if (!dst || n == 0) return;
+        if (is_device_ptr(dst)) {
+            d = dst;
+            return;
+        }
+        host = dst;
+        buf.alloc(n, s);
+        d = buf.p;
+    }
+    void finish() {
+        if (host) SFB_CUDA(cudaMemcpyAsync(host, d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+};
+
+void sync(cudaStream_t s) { SFB_CUDA(cudaStreamSynchronize(s)); }
+
+sf_grid* new_grid(int nx, int ny, int nz, double vs, const double o[3]) {
+    if (nx <= 0 || ny <= 0 || nz <= 0) fail(SF_ERR_BAD_DIMS, "density grid: dims must be positive");
+    if (!(vs > 0.0)) fail(SF_ERR_BAD_VALUE, "density grid: voxel_size must be positive");
+    auto g = std::make_unique<sf_grid>();
+    g->nx = nx;
+    g->ny = ny;
+    g->nz = nz;
+    g->vs = vs;
+    for (int i = 0; i < 3; ++i) g->origin[i] = o[i];
+    // DensityGrid::bounds: origin + Vec3{nx*vs, ny*vs, nz*vs} (src/volume_grid.cpp:35-38)
+    g->hi[0] = o[0] + nx * vs;
+    g->hi[1] = o[1] + ny * vs;
+    g->hi[2] = o[2] + nz * vs;
+    SFB_CUDA(cudaMalloc(&g->d, g->count() * sizeof(float)));
+    return g.release();
+}
+
+void free_grid(sf_grid* g) {
+    if (!g) return;
+    if (g->owned && g->d) cudaFree(g->d);
+    delete g;
+}
+
+bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// ---- reference RNG + init (inc/rng.h:12-66, src/neural.cpp:444-452) ----------------
+uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+struct Pcg32 {
+    uint64_t state = 0, inc = 0;
+    Pcg32(uint64_t seed, uint64_t seq) {
+        inc = (splitmix64(seq) << 1u) | 1u;
+        next();
+        state += splitmix64(seed);
+        next();
+    }
+    uint32_t next() {
+        uint64_t old = state;
+        state = old * 6364136223846793005ULL + inc;
+        uint32_t xs = uint32_t(((old >> 18u) ^ old) >> 27u);
+        uint32_t rot = uint32_t(old >> 59u);
+        return (xs >> rot) | (xs << ((~rot + 1u) & 31));
+    }
+    double next_double() {
+        uint64_t hi = next();
+        uint64_t lo = next();
+        return double((hi << 21) ^ (lo >> 11)) * 0x1p-53;
+    }
+};
+
+// walk_params (src/predictor.cpp:62-109): fn(rows, cols, fan_in), cols = 0 for biases.
+template <typename F>
+void walk_params(const sf_backbone_config& c, F&& fn) {
+    const int W = c.width;
+    for (int k = 0; k < 2; ++k) {
+        int nl = k == 0 ? c.n_diffuse_layers : c.n_highlight_layers;
+        const int* counts = k == 0 ? c.diffuse_counts : c.highlight_counts;
+        for (int t = 0; t < 3; ++t) {
+            fn(W, 7, 7);
+            fn(W, 0, 0);
+            for (int i = 0; i < nl; ++i) {
+                if (!c.literal_attention) {
+                    fn(4, 8, 8);
+                    fn(4, 0, 0);
+                    fn(3, 4, 4);
+                    fn(3, 0, 0);
+                }
+                int ld = counts[i] + 2;
+                fn(W, W + ld, W + ld);
+                fn(W, 0, 0);
+                fn(W, W, W);
+                fn(W, 0, 0);
+            }
+        }
+    }
+    const int M = c.merge_width;
+    for (int t = 0; t < 3; ++t) {
+        fn(M, 2 * W, 2 * W);
+        fn(M, 0, 0);
+    }
+    fn(M, 3 * M, 3 * M);
+    fn(M, 0, 0);
+    const int H = c.head_width;
+    const int outs[3] = {H, H, 3}, ins[3] = {M, H, H};
+    for (int l = 0; l < 3; ++l) {
+        fn(outs[l], ins[l], ins[l]);
+        fn(outs[l], 0, 0);
+    }
+}
+
+BackboneLayout make_layout(const sf_backbone_config& c) {
+    BackboneLayout L{};
+    int64_t off = 0;
+    int idx = 0;
+    // per-stack tensor counts: 2 + nl*(4 or 8)
+    const int per_blk = c.literal_attention ? 4 : 8;
+    const int n_d = 2 + c.n_diffuse_layers * per_blk, n_h = 2 + c.n_highlight_layers * per_blk;
+    walk_params(c, [&](int rows, int cols, int) {
+        // record the start of each stack / merge / cross / head tensor group
+        int i = idx;
+        if (i < 3 * n_d) {
+            if (i % n_d == 0) L.stack_off[0][i / n_d] = off;
+        } else if (i < 3 * n_d + 3 * n_h) {
+            int j = i - 3 * n_d;
+            if (j % n_h == 0) L.stack_off[1][j / n_h] = off;
+        } else {
+            int j = i - 3 * n_d - 3 * n_h;
+            if (j == 0) L.merge_off = off;
+            if (j == 6) L.cross_off = off;
+            if (j == 8) L.head_off[0] = off;
+            if (j == 10) L.head_off[1] = off;
+            if (j == 12) L.head_off[2] = off;
+        }
+        off += int64_t(rows) * (cols > 0 ? cols : 1);
+        ++idx;
+    });
+    L.total = off;
+    return L;
+}
+
+std::vector<float> he_init(const sf_backbone_config& c) {
+    std::vector<float> out;
+    uint64_t ordinal = 0;
+    walk_params(c, [&](int rows, int cols, int fan_in) {
+        size_t n = size_t(rows) * size_t(cols > 0 ? cols : 1);
+        uint64_t seed = splitmix64(c.seed + 0x5eedu * (ordinal + 1));
+        if (fan_in > 0) {
+            double bound = std::sqrt(6.0 / double(fan_in));
+            Pcg32 rng(seed, 0xfeedu);
+            for (size_t i = 0; i < n; ++i) out.push_back(float((2.0 * rng.next_double() - 1.0) * bound));
+        } else {
+            out.insert(out.end(), n, 0.0f);
+        }
+        ++ordinal;
+    });
+    return out;
+}
+
+// Gauss-Legendre nodes (src/quadrature.cpp:16-44), same Newton iteration.
+void gauss_legendre(int n, std::vector<double>& x_out, std::vector<double>& w_out) {
+    x_out.assign(size_t(n), 0.0);
+    w_out.assign(size_t(n), 0.0);
+    const int m = (n + 1) / 2;
+    for (int i = 0; i < m; ++i) {
+        double x = std::cos(3.14159265358979323846 * (i + 0.75) / (n + 0.5));
+        double pp = 0.0;
+        for (int iter = 0; iter < 100; ++iter) {
+            double p0 = 1.0, p1 = 0.0;
+            for (int j = 0; j < n; ++j) {
+                double p2 = p1;
+                p1 = p0;
+                p0 = ((2.0 * j + 1.0) * x * p1 - j * p2) / (j + 1.0);
+            }
+            pp = n * (x * p0 - p1) / (x * x - 1.0);
+            double dx = p0 / pp;
+            x -= dx;
+            if (std::abs(dx) < 1e-15) break;
+        }
+        x_out[size_t(i)] = -x;
+        x_out[size_t(n - 1 - i)] = x;
+        double w = 2.0 / ((1.0 - x * x) * pp * pp);
+        w_out[size_t(i)] = w;
+        w_out[size_t(n - 1 - i)] = w;
+    }
+}
+
+void validate_backbone_config(const sf_backbone_config& c) {
+    if (c.n_diffuse_layers < 1 || c.n_highlight_layers < 1 || c.n_diffuse_layers > 16 ||
+        c.n_highlight_layers > 16)
+        fail(SF_ERR_INVALID_ARGUMENT, "backbone needs 1..16 layers per template kind");
+    if (c.width < 1 || c.merge_width < 1 || c.head_width < 1)
+        fail(SF_ERR_INVALID_ARGUMENT, "backbone widths must be positive");
+    for (int i = 0; i < c.n_diffuse_layers; ++i)
+        if (c.diffuse_counts[i] < 1) fail(SF_ERR_INVALID_ARGUMENT, "layer counts must be positive");
+    for (int i = 0; i < c.n_highlight_layers; ++i)
+        if (c.highlight_counts[i] < 1) fail(SF_ERR_INVALID_ARGUMENT, "layer counts must be positive");
+}
+
+void validate_albedo(const double a[3]) {
+    for (int i = 0; i < 3; ++i)
+        if (!(a[i] > 0.0 && a[i] < 1.0)) fail(SF_ERR_BAD_VALUE, "albedo components must lie in (0,1)");
+}
+
+void validate_phase_model(const sf_phase_model& m) {
+    if (m.kind < 0 || m.kind > 2) fail(SF_ERR_BAD_VALUE, "phase: unknown kind");
+    if (m.kind == SF_PHASE_ISOTROPIC) return;
+    if (m.n_lobes < 1 || m.n_lobes > 3) fail(SF_ERR_BAD_VALUE, "phase: model has no lobes");
+    double sum = 0.0;
+    for (int k = 0; k < m.n_lobes; ++k) {
+        if (!(m.weight[k] >= 0.0)) fail(SF_ERR_BAD_VALUE, "phase: lobe weight must be nonnegative");
+        if (!(m.g[k] > -1.0 && m.g[k] < 1.0)) fail(SF_ERR_BAD_VALUE, "phase: asymmetry must lie in (-1, 1)");
+        sum += m.weight[k];
+    }
+    if (std::abs(sum - 1.0) > 1e-9) fail(SF_ERR_BAD_VALUE, "phase: lobe weights must sum to 1");
+}
+
+int nd_total(const sf_template* t) { return t ? t->total : 0; }
+
+}  // namespace
+
+namespace sfb {
+int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+}  // namespace sfb
+
+extern "C" {
+
+const char* sf_last_error(void) { return g_last_error.c_str(); }
+const char* sf_version(void) { return "scatterfield-b200 0.1 (sm_100a)"; }
+int sf_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// ---- DensityGrid -------------------------------------------------------------------
+int sf_grid_create(int nx, int ny, int nz, double vs, const double origin[3], const float* values,
+                   sf_grid** out) {
+    return guard([&] {
+        std::unique_ptr<sf_grid, void (*)(sf_grid*)> g(new_grid(nx, ny, nz, vs, origin), free_grid);
+        size_t bytes = g->count() * sizeof(float);
+        if (values)
+            SFB_CUDA(cudaMemcpy(g->d, values, bytes, cudaMemcpyDefault));
+        else
+            SFB_CUDA(cudaMemset(g->d, 0, bytes));
+        *out = g.release();
+    });
+}
+
+int sf_grid_info(const sf_grid* g, int dims[3], double* vs, double origin[3]) {
+    return guard([&] {
+        if (!g) fail(SF_ERR_INVALID_ARGUMENT, "null grid");
+        dims[0] = g->nx;
+        dims[1] = g->ny;
+        dims[2] = g->nz;
+        if (vs) *vs = g->vs;
+        if (origin)
+            for (int i = 0; i < 3; ++i) origin[i] = g->origin[i];
+    });
+}
+
+const float* sf_grid_device_ptr(const sf_grid* g) { return g ? g->d : nullptr; }
+
+int sf_grid_download(const sf_grid* g, float* dst, sf_stream stream) {
+    return guard([&] {
+        SFB_CUDA(cudaMemcpyAsync(dst, g->d, g->count() * sizeof(float), cudaMemcpyDefault, stream));
+        sync(stream);
+    });
+}
+
+void sf_grid_destroy(sf_grid* g) { free_grid(g); }
+
+int sf_grid_sample_trilinear(const sf_grid* g, int64_t n, const double* pts, double* out,
+                             sf_stream stream) {
+    return guard([&] {
+        if (n <= 0) return;
+        In<double> ip(pts, size_t(n) * 3, stream);
+        Out<double> op(out, size_t(n), stream);
+        sfb::launch_sample_trilinear(*g, n, ip.d, op.d, stream);
+        op.finish();
+        sync(stream);
+    });
+}
+
+// ---- DensityPyramid ------------------------------------------------------------------
+int sf_pyramid_build(const sf_grid* finest, sf_pyramid** out, sf_stream stream) {
+    return guard([&] {
+        if (!is_pow2(finest->nx) || !is_pow2(finest->ny) || !is_pow2(finest->nz))
+            fail(SF_ERR_BAD_DIMS, "pyramid: dims must be powers of two");
+        auto p = std::make_unique<sf_pyramid>();
+        auto cleanup = [&] {
+            for (sf_grid* l : p->levels) free_grid(l);
+            p->levels.clear();
+        };
+        try {
+            sf_grid* l0 = new_grid(finest->nx, finest->ny, finest->nz, finest->vs, finest->origin);
+            p->levels.push_back(l0);
+            SFB_CUDA(cudaMemcpyAsync(l0->d, finest->d, l0->count() * sizeof(float),
+                                     cudaMemcpyDeviceToDevice, stream));
+            while (std::max({p->levels.back()->nx, p->levels.back()->ny, p->levels.back()->nz}) > 1) {
+                const sf_grid* src = p->levels.back();
+                sf_grid* dst = new_grid(std::max(1, src->nx / 2), std::max(1, src->ny / 2),
+                                        std::max(1, src->nz / 2), src->vs * 2.0, src->origin);
+                p->levels.push_back(dst);
+                sfb::launch_pyramid_down(*src, *dst, stream);
+            }
+            sync(stream);
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        *out = p.release();
+    });
+}
+
+int sf_pyramid_level_count(const sf_pyramid* p) { return p ? int(p->levels.size()) : 0; }
+
+const sf_grid* sf_pyramid_level(const sf_pyramid* p, int level) {
+    if (!p || level < 0 || level >= int(p->levels.size())) return nullptr;
+    return p->levels[size_t(level)];
+}
+
+void sf_pyramid_destroy(sf_pyramid* p) {
+    if (!p) return;
+    for (sf_grid* l : p->levels) free_grid(l);
+    delete p;
+}
+
+// ---- transmittance ---------------------------------------------------------------------
+namespace {
+void normalize3(const double l[3], double o[3]) {
+    double len = std::sqrt(l[0] * l[0] + l[1] * l[1] + l[2] * l[2]);
+    o[0] = l[0] / len;
+    o[1] = l[1] / len;
+    o[2] = l[2] / len;
+}
+
+sf_grid* graded_level(const sf_pyramid* p, int level, const double light[3], double lambda,
+                      double step, cudaStream_t s) {
+    if (level < 0 || level >= int(p->levels.size()))
+        fail(SF_ERR_INVALID_ARGUMENT, "graded_transmittance: invalid level");
+    if (!(lambda > 0.0 && lambda < 1.0))
+        fail(SF_ERR_INVALID_ARGUMENT, "graded_transmittance: lambda outside (0,1)");
+    if (!(step > 0.0)) fail(SF_ERR_INVALID_ARGUMENT, "optical_depth: step must be positive");
+    const sf_grid* rho = p->levels[size_t(level)];
+    double ld[3];
+    normalize3(light, ld);
+    double ts[3] = {-ld[0], -ld[1], -ld[2]};
+    double coeff = std::pow(lambda, level + 1);
+    sf_grid* out = new_grid(rho->nx, rho->ny, rho->nz, rho->vs, rho->origin);
+    try {
+        sfb::launch_graded(*rho, ts, coeff, step, out->d, s);
+    } catch (...) {
+        free_grid(out);
+        throw;
+    }
+    return out;
+}
+
+sf_tvol* combine(const std::vector<const sf_grid*>& fields, const float* kernels,
+                 const float* scales, const double light[3], cudaStream_t s) {
+    if (fields.empty()) fail(SF_ERR_INVALID_ARGUMENT, "combine_transmittance: no fields");
+    const sf_grid& base = *fields[0];
+    int L = int(fields.size());
+    std::vector<float> K(size_t(L) * 27, 0.0f), S(static_cast<size_t>(L), 0.0f);
+    if (kernels) {
+        std::memcpy(K.data(), kernels, K.size() * sizeof(float));
+        std::memcpy(S.data(), scales, S.size() * sizeof(float));
+    } else {  // CombinerWeights::identity (src/feature_pipeline.cpp:29-35)
+        for (int l = 0; l < L; ++l) {
+            K[size_t(l) * 27 + 13] = 1.0f;
+            S[size_t(l)] = float(1.0 / L);
+        }
+    }
+    auto t = std::make_unique<sf_tvol>();
+    normalize3(light, t->light);
+    t->kernels = K;
+    t->scales = S;
+    std::vector<sf_grid*> conv;
+    try {
+        for (int l = 0; l < L; ++l) {
+            const sf_grid& f = *fields[size_t(l)];
+            sf_grid* c = new_grid(f.nx, f.ny, f.nz, f.vs, f.origin);
+            conv.push_back(c);
+            sfb::launch_conv3(f, &K[size_t(l) * 27], c->d, s);
+        }
+        t->values = new_grid(base.nx, base.ny, base.nz, base.vs, base.origin);
+        std::vector<const sf_grid*> cv(conv.begin(), conv.end());
+        sfb::launch_combine(cv, S, base, t->values->d, s);
+        sync(s);
+    } catch (...) {
+        for (sf_grid* c : conv) free_grid(c);
+        if (t->values) free_grid(t->values);
+        throw;
+    }
+    for (sf_grid* c : conv) free_grid(c);
+    return t.release();
+}
+}  // namespace
+
+int sf_graded_transmittance(const sf_pyramid* p, int level, const double light[3], double lambda,
+                            double step, sf_grid** out, sf_stream stream) {
+    return guard([&] {
+        sf_grid* g = graded_level(p, level, light, lambda, step, stream);
+        try {
+            sync(stream);
+        } catch (...) {
+            free_grid(g);
+            throw;
+        }
+        *out = g;
+    });
+}
+
+int sf_conv3_replicate(const sf_grid* in, const float kernel[27], sf_grid** out,
+                       sf_stream stream) {
+    return guard([&] {
+        sf_grid* g = new_grid(in->nx, in->ny, in->nz, in->vs, in->origin);
+        try {
+            sfb::launch_conv3(*in, kernel, g->d, stream);
+            sync(stream);
+        } catch (...) {
+            free_grid(g);
+            throw;
+        }
+        *out = g;
+    });
+}
+
+int sf_combine_transmittance(const sf_grid* const* fields, int n, const float* kernels,
+                             const float* scales, const double light[3], sf_tvol** out,
+                             sf_stream stream) {
+    return guard([&] {
+        if (n <= 0) fail(SF_ERR_INVALID_ARGUMENT, "combine_transmittance: no fields");
+        if (!kernels || !scales) fail(SF_ERR_SHAPE_MISMATCH, "combine_transmittance: weight/level mismatch");
+        std::vector<const sf_grid*> f(fields, fields + n);
+        *out = combine(f, kernels, scales, light, stream);
+    });
+}
+
+int sf_build_transmittance_volume(const sf_pyramid* p, const double light[3], const float* kernels,
+                                  const float* scales, double lambda, double step_scale,
+                                  sf_tvol** out, sf_stream stream) {
+    return guard([&] {
+        std::vector<sf_grid*> fields;
+        try {
+            for (int i = 0; i < int(p->levels.size()); ++i) {
+                double step = step_scale * p->levels[size_t(i)]->vs;
+                fields.push_back(graded_level(p, i, light, lambda, step, stream));
+            }
+            std::vector<const sf_grid*> f(fields.begin(), fields.end());
+            *out = combine(f, kernels, scales, light, stream);
+        } catch (...) {
+            for (sf_grid* g : fields) free_grid(g);
+            throw;
+        }
+        for (sf_grid* g : fields) free_grid(g);
+    });
+}
+
+const sf_grid* sf_tvol_values(const sf_tvol* t) { return t ? t->values : nullptr; }
+
+void sf_tvol_destroy(sf_tvol* t) {
+    if (!t) return;
+    free_grid(t->values);
+    delete t;
+}
+
+int sf_light_entry_point(const double lo[3], const double hi[3], const double p[3],
+                         const double light[3], double out[3]) {
+    return guard([&] {
+        double ld[3];
+        normalize3(light, ld);
+        double ts[3] = {-ld[0], -ld[1], -ld[2]};
+        double t0 = -1e300, t1 = 1e300;
+        bool hit = true;
+        for (int i = 0; i < 3 && hit; ++i) {
+            if (ts[i] == 0.0) {
+                if (p[i] < lo[i] || p[i] > hi[i]) hit = false;
+                continue;
+            }
+            double inv = 1.0 / ts[i];
+            double ta = (lo[i] - p[i]) * inv, tb = (hi[i] - p[i]) * inv;
+            if (ta > tb) std::swap(ta, tb);
+            t0 = std::max(t0, ta);
+            t1 = std::min(t1, tb);
+            if (t0 > t1) hit = false;
+        }
+        if (!hit) {
+            for (int i = 0; i < 3; ++i) out[i] = p[i] - ld[i] * 1e-9;
+            return;
+        }
+        double t = std::max(t1, 1e-9);
+        for (int i = 0; i < 3; ++i) out[i] = p[i] + ts[i] * t;
+    });
+}
+
+// ---- PhaseTable ------------------------------------------------------------------------
+int sf_phase_table_build(int gr, int ar, int hr, int nodes, sf_phase_table** out, sf_stream stream) {
+    return guard([&] {
+        if (gr < 2 || ar < 2 || hr < 2) fail(SF_ERR_INVALID_ARGUMENT, "phase table: resolutions must be >= 2");
+        if (nodes < 1) fail(SF_ERR_INVALID_ARGUMENT, "gauss_legendre: n must be positive");
+        std::vector<double> x, w;
+        gauss_legendre(nodes, x, w);
+        auto t = std::make_unique<sf_phase_table>();
+        t->g = gr;
+        t->a = ar;
+        t->h = hr;
+        SFB_CUDA(cudaMalloc(&t->d, size_t(gr) * ar * hr * sizeof(float)));
+        try {
+            sfb::launch_phase_table(gr, ar, hr, x, w, t->d, stream);
+            sync(stream);
+        } catch (...) {
+            cudaFree(t->d);
+            throw;
+        }
+        *out = t.release();
+    });
+}
+
+int sf_phase_table_from_values(int gr, int ar, int hr, const float* values, sf_phase_table** out) {
+    return guard([&] {
+        if (gr < 2 || ar < 2 || hr < 2) fail(SF_ERR_SHAPE_MISMATCH, "phase table: value count mismatch");
+        auto t = std::make_unique<sf_phase_table>();
+        t->g = gr;
+        t->a = ar;
+        t->h = hr;
+        size_t bytes = size_t(gr) * ar * hr * sizeof(float);
+        SFB_CUDA(cudaMalloc(&t->d, bytes));
+        cudaError_t e = cudaMemcpy(t->d, values, bytes, cudaMemcpyDefault);
+        if (e != cudaSuccess) {
+            cudaFree(t->d);
+            sfb::cuda_check(e, "phase table upload");
+        }
+        *out = t.release();
+    });
+}
+
+int sf_phase_table_info(const sf_phase_table* t, int dims[3]) {
+    return guard([&] {
+        dims[0] = t->g;
+        dims[1] = t->a;
+        dims[2] = t->h;
+    });
+}
+
+int sf_phase_table_download(const sf_phase_table* t, float* dst, sf_stream stream) {
+    return guard([&] {
+        SFB_CUDA(cudaMemcpyAsync(dst, t->d, size_t(t->g) * t->a * t->h * sizeof(float),
+                                 cudaMemcpyDefault, stream));
+        sync(stream);
+    });
+}
+
+int sf_phase_table_lookup_hg(const sf_phase_table* t, int64_t n, const double* g,
+                             const double* angle, const double* half, double* out,
+                             sf_stream stream) {
+    return guard([&] {
+        if (n <= 0) return;
+        In<double> a(g, size_t(n), stream), b(angle, size_t(n), stream), c(half, size_t(n), stream);
+        Out<double> o(out, size_t(n), stream);
+        sfb::launch_lookup_hg(*t, n, a.d, b.d, c.d, o.d, stream);
+        o.finish();
+        sync(stream);
+    });
+}
+
+void sf_phase_table_destroy(sf_phase_table* t) {
+    if (!t) return;
+    cudaFree(t->d);
+    delete t;
+}
+
+// ---- SamplingTemplate ------------------------------------------------------------------
+int sf_template_create(int kind, int n_layers, const int* counts, const double* points,
+                       const double* caps, double gen_distance, double cone_half_angle,
+                       sf_template** out) {
+    return guard([&] {
+        if (kind != SF_TEMPLATE_DIFFUSE && kind != SF_TEMPLATE_HIGHLIGHT)
+            fail(SF_ERR_BAD_VALUE, "template: unknown kind");
+        if (n_layers < 1) fail(SF_ERR_INVALID_ARGUMENT, "template: no layers");
+        if (kind == SF_TEMPLATE_HIGHLIGHT && !(gen_distance > 0.0))
+            fail(SF_ERR_INVALID_ARGUMENT, "highlight template: zero entry distance");
+        auto t = std::make_unique<sf_template>();
+        t->kind = kind;
+        t->n_layers = n_layers;
+        t->counts.assign(counts, counts + n_layers);
+        for (int c : t->counts)
+            if (c < 0) fail(SF_ERR_INVALID_ARGUMENT, "template: negative layer count");
+        for (int c : t->counts) t->total += c;
+        t->points.assign(points, points + size_t(t->total) * 3);
+        t->caps.assign(caps, caps + n_layers);
+        t->gen_distance = gen_distance;
+        t->cone_half_angle = cone_half_angle;
+        std::vector<double> pc;
+        for (int l = 0; l < n_layers; ++l) pc.insert(pc.end(), size_t(t->counts[size_t(l)]), caps[l]);
+        size_t np = std::max<size_t>(1, size_t(t->total));
+        SFB_CUDA(cudaMalloc(&t->d_points, np * 3 * sizeof(double)));
+        SFB_CUDA(cudaMalloc(&t->d_caps, np * sizeof(double)));
+        if (t->total) {
+            SFB_CUDA(cudaMemcpy(t->d_points, t->points.data(), t->points.size() * sizeof(double),
+                                cudaMemcpyHostToDevice));
+            SFB_CUDA(cudaMemcpy(t->d_caps, pc.data(), pc.size() * sizeof(double), cudaMemcpyHostToDevice));
+        }
+        *out = t.release();
+    });
+}
+
+int sf_template_total_points(const sf_template* t) { return t ? t->total : 0; }
+
+int sf_place_template(const sf_template* t, int64_t n, const double* p, const double* omega,
+                      const double* entry, double ts, double* out_pts, double* out_caps,
+                      sf_stream stream) {
+    return guard([&] {
+        if (n <= 0) return;
+        In<double> ip(p, size_t(n) * 3, stream), iw(omega, size_t(n) * 3, stream),
+            ie(entry, size_t(n) * 3, stream);
+        Out<double> op(out_pts, size_t(n) * t->total * 3, stream), oc(out_caps, size_t(n) * t->total, stream);
+        Scratch<int> err(1, stream);
+        SFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
+        sfb::launch_place_template(*t, n, ip.d, iw.d, ie.d, ts, op.d, oc.d, err.p, stream);
+        int herr = 0;
+        SFB_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        op.finish();
+        oc.finish();
+        sync(stream);
+        if (herr) fail(SF_ERR_INVALID_ARGUMENT, "place_template: entry coincides with p");
+    });
+}
+
+void sf_template_destroy(sf_template* t) {
+    if (!t) return;
+    cudaFree(t->d_points);
+    cudaFree(t->d_caps);
+    delete t;
+}
+
+// ---- sample_features --------------------------------------------------------------------
+int sf_sample_features(const sf_grid* density, const sf_tvol* tvol, const sf_template* tmpl,
+                       const sf_phase_model* model, const sf_phase_table* table, double ts,
+                       int64_t n, const double* queries, float* out, sf_stream stream) {
+    return guard([&] {
+        if (n <= 0) return;
+        validate_phase_model(*model);
+        const sf_grid& tv = *tvol->values;
+        if (tv.nx != density->nx || tv.ny != density->ny || tv.nz != density->nz)
+            fail(SF_ERR_SHAPE_MISMATCH, "sample_features: transmittance volume geometry differs");
+        In<double> iq(queries, size_t(n) * 9, stream);
+        Out<float> of(out, size_t(n) * 3 * tmpl->total, stream);
+        Scratch<int> err(1, stream);
+        SFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
+        sfb::SceneDev sc = sfb::scene_dev(*density, tv, nullptr, *model, *table, ts);
+        sfb::launch_sample_features(sc, sfb::template_dev(*tmpl), n, iq.d, of.d, 3 * tmpl->total, 0,
+                                    err.p, stream);
+        int herr = 0;
+        SFB_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        of.finish();
+        sync(stream);
+        if (herr) fail(SF_ERR_INVALID_ARGUMENT, "place_template: entry coincides with p");
+    });
+}
+
+// ---- Backbone ------------------------------------------------------------------------------
+int sf_backbone_create(const sf_backbone_config* config, const float* params, sf_backbone** out) {
+    return guard([&] {
+        validate_backbone_config(*config);
+        auto b = std::make_unique<sf_backbone>();
+        b->cfg = *config;
+        b->layout = make_layout(*config);
+        size_t bytes = size_t(b->layout.total) * sizeof(float);
+        SFB_CUDA(cudaMalloc(&b->d_params, bytes));
+        cudaError_t e;
+        if (params) {
+            e = cudaMemcpy(b->d_params, params, bytes, cudaMemcpyDefault);
+        } else {
+            std::vector<float> init = he_init(*config);
+            e = cudaMemcpy(b->d_params, init.data(), bytes, cudaMemcpyHostToDevice);
+        }
+        if (e != cudaSuccess) {
+            cudaFree(b->d_params);
+            sfb::cuda_check(e, "backbone upload");
+        }
+        *out = b.release();
+    });
+}
+
+int64_t sf_backbone_param_count(const sf_backbone* b) { return b ? b->layout.total : 0; }
+
+int sf_backbone_download_params(const sf_backbone* b, float* dst, sf_stream stream) {
+    return guard([&] {
+        SFB_CUDA(cudaMemcpyAsync(dst, b->d_params, size_t(b->layout.total) * sizeof(float),
+                                 cudaMemcpyDefault, stream));
+        sync(stream);
+    });
+}
+
+void sf_backbone_destroy(sf_backbone* b);
+
+namespace {
+void run_backbone(const sf_backbone& b, int precision, int64_t n, const float* slices,
+                  const double* cfg8, float* y, double* F, cudaStream_t s) {
+    if (precision == SF_PRECISION_FP32) {
+        sfb::launch_backbone_fp32(b, n, slices, cfg8, y, F, s);
+    } else if (precision == SF_PRECISION_BF16) {
+        if (!sfb::tc_supported(b.cfg))
+            fail(SF_ERR_INVALID_ARGUMENT, "bf16 tensor-core backbone needs the default widths (32/64/64)");
+        sfb::tc_prepare(const_cast<sf_backbone&>(b), s);
+        sfb::launch_backbone_tc(b, n, slices, cfg8, y, F, s);
+    } else {
+        fail(SF_ERR_INVALID_ARGUMENT, "unknown precision");
+    }
+}
+}  // namespace
+
+int sf_predict(const sf_backbone* b, int64_t n, const float* features, const double* config8,
+               int precision, float* y_out, double* F_out, sf_stream stream) {
+    return guard([&] {
+        if (n <= 0) return;
+        const sf_backbone_config& c = b->cfg;
+        int64_t feat = 0;
+        for (int i = 0; i < c.n_diffuse_layers; ++i) feat += 3 * c.diffuse_counts[i];
+        for (int i = 0; i < c.n_highlight_layers; ++i) feat += 3 * c.highlight_counts[i];
+        if (!is_device_ptr(config8))
+            for (int64_t i = 0; i < n; ++i) validate_albedo(config8 + 8 * i + 4);
+        In<float> f(features, size_t(n) * feat, stream);
+        In<double> cf(config8, size_t(n) * 8, stream);
+        Out<float> oy(y_out, size_t(n) * 3, stream);
+        Out<double> oF(F_out, size_t(n) * 3, stream);
+        Scratch<float> slices(size_t(n) * sfb::slices_per_query(c), stream);
+        sfb::launch_slice(c, n, f.d, slices.p, stream);
+        run_backbone(*b, precision, n, slices.p, cf.d, oy.d, oF.d, stream);
+        oy.finish();
+        oF.finish();
+        sync(stream);
+    });
+}
+
+// ---- fused query -----------------------------------------------------------------------------
+int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_template* dt,
+                    const sf_template* ht, const sf_phase_model* model, const sf_phase_table* table,
+                    double ts, sf_scene** out) {
+    return guard([&] {
+        validate_phase_model(*model);
+        if (dt->kind != SF_TEMPLATE_DIFFUSE || ht->kind != SF_TEMPLATE_HIGHLIGHT)
+            fail(SF_ERR_INVALID_ARGUMENT, "scene: need a diffuse and a highlight template");
+        const sf_grid& tv = *tvol->values;
+        if (tv.nx != density->nx || tv.ny != density->ny || tv.nz != density->nz)
+            fail(SF_ERR_SHAPE_MISMATCH, "scene: transmittance volume geometry differs");
+        auto s = std::make_unique<sf_scene>();
+        s->density = density;
+        s->tvol = tvol;
+        s->dt = dt;
+        s->ht = ht;
+        s->model = *model;
+        s->table = table;
+        s->template_scale = ts;
+        SFB_CUDA(cudaMalloc(&s->d_dt, density->count() * sizeof(float2)));
+        try {
+            sfb::launch_interleave(density->d, tv.d, s->d_dt, density->count(), nullptr);
+            SFB_CUDA(cudaDeviceSynchronize());
+        } catch (...) {
+            cudaFree(s->d_dt);
+            throw;
+        }
+        *out = s.release();
+    });
+}
+
+void sf_scene_destroy(sf_scene* s) {
+    if (!s) return;
+    cudaFree(s->d_dt);
+    delete s;
+}
+
+int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium, int64_t n,
+             const double* queries, int precision, double* F_out, float* y_out, sf_stream stream) {
+    return guard([&] {
+        if (n <= 0) return;
+        validate_albedo(medium->albedo);
+        const sf_backbone_config& c = b->cfg;
+        int nd = 0, nh = 0;
+        for (int i = 0; i < c.n_diffuse_layers; ++i) nd += c.diffuse_counts[i];
+        for (int i = 0; i < c.n_highlight_layers; ++i) nh += c.highlight_counts[i];
+        if (nd != s->dt->total || nh != s->ht->total)
+            fail(SF_ERR_SHAPE_MISMATCH, "feature block does not match template counts");
+        In<double> iq(queries, size_t(n) * 9, stream);
+        Out<double> oF(F_out, size_t(n) * 3, stream);
+        Out<float> oy(y_out, size_t(n) * 3, stream);
+        const int64_t chunk = std::min<int64_t>(n, 1 << 17);
+        const int64_t feat = 3 * int64_t(nd + nh);
+        Scratch<float> feats(size_t(chunk) * feat, stream);
+        Scratch<float> slices(size_t(chunk) * sfb::slices_per_query(c), stream);
+        Scratch<double> cfg8(size_t(chunk) * 8, stream);
+        Scratch<int> err(1, stream);
+        SFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
+        sfb::SceneDev sc = sfb::scene_dev(*s->density, *s->tvol->values, s->d_dt, s->model, *s->table,
+                                          s->template_scale);
+        for (int64_t q0 = 0; q0 < n; q0 += chunk) {
+            int64_t m = std::min(chunk, n - q0);
+            const double* qd = iq.d + 9 * q0;
+            sfb::launch_make_cfg8(*medium, m, qd, cfg8.p, stream);
+            sfb::launch_sample_features(sc, sfb::template_dev(*s->dt), m, qd, feats.p, feat, 0, err.p,
+                                        stream);
+            sfb::launch_sample_features(sc, sfb::template_dev(*s->ht), m, qd, feats.p, feat, 3 * nd,
+                                        err.p, stream);
+            sfb::launch_slice(c, m, feats.p, slices.p, stream);
+            run_backbone(*b, precision, m, slices.p, cfg8.p, oy.d ? oy.d + 3 * q0 : nullptr,
+                         oF.d ? oF.d + 3 * q0 : nullptr, stream);
+        }
+        int herr = 0;
+        SFB_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        oF.finish();
+        oy.finish();
+        sync(stream);
+        if (herr) fail(SF_ERR_INVALID_ARGUMENT, "place_template: entry coincides with p");
+    });
+}
+
+}  // extern "C"
+
+extern "C" void sf_backbone_destroy(sf_backbone* b) {
+    if (!b) return;
+    cudaFree(b->d_params);
+    sfb::tc_release(*b);
+    delete b;
+}

@@ -1,0 +1,168 @@
+// sf_internal.h — handle layouts and launcher declarations shared by the
+// translation units of libsf_b200.so (not part of the public ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/scatterfield_b200.h"
+#include "sf_device.cuh"
+
+// ---- error plumbing ---------------------------------------------------------
+namespace sfb {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(SF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define SFB_CUDA(x) ::sfb::cuda_check((x), #x)
+
+// ---- launch configuration helpers --------------------------------------------
+int sm_count();
+
+}  // namespace sfb
+
+// ---- handle layouts ----------------------------------------------------------
+struct sf_grid {
+    int nx = 0, ny = 0, nz = 0;
+    double vs = 1.0;
+    double origin[3] = {0, 0, 0};
+    double hi[3] = {0, 0, 0};  // origin + n*vs (DensityGrid::bounds)
+    float* d = nullptr;
+    bool owned = true;
+    size_t count() const { return size_t(nx) * ny * nz; }
+    sfb::GridDev dev() const {
+        int e;
+        double ivs = std::frexp(vs, &e) == 0.5 ? 1.0 / vs : 0.0;
+        return sfb::GridDev{d,         nx,        ny,    nz,    vs,    origin[0],
+                            origin[1], origin[2], hi[0], hi[1], hi[2], ivs};
+    }
+};
+
+struct sf_pyramid {
+    std::vector<sf_grid*> levels;  // level 0 is a copy of the finest grid
+};
+
+struct sf_tvol {
+    double light[3] = {0, 0, 0};
+    sf_grid* values = nullptr;
+    std::vector<float> kernels, scales;
+};
+
+struct sf_phase_table {
+    int g = 0, a = 0, h = 0;
+    float* d = nullptr;
+};
+
+struct sf_template {
+    int kind = 0;
+    int n_layers = 0;
+    int total = 0;
+    std::vector<int> counts;
+    std::vector<double> points;  // [total][3]
+    std::vector<double> caps;    // [n_layers] layer cap_radius
+    double gen_distance = 0.0, cone_half_angle = 0.0;
+    double* d_points = nullptr;  // [total][3]
+    double* d_caps = nullptr;    // [total] per-point layer cap radius (unscaled)
+};
+
+// Parameter layout of one stack and of the whole net, in walk_params order
+// (src/predictor.cpp:62-109).
+struct BackboneLayout {
+    int64_t total = 0;
+    int64_t stack_off[2][3];  // [kind][tau]
+    int64_t merge_off;        // 3 x (W [M][2W], b [M])
+    int64_t cross_off;        // W [M][3M], b [M]
+    int64_t head_off[3];      // W, b
+};
+
+struct sf_backbone {
+    sf_backbone_config cfg{};
+    BackboneLayout layout{};
+    float* d_params = nullptr;  // canonical f32 params
+    void* tc = nullptr;         // packed bf16 operands for the tensor-core path (lazy)
+};
+
+struct sf_scene {
+    const sf_grid* density = nullptr;
+    const sf_tvol* tvol = nullptr;
+    const sf_template* dt = nullptr;
+    const sf_template* ht = nullptr;
+    sf_phase_model model{};
+    const sf_phase_table* table = nullptr;
+    double template_scale = 1.0;
+    float2* d_dt = nullptr;  // interleaved {density, transmittance} level-0 volume
+};
+
+// ---- launchers (defined in the .cu files) --------------------------------------
+namespace sfb {
+
+void launch_pyramid_down(const sf_grid& src, sf_grid& dst, cudaStream_t s);
+void launch_graded(const sf_grid& level, const double to_source[3], double coeff, double step,
+                   float* out, cudaStream_t s);
+void launch_conv3(const sf_grid& in, const float k27[27], float* out, cudaStream_t s);
+void launch_combine(const std::vector<const sf_grid*>& conv, const std::vector<float>& scales,
+                    const sf_grid& base, float* out, cudaStream_t s);
+void launch_interleave(const float* density, const float* tvol, float2* out, size_t n,
+                       cudaStream_t s);
+void launch_phase_table(int gr, int ar, int hr, const std::vector<double>& nodes,
+                        const std::vector<double>& weights, float* out, cudaStream_t s);
+void launch_lookup_hg(const sf_phase_table& t, int64_t n, const double* g, const double* a,
+                      const double* h, double* out, cudaStream_t s);
+void launch_sample_trilinear(const sf_grid& g, int64_t n, const double* pts, double* out,
+                             cudaStream_t s);
+void launch_place_template(const sf_template& t, int64_t n, const double* p,
+                           const double* omega, const double* entry, double ts, double* pts,
+                           double* caps, int* err, cudaStream_t s);
+
+// Query-side scene view (sampling).
+struct SceneDev {
+    GridDev grid;          // density geometry (v = density)
+    const float2* dt;      // interleaved {density, tvol}
+    const float* tvol;     // plain tvol (when dt == nullptr)
+    PhaseDev phase;
+    double template_scale;
+};
+struct TemplateDev {
+    int kind;
+    int total;
+    const double* pts;
+    const double* caps;
+    double gen_distance;
+};
+SceneDev scene_dev(const sf_grid& density, const sf_grid& tvol, const float2* dt,
+                   const sf_phase_model& m, const sf_phase_table& t, double ts);
+TemplateDev template_dev(const sf_template& t);
+
+void launch_sample_features(const SceneDev& sc, const TemplateDev& td, int64_t n,
+                            const double* queries, float* out, int64_t row_stride,
+                            int64_t col_offset, int* err, cudaStream_t s);
+int64_t slices_per_query(const sf_backbone_config& c);
+void launch_slice(const sf_backbone_config& c, int64_t n, const float* feats, float* slices,
+                  cudaStream_t s);
+void launch_backbone_fp32(const sf_backbone& b, int64_t n, const float* slices,
+                          const double* cfg8, float* y, double* F, cudaStream_t s);
+void launch_make_cfg8(const sf_medium_params& m, int64_t n, const double* queries,
+                      double* cfg8, cudaStream_t s);
+
+// Tensor-core (tcgen05, bf16 operands / fp32 accumulation) backbone.
+bool tc_supported(const sf_backbone_config& c);
+void tc_prepare(sf_backbone& b, cudaStream_t s);
+void tc_release(sf_backbone& b);
+void launch_backbone_tc(const sf_backbone& b, int64_t n, const float* slices,
+                        const double* cfg8, float* y, double* F, cudaStream_t s);
+
+}  // namespace sfb

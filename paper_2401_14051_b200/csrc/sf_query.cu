@@ -1,0 +1,515 @@
+// sf_query.cu — per-shading-point kernels: template placement + feature
+// sampling (K5), per-layer sort / pool (K6), the FP32 SIMT backbone forward that
+// reproduces the reference's sequential FP32 arithmetic (K7-fp32), and decode.
+//
+// The feature kernel gathers density and transmittance from ONE interleaved
+// float2 level-0 volume ({rho, T} share the lattice, src/feature_pipeline.cpp:
+// 107-112 and :159-160), so each trilinear corner is a single 8-byte load; the
+// phase table (1 MiB at 64x128x32) stays L2-resident.
+#include "sf_internal.h"
+
+namespace sfb {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+inline unsigned grid_for(size_t n, int block = kBlock) {
+    size_t g = (n + block - 1) / block;
+    return unsigned(g > 0x7fffffff ? 0x7fffffff : (g == 0 ? 1 : g));
+}
+
+// {density, transmittance} at s (sample_trilinear + TransmittanceFeatureVolume::sample,
+// src/volume_grid.cpp:40-62, inc/feature_pipeline.h:44-46).
+__device__ __forceinline__ void sample_dt(const SceneDev& sc, const double* s, double& rho,
+                                          double& tr) {
+    const GridDev& g = sc.grid;
+    if (!in_box(g, s[0], s[1], s[2])) {
+        rho = 0.0;
+        tr = 1.0;
+        return;
+    }
+    if (sc.dt == nullptr) {
+        rho = trilinear(g, s[0], s[1], s[2]);
+        GridDev t = g;
+        t.v = sc.tvol;
+        tr = trilinear(t, s[0], s[1], s[2]);
+        return;
+    }
+    Cell c = cell_of(g, s[0], s[1], s[2]);
+    const size_t sy = size_t(g.nx), sz = size_t(g.nx) * g.ny;
+    const float2* v = sc.dt;
+    float2 a000 = __ldg(v + c.z0 * sz + c.y0 * sy + c.x0), a100 = __ldg(v + c.z0 * sz + c.y0 * sy + c.x1);
+    float2 a010 = __ldg(v + c.z0 * sz + c.y1 * sy + c.x0), a110 = __ldg(v + c.z0 * sz + c.y1 * sy + c.x1);
+    float2 a001 = __ldg(v + c.z1 * sz + c.y0 * sy + c.x0), a101 = __ldg(v + c.z1 * sz + c.y0 * sy + c.x1);
+    float2 a011 = __ldg(v + c.z1 * sz + c.y1 * sy + c.x0), a111 = __ldg(v + c.z1 * sz + c.y1 * sy + c.x1);
+    double c00 = lerp1(a000.x, a100.x, c.tx), c10 = lerp1(a010.x, a110.x, c.tx);
+    double c01 = lerp1(a001.x, a101.x, c.tx), c11 = lerp1(a011.x, a111.x, c.tx);
+    rho = lerp1(lerp1(c00, c10, c.ty), lerp1(c01, c11, c.ty), c.tz);
+    c00 = lerp1(a000.y, a100.y, c.tx);
+    c10 = lerp1(a010.y, a110.y, c.tx);
+    c01 = lerp1(a001.y, a101.y, c.tx);
+    c11 = lerp1(a011.y, a111.y, c.tx);
+    tr = lerp1(lerp1(c00, c10, c.ty), lerp1(c01, c11, c.ty), c.tz);
+}
+
+// Placement of template point i for query (p, omega, light): place_template +
+// placed_cap_radii (src/templates.cpp:207-256), entry from light_entry_point.
+// Returns false when the highlight entry coincides with p (the reference throws).
+__device__ __forceinline__ bool place_point(const SceneDev& sc, const TemplateDev& td, int i,
+                                            const double* p, const double* omega,
+                                            const double* light, double* s, double& cap) {
+    const double* q = td.pts + 3 * i;
+    if (td.kind == 0) {
+        s[0] = p[0] + q[0] * sc.template_scale;
+        s[1] = p[1] + q[1] * sc.template_scale;
+        s[2] = p[2] + q[2] * sc.template_scale;
+        cap = td.caps[i] * sc.template_scale;
+        return true;
+    }
+    const double lo[3] = {sc.grid.ox, sc.grid.oy, sc.grid.oz};
+    const double hi[3] = {sc.grid.hx, sc.grid.hy, sc.grid.hz};
+    double entry[3];
+    light_entry(lo, hi, p, light, entry);
+    double span[3] = {p[0] - entry[0], p[1] - entry[1], p[2] - entry[2]};
+    double len = sqrt(dot3(span, span));
+    if (len <= 0.0) return false;
+    double il = 1.0 / len;
+    double axis[3] = {span[0] * il, span[1] * il, span[2] * il};
+    double od = dot3(omega, axis);
+    double t[3] = {omega[0] - axis[0] * od, omega[1] - axis[1] * od, omega[2] - axis[2] * od};
+    double tl = sqrt(dot3(t, t));
+    double b[3];
+    if (tl > 1e-9) {
+        double it = 1.0 / tl;
+        t[0] = t[0] * it;
+        t[1] = t[1] * it;
+        t[2] = t[2] * it;
+        b[0] = axis[1] * t[2] - axis[2] * t[1];
+        b[1] = axis[2] * t[0] - axis[0] * t[2];
+        b[2] = axis[0] * t[1] - axis[1] * t[0];
+    } else {
+        orthonormal_basis(axis, t, b);
+    }
+    double scale = len / td.gen_distance;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double v = t[c] * q[0] + b[c] * q[1];
+        v = v + axis[c] * q[2];
+        s[c] = entry[c] + v * scale;
+    }
+    cap = td.caps[i] * scale;
+    return true;
+}
+
+// K5: sample_features (src/feature_pipeline.cpp:139-172) for a batch of queries.
+// Thread = (query, template point); output rows are SoA per block:
+// out[q*row_stride + col_offset + {0,1,2}*total + i] = {density, trans, phase}.
+__global__ void k_sample_features(SceneDev sc, TemplateDev td, int64_t n,
+                                  const double* __restrict__ queries, float* __restrict__ out,
+                                  int64_t row_stride, int64_t col_offset, int* err) {
+    int64_t total = int64_t(n) * td.total;
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        int64_t qi = idx / td.total;
+        int i = int(idx - qi * td.total);
+        const double* c = queries + 9 * qi;
+        double p[3] = {c[0], c[1], c[2]}, omega[3] = {c[3], c[4], c[5]}, light[3] = {c[6], c[7], c[8]};
+        double s[3], cap;
+        float* o = out + qi * row_stride + col_offset;
+        if (!place_point(sc, td, i, p, omega, light, s, cap)) {
+            atomicExch(err, 1);
+            o[i] = o[td.total + i] = o[2 * td.total + i] = __int_as_float(0x7fc00000);
+            continue;
+        }
+        double rho, tr;
+        sample_dt(sc, s, rho, tr);
+        double d[3] = {s[0] - p[0], s[1] - p[1], s[2] - p[2]};
+        double dist = sqrt(dot3(d, d));
+        double f;
+        if (dist <= 0.0) {
+            f = 1.0;  // diffuse centre: both caps are the full sphere
+        } else {
+            double half = cap >= dist ? kPi : asin(cap / dist);
+            double il = 1.0 / dist;
+            double axis[3] = {d[0] * il, d[1] * il, d[2] * il};
+            f = phase_lookup(sc.phase, omega, axis, half) * phase_lookup(sc.phase, light, axis, half);
+        }
+        o[i] = float(rho);
+        o[td.total + i] = float(tr);
+        o[2 * td.total + i] = float(f);
+    }
+}
+
+__global__ void k_place_template(SceneDev sc, TemplateDev td, int64_t n,
+                                 const double* __restrict__ p, const double* __restrict__ omega,
+                                 const double* __restrict__ entry, double* __restrict__ pts,
+                                 double* __restrict__ caps, int* err) {
+    int64_t total = int64_t(n) * td.total;
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        int64_t qi = idx / td.total;
+        int i = int(idx - qi * td.total);
+        const double* pq = p + 3 * qi;
+        const double* q = td.pts + 3 * i;
+        double* s = pts + 3 * idx;
+        if (td.kind == 0) {
+            for (int c = 0; c < 3; ++c) s[c] = pq[c] + q[c] * sc.template_scale;
+            caps[idx] = td.caps[i] * sc.template_scale;
+            continue;
+        }
+        const double* e = entry + 3 * qi;
+        const double* w = omega + 3 * qi;
+        double span[3] = {pq[0] - e[0], pq[1] - e[1], pq[2] - e[2]};
+        double len = sqrt(dot3(span, span));
+        if (len <= 0.0) {
+            atomicExch(err, 1);
+            continue;
+        }
+        double il = 1.0 / len;
+        double axis[3] = {span[0] * il, span[1] * il, span[2] * il};
+        double od = dot3(w, axis);
+        double t[3] = {w[0] - axis[0] * od, w[1] - axis[1] * od, w[2] - axis[2] * od};
+        double tl = sqrt(dot3(t, t));
+        double b[3];
+        if (tl > 1e-9) {
+            double it = 1.0 / tl;
+            t[0] = t[0] * it;
+            t[1] = t[1] * it;
+            t[2] = t[2] * it;
+            b[0] = axis[1] * t[2] - axis[2] * t[1];
+            b[1] = axis[2] * t[0] - axis[0] * t[2];
+            b[2] = axis[0] * t[1] - axis[1] * t[0];
+        } else {
+            orthonormal_basis(axis, t, b);
+        }
+        double scale = len / td.gen_distance;
+        for (int c = 0; c < 3; ++c) {
+            double v = t[c] * q[0] + b[c] * q[1];
+            v = v + axis[c] * q[2];
+            s[c] = e[c] + v * scale;
+        }
+        caps[idx] = td.caps[i] * scale;
+    }
+}
+
+// ---- sort / pool (src/predictor.cpp:153-191) --------------------------------------
+constexpr int kMaxSegs = 96;
+constexpr int kMaxLayerPoints = 64;
+struct SegTable {
+    int n_segs;
+    int n[kMaxSegs];        // points in the layer
+    int src[kMaxSegs];      // column of the first value in the feature row
+    int dst[kMaxSegs];      // slice offset of the sorted run (then mean, max)
+};
+
+// K6: one thread per (query, kind, layer, tau); insertion sort descending, then
+// float mean in sorted order and max = first element. Slices are stored
+// [slice_col][query] so the backbone's per-query reads coalesce across a warp.
+__global__ void k_slice(SegTable st, int64_t n, int64_t feat_stride,
+                        const float* __restrict__ feats, float* __restrict__ slices) {
+    int64_t total = n * st.n_segs;
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        int64_t q = idx % n;
+        int seg = int(idx / n);
+        int cnt = st.n[seg];
+        const float* src = feats + q * feat_stride + st.src[seg];
+        float a[kMaxLayerPoints];
+        for (int j = 0; j < cnt; ++j) {
+            float v = src[j];
+            int k = j - 1;
+            while (k >= 0 && a[k] < v) {
+                a[k + 1] = a[k];
+                --k;
+            }
+            a[k + 1] = v;
+        }
+        float acc = 0.0f;
+        for (int j = 0; j < cnt; ++j) acc += a[j];
+        float* dst = slices + int64_t(st.dst[seg]) * n + q;
+        for (int j = 0; j < cnt; ++j) dst[int64_t(j) * n] = a[j];
+        dst[int64_t(cnt) * n] = acc / float(cnt);
+        dst[int64_t(cnt + 1) * n] = a[0];
+    }
+}
+
+// ---- FP32 backbone (src/predictor.cpp:206-235, 352-409; src/neural.cpp:86-122) ------
+struct NetDesc {
+    int nl[2];
+    int counts[2][16];
+    int slice_off[2][16];  // slice column of (kind, layer) group
+    int W, M, H;
+    int literal;
+    double gamma;
+    int64_t stack_off[2][3];
+    int64_t merge_off, cross_off, head_off[3];
+};
+
+__device__ __forceinline__ float relu(float v) { return (v < 0.0f) ? 0.0f : v; }
+// 1/(1+exp(-v)) in float; exp rounded from FP64 so it matches the correctly
+// rounded expf of the CPU reference (src/neural.cpp:190-193).
+__device__ __forceinline__ float sigmoid_ref(float v) {
+    return 1.0f / (1.0f + float(exp(double(-v))));
+}
+
+// Tape<float>::dense: acc = b; acc += w*x (no contraction; built --fmad=false).
+template <int MAXM>
+__device__ __forceinline__ void dense_f32(const float* __restrict__ W, const float* __restrict__ b,
+                                          int m, int n, const float* x, float* y) {
+    for (int i = 0; i < m; ++i) {
+        float acc = __ldg(b + i);
+        const float* row = W + int64_t(i) * n;
+        for (int j = 0; j < n; ++j) acc += __ldg(row + j) * x[j];
+        y[i] = acc;
+    }
+}
+
+__device__ void run_stack_f32(const NetDesc& nd, const float* __restrict__ P, int k, int tau,
+                              const float* cfgv, const float* __restrict__ slices, int64_t n,
+                              int64_t q, float g_mean, float alpha, float* o_out) {
+    const int W = nd.W;
+    int64_t off = nd.stack_off[k][tau];
+    float o[64], o_att[64], u[64], t2[64], x[160];
+    dense_f32<64>(P + off, P + off + W * 7, W, 7, cfgv, o);
+    off += W * 7 + W;
+    for (int j = 0; j < W; ++j) o[j] = relu(o[j]);
+    for (int i = 0; i < nd.nl[k]; ++i) {
+        const int cnt = nd.counts[k][i];
+        const float* sl = slices + int64_t(nd.slice_off[k][i]) * n + q;
+        // tau blocks of (cnt + 2): sorted, mean, max
+        float v[8];
+        for (int t = 0; t < 3; ++t) {
+            v[t] = sl[int64_t(t * (cnt + 2) + cnt) * n];
+            v[3 + t] = sl[int64_t(t * (cnt + 2) + cnt + 1) * n];
+        }
+        v[6] = g_mean;
+        v[7] = alpha;
+        float w;
+        if (nd.literal) {
+            float acc = 0.0f;
+            for (int j = 0; j < 8; ++j) acc += (v[j] < 0.0f) ? 0.0f : v[j];
+            w = sigmoid_ref(acc / 8.0f);
+        } else {
+            float h[4], w3[3];
+            dense_f32<4>(P + off, P + off + 32, 4, 8, v, h);
+            for (int j = 0; j < 4; ++j) h[j] = relu(h[j]);
+            dense_f32<3>(P + off + 36, P + off + 48, 3, 4, h, w3);
+            w = sigmoid_ref(w3[tau]);
+            off += 51;
+        }
+        for (int j = 0; j < W; ++j) o_att[j] = o[j] * w;
+        const int K = W + cnt + 2;
+        for (int j = 0; j < W; ++j) x[j] = o_att[j];
+        const float* st = sl + int64_t(tau * (cnt + 2)) * n;
+        for (int j = 0; j < cnt + 2; ++j) x[W + j] = st[int64_t(j) * n];
+        dense_f32<64>(P + off, P + off + int64_t(W) * K, W, K, x, u);
+        off += int64_t(W) * K + W;
+        for (int j = 0; j < W; ++j) u[j] = relu(u[j]);
+        dense_f32<64>(P + off, P + off + W * W, W, W, u, t2);
+        off += W * W + W;
+        for (int j = 0; j < W; ++j) o[j] = relu(t2[j]) + o_att[j];
+    }
+    for (int j = 0; j < W; ++j) o_out[j] = o[j];
+}
+
+__global__ void __launch_bounds__(128) k_backbone_fp32(NetDesc nd, const float* __restrict__ P,
+                                                       int64_t n, const float* __restrict__ slices,
+                                                       const double* __restrict__ cfg8,
+                                                       float* __restrict__ y_out,
+                                                       double* __restrict__ F_out) {
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        const double* c8 = cfg8 + 8 * q;
+        int ng = int(c8[0]);
+        float g_mean = 0.0f;
+        for (int i = 0; i < ng; ++i) g_mean += float(c8[1 + i]);
+        if (ng > 0) g_mean /= float(double(ng));
+        float alpha = float(c8[7]);
+        float cfgv[7] = {0.0f, 0.0f, 0.0f, float(c8[4]), float(c8[5]), float(c8[6]), float(c8[7])};
+        for (int i = 0; i < ng && i < 3; ++i) cfgv[i] = float(c8[1 + i]);
+        const int W = nd.W, M = nd.M, H = nd.H;
+        float merged[3 * 128], cat[128], od[64], oh[64], h1[128], h2[128], y[3];
+        for (int t = 0; t < 3; ++t) {
+            run_stack_f32(nd, P, 0, t, cfgv, slices, n, q, g_mean, alpha, od);
+            run_stack_f32(nd, P, 1, t, cfgv, slices, n, q, g_mean, alpha, oh);
+            for (int j = 0; j < W; ++j) {
+                cat[j] = od[j];
+                cat[W + j] = oh[j];
+            }
+            const float* mW = P + nd.merge_off + int64_t(t) * (int64_t(M) * 2 * W + M);
+            dense_f32<128>(mW, mW + int64_t(M) * 2 * W, M, 2 * W, cat, merged + t * M);
+            for (int j = 0; j < M; ++j) merged[t * M + j] = relu(merged[t * M + j]);
+        }
+        dense_f32<128>(P + nd.cross_off, P + nd.cross_off + int64_t(M) * 3 * M, M, 3 * M, merged,
+                       h1);
+        for (int j = 0; j < M; ++j) h1[j] = relu(h1[j]);
+        dense_f32<128>(P + nd.head_off[0], P + nd.head_off[0] + int64_t(H) * M, H, M, h1, h2);
+        for (int j = 0; j < H; ++j) h2[j] = relu(h2[j]);
+        dense_f32<128>(P + nd.head_off[1], P + nd.head_off[1] + int64_t(H) * H, H, H, h2, h1);
+        for (int j = 0; j < H; ++j) h1[j] = relu(h1[j]);
+        dense_f32<3>(P + nd.head_off[2], P + nd.head_off[2] + 3 * H, 3, H, h1, y);
+        for (int c = 0; c < 3; ++c) {
+            y[c] = fabsf(y[c]);
+            if (y_out) y_out[3 * q + c] = y[c];
+            // decode_prediction (src/predictor.cpp:406-409)
+            if (F_out) F_out[3 * q + c] = pow(c8[4 + c], nd.gamma) * expm1(double(y[c]));
+        }
+    }
+}
+
+// make_config (src/predictor.cpp:261-274): g params + albedo of the medium,
+// alpha = angle_between(omega, light) per query.
+__global__ void k_make_cfg8(sf_medium_params m, int64_t n, const double* __restrict__ queries,
+                            double* __restrict__ cfg8) {
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        const double* c = queries + 9 * q;
+        double* o = cfg8 + 8 * q;
+        o[0] = m.n_g;
+        o[1] = m.n_g > 0 ? m.g[0] : 0.0;
+        o[2] = m.n_g > 1 ? m.g[1] : 0.0;
+        o[3] = m.n_g > 2 ? m.g[2] : 0.0;
+        o[4] = m.albedo[0];
+        o[5] = m.albedo[1];
+        o[6] = m.albedo[2];
+        o[7] = angle_between(c + 3, c + 6);
+    }
+}
+
+}  // namespace
+
+SceneDev scene_dev(const sf_grid& density, const sf_grid& tvol, const float2* dt,
+                   const sf_phase_model& m, const sf_phase_table& t, double ts) {
+    SceneDev s{};
+    s.grid = density.dev();
+    s.dt = dt;
+    s.tvol = tvol.d;
+    s.phase.kind = m.kind;
+    s.phase.n_lobes = m.n_lobes;
+    for (int k = 0; k < 3; ++k) {
+        s.phase.w[k] = m.weight[k];
+        s.phase.g[k] = m.g[k];
+    }
+    s.phase.table = t.d;
+    s.phase.gr = t.g;
+    s.phase.ar = t.a;
+    s.phase.hr = t.h;
+    s.template_scale = ts;
+    return s;
+}
+
+TemplateDev template_dev(const sf_template& t) {
+    return TemplateDev{t.kind, t.total, t.d_points, t.d_caps, t.gen_distance};
+}
+
+void launch_sample_features(const SceneDev& sc, const TemplateDev& td, int64_t n,
+                            const double* queries, float* out, int64_t row_stride,
+                            int64_t col_offset, int* err, cudaStream_t s) {
+    if (n <= 0) return;
+    k_sample_features<<<grid_for(size_t(n) * td.total, 128), 128, 0, s>>>(
+        sc, td, n, queries, out, row_stride, col_offset, err);
+    SFB_CUDA(cudaGetLastError());
+}
+
+void launch_place_template(const sf_template& t, int64_t n, const double* p,
+                           const double* omega, const double* entry, double ts, double* pts,
+                           double* caps, int* err, cudaStream_t s) {
+    if (n <= 0) return;
+    SceneDev sc{};
+    sc.template_scale = ts;
+    k_place_template<<<grid_for(size_t(n) * t.total), kBlock, 0, s>>>(sc, template_dev(t), n, p,
+                                                                       omega, entry, pts, caps, err);
+    SFB_CUDA(cudaGetLastError());
+}
+
+int64_t slices_per_query(const sf_backbone_config& c) {
+    int64_t s = 0;
+    for (int i = 0; i < c.n_diffuse_layers; ++i) s += 3 * (c.diffuse_counts[i] + 2);
+    for (int i = 0; i < c.n_highlight_layers; ++i) s += 3 * (c.highlight_counts[i] + 2);
+    return s;
+}
+
+static void seg_table(const sf_backbone_config& c, SegTable& st, NetDesc* nd) {
+    st.n_segs = 0;
+    int nd_total = 0, nh_total = 0;
+    for (int i = 0; i < c.n_diffuse_layers; ++i) nd_total += c.diffuse_counts[i];
+    for (int i = 0; i < c.n_highlight_layers; ++i) nh_total += c.highlight_counts[i];
+    int dst = 0;
+    for (int k = 0; k < 2; ++k) {
+        int nl = k == 0 ? c.n_diffuse_layers : c.n_highlight_layers;
+        const int* counts = k == 0 ? c.diffuse_counts : c.highlight_counts;
+        int ntot = k == 0 ? nd_total : nh_total;
+        int base = k == 0 ? 0 : 3 * nd_total;
+        int start = 0;
+        for (int i = 0; i < nl; ++i) {
+            if (nd) nd->slice_off[k][i] = dst;
+            for (int tau = 0; tau < 3; ++tau) {
+                // tau order {density, phase, transmittance}; feature channels are
+                // {density, transmittance, phase} (src/predictor.cpp:168-169).
+                int ch = tau == 0 ? 0 : (tau == 1 ? 2 : 1);
+                if (st.n_segs >= kMaxSegs) fail(SF_ERR_INVALID_ARGUMENT, "too many template layers");
+                st.n[st.n_segs] = counts[i];
+                st.src[st.n_segs] = base + ch * ntot + start;
+                st.dst[st.n_segs] = dst;
+                ++st.n_segs;
+                dst += counts[i] + 2;
+            }
+            start += counts[i];
+        }
+    }
+}
+
+void launch_slice(const sf_backbone_config& c, int64_t n, const float* feats, float* slices,
+                  cudaStream_t s) {
+    if (n <= 0) return;
+    for (int i = 0; i < c.n_diffuse_layers; ++i)
+        if (c.diffuse_counts[i] > kMaxLayerPoints) fail(SF_ERR_INVALID_ARGUMENT, "layer too large");
+    for (int i = 0; i < c.n_highlight_layers; ++i)
+        if (c.highlight_counts[i] > kMaxLayerPoints) fail(SF_ERR_INVALID_ARGUMENT, "layer too large");
+    SegTable st{};
+    seg_table(c, st, nullptr);
+    int64_t stride = 0;
+    for (int i = 0; i < c.n_diffuse_layers; ++i) stride += 3 * c.diffuse_counts[i];
+    for (int i = 0; i < c.n_highlight_layers; ++i) stride += 3 * c.highlight_counts[i];
+    k_slice<<<grid_for(size_t(n) * st.n_segs), kBlock, 0, s>>>(st, n, stride, feats, slices);
+    SFB_CUDA(cudaGetLastError());
+}
+
+void launch_backbone_fp32(const sf_backbone& b, int64_t n, const float* slices,
+                          const double* cfg8, float* y, double* F, cudaStream_t s) {
+    if (n <= 0) return;
+    const sf_backbone_config& c = b.cfg;
+    if (c.width > 64 || c.merge_width > 128 || c.head_width > 128)
+        fail(SF_ERR_INVALID_ARGUMENT, "fp32 backbone: width>64 or merge/head width>128 unsupported");
+    NetDesc nd{};
+    SegTable st{};
+    seg_table(c, st, &nd);
+    nd.nl[0] = c.n_diffuse_layers;
+    nd.nl[1] = c.n_highlight_layers;
+    for (int i = 0; i < 16; ++i) {
+        nd.counts[0][i] = c.diffuse_counts[i];
+        nd.counts[1][i] = c.highlight_counts[i];
+    }
+    nd.W = c.width;
+    nd.M = c.merge_width;
+    nd.H = c.head_width;
+    nd.literal = c.literal_attention;
+    nd.gamma = c.gamma;
+    for (int k = 0; k < 2; ++k)
+        for (int t = 0; t < 3; ++t) nd.stack_off[k][t] = b.layout.stack_off[k][t];
+    nd.merge_off = b.layout.merge_off;
+    nd.cross_off = b.layout.cross_off;
+    for (int l = 0; l < 3; ++l) nd.head_off[l] = b.layout.head_off[l];
+    k_backbone_fp32<<<grid_for(size_t(n), 128), 128, 0, s>>>(nd, b.d_params, n, slices, cfg8, y, F);
+    SFB_CUDA(cudaGetLastError());
+}
+
+void launch_make_cfg8(const sf_medium_params& m, int64_t n, const double* queries, double* cfg8,
+                      cudaStream_t s) {
+    if (n <= 0) return;
+    k_make_cfg8<<<grid_for(size_t(n)), kBlock, 0, s>>>(m, n, queries, cfg8);
+    SFB_CUDA(cudaGetLastError());
+}
+
+}  // namespace sfb
