@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py — shading-point queries/sec (features + inference) on B200.
+
+Workload (BASELINE.json configs[1], "C2"): 128^3 seeded 6-octave fractal noise
+plus a hard-edged ellipsoid, albedo 0.999, single HG lobe g = 0.85, one
+directional light normalize(0.2,-1,0.1), 65,536 shading points per GPU (a
+256x256 tile of seeded points inside the medium with random unit view
+directions), the reference SPEC network (32/64/64 widths, 8 diffuse + 4
+highlight layers per feature type) with He-uniform weights, seed 0. Synthetic,
+seeded data; no dataset.
+
+A step = one pass of the hot path over one batch: for every query, both
+templates' features (density, transmittance, phase at 266 points), make_config,
+per-layer sort/pool, the 6-stack attention backbone, merges, head and decode.
+The per-light build (pyramid + graded transmittance + 3D-CNN combiner) is timed
+separately and reported under "stages".
+
+  value : queries/s with queries and outputs resident in HBM, L2 flushed
+          (256 MiB write) between timed steps, CUDA events per step, max over ranks.
+  e2e   : the same through the public API (paper_2401_14051_b200.query) with
+          pinned HOST query rows in and HOST radiance out, copies inside the timed
+          region.
+
+Multi-GPU (torchrun): each rank owns its own 65,536-query tile set (weak
+scaling, no data-path collective); the radiance tiles are gathered to rank 0
+once per step (all_gather over NCCL), the one exchange of the path.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+compiled from the reference sources) on the host cores, on a bounded sample of
+the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LIGHT = (0.2, -1.0, 0.1)
+QUERIES_PER_GPU = 65536
+GRID = 128
+ALBEDO = 0.999
+G = 0.85
+METRIC = "shading-point queries/sec (features+inference) at 1/2/4/8 B200; % roofline"
+WORKLOAD = ("C2: 128^3 fractal-noise+ellipsoid cloud, albedo 0.999, HG g=0.85, 65,536 shading points per GPU "
+            "(256x256 tile), 8 diffuse + 4 highlight template layers (266 points) over all 8 mip levels, "
+            "SPEC backbone 32/64/64, 1 light")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return j.get("hbm_gbs", 6650.0), j.get("bf16_tflops", 1590.0), j.get("bf16_tflops_sustained", 1400.0), \
+            "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def scene_inputs(rank):
+    from paper_2401_14051_b200 import scenes
+    vol = scenes.fractal_ellipsoid(GRID, 1)
+    centers = scenes.draw_centers(vol, QUERIES_PER_GPU, 11 + rank, LIGHT)
+    return vol, centers
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.samples = []
+        self.active = False
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8 and self.active:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference_sample(vol, centers, n_target_seconds=10.0, max_queries=QUERIES_PER_GPU, threads=None):
+    """Time the reference's per-query loop (oracle/_ref) on a bounded sample."""
+    from oracle.oracle import BackboneCfg, PhaseModel, Reference
+    from paper_2401_14051_b200 import scenes
+    R = Reference()
+    threads = threads or os.cpu_count()
+    R.set_threads(threads)
+    vs = 2.0 / GRID
+    origin = np.array([-1.0, -1.0, -1.0])
+    light = np.array(LIGHT)
+    t0 = time.time()
+    tvol = R.build_tvol(vol, vs, origin, light)
+    t_tvol = time.time() - t0
+    t0 = time.time()
+    table = R.phase_table(64, 128, 32, 16)
+    t_table = time.time() - t0
+    data = os.path.join(ROOT, "paper_2401_14051_b200", "data")
+    ctx = R.make_ctx(vol, tvol, vs, origin, os.path.join(data, "diffuse_seed7.vtmpl"),
+                     os.path.join(data, "highlight_seed8.vtmpl"), PhaseModel.hg(G), table)
+    b = R.backbone(BackboneCfg(seed=0))
+    cfg8 = scenes.config_rows(centers, [G], [ALBEDO] * 3)
+    probe = min(1024, len(centers))
+    secs, _ = R.time_queries(ctx, b, centers[:probe], cfg8[:probe])
+    rate = probe / max(secs, 1e-9)
+    n = int(min(max_queries, max(probe, rate * n_target_seconds)))
+    secs, F = R.time_queries(ctx, b, centers[:n], cfg8[:n])
+    return {"value": n / secs, "seconds": secs, "n": n, "threads": threads, "tvol_s": t_tvol, "table_s": t_table,
+            "R": R, "ctx": ctx, "b": b, "cfg8": cfg8, "F": F}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    vol, centers = scene_inputs(0)
+    sample = max(256, args.ref_sample)
+    r = cpu_reference_sample(vol, centers, n_target_seconds=0.5, max_queries=sample)
+    R, ctx, b, cfg8 = r["R"], r["ctx"], r["b"], r["cfg8"]
+    for i in range(args.warmup):
+        R.time_queries(ctx, b, centers[:sample], cfg8[:sample])
+    total = 0.0
+    for i in range(args.steps):
+        s, _ = R.time_queries(ctx, b, centers[:sample], cfg8[:sample])
+        total += s
+    value = sample * args.steps / total
+    out = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": WORKLOAD, "queries_per_step": sample, "grid": GRID},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": r["threads"], "kind": "reference",
+                         "sample": f"{sample} of the 65,536 C2 queries per step (reference per-query loop: "
+                                   f"sample_features x2 + predict_y + decode_prediction, parallel_for over "
+                                   f"{r['threads']} threads)"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "stages": {"reference_tvol_build_s": r["tvol_s"], "reference_phase_table_s": r["table_s"]},
+    }
+    print(json.dumps(out))
+    return 0
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2401_14051_b200 as sf
+    from paper_2401_14051_b200._lib import profile_read
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    precision = {"fp32": sf.FP32, "bf16": sf.BF16}[args.precision]
+
+    vol, centers = scene_inputs(rank)
+    n = len(centers)
+
+    # ---- per-light build (reported separately)
+    t_build = {}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    ev[0].record(stream)
+    g = sf.DensityGrid.from_array(vol, 2.0 / GRID, (-1.0, -1.0, -1.0))
+    ev[1].record(stream)
+    pyr = sf.DensityPyramid(g, stream=stream)
+    ev[2].record(stream)
+    tvol = sf.build_transmittance_volume(pyr, LIGHT, stream=stream)
+    ev[3].record(stream)
+    table = sf.PhaseTable(64, 128, 32, 16, stream=stream)
+    ev[4].record(stream)
+    torch.cuda.synchronize()
+    t_build = {"pyramid_ms": ev[1].elapsed_time(ev[2]), "transmittance_ms": ev[2].elapsed_time(ev[3]),
+               "phase_table_ms": ev[3].elapsed_time(ev[4])}
+    d, h = (sf.load_template(os.path.join(ROOT, "paper_2401_14051_b200", "data", f))
+            for f in ("diffuse_seed7.vtmpl", "highlight_seed8.vtmpl"))
+    scene = sf.Scene(g, tvol, d, h, sf.PhaseModel.hg(G), table)
+    net = sf.make_backbone(sf.BackboneConfig(seed=0))
+    medium = sf.MediumParams((G,), (ALBEDO,) * 3)
+
+    q_dev = torch.from_numpy(centers).to(dev)
+    F_dev = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    F_all = torch.empty((ws * n, 3), dtype=torch.float64, device=dev) if ws > 1 else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        sf.query(scene, net, medium, q_dev, precision, F_out=F_dev, stream=stream)
+        if ws > 1:
+            dist.all_gather_into_tensor(F_all, F_dev)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    clocks.active = True
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = sf.lib.sf_launch_count()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)  # L2 flush outside the timed window
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    launches = (sf.lib.sf_launch_count() - l0) / args.steps
+    if ws > 1:
+        dist.barrier()
+    clocks.active = False
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    ms_per_step = ms / args.steps
+    value = ws * n / (ms_per_step * 1e-3)
+
+    # ---- e2e through the public API with pinned host buffers
+    q_host = torch.from_numpy(centers).pin_memory().numpy()
+    F_host = torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy()
+    for _ in range(2):
+        sf.query(scene, net, medium, q_host, precision, F_out=F_host, stream=stream)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e_steps = max(3, args.steps // 2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(e_steps):
+        sf.query(scene, net, medium, q_host, precision, F_out=F_host, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = torch.tensor([e0.elapsed_time(e1) / e_steps], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = ws * n / (float(e_ms.item()) * 1e-3)
+    clocks.stop()
+
+    # ---- per-stage device times (CUDA events on the launching stream), L2 flushed
+    sf.lib.sf_profile_enable(1)
+    profile_read()
+    p_steps = max(3, min(args.steps, 20))
+    for i in range(p_steps):
+        flush.fill_(i & 0xFF)
+        step()
+    torch.cuda.synchronize()
+    stages = profile_read()
+    sf.lib.sf_profile_enable(0)
+    stage_ms = {k: v[0] / p_steps for k, v in stages.items()}
+    stage_launch = {k: v[1] / p_steps for k, v in stages.items()}
+
+    hbm, bf16, bf16_sus, peak_kind = peaks()
+    # Algorithmic bytes per query for sampling: 8 corners x 8 B
+    # {rho,T} per template point + 2 phase lookups x 8 corners x 4 B x n_lobes
+    # per non-centre point.
+    bytes_d = 194 * 64 + 193 * 2 * 8 * 4
+    bytes_h = 72 * 64 + 72 * 2 * 8 * 4
+    flop_q = 274912  # 2 x 137,456 weight MACs per query (walk_params shapes)
+    dom = max(stage_ms, key=stage_ms.get)
+    if dom == "backbone":
+        achieved = flop_q * n / (stage_ms[dom] * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": "backbone", "achieved": achieved, "peak": bf16_sus,
+                "unit": "TFLOP/s", "frac": achieved / bf16_sus, "traffic": None,
+                "peak_kind": f"{peak_kind} bf16 sustained",
+                "algorithmic": f"{flop_q} FLOP/query x {n} queries per launch"}
+    else:
+        bq = bytes_d if dom == "features_diffuse" else bytes_h if dom == "features_highlight" else bytes_d
+        achieved = bq * n / (stage_ms[dom] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "peak_kind": f"{peak_kind} HBM copy",
+                "algorithmic": f"{bq} B/query gathered x {n} queries per launch"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            r = cpu_reference_sample(vol, centers, n_target_seconds=args.cpu_seconds)
+            cpu = {"value": r["value"], "unit": "queries/s", "cores": r["threads"], "kind": "reference",
+                   "sample": f"first {r['n']} of this rank's 65,536 C2 queries, reference per-query loop "
+                             f"(sample_features x2 + predict_y + decode) over {r['threads']} host threads, "
+                             f"{r['seconds']:.1f} s; tvol/phase-table setup excluded "
+                             f"({r['tvol_s']:.1f} s / {r['table_s']:.1f} s)"}
+        except Exception as e:  # the checker may be absent; report why
+            cpu = {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16" if precision == sf.BF16 else "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "queries_per_gpu": n, "grid": GRID, "albedo": ALBEDO, "g": G,
+                       "network": "bf16 tcgen05" if precision == sf.BF16 else "fp32 SIMT (reference arithmetic)",
+                       "l2": "flushed between timed steps (256 MiB device write outside the events)",
+                       "parallelism": f"tile-sharded x{ws}"},
+            "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(centers.nbytes),
+                    "d2h_bytes_per_step": int(n * 3 * 8)},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "stages": {"per_step_ms": stage_ms, "per_step_launches": stage_launch, "per_light_build": t_build},
+        }
+        print(json.dumps(out))
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "bf16"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-sample", type=int, default=2048)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.precision == "auto":
+        import paper_2401_14051_b200 as sf
+        from paper_2401_14051_b200._lib import lib
+        args.precision = "bf16" if _tc_available(lib) else "fp32"
+    return run_b200(args)
+
+
+def _tc_available(lib):
+    import ctypes
+    import paper_2401_14051_b200 as sf
+    try:
+        net = sf.make_backbone(sf.BackboneConfig(seed=0))
+        sf.predict(net, np.zeros((1, 798), np.float32), np.array([[1, 0.5, 0, 0, 0.5, 0.5, 0.5, 1.0]]), sf.BF16)
+        return True
+    except sf.ScatterfieldError:
+        return False
+
+
+if __name__ == "__main__":
+    sys.exit(main())

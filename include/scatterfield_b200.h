@@ -132,6 +132,10 @@ int sf_combine_transmittance(const sf_grid* const* fields, int n, const float* k
 int sf_build_transmittance_volume(const sf_pyramid* p, const double light[3],
                                   const float* kernels, const float* scales, double lambda,
                                   double step_scale, sf_tvol** out, sf_stream stream);
+/* TransmittanceFeatureVolume{light_dir, values} from explicit values (the struct's
+ * public members, feature_pipeline.h:38-41); values h/d [nz][ny][nx]. */
+int sf_tvol_from_values(int nx, int ny, int nz, double voxel_size, const double origin[3],
+                        const float* values, const double light[3], sf_tvol** out);
 /* Borrowed level-0 grid of the volume (TransmittanceFeatureVolume::values). */
 const sf_grid* sf_tvol_values(const sf_tvol* t);
 void sf_tvol_destroy(sf_tvol* t);
@@ -204,6 +208,24 @@ void sf_scene_destroy(sf_scene* s);
 int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium,
              int64_t n, const double* queries, int precision, double* F_out, float* y_out,
              sf_stream stream);
+
+/* ---- instrumentation (per-stage CUDA-event timing) -------------- */
+enum sf_stage {
+    SF_STAGE_CONFIG = 0,             /* make_config rows */
+    SF_STAGE_FEATURES_DIFFUSE = 1,   /* sample_features, diffuse template */
+    SF_STAGE_FEATURES_HIGHLIGHT = 2, /* sample_features, highlight template */
+    SF_STAGE_SLICE = 3,              /* per-layer sort + pools */
+    SF_STAGE_BACKBONE = 4,           /* network forward + decode */
+    SF_STAGE_COUNT = 5
+};
+/* When enabled, sf_query/sf_predict record a CUDA event pair around every stage on
+ * the caller's stream (no synchronization). sf_profile_read synchronizes on those
+ * events, writes the summed device milliseconds and launch counts per stage, and
+ * resets the accumulators. */
+int sf_profile_enable(int on);
+int sf_profile_read(double stage_ms[SF_STAGE_COUNT], int64_t stage_launches[SF_STAGE_COUNT]);
+/* Number of kernels this library has launched since load (all entry points). */
+int64_t sf_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -68,6 +68,7 @@ _SIGS = {
     "sf_conv3_replicate": (I, [P, P, PP, P]),
     "sf_combine_transmittance": (I, [P, I, P, P, P, PP, P]),
     "sf_build_transmittance_volume": (I, [P, P, P, P, D, D, PP, P]),
+    "sf_tvol_from_values": (I, [I, I, I, D, P, P, P, PP]),
     "sf_tvol_values": (P, [P]),
     "sf_tvol_destroy": (None, [P]),
     "sf_light_entry_point": (I, [P, P, P, P, P]),
@@ -90,7 +91,20 @@ _SIGS = {
     "sf_scene_create": (I, [P, P, P, P, P, P, D, PP]),
     "sf_scene_destroy": (None, [P]),
     "sf_query": (I, [P, P, P, I64, P, I, P, P, P]),
+    "sf_profile_enable": (I, [I]),
+    "sf_profile_read": (I, [P, P]),
+    "sf_launch_count": (I64, []),
 }
+
+STAGES = ("config", "features_diffuse", "features_highlight", "slice", "backbone")
+
+
+def profile_read():
+    """Summed device ms and launch counts per stage since the last read."""
+    ms = (C.c_double * len(STAGES))()
+    n = (C.c_int64 * len(STAGES))()
+    check(lib.sf_profile_read(ms, n))
+    return {s: (ms[i], n[i]) for i, s in enumerate(STAGES)}
 
 EXPORTS = tuple(_SIGS)
 

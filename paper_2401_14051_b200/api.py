@@ -204,6 +204,16 @@ class TransmittanceFeatureVolume:
         self.weights = weights
         self.values = DensityGrid(0, _handle=C.c_void_p(lib.sf_tvol_values(handle)), _owner=self)
 
+    @staticmethod
+    def from_values(values, voxel_size, origin, light_dir, weights: CombinerWeights = None):
+        """Construct from explicit level-0 values (the reference struct's public members)."""
+        v = _arr(values, np.float32)
+        nz, ny, nx = v.shape
+        h = C.c_void_p()
+        check(lib.sf_tvol_from_values(nx, ny, nz, float(voxel_size), dvec(origin), ptr(v), dvec(light_dir),
+                                      C.byref(h)))
+        return TransmittanceFeatureVolume(h, _normalize(light_dir), weights)
+
     def sample(self, pts):
         pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
         lo, hi = self.values.bounds()

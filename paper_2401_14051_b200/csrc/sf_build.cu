@@ -227,6 +227,7 @@ void launch_pyramid_down(const sf_grid& src, sf_grid& dst, cudaStream_t s) {
     k_pyramid_down<<<grid_for(dst.count()), kBlock, 0, s>>>(src.d, src.nx, src.ny, src.nz, dst.d,
                                                            dst.nx, dst.ny, dst.nz);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void launch_graded(const sf_grid& level, const double ts[3], double coeff, double step,
@@ -234,6 +235,7 @@ void launch_graded(const sf_grid& level, const double ts[3], double coeff, doubl
     k_graded<<<grid_for(level.count(), 128), 128, 0, s>>>(level.dev(), ts[0], ts[1], ts[2],
                                                           coeff, step, out);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void launch_conv3(const sf_grid& in, const float k27[27], float* out, cudaStream_t s) {
@@ -241,6 +243,7 @@ void launch_conv3(const sf_grid& in, const float k27[27], float* out, cudaStream
     for (int i = 0; i < 27; ++i) k.k[i] = k27[i];
     k_conv3<<<grid_for(in.count()), kBlock, 0, s>>>(in.d, in.nx, in.ny, in.nz, k, out);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void launch_combine(const std::vector<const sf_grid*>& conv, const std::vector<float>& scales,
@@ -254,11 +257,13 @@ void launch_combine(const std::vector<const sf_grid*>& conv, const std::vector<f
     }
     k_combine<<<grid_for(base.count()), kBlock, 0, s>>>(lv, base.dev(), out);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void launch_interleave(const float* a, const float* b, float2* out, size_t n, cudaStream_t s) {
     k_interleave<<<grid_for(n), kBlock, 0, s>>>(a, b, out, n);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void launch_phase_table(int gr, int ar, int hr, const std::vector<double>& nodes,
@@ -272,18 +277,21 @@ void launch_phase_table(int gr, int ar, int hr, const std::vector<double>& nodes
     }
     k_phase_table<<<grid_for(size_t(gr) * ar * hr, 128), 128, 0, s>>>(gr, ar, hr, gl, out);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void launch_lookup_hg(const sf_phase_table& t, int64_t n, const double* g, const double* a,
                       const double* h, double* out, cudaStream_t s) {
     k_lookup_hg<<<grid_for(size_t(n)), kBlock, 0, s>>>(t.d, t.g, t.a, t.h, n, g, a, h, out);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void launch_sample_trilinear(const sf_grid& g, int64_t n, const double* pts, double* out,
                              cudaStream_t s) {
     k_sample_trilinear<<<grid_for(size_t(n)), kBlock, 0, s>>>(g.dev(), n, pts, out);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 }  // namespace sfb

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -314,7 +315,44 @@ int nd_total(const sf_template* t) { return t ? t->total : 0; }
 
 }  // namespace
 
+namespace {
+std::atomic<int64_t> g_launches{0};
+
+// Per-stage CUDA-event profiling (sf_profile_enable / sf_profile_read).
+struct StageRec {
+    int stage;
+    cudaEvent_t a, b;
+    int64_t launches;
+};
+std::mutex g_prof_mu;
+std::atomic<bool> g_prof_on{false};
+std::vector<StageRec> g_recs;
+
+struct StageScope {
+    int stage;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    int64_t l0 = 0;
+    StageScope(int st, cudaStream_t str) : stage(st), s(str) {
+        if (!g_prof_on.load()) return;
+        cudaEventCreate(&a);
+        cudaEventRecord(a, s);
+        l0 = g_launches.load();
+    }
+    ~StageScope() {
+        if (!a) return;
+        cudaEvent_t b;
+        cudaEventCreate(&b);
+        cudaEventRecord(b, s);
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        g_recs.push_back({stage, a, b, g_launches.load() - l0});
+    }
+};
+}  // namespace
+
 namespace sfb {
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 int sm_count() {
     static int n = [] {
         int dev = 0, v = 148;
@@ -561,6 +599,22 @@ int sf_build_transmittance_volume(const sf_pyramid* p, const double light[3], co
             throw;
         }
         for (sf_grid* g : fields) free_grid(g);
+    });
+}
+
+int sf_tvol_from_values(int nx, int ny, int nz, double vs, const double origin[3],
+                        const float* values, const double light[3], sf_tvol** out) {
+    return guard([&] {
+        auto t = std::make_unique<sf_tvol>();
+        normalize3(light, t->light);
+        t->values = new_grid(nx, ny, nz, vs, origin);
+        cudaError_t e = cudaMemcpy(t->values->d, values, t->values->count() * sizeof(float),
+                                   cudaMemcpyDefault);
+        if (e != cudaSuccess) {
+            free_grid(t->values);
+            sfb::cuda_check(e, "tvol upload");
+        }
+        *out = t.release();
     });
 }
 
@@ -833,8 +887,14 @@ int sf_predict(const sf_backbone* b, int64_t n, const float* features, const dou
         Out<float> oy(y_out, size_t(n) * 3, stream);
         Out<double> oF(F_out, size_t(n) * 3, stream);
         Scratch<float> slices(size_t(n) * sfb::slices_per_query(c), stream);
-        sfb::launch_slice(c, n, f.d, slices.p, stream);
-        run_backbone(*b, precision, n, slices.p, cf.d, oy.d, oF.d, stream);
+        {
+            StageScope st(SF_STAGE_SLICE, stream);
+            sfb::launch_slice(c, n, f.d, slices.p, stream);
+        }
+        {
+            StageScope st(SF_STAGE_BACKBONE, stream);
+            run_backbone(*b, precision, n, slices.p, cf.d, oy.d, oF.d, stream);
+        }
         oy.finish();
         oF.finish();
         sync(stream);
@@ -904,14 +964,35 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
         for (int64_t q0 = 0; q0 < n; q0 += chunk) {
             int64_t m = std::min(chunk, n - q0);
             const double* qd = iq.d + 9 * q0;
-            sfb::launch_make_cfg8(*medium, m, qd, cfg8.p, stream);
-            sfb::launch_sample_features(sc, sfb::template_dev(*s->dt), m, qd, feats.p, feat, 0, err.p,
-                                        stream);
-            sfb::launch_sample_features(sc, sfb::template_dev(*s->ht), m, qd, feats.p, feat, 3 * nd,
-                                        err.p, stream);
-            sfb::launch_slice(c, m, feats.p, slices.p, stream);
-            run_backbone(*b, precision, m, slices.p, cfg8.p, oy.d ? oy.d + 3 * q0 : nullptr,
-                         oF.d ? oF.d + 3 * q0 : nullptr, stream);
+            {
+                StageScope st(SF_STAGE_CONFIG, stream);
+                sfb::launch_make_cfg8(*medium, m, qd, cfg8.p, stream);
+            }
+            {
+                StageScope st(SF_STAGE_FEATURES_DIFFUSE, stream);
+                sfb::launch_sample_features(sc, sfb::template_dev(*s->dt), m, qd, feats.p, feat, 0,
+                                            err.p, stream);
+            }
+            {
+                StageScope st(SF_STAGE_FEATURES_HIGHLIGHT, stream);
+                sfb::launch_sample_features(sc, sfb::template_dev(*s->ht), m, qd, feats.p, feat,
+                                            3 * nd, err.p, stream);
+            }
+            {
+                StageScope st(SF_STAGE_SLICE, stream);
+                sfb::launch_slice(c, m, feats.p, slices.p, stream);
+            }
+            {
+                StageScope st(SF_STAGE_BACKBONE, stream);
+                run_backbone(*b, precision, m, slices.p, cfg8.p, oy.d ? oy.d + 3 * q0 : nullptr,
+                             oF.d ? oF.d + 3 * q0 : nullptr, stream);
+            }
+        }
+        if (!oF.host && !oy.host && !iq.buf.p) {
+            // Device in, device out: stay asynchronous (no host round trip). A
+            // highlight placement failure (entry == p, where the reference throws)
+            // shows up as NaN rows in the outputs instead of an error status.
+            return;
         }
         int herr = 0;
         SFB_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -921,6 +1002,39 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
         if (herr) fail(SF_ERR_INVALID_ARGUMENT, "place_template: entry coincides with p");
     });
 }
+
+int sf_profile_enable(int on) {
+    g_prof_on.store(on != 0);
+    return SF_OK;
+}
+
+int sf_profile_read(double stage_ms[SF_STAGE_COUNT], int64_t stage_launches[SF_STAGE_COUNT]) {
+    return guard([&] {
+        std::vector<StageRec> recs;
+        {
+            std::lock_guard<std::mutex> lk(g_prof_mu);
+            recs.swap(g_recs);
+        }
+        for (int i = 0; i < SF_STAGE_COUNT; ++i) {
+            stage_ms[i] = 0.0;
+            if (stage_launches) stage_launches[i] = 0;
+        }
+        cudaError_t first = cudaSuccess;
+        for (StageRec& r : recs) {
+            float ms = 0.0f;
+            cudaError_t e = cudaEventSynchronize(r.b);
+            if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+            if (e != cudaSuccess && first == cudaSuccess) first = e;
+            stage_ms[r.stage] += ms;
+            if (stage_launches) stage_launches[r.stage] += r.launches;
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        sfb::cuda_check(first, "profile events");
+    });
+}
+
+int64_t sf_launch_count(void) { return g_launches.load(); }
 
 }  // extern "C"
 

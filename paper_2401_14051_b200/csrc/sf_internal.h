@@ -32,6 +32,7 @@ inline void cuda_check(cudaError_t e, const char* what) {
 
 // ---- launch configuration helpers --------------------------------------------
 int sm_count();
+void count_launch();  // every kernel launch of the library increments sf_launch_count()
 
 }  // namespace sfb
 

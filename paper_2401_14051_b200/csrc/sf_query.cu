@@ -410,6 +410,7 @@ void launch_sample_features(const SceneDev& sc, const TemplateDev& td, int64_t n
     k_sample_features<<<grid_for(size_t(n) * td.total, 128), 128, 0, s>>>(
         sc, td, n, queries, out, row_stride, col_offset, err);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void launch_place_template(const sf_template& t, int64_t n, const double* p,
@@ -421,6 +422,7 @@ void launch_place_template(const sf_template& t, int64_t n, const double* p,
     k_place_template<<<grid_for(size_t(n) * t.total), kBlock, 0, s>>>(sc, template_dev(t), n, p,
                                                                        omega, entry, pts, caps, err);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 int64_t slices_per_query(const sf_backbone_config& c) {
@@ -474,6 +476,7 @@ void launch_slice(const sf_backbone_config& c, int64_t n, const float* feats, fl
     for (int i = 0; i < c.n_highlight_layers; ++i) stride += 3 * c.highlight_counts[i];
     k_slice<<<grid_for(size_t(n) * st.n_segs), kBlock, 0, s>>>(st, n, stride, feats, slices);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void launch_backbone_fp32(const sf_backbone& b, int64_t n, const float* slices,
@@ -503,6 +506,7 @@ void launch_backbone_fp32(const sf_backbone& b, int64_t n, const float* slices,
     for (int l = 0; l < 3; ++l) nd.head_off[l] = b.layout.head_off[l];
     k_backbone_fp32<<<grid_for(size_t(n), 128), 128, 0, s>>>(nd, b.d_params, n, slices, cfg8, y, F);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void launch_make_cfg8(const sf_medium_params& m, int64_t n, const double* queries, double* cfg8,
@@ -510,6 +514,7 @@ void launch_make_cfg8(const sf_medium_params& m, int64_t n, const double* querie
     if (n <= 0) return;
     k_make_cfg8<<<grid_for(size_t(n)), kBlock, 0, s>>>(m, n, queries, cfg8);
     SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 }  // namespace sfb

@@ -1,0 +1,345 @@
+"""GPU parity: every kernel of the hot path, called through the C ABI, against the
+reference (golden fixtures produced by the reference itself) and the oracle.
+
+Tolerances (north_star / SURVEY.md §8d):
+  * pyramid, conv3, sort/pool, placement: bit-exact.
+  * graded transmittance, combiner, phase table: <= 1 float ulp (device exp/cos
+    vs glibc, then rounded to float); in practice almost all values bit-exact.
+  * features: |d - r| <= 1e-5 * max(|r|, 1e-6 * max|r|)  (relative with abs floor).
+  * FP32 radiance: y within 1e-6 abs, F within 1e-3 relative (floor 1e-6 * max F).
+  * BF16 tensor-core radiance: see test_bf16_* (stated bound on y, F relative to
+    a floor of 1e-2 * max F).
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import DATA, LIGHT, ORIGIN, ROOT, pyramid_dims, rel_err
+
+pytestmark = pytest.mark.gpu
+
+sf = pytest.importorskip("paper_2401_14051_b200")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def need_gpu():
+    if sf.lib.sf_device_count() == 0:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+
+
+def ulp_diff(a, b):
+    a = np.ascontiguousarray(a, np.float32).view(np.int32).astype(np.int64)
+    b = np.ascontiguousarray(b, np.float32).view(np.int32).astype(np.int64)
+    return np.abs(a - b)
+
+
+@pytest.fixture(scope="module")
+def tmpl():
+    return (sf.load_template(os.path.join(DATA, "diffuse_seed7.vtmpl")),
+            sf.load_template(os.path.join(DATA, "highlight_seed8.vtmpl")))
+
+
+@pytest.fixture(scope="module")
+def small_dev(small):
+    g = sf.DensityGrid.from_array(small["grid"], 2.0 / 16, ORIGIN)
+    pyr = sf.DensityPyramid(g)
+    return g, pyr
+
+
+def test_pyramid_bit_exact(small, small_dev):
+    g, pyr = small_dev
+    assert pyr.level_count() == 5
+    got = np.concatenate([pyr.level(i).values().reshape(-1) for i in range(pyr.level_count())])
+    assert np.array_equal(got, small["levels"])
+    # top level = global mean (tests/test_volume_grid.cpp:95-127)
+    assert abs(pyr.level(4).values()[0, 0, 0] - small["grid"].astype(np.float64).mean()) < 1e-5
+
+
+def test_graded_transmittance(small, small_dev):
+    _, pyr = small_dev
+    vs = 2.0 / 16
+    out = []
+    for i in range(pyr.level_count()):
+        f = sf.graded_transmittance(pyr, i, LIGHT, 0.6, 0.5 * vs * 2 ** i)
+        out.append(f.values.values().reshape(-1))
+    got = np.concatenate(out)
+    assert ulp_diff(got, small["graded"]).max() <= 1
+    assert np.mean(got == small["graded"]) > 0.99
+
+
+def test_conv3_bit_exact(small):
+    n = 16
+    g0 = sf.DensityGrid.from_array(small["graded"][: n ** 3].reshape(n, n, n), 2.0 / n, ORIGIN)
+    out = sf.conv3_replicate(g0, small["kern"][0]).values()
+    assert np.array_equal(out, small["conv_out"])
+    ident = np.zeros(27, np.float32)
+    ident[13] = 1
+    assert np.array_equal(sf.conv3_replicate(g0, ident).values(), small["graded"][: n ** 3].reshape(n, n, n))
+
+
+def test_transmittance_volume(small, small_dev):
+    _, pyr = small_dev
+    t_id = sf.build_transmittance_volume(pyr, LIGHT).values.values()
+    assert ulp_diff(t_id, small["tvol_id"]).max() <= 2 and np.mean(t_id == small["tvol_id"]) > 0.99
+    w = sf.CombinerWeights(small["kern"], small["scales"])
+    t_r = sf.build_transmittance_volume(pyr, LIGHT, w).values.values()
+    assert np.abs(t_r - small["tvol_rand"]).max() <= 1e-6 and np.mean(t_r == small["tvol_rand"]) > 0.99
+    # combine_transmittance from explicitly built fields == build_transmittance_volume
+    vs = 2.0 / 16
+    fields = [sf.graded_transmittance(pyr, i, LIGHT, 0.6, 0.5 * vs * 2 ** i) for i in range(pyr.level_count())]
+    t_c = sf.combine_transmittance(fields, w).values.values()
+    assert np.array_equal(t_c, t_r)
+    # linear in the per-level scales (tests/test_feature_pipeline.cpp:132-149)
+    w3 = sf.CombinerWeights(small["kern"], small["scales"] * 3)
+    t3 = sf.build_transmittance_volume(pyr, LIGHT, w3).values.values()
+    assert np.allclose(t3, 3 * t_r, rtol=1e-5)
+
+
+def test_phase_table_build(small, full_table):
+    t = sf.PhaseTable(17, 33, 9, 8).values()
+    assert ulp_diff(t, small["table"]).max() <= 1
+    T = sf.PhaseTable(64, 128, 32, 16).values()
+    d = ulp_diff(T, full_table)
+    assert d.max() <= 1 and np.mean(d == 0) > 0.99
+
+
+def test_lookup_hg(small):
+    t = sf.PhaseTable.from_values(17, 33, 9, small["table"])
+    li = small["lookup_in"]
+    got = t.lookup_hg(li[:, 0], li[:, 1], li[:, 2])
+    assert np.array_equal(got, small["lookup_out"])
+
+
+def test_sample_trilinear_exact(small, oracle, small_dev):
+    g, _ = small_dev
+    rng = np.random.default_rng(3)
+    pts = rng.uniform(-1.2, 1.2, (4096, 3))
+    pts[:6] = [[-1, -1, -1], [1, 1, 1], [1.0000001, 0, 0], [0, 0, 0], [-1, 0.5, 1], [0.999, -0.999, 0.0]]
+    got = g.sample_trilinear(pts)
+    want = np.array([oracle.sample_trilinear(small["grid"], 2.0 / 16, ORIGIN, p) for p in pts])
+    assert np.array_equal(got, want)
+
+
+def test_light_entry_point():
+    """tests/test_feature_pipeline.cpp:161-178."""
+    box = ((-1, -1, -1), (1, 1, 1))
+    e = sf.light_entry_point(box, (0.25, -0.5, 0.1), (0.0, -1.0, 0.0))
+    assert abs(e[0] - 0.25) < 1e-12 and abs(e[1] - 1.0) < 1e-12 and abs(e[2] - 0.1) < 1e-12
+    l = np.array([1.0, -2.0, 0.5]) / np.linalg.norm([1.0, -2.0, 0.5])
+    p = np.array([0.3, 0.2, -0.4])
+    e = np.array(sf.light_entry_point(box, p, l))
+    assert abs(np.abs(e).max() - 1.0) < 1e-9
+    seg = (p - e) / np.linalg.norm(p - e)
+    assert abs(seg @ l - 1.0) < 1e-9
+
+
+def test_place_template(tmpl, oracle, small, templates):
+    d, h = tmpl
+    c = small["centers"]
+    lo, hi = np.full(3, -1.0), np.full(3, 1.0)
+    entry = np.array([oracle.light_entry_point(lo, hi, q[:3], q[6:9]) for q in c])
+    pts, caps = sf.place_template(d, c[:, :3], c[:, 3:6], entry, 2.5)
+    flat = np.concatenate([l.points for l in d.layers])
+    assert np.array_equal(pts, c[:, None, :3] + flat[None] * 2.5)
+    assert np.array_equal(caps[0], np.repeat([l.cap_radius * 2.5 for l in d.layers], d.counts()))
+    pts, caps = sf.place_template(h, c[:, :3], c[:, 3:6], entry, 1.0)
+    scene = oracle.make_scene(small["grid"], small["tvol_rand"], 2.0 / 16, ORIGIN, *templates,
+                              __import__("oracle.oracle", fromlist=["PhaseModel"]).PhaseModel.hg(0.7),
+                              small["table"])
+    for i in range(len(c)):
+        op, oc = np.zeros((72, 3)), np.zeros(72)
+        oracle.L.or_place_highlight(scene, c[i, :3].copy(), c[i, 3:6].copy(), entry[i].copy(), op, oc)
+        assert np.array_equal(pts[i], op) and np.array_equal(caps[i], oc)
+
+
+def _feature_tol(got, want):
+    floor = 1e-6 * max(1.0, np.abs(want).max())
+    return rel_err(got, want, floor).max()
+
+
+@pytest.mark.parametrize("name", ["hg", "multi", "iso", "scaled"])
+def test_sample_features_small(small, tmpl, name):
+    model = {"hg": sf.PhaseModel.hg(0.7), "multi": sf.PhaseModel.multi_hg([(0.7, 0.6), (0.3, -0.2)]),
+             "iso": sf.PhaseModel.isotropic(), "scaled": sf.PhaseModel.hg(0.7)}[name]
+    ts = 3.0 if name == "scaled" else 1.0
+    g = sf.DensityGrid.from_array(small["grid"], 2.0 / 16, ORIGIN)
+    # the reference's own tvol, so the check isolates sample_features
+    tv = sf.TransmittanceFeatureVolume.from_values(small["tvol_rand"], 2.0 / 16, ORIGIN, LIGHT)
+    table = sf.PhaseTable.from_values(17, 33, 9, small["table"])
+    d, h = tmpl
+    want = small[f"feats_{name}"]
+    fd = sf.sample_features(small["centers"], d, g, tv, model, table, ts)
+    fh = sf.sample_features(small["centers"], h, g, tv, model, table, ts)
+    got = np.concatenate([fd.reshape(len(fd), -1), fh.reshape(len(fh), -1)], axis=1)
+    assert _feature_tol(got, want) <= 1e-5
+    assert np.mean(got == want) > 0.999
+    if name != "scaled":
+        assert np.all(got[:, 2 * 194] == 1.0)  # diffuse centre phase (feature_pipeline.cpp:163-164)
+
+
+@pytest.fixture(scope="module")
+def c1_scene(tmpl, full_table):
+    from paper_2401_14051_b200.scenes import procedural_cloud
+    g = sf.DensityGrid.from_array(procedural_cloud(64, 0), 2.0 / 64, ORIGIN)
+    pyr = sf.DensityPyramid(g)
+    tv = sf.build_transmittance_volume(pyr, LIGHT)
+    table = sf.PhaseTable(64, 128, 32, 16)
+    return g, tv, table
+
+
+def test_c1_transmittance_volume(c1, c1_scene):
+    _, tv, _ = c1_scene
+    got = tv.values.values()
+    assert ulp_diff(got, c1["tvol"]).max() <= 2 and np.mean(got == c1["tvol"]) > 0.99
+
+
+def test_c1_features(c1, c1_scene, tmpl):
+    g, tv, table = c1_scene
+    d, h = tmpl
+    model = sf.PhaseModel.hg(0.7)
+    fd = sf.sample_features(c1["centers"], d, g, tv, model, table)
+    fh = sf.sample_features(c1["centers"], h, g, tv, model, table)
+    got = np.concatenate([fd.reshape(len(fd), -1), fh.reshape(len(fh), -1)], axis=1)
+    assert _feature_tol(got, c1["feats"]) <= 1e-5
+
+
+def _net(seed=0, **kw):
+    return sf.make_backbone(sf.BackboneConfig(seed=seed, **kw))
+
+
+def test_backbone_init_matches_reference(small):
+    p = _net(0).params()
+    assert len(p) == 140591
+    assert np.array_equal(p[:4096], small["params0_head"]) and np.array_equal(p[-4096:], small["params0_tail"])
+
+
+@pytest.mark.parametrize("which", ["hg", "multi", "literal"])
+def test_predict_fp32(small, which):
+    if which == "literal":
+        net, feats, cfg8, y_ref, F_ref = _net(21, literal_attention=True), small["feats_hg"], small["cfg8"], \
+            small["y_lit"], small["F_lit"]
+    elif which == "multi":
+        net, feats, cfg8, y_ref, F_ref = _net(0), small["feats_multi"], small["cfg8_m"], small["y_m"], small["F_m"]
+    else:
+        net, feats, cfg8, y_ref, F_ref = _net(0), small["feats_hg"], small["cfg8"], small["y_hg"], small["F_hg"]
+    y, F = sf.predict(net, feats, cfg8, sf.FP32)
+    assert np.abs(y - y_ref).max() <= 1e-6
+    assert rel_err(F, F_ref, 1e-6 * np.abs(F_ref).max()).max() <= 1e-3
+    assert np.mean(y == y_ref.astype(np.float32)) > 0.95
+
+
+def test_query_c1_end_to_end(c1, c1_scene, tmpl):
+    """Fused product path (GPU tvol, GPU phase table, features, config, backbone, decode)
+    against the reference's F on config 1, FP32 end to end."""
+    g, tv, table = c1_scene
+    d, h = tmpl
+    scene = sf.Scene(g, tv, d, h, sf.PhaseModel.hg(0.7), table)
+    net = _net(0)
+    F = sf.query(scene, net, sf.MediumParams((0.7,), (0.99, 0.99, 0.99)), c1["centers"], sf.FP32)
+    assert rel_err(F, c1["F"], 1e-6 * np.abs(c1["F"]).max()).max() <= 1e-3
+    # same answer via features + predict (the two product paths agree exactly)
+    fd = sf.sample_features(c1["centers"], d, g, tv, sf.PhaseModel.hg(0.7), table)
+    fh = sf.sample_features(c1["centers"], h, g, tv, sf.PhaseModel.hg(0.7), table)
+    feats = np.concatenate([fd.reshape(len(fd), -1), fh.reshape(len(fh), -1)], axis=1)
+    _, F2 = sf.predict(net, feats, c1["cfg8"], sf.FP32)
+    assert np.array_equal(F, F2)
+
+
+def test_permutation_invariance_bit_exact(small):
+    """tests/test_predictor.cpp:119-159."""
+    net = _net(0)
+    f = small["feats_hg"].copy()
+    y0, _ = sf.predict(net, f, small["cfg8"])
+    p = f.copy()
+    for ch in range(3):  # rotate diffuse layer 1 (points 6..13) in every channel
+        seg = p[:, ch * 194 + 6: ch * 194 + 14]
+        p[:, ch * 194 + 6: ch * 194 + 14] = np.roll(seg, 3, axis=1)
+    y1, _ = sf.predict(net, p, small["cfg8"])
+    assert np.array_equal(y0, y1)
+    q = f.copy()
+    q[:, [0, 20]] = q[:, [20, 0]]
+    y2, _ = sf.predict(net, q, small["cfg8"])
+    assert not np.array_equal(y0, y2)
+
+
+def test_zero_head_gives_zero(small):
+    """tests/test_predictor.cpp:161-180."""
+    cfg = sf.BackboneConfig(seed=0)
+    p = _net(0).params()
+    p[-(3 * 64 + 3):] = 0.0  # head/2/W [3][64] and head/2/b [3]
+    net = sf.make_backbone(cfg, p)
+    y, F = sf.predict(net, small["feats_hg"], small["cfg8"])
+    assert np.all(y == 0.0) and np.all(F == 0.0)
+
+
+def test_ragged_tiny_config(oracle):
+    """A non-default layer plan (tests/test_predictor.cpp:52-61 tiny_config)."""
+    from oracle.oracle import BackboneCfg
+    bc = BackboneCfg(diffuse_counts=(2, 3), highlight_counts=(2,), width=4, merge_width=6, head_width=5, seed=21)
+    cfg = sf.BackboneConfig(diffuse_counts=(2, 3), highlight_counts=(2,), width=4, merge_width=6, head_width=5,
+                            seed=21)
+    net = sf.make_backbone(cfg)
+    assert np.array_equal(net.params(), oracle.backbone_init(bc))
+    rng = np.random.default_rng(5)
+    feats = rng.uniform(0, 2, (33, 3 * 7)).astype(np.float32)
+    cfg8 = np.tile([2, 0.6, -0.2, 0, 0.9, 0.85, 0.8, 1.2], (33, 1))
+    y, F = sf.predict(net, feats, cfg8)
+    yo, Fo = oracle.predict(bc, oracle.backbone_init(bc), feats, cfg8)
+    assert np.abs(y - yo).max() <= 1e-6 and rel_err(F, Fo, 1e-9).max() <= 1e-4
+
+
+def test_empty_batch_and_errors(small, small_dev):
+    g, pyr = small_dev
+    net = _net(0)
+    y, F = sf.predict(net, np.zeros((0, 798), np.float32), np.zeros((0, 8)))
+    assert y.shape == (0, 3)
+    with pytest.raises(sf.ScatterfieldError) as e:
+        sf.graded_transmittance(pyr, 0, LIGHT, 1.5, 0.1)
+    assert e.value.errc == "invalid_argument"
+    with pytest.raises(sf.ScatterfieldError) as e:
+        sf.DensityPyramid(sf.DensityGrid(6, 8, 8, 0.25, ORIGIN))
+    assert e.value.errc == "bad_dims"
+    bad = small["cfg8"][:2].copy()
+    bad[:, 4] = 1.0
+    with pytest.raises(sf.ScatterfieldError) as e:
+        sf.predict(net, small["feats_hg"][:2], bad)
+    assert e.value.errc == "bad_value"
+
+
+def test_c2_full_size_properties(tmpl):
+    """Config 2 sizes (128^3, 65,536 queries): size-independent properties."""
+    from paper_2401_14051_b200 import scenes
+    vol = scenes.fractal_ellipsoid(128, 1)
+    g = sf.DensityGrid.from_array(vol, 2.0 / 128, ORIGIN)
+    pyr = sf.DensityPyramid(g)
+    assert pyr.level_count() == 8
+    tv = sf.build_transmittance_volume(pyr, LIGHT)
+    t = tv.values.values()
+    assert np.all(t > 0) and np.all(t <= 1.0 + 1e-6)
+    # vacuum: an empty medium transmits fully (tests/test_feature_pipeline.cpp:151-159)
+    e = sf.build_transmittance_volume(sf.DensityPyramid(sf.DensityGrid(128, 128, 128, 2.0 / 128, ORIGIN)), LIGHT)
+    assert np.all(e.values.values() == 1.0)
+    d, h = tmpl
+    table = sf.PhaseTable(64, 128, 32, 16)
+    scene = sf.Scene(g, tv, d, h, sf.PhaseModel.hg(0.85), table)
+    centers = scenes.draw_centers(vol, 65536, 11, scenes.LIGHT)
+    net = _net(0)
+    F = sf.query(scene, net, sf.MediumParams((0.85,), (0.999,) * 3), centers, sf.FP32)
+    assert np.all(np.isfinite(F)) and np.all(F >= 0)
+    # results independent of batch split / order (deterministic per query)
+    perm = np.random.default_rng(0).permutation(len(centers))[:4096]
+    F_sub = sf.query(scene, net, sf.MediumParams((0.85,), (0.999,) * 3), centers[perm], sf.FP32)
+    assert np.array_equal(F_sub, F[perm])
+
+
+def test_cpp_shim_runs(tmp_path):
+    exe = tmp_path / "shim_smoke"
+    lib_dir = os.path.join(ROOT, "paper_2401_14051_b200")
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "shim_smoke.cpp"), "-L", lib_dir, "-lsf_b200",
+                        f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
