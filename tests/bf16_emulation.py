@@ -1,0 +1,104 @@
+"""Numpy emulation of the tensor-core backbone's arithmetic (test helper).
+
+Same network as the reference forward (src/predictor.cpp:206-235, 352-387), with
+the tcgen05 kernel's precision recipe: every GEMM operand (weights and
+activations) rounded to bf16, fp32 accumulation, fp32 bias / activation /
+residual; the SIMT parts (conditioning layer, attention, 64->3 output layer) in
+fp32. The kernel must match this to fp32 accumulation-order noise; the
+difference between this emulation and the FP32 reference is the bf16 error
+budget stated in tests/test_gpu_parity.py.
+"""
+import numpy as np
+
+
+def bf16(x):
+    x = np.ascontiguousarray(x, np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32)
+
+
+def relu(x):
+    return np.maximum(x, 0.0).astype(np.float32)
+
+
+def slices(feats, counts_d, counts_h):
+    """Per (kind, layer, tau): sorted descending, mean (sorted order), max."""
+    q = feats.shape[0]
+    nd, nh = sum(counts_d), sum(counts_h)
+    out = {}
+    for kind, counts, base, ntot in ((0, counts_d, 0, nd), (1, counts_h, 3 * nd, nh)):
+        start = 0
+        for i, n in enumerate(counts):
+            for tau, ch in ((0, 0), (1, 2), (2, 1)):
+                v = feats[:, base + ch * ntot + start: base + ch * ntot + start + n]
+                s = -np.sort(-v, axis=1)
+                acc = np.zeros(q, np.float32)
+                for j in range(n):
+                    acc = (acc + s[:, j]).astype(np.float32)
+                out[(kind, i, tau)] = (s.astype(np.float32), (acc / np.float32(n)).astype(np.float32),
+                                       s[:, 0].astype(np.float32))
+            start += n
+    return out
+
+
+def forward(params, feats, cfg8, counts_d=(6, 8, 12, 16, 24, 32, 48, 48), counts_h=(32, 16, 16, 8)):
+    P = np.asarray(params, np.float32)
+    q = feats.shape[0]
+    W, M, H = 32, 64, 64
+    sl = slices(np.asarray(feats, np.float32), counts_d, counts_h)
+    ng = cfg8[:, 0].astype(int)
+    g_mean = np.zeros(q, np.float32)
+    for i in range(3):
+        g_mean = np.where(i < ng, (g_mean + cfg8[:, 1 + i].astype(np.float32)).astype(np.float32), g_mean)
+    g_mean = np.where(ng > 0, g_mean / ng.astype(np.float32), g_mean).astype(np.float32)
+    alpha = cfg8[:, 7].astype(np.float32)
+    cfgv = np.zeros((q, 7), np.float32)
+    for i in range(3):
+        cfgv[:, i] = np.where(i < ng, cfg8[:, 1 + i], 0.0)
+    cfgv[:, 3:7] = cfg8[:, 4:8]
+
+    off = 0
+
+    def take(n):
+        nonlocal off
+        r = P[off: off + n]
+        off += n
+        return r
+
+    stacks = {}
+    for kind, counts in ((0, counts_d), (1, counts_h)):
+        for tau in range(3):
+            iW = take(W * 7).reshape(W, 7)
+            ib = take(W)
+            o = relu(cfgv @ iW.T + ib)
+            for i, n in enumerate(counts):
+                W1, b1, W2, b2 = take(32).reshape(4, 8), take(4), take(12).reshape(3, 4), take(3)
+                v = np.stack([sl[(kind, i, 0)][1], sl[(kind, i, 1)][1], sl[(kind, i, 2)][1],
+                              sl[(kind, i, 0)][2], sl[(kind, i, 1)][2], sl[(kind, i, 2)][2], g_mean, alpha], 1)
+                h = relu(v @ W1.T + b1)
+                w3 = (1.0 / (1.0 + np.exp(-(h @ W2.T + b2)))).astype(np.float32)
+                oa = (o * w3[:, tau:tau + 1]).astype(np.float32)
+                K = W + n + 2
+                f1W, f1b = take(W * K).reshape(W, K), take(W)
+                f2W, f2b = take(W * W).reshape(W, W), take(W)
+                s, mean, mx = sl[(kind, i, tau)]
+                x = np.concatenate([oa, s, mean[:, None], mx[:, None]], 1)
+                u = relu(bf16(x) @ bf16(f1W).T + f1b)
+                o = (relu(bf16(u) @ bf16(f2W).T + f2b) + oa).astype(np.float32)
+            stacks[(kind, tau)] = o
+    merged = []
+    for tau in range(3):
+        mW, mb = take(M * 2 * W).reshape(M, 2 * W), take(M)
+        x = np.concatenate([stacks[(0, tau)], stacks[(1, tau)]], 1)
+        merged.append(relu(bf16(x) @ bf16(mW).T + mb))
+    cW, cb = take(M * 3 * M).reshape(M, 3 * M), take(M)
+    h = relu(bf16(np.concatenate(merged, 1)) @ bf16(cW).T + cb)
+    h0W, h0b = take(H * M).reshape(H, M), take(H)
+    h = relu(bf16(h) @ bf16(h0W).T + h0b)
+    h1W, h1b = take(H * H).reshape(H, H), take(H)
+    h = relu(bf16(h) @ bf16(h1W).T + h1b)
+    h2W, h2b = take(3 * H).reshape(3, H), take(3)
+    y = np.abs(h @ h2W.T + h2b).astype(np.float32)
+    F = np.power(cfg8[:, 4:7], 4.0) * np.expm1(y.astype(np.float64))
+    return y, F
