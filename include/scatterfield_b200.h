@@ -216,7 +216,8 @@ enum sf_stage {
     SF_STAGE_FEATURES_HIGHLIGHT = 2, /* sample_features, highlight template */
     SF_STAGE_SLICE = 3,              /* per-layer sort + pools */
     SF_STAGE_BACKBONE = 4,           /* network forward + decode */
-    SF_STAGE_COUNT = 5
+    SF_STAGE_SAMPLE_SORT = 5,        /* fused features + sort/pool + bf16 operand packing */
+    SF_STAGE_COUNT = 6
 };
 /* When enabled, sf_query/sf_predict record a CUDA event pair around every stage on
  * the caller's stream (no synchronization). sf_profile_read synchronizes on those

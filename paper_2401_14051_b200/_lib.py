@@ -96,7 +96,7 @@ _SIGS = {
     "sf_launch_count": (I64, []),
 }
 
-STAGES = ("config", "features_diffuse", "features_highlight", "slice", "backbone")
+STAGES = ("config", "features_diffuse", "features_highlight", "slice", "backbone", "sample_sort")
 
 
 def profile_read():

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "sf_internal.h"
+#include "sf_umma.cuh"
 
 using sfb::fail;
 
@@ -857,17 +858,30 @@ int sf_backbone_download_params(const sf_backbone* b, float* dst, sf_stream stre
 void sf_backbone_destroy(sf_backbone* b);
 
 namespace {
-void run_backbone(const sf_backbone& b, int precision, int64_t n, const float* slices,
-                  const double* cfg8, float* y, double* F, cudaStream_t s) {
-    if (precision == SF_PRECISION_FP32) {
-        sfb::launch_backbone_fp32(b, n, slices, cfg8, y, F, s);
-    } else if (precision == SF_PRECISION_BF16) {
-        if (!sfb::tc_supported(b.cfg))
-            fail(SF_ERR_INVALID_ARGUMENT, "bf16 tensor-core backbone needs the default widths (32/64/64)");
-        sfb::tc_prepare(const_cast<sf_backbone&>(b), s);
-        sfb::launch_backbone_tc(b, n, slices, cfg8, y, F, s);
-    } else {
-        fail(SF_ERR_INVALID_ARGUMENT, "unknown precision");
+std::mutex g_tc_mu;
+
+void check_precision(const sf_backbone& b, int precision, cudaStream_t s) {
+    if (precision == SF_PRECISION_FP32) return;
+    if (precision != SF_PRECISION_BF16) fail(SF_ERR_INVALID_ARGUMENT, "unknown precision");
+    if (!sfb::tc_supported(b.cfg))
+        fail(SF_ERR_INVALID_ARGUMENT,
+             "bf16 tensor-core backbone needs widths 32/64/64 and layers of at most 62 points");
+    std::lock_guard<std::mutex> lk(g_tc_mu);
+    sfb::tc_prepare(const_cast<sf_backbone&>(b), s);
+}
+
+// bf16 path over one chunk: fused sample+sort (or sort of given features) -> tcgen05 backbone.
+void run_bf16_chunk(const sf_backbone& b, const sfb::SortLayout& L, const sfb::SceneDev* sc,
+                    const sfb::TemplateDev* dt, const sfb::TemplateDev* ht, const float* planes, int n_planes,
+                    int64_t m, const double* queries, const float* feats, const double* cfg8, uint8_t* ops,
+                    float* mms, int* err, float* y, double* F, cudaStream_t s) {
+    {
+        StageScope st(SF_STAGE_SAMPLE_SORT, s);
+        sfb::launch_sample_sort(sc, dt, ht, planes, n_planes, L, m, queries, feats, ops, mms, err, s);
+    }
+    {
+        StageScope st(SF_STAGE_BACKBONE, s);
+        sfb::launch_backbone_tc(b, m, ops, mms, cfg8, y, F, s);
     }
 }
 }  // namespace
@@ -882,18 +896,28 @@ int sf_predict(const sf_backbone* b, int64_t n, const float* features, const dou
         for (int i = 0; i < c.n_highlight_layers; ++i) feat += 3 * c.highlight_counts[i];
         if (!is_device_ptr(config8))
             for (int64_t i = 0; i < n; ++i) validate_albedo(config8 + 8 * i + 4);
+        check_precision(*b, precision, stream);
         In<float> f(features, size_t(n) * feat, stream);
         In<double> cf(config8, size_t(n) * 8, stream);
         Out<float> oy(y_out, size_t(n) * 3, stream);
         Out<double> oF(F_out, size_t(n) * 3, stream);
-        Scratch<float> slices(size_t(n) * sfb::slices_per_query(c), stream);
-        {
-            StageScope st(SF_STAGE_SLICE, stream);
-            sfb::launch_slice(c, n, f.d, slices.p, stream);
-        }
-        {
-            StageScope st(SF_STAGE_BACKBONE, stream);
-            run_backbone(*b, precision, n, slices.p, cf.d, oy.d, oF.d, stream);
+        if (precision == SF_PRECISION_FP32) {
+            Scratch<float> slices(size_t(n) * sfb::slices_per_query(c), stream);
+            {
+                StageScope st(SF_STAGE_SLICE, stream);
+                sfb::launch_slice(c, n, f.d, slices.p, stream);
+            }
+            {
+                StageScope st(SF_STAGE_BACKBONE, stream);
+                sfb::launch_backbone_fp32(*b, n, slices.p, cf.d, oy.d, oF.d, stream);
+            }
+        } else {
+            const sfb::SortLayout L = sfb::sort_layout(c);
+            const int64_t tiles = (n + sfb::kUmmaM - 1) / sfb::kUmmaM;
+            Scratch<uint8_t> ops(size_t(tiles) * L.tile_bytes, stream);
+            Scratch<float> mms(size_t(L.n_layers) * tiles * sfb::kUmmaM * 8, stream);
+            run_bf16_chunk(*b, L, nullptr, nullptr, nullptr, nullptr, 0, n, nullptr, f.d, cf.d, ops.p, mms.p,
+                           nullptr, oy.d, oF.d, stream);
         }
         oy.finish();
         oF.finish();
@@ -920,12 +944,16 @@ int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_templa
         s->model = *model;
         s->table = table;
         s->template_scale = ts;
+        s->n_planes = model->kind == SF_PHASE_ISOTROPIC ? 1 : model->n_lobes;
         SFB_CUDA(cudaMalloc(&s->d_dt, density->count() * sizeof(float2)));
         try {
+            SFB_CUDA(cudaMalloc(&s->d_planes, size_t(s->n_planes) * table->a * table->h * sizeof(float)));
             sfb::launch_interleave(density->d, tv.d, s->d_dt, density->count(), nullptr);
+            sfb::launch_blend_planes(*table, *model, s->d_planes, nullptr);
             SFB_CUDA(cudaDeviceSynchronize());
         } catch (...) {
             cudaFree(s->d_dt);
+            cudaFree(s->d_planes);
             throw;
         }
         *out = s.release();
@@ -935,6 +963,7 @@ int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_templa
 void sf_scene_destroy(sf_scene* s) {
     if (!s) return;
     cudaFree(s->d_dt);
+    cudaFree(s->d_planes);
     delete s;
 }
 
@@ -949,9 +978,43 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
         for (int i = 0; i < c.n_highlight_layers; ++i) nh += c.highlight_counts[i];
         if (nd != s->dt->total || nh != s->ht->total)
             fail(SF_ERR_SHAPE_MISMATCH, "feature block does not match template counts");
+        check_precision(*b, precision, stream);
         In<double> iq(queries, size_t(n) * 9, stream);
         Out<double> oF(F_out, size_t(n) * 3, stream);
         Out<float> oy(y_out, size_t(n) * 3, stream);
+        if (precision == SF_PRECISION_BF16) {
+            // production path: fused sample+sort -> tcgen05 backbone, chunked by tiles
+            const sfb::SortLayout L = sfb::sort_layout(c);
+            const int64_t chunk = std::min<int64_t>((n + sfb::kUmmaM - 1) / sfb::kUmmaM * sfb::kUmmaM, 1 << 19);
+            const int64_t tiles = chunk / sfb::kUmmaM;
+            Scratch<uint8_t> ops(size_t(tiles) * L.tile_bytes, stream);
+            Scratch<float> mms(size_t(L.n_layers) * tiles * sfb::kUmmaM * 8, stream);
+            Scratch<double> cfg8(size_t(chunk) * 8, stream);
+            Scratch<int> err(1, stream);
+            SFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
+            sfb::SceneDev sc = sfb::scene_dev(*s->density, *s->tvol->values, s->d_dt, s->model, *s->table,
+                                              s->template_scale);
+            sfb::TemplateDev dt = sfb::template_dev(*s->dt), ht = sfb::template_dev(*s->ht);
+            for (int64_t q0 = 0; q0 < n; q0 += chunk) {
+                int64_t m = std::min(chunk, n - q0);
+                const double* qd = iq.d + 9 * q0;
+                {
+                    StageScope st(SF_STAGE_CONFIG, stream);
+                    sfb::launch_make_cfg8(*medium, m, qd, cfg8.p, stream);
+                }
+                run_bf16_chunk(*b, L, &sc, &dt, &ht, s->d_planes, s->n_planes, m, qd, nullptr, cfg8.p, ops.p,
+                               mms.p, err.p, oy.d ? oy.d + 3 * q0 : nullptr, oF.d ? oF.d + 3 * q0 : nullptr,
+                               stream);
+            }
+            if (!oF.host && !oy.host && !iq.buf.p) return;  // device in/out: asynchronous (see below)
+            int herr = 0;
+            SFB_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+            oF.finish();
+            oy.finish();
+            sync(stream);
+            if (herr) fail(SF_ERR_INVALID_ARGUMENT, "place_template: entry coincides with p");
+            return;
+        }
         const int64_t chunk = std::min<int64_t>(n, 1 << 17);
         const int64_t feat = 3 * int64_t(nd + nh);
         Scratch<float> feats(size_t(chunk) * feat, stream);
@@ -984,8 +1047,8 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
             }
             {
                 StageScope st(SF_STAGE_BACKBONE, stream);
-                run_backbone(*b, precision, m, slices.p, cfg8.p, oy.d ? oy.d + 3 * q0 : nullptr,
-                             oF.d ? oF.d + 3 * q0 : nullptr, stream);
+                sfb::launch_backbone_fp32(*b, m, slices.p, cfg8.p, oy.d ? oy.d + 3 * q0 : nullptr,
+                                          oF.d ? oF.d + 3 * q0 : nullptr, stream);
             }
         }
         if (!oF.host && !oy.host && !iq.buf.p) {

@@ -106,6 +106,8 @@ struct sf_scene {
     const sf_phase_table* table = nullptr;
     double template_scale = 1.0;
     float2* d_dt = nullptr;  // interleaved {density, transmittance} level-0 volume
+    float* d_planes = nullptr;  // phase table pre-blended at each lobe's g [n_planes][A][H]
+    int n_planes = 0;
 };
 
 // ---- launchers (defined in the .cu files) --------------------------------------
@@ -159,11 +161,40 @@ void launch_backbone_fp32(const sf_backbone& b, int64_t n, const float* slices,
 void launch_make_cfg8(const sf_medium_params& m, int64_t n, const double* queries,
                       double* cfg8, cudaStream_t s);
 
+// Layout of the sorted-feature operand blocks produced by k_sample_sort and
+// consumed by the tensor-core backbone: for every (kind, layer, tau) segment a
+// [n_tiles][128 x kf] bf16 block in UMMA canonical layout (kf = pad16(n + 2):
+// sorted values, mean, max, zeros), and for every (kind, layer) a
+// [n_tiles*128][8] fp32 block {mean d,p,t, max d,p,t, 0, 0} for the attention.
+struct SortLayout {
+    int nl[2];
+    int npts[2];
+    int counts[2][16];
+    int start[2][16];
+    int kf[2][16];
+    int mm_layer[2][16];
+    int64_t seg_prefix[2][16][3];  // bytes per tile preceding the segment
+    int64_t tile_bytes;            // all segments of one tile
+    int n_layers;
+};
+SortLayout sort_layout(const sf_backbone_config& c);
+
 // Tensor-core (tcgen05, bf16 operands / fp32 accumulation) backbone.
 bool tc_supported(const sf_backbone_config& c);
 void tc_prepare(sf_backbone& b, cudaStream_t s);
 void tc_release(sf_backbone& b);
-void launch_backbone_tc(const sf_backbone& b, int64_t n, const float* slices,
+void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, const float* mms,
                         const double* cfg8, float* y, double* F, cudaStream_t s);
+
+// Fused feature sampling + per-layer sort/pool + bf16 operand packing (K5+K6).
+// Samples the scene when `feats` is null, else sorts the given feature rows.
+void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht,
+                        const float* planes, int n_planes, const SortLayout& L, int64_t n,
+                        const double* queries, const float* feats, uint8_t* ops, float* mms,
+                        int* err, cudaStream_t s);
+// Pre-blended phase planes: for each lobe, the table interpolated at that lobe's g
+// (PhaseTable::lookup_hg's g axis, src/phase.cpp:191-219), [n_lobes][angle][aperture].
+void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float* planes,
+                         cudaStream_t s);
 
 }  // namespace sfb

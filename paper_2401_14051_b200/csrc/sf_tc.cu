@@ -1,234 +1,146 @@
 // sf_tc.cu — the backbone forward on 5th-generation tensor cores (tcgen05).
 //
 // One CTA = one tile of 128 shading points = UMMA_M. Thread t owns query row t,
-// which is also TMEM lane t, so every epilogue is a private tcgen05.ld of the
-// thread's own accumulator row. Every dense layer of the reference network
-// (src/predictor.cpp:206-235, 352-387) whose K is large enough becomes one
-// tcgen05.mma chain D[128 x N] (fp32, TMEM) = A[128 x K] (bf16, SMEM) * W^T:
+// which is also TMEM lane t, so each epilogue is a private tcgen05.ld of the
+// thread's own accumulator row. The reference network (src/predictor.cpp:206-235,
+// 352-387) becomes a chain of tcgen05.mma GEMMs D[128 x N] (fp32, TMEM) = A * W^T:
 //
-//   FC-1 (N=32, K = 32 + n_i + 2 -> padded to 16), FC-2 (N=32, K=32),
-//   per-type merge (N=64, K=64), cross merge (N=64, K=192 as 3 x 64),
-//   head 0/1 (N=64, K=64)
+//   FC-1  = [o_att | sorted_tau, mean, max] W1^T as two MMAs into one accumulator:
+//           A_att (K=32, written by the threads) x W1[:, :32]  +
+//           F     (K=pad16(n+2), bulk-copied, produced by k_sample_sort) x W1[:, 32:]
+//   FC-2  (N=32, K=32), per-type merge (N=64, K=64), cross merge accumulated
+//   chunk by chunk as each merged_tau appears (3 x K=64), head 0/1 (N=64, K=64).
 //
 // The reference's W[out][in] row-major is exactly UMMA's K-major B operand, so
-// weights are pre-packed once (tc_prepare) into the no-swizzle canonical layout
-// and streamed per layer with cp.async.bulk (TMA bulk copy) into a 2-deep SMEM
-// ring, the copy of layer j+1 overlapping layer j. The tiny SIMT parts (the 7->32
-// conditioning layer, the 8->4->3 channel attention and the 64->3 output layer)
-// stay FP32 on the CUDA cores, as does the residual stream o.
+// weights are packed once (tc_prepare) into the no-swizzle canonical layout.
+// Everything a step needs (weight blob, the tile's sorted-feature operand block
+// and its mean/max block) is one bundle of cp.async.bulk copies into a 3-slot
+// SMEM ring completing on one mbarrier; bundle j+2 is in flight while step j
+// runs. The SIMT pieces (7->32 conditioning layer, 8->4->3 channel attention,
+// 64->3 output layer) and the residual stream stay FP32 on the CUDA cores.
 //
-// Precision: bf16 operands (weights, o_att, features, u, merges), fp32
-// accumulation and fp32 residual/bias/activation; see tests/test_gpu_parity.py
-// test_bf16_* for the stated tolerance.
-#include <cuda_bf16.h>
-
+// Precision: bf16 GEMM operands (weights, o_att, features, u, merges), fp32
+// accumulation, fp32 bias / activation / residual (tests/bf16_emulation.py).
 #include <cstring>
 #include <vector>
 
 #include "sf_internal.h"
+#include "sf_umma.cuh"
 
 namespace sfb {
 
 namespace {
 
-constexpr int kTile = 128;        // queries per CTA (UMMA_M)
 constexpr int kThreads = 128;     // one thread per query row / TMEM lane
-constexpr int kTmemCols = 128;    // fc1 [0,32), fc2 [32,64), merge/cross/head [64,128)
-constexpr int kBlobMax = 8192;    // largest weight blob (64 x 64 bf16)
-constexpr int kMaxBlobs = 128;
+constexpr int kTmemCols = 256;    // fc1 [0,32) fc2 [32,64) merge/head [64,128) cross [128,192)
+constexpr int kSlots = 3;
+constexpr int kSlotBytes = 27648;
+constexpr int kSlotW1a = 0, kSlotW1b = 2048, kSlotFeat = 6144, kSlotMM = 22528;
+constexpr int kMaxSteps = 96;
 
-// --- UMMA descriptors (no swizzle, K-major canonical layout) -------------------------
-// element (r, k) of an R x K operand lives at byte (r/8)*SBO + (k/8)*LBO + (r%8)*16 + (k%8)*2
-// with LBO = 128 (adjacent 8-element K chunks) and SBO = K*16 (adjacent 8-row groups).
-__host__ __device__ constexpr uint32_t canon_off(int r, int k, int K) {
-    return uint32_t((r >> 3) * (K * 16) + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
-}
+struct Copy {
+    int32_t kind;     // 0 weights (absolute), 1 sorted-feature blocks, 2 mean/max blocks
+    uint32_t dst;     // byte offset in the slot
+    uint32_t bytes;
+    uint32_t pad;
+    int64_t a;        // kind 0: byte offset; kind 1: per-tile prefix bytes (x n_tiles); kind 2: layer index
+    int64_t stride;   // per-tile stride in bytes (0 for weights)
+};
 
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= uint64_t((saddr >> 4) & 0x3FFF);
-    d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
-    d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
-    d |= uint64_t(1) << 46;  // descriptor version for tcgen05
-    return d;                 // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
-}
-
-// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128.
-__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(kTile >> 4) << 24);
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "SF_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra SF_DONE_%=;\n\t"
-        "bra SF_WAIT_%=;\n"
-        "SF_DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
-}
-
-// 32 consecutive fp32 TMEM columns of this thread's lane.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-}
-
-// Row `row` of a K-wide canonical operand: 8 elements (16 B) per chunk.
-__device__ __forceinline__ void store_chunk(uint8_t* base, int row, int kchunk, int K, const float* v8) {
-    uint4 u;
-    u.x = pack_bf16(v8[0], v8[1]);
-    u.y = pack_bf16(v8[2], v8[3]);
-    u.z = pack_bf16(v8[4], v8[5]);
-    u.w = pack_bf16(v8[6], v8[7]);
-    *reinterpret_cast<uint4*>(base + canon_off(row, kchunk * 8, K)) = u;
-}
-
-struct Blob {
-    uint32_t off;    // byte offset into the packed weight buffer
-    uint16_t bytes;  // blob size
-    uint16_t K;      // operand K (multiple of 16)
+struct Step {
+    int32_t ncopy;
+    uint32_t total;
+    int32_t k2;       // K of the second GEMM operand (fc1 feature part) or the only GEMM's K
+    int32_t pad;
+    Copy c[4];
 };
 
 struct TcDesc {
     int nl[2];
     int counts[2][16];
-    int slice_off[2][16];
     int W, M, H;
     int literal;
     double gamma;
     int64_t stack_off[2][3];
     int64_t merge_off, cross_off, head_off[3];
-    int n_blobs;
-    int kp1_max;
-    Blob blobs[kMaxBlobs];
+    int n_steps;
 };
 
-struct TcState {
-    uint8_t* smem_a1;  // fc1 A [128 x kp1_max]
-    uint8_t* smem_a2;  // fc2/merge/head A [128 x 64]
-    uint8_t* smem_ac;  // cross A [128 x 192]
-    uint8_t* smem_w[2];
-    uint64_t* wbar;    // [2]
-    uint64_t* mbar;
-    uint32_t tmem;
-    uint32_t wpar[2];
+struct TcPack {
+    uint8_t* d_blobs = nullptr;
+    Step* d_steps = nullptr;
+    TcDesc desc{};
+    std::vector<Step> steps;
+};
+
+struct Ring {
+    uint8_t* slot[kSlots];
+    uint64_t* full;   // [kSlots]
+    uint64_t* mma;
+    uint32_t par[kSlots];
     uint32_t mpar;
-    int next_blob;     // next blob index to be loaded
-    int cur_blob;      // blob index consumed by the next MMA
+    int step;
 };
 
-// Thread 0: start the bulk copy of blob `j` into ring slot j % 2.
-__device__ __forceinline__ void issue_blob(TcState& s, const TcDesc& d, const uint8_t* wpk, int j) {
-    if (j >= d.n_blobs) return;
-    const Blob& b = d.blobs[j];
-    uint64_t* bar = &s.wbar[j & 1];
-    mbar_expect_tx(bar, b.bytes);
-    bulk_g2s(s.smem_w[j & 1], wpk + b.off, b.bytes, bar);
+__device__ __forceinline__ void issue_step(const Ring& r, const Step* __restrict__ steps, int n_steps, int j,
+                                           const uint8_t* wpk, const uint8_t* ops, const uint8_t* mms,
+                                           int tile, int n_tiles) {
+    if (j >= n_steps) return;
+    const Step& s = steps[j];
+    const int slot = j % kSlots;
+    uint64_t* bar = &r.full[slot];
+    mbar_expect_tx(bar, s.total);
+    for (int c = 0; c < s.ncopy; ++c) {
+        const Copy& cp = s.c[c];
+        const uint8_t* src;
+        if (cp.kind == 0)
+            src = wpk + cp.a;
+        else if (cp.kind == 1)
+            src = ops + cp.a * n_tiles + int64_t(tile) * cp.stride;
+        else
+            src = mms + cp.a * int64_t(n_tiles) * 4096 + int64_t(tile) * 4096;
+        bulk_g2s(r.slot[slot] + cp.dst, src, cp.bytes, bar);
+    }
 }
 
-// One synchronous GEMM step: D[tmem_col, +N) (+)= A * Wblob^T, then wait.
-// Called by all threads after their SMEM operand rows are written.
-__device__ __forceinline__ void gemm_step(TcState& s, const TcDesc& d, const uint8_t* wpk,
-                                          uint32_t a_saddr, uint32_t a_sbo, int n, uint32_t tmem_col,
-                                          bool accumulate) {
+// Wait for step j's bundle (all threads: some read the mean/max block).
+__device__ __forceinline__ uint8_t* acquire(Ring& r) {
+    const int slot = r.step % kSlots;
+    mbar_wait(&r.full[slot], r.par[slot]);
+    r.par[slot] ^= 1;
+    return r.slot[slot];
+}
+
+// Issue the step's MMAs (thread 0), prefetch bundle j+2, wait for completion.
+// a0/k0: first GEMM operand (SMEM) x slot weights at w0; optional second
+// operand a1/k1 x slot weights at w1, accumulating into the same columns.
+__device__ __forceinline__ void run_mma(Ring& r, const Step* steps, int n_steps, const uint8_t* wpk,
+                                        const uint8_t* ops, const uint8_t* mms, int tile, int n_tiles,
+                                        uint32_t tmem_d, int n, uint32_t a0, int k0, uint32_t w0, uint32_t a1,
+                                        int k1, uint32_t w1, bool accumulate) {
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
-    const int j = s.cur_blob;
-    const int slot = j & 1;
     if (threadIdx.x == 0) {
-        mbar_wait(&s.wbar[slot], s.wpar[slot]);
         tc_fence_after();
-        const Blob& b = d.blobs[j];
-        const uint32_t w_saddr = smem_u32(s.smem_w[slot]);
-        const uint32_t b_sbo = uint32_t(b.K) * 16;
         const uint32_t id = idesc_bf16(n);
-        for (int k = 0; k < b.K / 16; ++k) {
-            uint64_t da = smem_desc(a_saddr + k * 256, 128, a_sbo);
-            uint64_t db = smem_desc(w_saddr + k * 256, 128, b_sbo);
-            umma_bf16(s.tmem + tmem_col, da, db, id, (accumulate || k > 0) ? 1u : 0u);
-        }
-        umma_commit(s.mbar);
-        // ring slot (j+1)&1 was read by MMA j-1, which completed before this step
-        issue_blob(s, d, wpk, j + 1);
+        for (int k = 0; k < k0 / 16; ++k)
+            umma_bf16(tmem_d, smem_desc(a0 + k * 256, 128, k0 * 16), smem_desc(w0 + k * 256, 128, k0 * 16), id,
+                      (accumulate || k > 0) ? 1u : 0u);
+        for (int k = 0; k < k1 / 16; ++k)
+            umma_bf16(tmem_d, smem_desc(a1 + k * 256, 128, k1 * 16), smem_desc(w1 + k * 256, 128, k1 * 16), id,
+                      1u);
+        umma_commit(r.mma);
+        issue_step(r, steps, n_steps, r.step + kSlots - 1, wpk, ops, mms, tile, n_tiles);
     }
-    s.wpar[slot] ^= 1;
-    s.cur_blob = j + 1;
-    mbar_wait(s.mbar, s.mpar);
-    s.mpar ^= 1;
+    mbar_wait(r.mma, r.mpar);
+    r.mpar ^= 1;
+    r.step += 1;
     tc_fence_after();
 }
 
 __device__ __forceinline__ float relu(float v) { return v > 0.0f ? v : 0.0f; }
 
-// dense y = W x + b (FP32 SIMT, sequential accumulation with FMA)
 __device__ __forceinline__ void dense_simt(const float* __restrict__ W, const float* __restrict__ b, int m,
                                            int n, const float* x, float* y) {
     for (int i = 0; i < m; ++i) {
@@ -240,52 +152,48 @@ __device__ __forceinline__ void dense_simt(const float* __restrict__ W, const fl
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
-    k_backbone_tc(TcDesc d, const float* __restrict__ P, const uint8_t* __restrict__ wpk, int64_t n,
-                  const float* __restrict__ slices, const double* __restrict__ cfg8, float* __restrict__ y_out,
+    k_backbone_tc(TcDesc d, const Step* __restrict__ steps, const float* __restrict__ P,
+                  const uint8_t* __restrict__ wpk, const uint8_t* __restrict__ ops, const uint8_t* __restrict__ mms,
+                  int n_tiles, int64_t n, const double* __restrict__ cfg8, float* __restrict__ y_out,
                   double* __restrict__ F_out) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    __shared__ uint64_t bars[3];
+    __shared__ uint64_t bars[kSlots + 1];
     __shared__ uint32_t tmem_slot;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
-    const int64_t q = int64_t(blockIdx.x) * kTile + tid;
+    const int tile = blockIdx.x;
+    const int64_t q = int64_t(tile) * kUmmaM + tid;
     const bool live = q < n;
-    const int W = d.W;  // == 32 (tc_supported)
+    constexpr int W = 32;
 
-    TcState s;
     uintptr_t base = (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023);
-    s.smem_a1 = reinterpret_cast<uint8_t*>(base);
-    s.smem_a2 = s.smem_a1 + kTile * d.kp1_max * 2;
-    s.smem_ac = s.smem_a2 + kTile * 64 * 2;
-    s.smem_w[0] = s.smem_ac + kTile * 192 * 2;
-    s.smem_w[1] = s.smem_w[0] + kBlobMax;
-    s.wbar = bars;
-    s.mbar = bars + 2;
-    s.wpar[0] = s.wpar[1] = 0;
-    s.mpar = 0;
-    s.cur_blob = 0;
+    uint8_t* a_att = reinterpret_cast<uint8_t*>(base);  // [128 x 32]
+    uint8_t* a2 = a_att + kUmmaM * 32 * 2;              // [128 x 64]
+    Ring r;
+    r.slot[0] = a2 + kUmmaM * 64 * 2;
+    for (int s = 1; s < kSlots; ++s) r.slot[s] = r.slot[s - 1] + kSlotBytes;
+    r.full = bars;
+    r.mma = bars + kSlots;
+    for (int s = 0; s < kSlots; ++s) r.par[s] = 0;
+    r.mpar = 0;
+    r.step = 0;
 
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(&tmem_slot)),
-                     "r"(kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
+    if (warp == 0) tmem_alloc(&tmem_slot, kTmemCols);
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        mbar_init(&bars[2], 1);
+        for (int s = 0; s <= kSlots; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    s.tmem = tmem_slot;
-    if (tid == 0) issue_blob(s, d, wpk, 0);
-    const uint32_t lane_base = uint32_t(warp * 32) << 16;
+    const uint32_t tmem = tmem_slot;
+    if (tid == 0)
+        for (int j = 0; j < kSlots - 1; ++j) issue_step(r, steps, d.n_steps, j, wpk, ops, mms, tile, n_tiles);
+    const uint32_t lane = uint32_t(warp * 32) << 16;
+    const uint32_t s_att = smem_u32(a_att), s_a2 = smem_u32(a2);
 
-    // ---- conditioning (make_config / cfg_vector, src/predictor.cpp:193-202)
+    // conditioning (cfg_vector, src/predictor.cpp:193-202)
     float cfgv[7] = {0, 0, 0, 0, 0, 0, 0};
     float g_mean = 0.0f, alpha = 0.0f;
     double alb[3] = {0.5, 0.5, 0.5};
@@ -296,10 +204,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (ng > 0) g_mean /= float(double(ng));
         alpha = float(c8[7]);
         for (int i = 0; i < ng && i < 3; ++i) cfgv[i] = float(c8[1 + i]);
-        cfgv[3] = float(c8[4]);
-        cfgv[4] = float(c8[5]);
-        cfgv[5] = float(c8[6]);
-        cfgv[6] = float(c8[7]);
+        for (int i = 0; i < 4; ++i) cfgv[3 + i] = float(c8[4 + i]);
         alb[0] = c8[4];
         alb[1] = c8[5];
         alb[2] = c8[6];
@@ -316,14 +221,11 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int j = 0; j < 32; ++j) o[j] = relu(o[j]);
             for (int i = 0; i < d.nl[kind]; ++i) {
                 const int cnt = d.counts[kind][i];
-                const float* sl = slices + int64_t(d.slice_off[kind][i]) * n + q;
-                // channel attention (src/neural.cpp:473-491), FP32
-                float v[8] = {0, 0, 0, 0, 0, 0, g_mean, alpha};
-                if (live)
-                    for (int t = 0; t < 3; ++t) {
-                        v[t] = __ldg(sl + int64_t(t * (cnt + 2) + cnt) * n);
-                        v[3 + t] = __ldg(sl + int64_t(t * (cnt + 2) + cnt + 1) * n);
-                    }
+                uint8_t* slot = acquire(r);
+                const uint32_t s_slot = smem_u32(slot);
+                // channel attention (src/neural.cpp:473-491) from the tile's mean/max block
+                const float* mm = reinterpret_cast<const float*>(slot + kSlotMM) + tid * 8;
+                float v[8] = {mm[0], mm[1], mm[2], mm[3], mm[4], mm[5], g_mean, alpha};
                 float w;
                 if (d.literal) {
                     float acc = 0.0f;
@@ -340,37 +242,29 @@ __global__ void __launch_bounds__(kThreads, 2)
                 float oa[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) oa[j] = o[j] * w;
-                // FC-1 operand row: [o_att | sorted_tau | mean | max | 0...]
-                const int K1 = d.blobs[s.cur_blob].K;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) store_chunk(s.smem_a1, tid, c, K1, oa + 8 * c);
-                const float* st = sl + int64_t(tau * (cnt + 2)) * n;
-                for (int c = 4; c < K1 / 8; ++c) {
-                    float v8[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        int k = c * 8 + e - 32;
-                        v8[e] = (live && k < cnt + 2) ? __ldg(st + int64_t(k) * n) : 0.0f;
-                    }
-                    store_chunk(s.smem_a1, tid, c, K1, v8);
-                }
-                gemm_step(s, d, wpk, smem_u32(s.smem_a1), uint32_t(K1) * 16, 32, 0, false);
+                for (int c = 0; c < 4; ++c) store_chunk(a_att, tid, c, 32, oa + 8 * c);
+                const int kf = steps[r.step].k2;
+                run_mma(r, steps, d.n_steps, wpk, ops, mms, tile, n_tiles, tmem + 0, 32, s_att, 32,
+                        s_slot + kSlotW1a, s_slot + kSlotFeat, kf, s_slot + kSlotW1b, false);
                 // FC-1 epilogue: u = relu(acc + b1) -> bf16 operand of FC-2
                 const float* b1 = P + off + int64_t(W) * (W + cnt + 2);
                 float acc[32];
-                tmem_ld32(s.tmem + lane_base + 0, acc);
+                tmem_ld32(tmem + lane + 0, acc);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     float v8[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) v8[e] = relu(acc[8 * c + e] + __ldg(b1 + 8 * c + e));
-                    store_chunk(s.smem_a2, tid, c, 32, v8);
+                    store_chunk(a2, tid, c, 32, v8);
                 }
                 off += int64_t(W) * (W + cnt + 2) + W;
-                gemm_step(s, d, wpk, smem_u32(s.smem_a2), 32 * 16, 32, 32, false);
+                uint8_t* slot2 = acquire(r);
+                run_mma(r, steps, d.n_steps, wpk, ops, mms, tile, n_tiles, tmem + 32, 32, s_a2, 32,
+                        smem_u32(slot2), 0, 0, 0, false);
                 // FC-2 epilogue + residual: o = relu(acc + b2) + o_att (fp32)
                 const float* b2 = P + off + W * W;
-                tmem_ld32(s.tmem + lane_base + 32, acc);
+                tmem_ld32(tmem + lane + 32, acc);
 #pragma unroll
                 for (int j = 0; j < 32; ++j) o[j] = relu(acc[j] + __ldg(b2 + j)) + oa[j];
                 off += W * W + W;
@@ -379,78 +273,73 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) od_pk[j] = pack_bf16(o[2 * j], o[2 * j + 1]);
             } else {
-                // merge operand row [od | oh] (K = 64)
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
-                    *reinterpret_cast<uint4*>(s.smem_a2 + canon_off(tid, 8 * c, 64)) =
+                    *reinterpret_cast<uint4*>(a2 + canon_off(tid, 8 * c, 64)) =
                         make_uint4(od_pk[4 * c], od_pk[4 * c + 1], od_pk[4 * c + 2], od_pk[4 * c + 3]);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) store_chunk(s.smem_a2, tid, 4 + c, 64, o + 8 * c);
+                for (int c = 0; c < 4; ++c) store_chunk(a2, tid, 4 + c, 64, o + 8 * c);
             }
         }
-        // merged_tau = relu(W_m [od; oh] + b) -> columns [64 tau, 64 tau + 64) of the cross operand
-        gemm_step(s, d, wpk, smem_u32(s.smem_a2), 64 * 16, 64, 64, false);
+        // merged_tau = relu(W_m [od; oh] + b)
+        uint8_t* slot = acquire(r);
+        run_mma(r, steps, d.n_steps, wpk, ops, mms, tile, n_tiles, tmem + 64, 64, s_a2, 64, smem_u32(slot), 0, 0,
+                0, false);
         const float* bm = P + d.merge_off + int64_t(tau) * (64 * 64 + 64) + 64 * 64;
         for (int half = 0; half < 2; ++half) {
             float acc[32];
-            tmem_ld32(s.tmem + lane_base + 64 + 32 * half, acc);
+            tmem_ld32(tmem + lane + 64 + 32 * half, acc);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 float v8[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) v8[e] = relu(acc[8 * c + e] + __ldg(bm + 32 * half + 8 * c + e));
-                store_chunk(s.smem_ac, tid, tau * 8 + half * 4 + c, 192, v8);
+                store_chunk(a2, tid, half * 4 + c, 64, v8);
             }
         }
+        // cross += W_c[:, 64 tau : 64 tau + 64] merged_tau (accumulated in TMEM)
+        slot = acquire(r);
+        run_mma(r, steps, d.n_steps, wpk, ops, mms, tile, n_tiles, tmem + 128, 64, s_a2, 64, smem_u32(slot), 0,
+                0, 0, tau > 0);
     }
-    // cross = relu(W_c [m0; m1; m2] + b): K = 192 streamed as three 64-wide blobs
-    for (int c = 0; c < 3; ++c)
-        gemm_step(s, d, wpk, smem_u32(s.smem_ac) + c * 8 * 128, 192 * 16, 64, 64, c > 0);
     float h[64];
     {
         const float* bc = P + d.cross_off + 64 * 192;
-        tmem_ld32(s.tmem + lane_base + 64, h);
-        tmem_ld32(s.tmem + lane_base + 96, h + 32);
+        tmem_ld32(tmem + lane + 128, h);
+        tmem_ld32(tmem + lane + 160, h + 32);
 #pragma unroll
         for (int j = 0; j < 64; ++j) h[j] = relu(h[j] + __ldg(bc + j));
     }
     for (int l = 0; l < 2; ++l) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) store_chunk(s.smem_a2, tid, c, 64, h + 8 * c);
-        gemm_step(s, d, wpk, smem_u32(s.smem_a2), 64 * 16, 64, 64, false);
+        for (int c = 0; c < 8; ++c) store_chunk(a2, tid, c, 64, h + 8 * c);
+        uint8_t* slot = acquire(r);
+        run_mma(r, steps, d.n_steps, wpk, ops, mms, tile, n_tiles, tmem + 64, 64, s_a2, 64, smem_u32(slot), 0, 0,
+                0, false);
         const float* bh = P + d.head_off[l] + 64 * 64;
-        tmem_ld32(s.tmem + lane_base + 64, h);
-        tmem_ld32(s.tmem + lane_base + 96, h + 32);
+        tmem_ld32(tmem + lane + 64, h);
+        tmem_ld32(tmem + lane + 96, h + 32);
 #pragma unroll
         for (int j = 0; j < 64; ++j) h[j] = relu(h[j] + __ldg(bh + j));
     }
-    // output layer 64 -> 3 (FP32 SIMT), |x|, decode_prediction
     float y[3];
     dense_simt(P + d.head_off[2], P + d.head_off[2] + 3 * 64, 3, 64, h, y);
     if (live) {
         for (int c = 0; c < 3; ++c) {
             float yc = fabsf(y[c]);
             if (y_out) y_out[3 * q + c] = yc;
-            if (F_out) F_out[3 * q + c] = pow(alb[c], d.gamma) * expm1(double(yc));
+            if (F_out) F_out[3 * q + c] = pow(alb[c], d.gamma) * expm1(double(yc));  // decode_prediction
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s.tmem), "r"(kTmemCols));
+    if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
-// ---- host-side packing -----------------------------------------------------------------
+// ---- host-side packing ------------------------------------------------------------
 
-struct TcPack {
-    uint8_t* d_blobs = nullptr;
-    size_t bytes = 0;
-    TcDesc desc{};
-};
-
-void pack_blob(std::vector<uint8_t>& buf, std::vector<Blob>& blobs, const float* W, int rows, int cols, int ld,
-               int col0, int Kp) {
-    // B operand of one GEMM: rows = N outputs, K = Kp (cols [col0, col0+cols) of W, zero padded)
+// B operand of one GEMM: rows = N outputs, cols [col0, col0+cols) of W (leading dim ld), zero padded to Kp.
+uint32_t pack_blob(std::vector<uint8_t>& buf, const float* W, int rows, int cols, int ld, int col0, int Kp) {
     size_t off = (buf.size() + 127) & ~size_t(127);
     size_t bytes = size_t(rows) * Kp * 2;
     buf.resize(off + bytes, 0);
@@ -460,72 +349,119 @@ void pack_blob(std::vector<uint8_t>& buf, std::vector<Blob>& blobs, const float*
             __nv_bfloat16 h = __float2bfloat16_rn(v);
             std::memcpy(&buf[off + canon_off(r, k, Kp)], &h, 2);
         }
-    blobs.push_back(Blob{uint32_t(off), uint16_t(bytes), uint16_t(Kp)});
+    return uint32_t(off);
 }
+
+Copy wcopy(uint32_t off, uint32_t bytes, uint32_t dst) { return Copy{0, dst, bytes, 0, int64_t(off), 0}; }
 
 }  // namespace
 
 bool tc_supported(const sf_backbone_config& c) {
     if (c.width != 32 || c.merge_width != 64 || c.head_width != 64) return false;
     for (int i = 0; i < c.n_diffuse_layers; ++i)
-        if (c.diffuse_counts[i] + 2 + 32 > 96) return false;
+        if (c.diffuse_counts[i] + 2 > 64) return false;
     for (int i = 0; i < c.n_highlight_layers; ++i)
-        if (c.highlight_counts[i] + 2 + 32 > 96) return false;
+        if (c.highlight_counts[i] + 2 > 64) return false;
     return true;
+}
+
+SortLayout sort_layout(const sf_backbone_config& c) {
+    SortLayout L{};
+    L.nl[0] = c.n_diffuse_layers;
+    L.nl[1] = c.n_highlight_layers;
+    int64_t prefix = 0;
+    int layer = 0;
+    for (int k = 0; k < 2; ++k) {
+        const int* counts = k == 0 ? c.diffuse_counts : c.highlight_counts;
+        int start = 0;
+        for (int i = 0; i < L.nl[k]; ++i) {
+            L.counts[k][i] = counts[i];
+            L.start[k][i] = start;
+            L.kf[k][i] = (counts[i] + 2 + 15) / 16 * 16;
+            L.mm_layer[k][i] = layer++;
+            start += counts[i];
+            for (int t = 0; t < 3; ++t) {
+                L.seg_prefix[k][i][t] = prefix;  // bytes per tile before this segment
+                prefix += int64_t(kUmmaM) * L.kf[k][i] * 2;
+            }
+        }
+        L.npts[k] = start;
+    }
+    L.tile_bytes = prefix;
+    L.n_layers = layer;
+    return L;
 }
 
 void tc_prepare(sf_backbone& b, cudaStream_t s) {
     if (b.tc) return;
     const sf_backbone_config& c = b.cfg;
     const BackboneLayout& L = b.layout;
+    const SortLayout S = sort_layout(c);
     std::vector<float> P(size_t(L.total));
     SFB_CUDA(cudaMemcpyAsync(P.data(), b.d_params, P.size() * sizeof(float), cudaMemcpyDeviceToHost, s));
     SFB_CUDA(cudaStreamSynchronize(s));
     auto pk = new TcPack();
-    TcDesc& d = pk->desc;
     std::vector<uint8_t> buf;
-    std::vector<Blob> blobs;
+    std::vector<Step>& steps = pk->steps;
     const int W = 32;
-    d.kp1_max = 0;
     for (int tau = 0; tau < 3; ++tau) {
         for (int kind = 0; kind < 2; ++kind) {
-            int nl = kind == 0 ? c.n_diffuse_layers : c.n_highlight_layers;
-            const int* counts = kind == 0 ? c.diffuse_counts : c.highlight_counts;
+            int nl = S.nl[kind];
             int64_t off = L.stack_off[kind][tau] + W * 7 + W;
             for (int i = 0; i < nl; ++i) {
                 if (!c.literal_attention) off += 51;
-                int K = W + counts[i] + 2;
-                int Kp = (K + 15) / 16 * 16;
-                d.kp1_max = std::max(d.kp1_max, Kp);
-                pack_blob(buf, blobs, P.data() + off, W, K, K, 0, Kp);
+                const int cnt = S.counts[kind][i];
+                const int K = W + cnt + 2, kf = S.kf[kind][i];
+                uint32_t oa = pack_blob(buf, P.data() + off, W, W, K, 0, W);
+                uint32_t ob = pack_blob(buf, P.data() + off, W, cnt + 2, K, W, kf);
+                Step st{};
+                st.ncopy = 4;
+                st.k2 = kf;
+                st.c[0] = wcopy(oa, W * W * 2, kSlotW1a);
+                st.c[1] = wcopy(ob, uint32_t(W * kf * 2), kSlotW1b);
+                st.c[2] = Copy{1, kSlotFeat, uint32_t(kUmmaM * kf * 2), 0, S.seg_prefix[kind][i][tau],
+                               int64_t(kUmmaM) * kf * 2};
+                st.c[3] = Copy{2, kSlotMM, uint32_t(kUmmaM * 8 * 4), 0, S.mm_layer[kind][i], 4096};
+                steps.push_back(st);
                 off += int64_t(W) * K + W;
-                pack_blob(buf, blobs, P.data() + off, W, W, W, 0, W);
+                uint32_t o2 = pack_blob(buf, P.data() + off, W, W, W, 0, W);
+                Step s2{};
+                s2.ncopy = 1;
+                s2.k2 = W;
+                s2.c[0] = wcopy(o2, W * W * 2, 0);
+                steps.push_back(s2);
                 off += W * W + W;
             }
         }
-        pack_blob(buf, blobs, P.data() + L.merge_off + int64_t(tau) * (64 * 64 + 64), 64, 64, 64, 0, 64);
+        Step sm{};
+        sm.ncopy = 1;
+        sm.k2 = 64;
+        sm.c[0] = wcopy(pack_blob(buf, P.data() + L.merge_off + int64_t(tau) * (64 * 64 + 64), 64, 64, 64, 0, 64),
+                        8192, 0);
+        steps.push_back(sm);
+        Step sc{};
+        sc.ncopy = 1;
+        sc.k2 = 64;
+        sc.c[0] = wcopy(pack_blob(buf, P.data() + L.cross_off, 64, 64, 192, 64 * tau, 64), 8192, 0);
+        steps.push_back(sc);
     }
-    for (int k = 0; k < 3; ++k) pack_blob(buf, blobs, P.data() + L.cross_off, 64, 64, 192, 64 * k, 64);
-    for (int l = 0; l < 2; ++l) pack_blob(buf, blobs, P.data() + L.head_off[l], 64, 64, 64, 0, 64);
-    if (blobs.size() > size_t(kMaxBlobs)) fail(SF_ERR_INVALID_ARGUMENT, "tc backbone: too many layers");
-    d.n_blobs = int(blobs.size());
-    for (size_t i = 0; i < blobs.size(); ++i) d.blobs[i] = blobs[i];
-    pk->bytes = buf.size();
-    SFB_CUDA(cudaMalloc(&pk->d_blobs, buf.size()));
-    SFB_CUDA(cudaMemcpy(pk->d_blobs, buf.data(), buf.size(), cudaMemcpyHostToDevice));
-    // network description (shared with the fp32 kernel's slice layout)
-    d.nl[0] = c.n_diffuse_layers;
-    d.nl[1] = c.n_highlight_layers;
-    int so = 0;
-    for (int kind = 0; kind < 2; ++kind) {
-        int nl = d.nl[kind];
-        const int* counts = kind == 0 ? c.diffuse_counts : c.highlight_counts;
-        for (int i = 0; i < nl; ++i) {
-            d.counts[kind][i] = counts[i];
-            d.slice_off[kind][i] = so;
-            so += 3 * (counts[i] + 2);
-        }
+    for (int l = 0; l < 2; ++l) {
+        Step sh{};
+        sh.ncopy = 1;
+        sh.k2 = 64;
+        sh.c[0] = wcopy(pack_blob(buf, P.data() + L.head_off[l], 64, 64, 64, 0, 64), 8192, 0);
+        steps.push_back(sh);
     }
+    if (steps.size() > size_t(kMaxSteps)) fail(SF_ERR_INVALID_ARGUMENT, "tc backbone: too many layers");
+    for (Step& st : steps) {
+        st.total = 0;
+        for (int k = 0; k < st.ncopy; ++k) st.total += st.c[k].bytes;
+    }
+    TcDesc& d = pk->desc;
+    d.nl[0] = S.nl[0];
+    d.nl[1] = S.nl[1];
+    for (int k = 0; k < 2; ++k)
+        for (int i = 0; i < S.nl[k]; ++i) d.counts[k][i] = S.counts[k][i];
     d.W = c.width;
     d.M = c.merge_width;
     d.H = c.head_width;
@@ -536,35 +472,38 @@ void tc_prepare(sf_backbone& b, cudaStream_t s) {
     d.merge_off = L.merge_off;
     d.cross_off = L.cross_off;
     for (int l = 0; l < 3; ++l) d.head_off[l] = L.head_off[l];
+    d.n_steps = int(steps.size());
+    SFB_CUDA(cudaMalloc(&pk->d_blobs, buf.size()));
+    SFB_CUDA(cudaMemcpy(pk->d_blobs, buf.data(), buf.size(), cudaMemcpyHostToDevice));
+    SFB_CUDA(cudaMalloc(&pk->d_steps, steps.size() * sizeof(Step)));
+    SFB_CUDA(cudaMemcpy(pk->d_steps, steps.data(), steps.size() * sizeof(Step), cudaMemcpyHostToDevice));
     b.tc = pk;
+}
+
+void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, const float* mms,
+                        const double* cfg8, float* y, double* F, cudaStream_t s) {
+    if (n <= 0) return;
+    auto pk = static_cast<const TcPack*>(b.tc);
+    const size_t smem = 1024 + kUmmaM * 32 * 2 + kUmmaM * 64 * 2 + size_t(kSlots) * kSlotBytes;
+    static bool attr_set = false;
+    if (!attr_set) {
+        SFB_CUDA(cudaFuncSetAttribute(k_backbone_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr_set = true;
+    }
+    const int n_tiles = int((n + kUmmaM - 1) / kUmmaM);
+    k_backbone_tc<<<n_tiles, kThreads, smem, s>>>(pk->desc, pk->d_steps, b.d_params, pk->d_blobs, ops,
+                                                  reinterpret_cast<const uint8_t*>(mms), n_tiles, n, cfg8, y, F);
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void tc_release(sf_backbone& b) {
     auto pk = static_cast<TcPack*>(b.tc);
     if (!pk) return;
     cudaFree(pk->d_blobs);
+    cudaFree(pk->d_steps);
     delete pk;
     b.tc = nullptr;
-}
-
-static size_t tc_smem_bytes(const TcDesc& d) {
-    return 1024 + size_t(kTile) * d.kp1_max * 2 + kTile * 64 * 2 + kTile * 192 * 2 + 2 * kBlobMax;
-}
-
-void launch_backbone_tc(const sf_backbone& b, int64_t n, const float* slices, const double* cfg8, float* y,
-                        double* F, cudaStream_t s) {
-    if (n <= 0) return;
-    auto pk = static_cast<const TcPack*>(b.tc);
-    size_t smem = tc_smem_bytes(pk->desc);
-    static bool attr_set = false;
-    if (!attr_set) {
-        SFB_CUDA(cudaFuncSetAttribute(k_backbone_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        attr_set = true;
-    }
-    unsigned grid = unsigned((n + kTile - 1) / kTile);
-    k_backbone_tc<<<grid, kThreads, smem, s>>>(pk->desc, b.d_params, pk->d_blobs, n, slices, cfg8, y, F);
-    SFB_CUDA(cudaGetLastError());
-    count_launch();
 }
 
 }  // namespace sfb
