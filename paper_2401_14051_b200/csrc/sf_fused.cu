@@ -45,6 +45,7 @@ struct SortDesc {
     // per output chunk (16 B = 8 bf16 of one row)
     uint8_t chunk_seg[kMaxChunks];
     uint8_t chunk_j[kMaxChunks];
+    uint8_t task_seg[kMaxSegs];  // segments ordered by sorting-network size
 };
 
 __device__ __forceinline__ void warp_sort64_desc(float& v0, float& v1, int lane) {
@@ -193,89 +194,145 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
     ph = fw * fl;
 }
 
-__global__ void __launch_bounds__(kWarps * 32)
+// Descending bitonic network on P (power of two) register values; all indices are
+// compile-time so the segment never leaves registers.
+template <int P>
+__device__ __forceinline__ void bitonic_desc(float* v) {
+#pragma unroll
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const float a = v[i], b = v[l];
+                    const float hi = fmaxf(a, b), lo = fminf(a, b);
+                    if ((i & k) == 0) {
+                        v[i] = hi;
+                        v[l] = lo;
+                    } else {
+                        v[i] = lo;
+                        v[l] = hi;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Sort one segment (cnt <= P values at seg) in registers, write it back sorted and
+// return mean (sequential float sum in sorted order / cnt) and max.
+template <int P>
+__device__ __forceinline__ void sort_segment(float* seg, int cnt, float& mean, float& mx) {
+    float v[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = j < cnt ? seg[j] : -INFINITY;
+    bitonic_desc<P>(v);
+    float acc = 0.0f;
+#pragma unroll
+    for (int j = 0; j < P; ++j)
+        if (j < cnt) acc += v[j];
+#pragma unroll
+    for (int j = 0; j < P; ++j)
+        if (j < cnt) seg[j] = v[j];
+    mean = acc / float(cnt);
+    mx = v[0];
+}
+
+// Block = 8 consecutive queries (one 8-row group of a UMMA tile).
+//  phase 1: warp w samples the 266 template points of query q0 + w (point-parallel,
+//           so a warp's gathers stay inside one template's footprint);
+//  phase 2: thread-per-(query, segment) register sorts, tasks ordered by network
+//           size so a warp runs one network;
+//  phase 3: the 8 rows of every 16-byte operand chunk are 128 contiguous bytes of
+//           the canonical layout, so each warp store is fully coalesced.
+__global__ void __launch_bounds__(kWarps * 32, 3)
     k_sample_sort(SceneDev sc, TemplateDev dt, TemplateDev ht, SortDesc d, const float* __restrict__ planes_g,
                   int64_t n, const double* __restrict__ queries, const float* __restrict__ feats,
                   uint8_t* __restrict__ ops, float* __restrict__ mms, int* err) {
     extern __shared__ __align__(16) float sm[];
     const int plane_floats = d.n_planes * d.A * d.H;
     for (int i = threadIdx.x; i < plane_floats; i += blockDim.x) sm[i] = planes_g[i];
-    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* scr = sm + plane_floats + warp * d.scr_floats;
-    float* seg_mm = scr + 3 * d.ntot;  // [n_segs][2]
+    float* scr_all = sm + plane_floats;                        // [8][scr_floats]
+    float* pools = scr_all + kWarps * d.scr_floats;            // [8][n_segs][2]
     const int64_t q_pad = int64_t(d.n_tiles) * kUmmaM;
+    const int64_t n_groups = q_pad / kWarps;
+    __syncthreads();
 
-    for (int64_t q = int64_t(blockIdx.x) * kWarps + warp; q < q_pad; q += int64_t(gridDim.x) * kWarps) {
-        const bool live = q < n;
-        if (!live) {
-            for (int i = lane; i < 3 * d.ntot; i += 32) scr[i] = 0.0f;
-        } else if (feats == nullptr) {
-            QueryCtx qc;
-            query_ctx(sc, ht, queries + 9 * q, qc);
-            if (!qc.ok && lane == 0) atomicExch(err, 1);
-            for (int i = lane; i < d.ntot; i += 32) {
-                float rho, tr, ph;
-                point_features(sc, dt, ht, qc, i, d.npts0, sm, d, rho, tr, ph);
-                scr[i] = rho;
-                scr[d.ntot + i] = tr;
-                scr[2 * d.ntot + i] = ph;
+    for (int64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+        const int64_t q0 = grp * kWarps;
+        // ---- phase 1: features
+        {
+            float* scr = scr_all + warp * d.scr_floats;
+            const int64_t q = q0 + warp;
+            if (q >= n) {
+                for (int i = lane; i < 3 * d.ntot; i += 32) scr[i] = 0.0f;
+            } else if (feats == nullptr) {
+                QueryCtx qc;
+                query_ctx(sc, ht, queries + 9 * q, qc);
+                if (!qc.ok && lane == 0) atomicExch(err, 1);
+                for (int i = lane; i < d.ntot; i += 32) {
+                    float rho, tr, ph;
+                    point_features(sc, dt, ht, qc, i, d.npts0, sm, d, rho, tr, ph);
+                    scr[i] = rho;
+                    scr[d.ntot + i] = tr;
+                    scr[2 * d.ntot + i] = ph;
+                }
+            } else {
+                const float* row = feats + q * d.feat_stride;
+                const int n0 = d.npts0, n1 = d.ntot - d.npts0;
+                for (int i = lane; i < d.ntot; i += 32)
+                    for (int ch = 0; ch < 3; ++ch)
+                        scr[ch * d.ntot + i] = i < n0 ? row[ch * n0 + i] : row[3 * n0 + ch * n1 + (i - n0)];
             }
-        } else {
-            // caller's feature row: diffuse {rho,T,f}[npts0], highlight {rho,T,f}[npts1]
-            const float* row = feats + q * d.feat_stride;
-            const int n0 = d.npts0, n1 = d.ntot - d.npts0;
-            for (int i = lane; i < d.ntot; i += 32) {
-                for (int ch = 0; ch < 3; ++ch)
-                    scr[ch * d.ntot + i] = i < n0 ? row[ch * n0 + i] : row[3 * n0 + ch * n1 + (i - n0)];
-            }
         }
-        __syncwarp();
-        // sort every (kind, layer, tau) segment descending (src/predictor.cpp:176-179)
-        for (int s = 0; s < d.n_segs; ++s) {
-            float* seg = scr + d.seg_scr[s];
+        __syncthreads();
+        // ---- phase 2: per-(query, segment) register sorts + pools
+        for (int t = threadIdx.x; t < d.n_segs * kWarps; t += blockDim.x) {
+            const int s = d.task_seg[t / kWarps], w = t % kWarps;
+            float* seg = scr_all + w * d.scr_floats + d.seg_scr[s];
             const int cnt = d.seg_n[s];
-            float v0 = lane < cnt ? seg[lane] : -INFINITY;
-            float v1 = lane + 32 < cnt ? seg[lane + 32] : -INFINITY;
-            warp_sort64_desc(v0, v1, lane);
-            __syncwarp();
-            if (lane < cnt) seg[lane] = v0;
-            if (lane + 32 < cnt) seg[lane + 32] = v1;
+            float mean, mx;
+            if (cnt <= 8)
+                sort_segment<8>(seg, cnt, mean, mx);
+            else if (cnt <= 16)
+                sort_segment<16>(seg, cnt, mean, mx);
+            else if (cnt <= 32)
+                sort_segment<32>(seg, cnt, mean, mx);
+            else
+                sort_segment<64>(seg, cnt, mean, mx);
+            pools[(w * d.n_segs + s) * 2] = mean;
+            pools[(w * d.n_segs + s) * 2 + 1] = mx;
         }
-        __syncwarp();
-        // pools in sorted order: one lane per segment
-        for (int s = lane; s < d.n_segs; s += 32) {
-            const float* seg = scr + d.seg_scr[s];
-            const int cnt = d.seg_n[s];
-            float acc = 0.0f;
-            for (int j = 0; j < cnt; ++j) acc += seg[j];
-            seg_mm[2 * s] = acc / float(cnt);
-            seg_mm[2 * s + 1] = seg[0];
-        }
-        __syncwarp();
-        // attention pools: {mean d,p,t, max d,p,t, 0, 0} per (kind, layer)
-        for (int l = lane; l < d.n_layers; l += 32) {
-            float4* o = reinterpret_cast<float4*>(mms + (int64_t(l) * q_pad + q) * 8);
-            o[0] = make_float4(seg_mm[6 * l], seg_mm[6 * l + 2], seg_mm[6 * l + 4], seg_mm[6 * l + 1]);
-            o[1] = make_float4(seg_mm[6 * l + 3], seg_mm[6 * l + 5], 0.0f, 0.0f);
-        }
-        // FC-1 feature operands (bf16, canonical layout of the 128-query tile)
-        const int64_t tile = q / kUmmaM;
-        const int row = int(q % kUmmaM);
-        for (int c = lane; c < d.n_chunks; c += 32) {
+        __syncthreads();
+        // ---- phase 3: outputs
+        const int64_t tile = q0 / kUmmaM;
+        const int row0 = int(q0 % kUmmaM);
+        for (int t = threadIdx.x; t < d.n_chunks * kWarps; t += blockDim.x) {
+            const int c = t / kWarps, w = t % kWarps;
             const int s = d.chunk_seg[c], j = d.chunk_j[c];
-            const float* seg = scr + d.seg_scr[s];
+            const float* seg = scr_all + w * d.scr_floats + d.seg_scr[s];
+            const float* pl = pools + (w * d.n_segs + s) * 2;
             const int cnt = d.seg_n[s], kf = d.seg_kf[s];
             float v8[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                int idx = 8 * j + e;
-                v8[e] = idx < cnt ? seg[idx] : (idx == cnt ? seg_mm[2 * s] : (idx == cnt + 1 ? seg_mm[2 * s + 1] : 0.0f));
+                const int idx = 8 * j + e;
+                v8[e] = idx < cnt ? seg[idx] : (idx == cnt ? pl[0] : (idx == cnt + 1 ? pl[1] : 0.0f));
             }
             uint8_t* blk = ops + d.seg_prefix[s] * d.n_tiles + tile * (int64_t(kUmmaM) * kf * 2);
-            store_chunk(blk, row, j, kf, v8);
+            store_chunk(blk, row0 + w, j, kf, v8);
         }
-        __syncwarp();
+        for (int t = threadIdx.x; t < d.n_layers * kWarps; t += blockDim.x) {
+            const int l = t / kWarps, w = t % kWarps;
+            const float* pl = pools + (w * d.n_segs + 3 * l) * 2;  // segments 3l + tau
+            float4* o = reinterpret_cast<float4*>(mms + (int64_t(l) * q_pad + q0 + w) * 8);
+            o[0] = make_float4(pl[0], pl[2], pl[4], pl[1]);
+            o[1] = make_float4(pl[3], pl[5], 0.0f, 0.0f);
+        }
+        __syncthreads();
     }
 }
 
@@ -345,16 +402,24 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
             }
     d.n_segs = segs;
     d.n_chunks = chunks;
-    d.scr_floats = (3 * d.ntot + 2 * segs + 31) / 32 * 32;
-    const size_t smem = size_t(d.n_planes * d.A * d.H + kWarps * d.scr_floats) * sizeof(float);
+    {
+        auto net = [](int c) { return c <= 8 ? 8 : c <= 16 ? 16 : c <= 32 ? 32 : 64; };
+        int t = 0;
+        for (int p : {64, 32, 16, 8})
+            for (int s2 = 0; s2 < segs; ++s2)
+                if (net(d.seg_n[s2]) == p) d.task_seg[t++] = uint8_t(s2);
+    }
+    d.scr_floats = (3 * d.ntot + 3) / 4 * 4;
+    const size_t smem =
+        size_t(d.n_planes * d.A * d.H + kWarps * d.scr_floats + kWarps * segs * 2) * sizeof(float);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         SFB_CUDA(cudaFuncSetAttribute(k_sample_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         attr = smem;
     }
     const int64_t q_pad = int64_t(d.n_tiles) * kUmmaM;
-    int64_t blocks = (q_pad + kWarps - 1) / kWarps;
-    int64_t cap = int64_t(sm_count()) * 8;
+    int64_t blocks = q_pad / kWarps;
+    int64_t cap = int64_t(sm_count()) * 3;
     if (blocks > cap) blocks = cap;
     SceneDev scd = sc ? *sc : SceneDev{};
     TemplateDev dtd = dt ? *dt : TemplateDev{};
