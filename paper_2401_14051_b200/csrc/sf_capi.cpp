@@ -873,11 +873,11 @@ void check_precision(const sf_backbone& b, int precision, cudaStream_t s) {
 // bf16 path over one chunk: fused sample+sort (or sort of given features) -> tcgen05 backbone.
 void run_bf16_chunk(const sf_backbone& b, const sfb::SortLayout& L, const sfb::SceneDev* sc,
                     const sfb::TemplateDev* dt, const sfb::TemplateDev* ht, const float* planes, int n_planes,
-                    int64_t m, const double* queries, const float* feats, const double* cfg8, uint8_t* ops,
-                    float* mms, int* err, float* y, double* F, cudaStream_t s) {
+                    const float2* pre, int64_t m, const double* queries, const float* feats, const double* cfg8,
+                    uint8_t* ops, float* mms, int* err, float* y, double* F, cudaStream_t s) {
     {
         StageScope st(SF_STAGE_SAMPLE_SORT, s);
-        sfb::launch_sample_sort(sc, dt, ht, planes, n_planes, L, m, queries, feats, ops, mms, err, s);
+        sfb::launch_sample_sort(sc, dt, ht, planes, n_planes, pre, L, m, queries, feats, ops, mms, err, s);
     }
     {
         StageScope st(SF_STAGE_BACKBONE, s);
@@ -916,8 +916,8 @@ int sf_predict(const sf_backbone* b, int64_t n, const float* features, const dou
             const int64_t tiles = (n + sfb::kUmmaM - 1) / sfb::kUmmaM;
             Scratch<uint8_t> ops(size_t(tiles) * L.tile_bytes, stream);
             Scratch<float> mms(size_t(L.n_layers) * tiles * sfb::kUmmaM * 8, stream);
-            run_bf16_chunk(*b, L, nullptr, nullptr, nullptr, nullptr, 0, n, nullptr, f.d, cf.d, ops.p, mms.p,
-                           nullptr, oy.d, oF.d, stream);
+            run_bf16_chunk(*b, L, nullptr, nullptr, nullptr, nullptr, 0, nullptr, n, nullptr, f.d, cf.d, ops.p,
+                           mms.p, nullptr, oy.d, oF.d, stream);
         }
         oy.finish();
         oF.finish();
@@ -945,15 +945,20 @@ int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_templa
         s->table = table;
         s->template_scale = ts;
         s->n_planes = model->kind == SF_PHASE_ISOTROPIC ? 1 : model->n_lobes;
-        SFB_CUDA(cudaMalloc(&s->d_dt, density->count() * sizeof(float2)));
         try {
-            SFB_CUDA(cudaMalloc(&s->d_planes, size_t(s->n_planes) * table->a * table->h * sizeof(float)));
+            SFB_CUDA(cudaMalloc(&s->d_dt, density->count() * sizeof(float2)));
+            SFB_CUDA(cudaMalloc(&s->d_dt4, density->count() * sizeof(float4)));
+            SFB_CUDA(cudaMalloc(&s->d_planes, size_t(s->n_planes) * table->a * table->h * sizeof(float2)));
+            SFB_CUDA(cudaMalloc(&s->d_pre, std::max<size_t>(1, size_t(dt->total)) * sizeof(float2)));
             sfb::launch_interleave(density->d, tv.d, s->d_dt, density->count(), nullptr);
+            sfb::launch_xpair(s->d_dt, density->nx, density->ny, density->nz, s->d_dt4, nullptr);
             sfb::launch_blend_planes(*table, *model, s->d_planes, nullptr);
             SFB_CUDA(cudaDeviceSynchronize());
         } catch (...) {
             cudaFree(s->d_dt);
+            cudaFree(s->d_dt4);
             cudaFree(s->d_planes);
+            cudaFree(s->d_pre);
             throw;
         }
         *out = s.release();
@@ -963,7 +968,9 @@ int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_templa
 void sf_scene_destroy(sf_scene* s) {
     if (!s) return;
     cudaFree(s->d_dt);
+    cudaFree(s->d_dt4);
     cudaFree(s->d_planes);
+    cudaFree(s->d_pre);
     delete s;
 }
 
@@ -994,7 +1001,12 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
             SFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
             sfb::SceneDev sc = sfb::scene_dev(*s->density, *s->tvol->values, s->d_dt, s->model, *s->table,
                                               s->template_scale);
+            sc.dt4 = s->d_dt4;
             sfb::TemplateDev dt = sfb::template_dev(*s->dt), ht = sfb::template_dev(*s->ht);
+            {
+                StageScope st(SF_STAGE_CONFIG, stream);
+                sfb::launch_diffuse_light(sc, dt, s->d_planes, s->n_planes, iq.d, s->d_pre, stream);
+            }
             for (int64_t q0 = 0; q0 < n; q0 += chunk) {
                 int64_t m = std::min(chunk, n - q0);
                 const double* qd = iq.d + 9 * q0;
@@ -1002,8 +1014,8 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
                     StageScope st(SF_STAGE_CONFIG, stream);
                     sfb::launch_make_cfg8(*medium, m, qd, cfg8.p, stream);
                 }
-                run_bf16_chunk(*b, L, &sc, &dt, &ht, s->d_planes, s->n_planes, m, qd, nullptr, cfg8.p, ops.p,
-                               mms.p, err.p, oy.d ? oy.d + 3 * q0 : nullptr, oF.d ? oF.d + 3 * q0 : nullptr,
+                run_bf16_chunk(*b, L, &sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, m, qd, nullptr, cfg8.p,
+                               ops.p, mms.p, err.p, oy.d ? oy.d + 3 * q0 : nullptr, oF.d ? oF.d + 3 * q0 : nullptr,
                                stream);
             }
             if (!oF.host && !oy.host && !iq.buf.p) return;  // device in/out: asynchronous (see below)

@@ -18,6 +18,8 @@
 // FP64 as the reference, interpolation weights and lerps in FP32, phase angles and
 // the phase-table bilinear in FP32 (survey: <= 3.2e-6 relative), all far inside
 // the bf16 rounding (3.9e-3) the operands undergo.
+#include <algorithm>
+
 #include "sf_internal.h"
 #include "sf_umma.cuh"
 
@@ -48,39 +50,27 @@ struct SortDesc {
     uint8_t task_seg[kMaxSegs];  // segments ordered by sorting-network size
 };
 
-__device__ __forceinline__ void warp_sort64_desc(float& v0, float& v1, int lane) {
-#pragma unroll
-    for (int k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j == 32) {
-                float a = fmaxf(v0, v1), b = fminf(v0, v1);
-                v0 = a;
-                v1 = b;
-            } else {
-                float o0 = __shfl_xor_sync(0xffffffffu, v0, j);
-                float o1 = __shfl_xor_sync(0xffffffffu, v1, j);
-                const bool lower = (lane & j) == 0;
-                const bool d0 = (lane & k) == 0, d1 = ((lane + 32) & k) == 0;
-                v0 = (lower == d0) ? fmaxf(v0, o0) : fminf(v0, o0);
-                v1 = (lower == d1) ? fmaxf(v1, o1) : fminf(v1, o1);
-            }
-        }
-    }
-}
-
-__device__ __forceinline__ float plane_lookup(const float* pl, int A, int H, float angle, float half) {
+// Bilinear lookup in a pre-blended phase plane stored as aperture pairs
+// pl[a][h] = {P(a,h), P(a,h+1)}: two 8-byte shared loads per lookup.
+__device__ __forceinline__ float plane_lookup(const float2* pl, int A, int H, float angle, float half) {
     float u = fminf(fmaxf(angle, 0.0f), float(kPi)) * (float(A - 1) / float(kPi));
     int i0 = min(int(u), A - 2);
     float t = u - float(i0);
     float v = fminf(fmaxf(half, 0.0f), float(kPi)) * (float(H - 1) / float(kPi));
     int j0 = min(int(v), H - 2);
     float s = v - float(j0);
-    const float* r0 = pl + i0 * H + j0;
-    const float* r1 = r0 + H;
-    float a = fmaf(s, r0[1] - r0[0], r0[0]);
-    float b = fmaf(s, r1[1] - r1[0], r1[0]);
+    const float2 r0 = pl[i0 * H + j0];
+    const float2 r1 = pl[(i0 + 1) * H + j0];
+    float a = fmaf(s, r0.y - r0.x, r0.x);
+    float b = fmaf(s, r1.y - r1.x, r1.x);
     return fmaf(t, b - a, a);
+}
+
+__device__ __forceinline__ float cap_phase(const float2* planes, int n_planes, const float* w, int A, int H,
+                                           float angle, float half) {
+    float f = 0.0f;
+    for (int k = 0; k < n_planes; ++k) f = fmaf(w[k], plane_lookup(planes + k * A * H, A, H, angle, half), f);
+    return f;
 }
 
 struct QueryCtx {
@@ -126,8 +116,9 @@ __device__ __forceinline__ void query_ctx(const SceneDev& sc, const TemplateDev&
 
 // density, transmittance and phase feature of template point i (0..ntot)
 __device__ __forceinline__ void point_features(const SceneDev& sc, const TemplateDev& dt, const TemplateDev& ht,
-                                               const QueryCtx& q, int i, int npts0, const float* planes,
-                                               const SortDesc& d, float& rho, float& tr, float& ph) {
+                                               const QueryCtx& q, int i, int npts0, const float2* planes,
+                                               const float2* pre, bool use_pre, const SortDesc& d, float& rho,
+                                               float& tr, float& ph) {
     double s[3];
     double cap;
     if (i < npts0) {
@@ -149,22 +140,39 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
         rho = 0.0f;
         tr = 1.0f;
     } else {
-        Cell c = cell_of(g, s[0], s[1], s[2]);
-        const float tx = float(c.tx), ty = float(c.ty), tz = float(c.tz);
+        // FP64 cell selection exactly as sample_trilinear; FP32 weights and lerps.
+        // x-pair records hold {rho, T} at x0 and clamp(x0 + 1): one 16-byte load per
+        // (y, z) corner row; a cell clamped at the low x edge has tx forced to 0.
+        double fx, fy, fz;
+        if (g.ivs != 0.0) {
+            fx = (s[0] - g.ox) * g.ivs - 0.5;
+            fy = (s[1] - g.oy) * g.ivs - 0.5;
+            fz = (s[2] - g.oz) * g.ivs - 0.5;
+        } else {
+            fx = (s[0] - g.ox) / g.vs - 0.5;
+            fy = (s[1] - g.oy) / g.vs - 0.5;
+            fz = (s[2] - g.oz) / g.vs - 0.5;
+        }
+        const double flx = floor(fx), fly = floor(fy), flz = floor(fz);
+        int x0 = int(flx), y0 = int(fly), z0 = int(flz);
+        float tx = float(fx - flx), ty = float(fy - fly), tz = float(fz - flz);
+        if (x0 < 0) tx = 0.0f;
+        const int y1 = clampi(y0 + 1, 0, g.ny - 1), z1 = clampi(z0 + 1, 0, g.nz - 1);
+        x0 = clampi(x0, 0, g.nx - 1);
+        y0 = clampi(y0, 0, g.ny - 1);
+        z0 = clampi(z0, 0, g.nz - 1);
         const size_t sy = size_t(g.nx), sz = size_t(g.nx) * g.ny;
-        const float2* v = sc.dt;
-        float2 a000 = __ldg(v + c.z0 * sz + c.y0 * sy + c.x0), a100 = __ldg(v + c.z0 * sz + c.y0 * sy + c.x1);
-        float2 a010 = __ldg(v + c.z0 * sz + c.y1 * sy + c.x0), a110 = __ldg(v + c.z0 * sz + c.y1 * sy + c.x1);
-        float2 a001 = __ldg(v + c.z1 * sz + c.y0 * sy + c.x0), a101 = __ldg(v + c.z1 * sz + c.y0 * sy + c.x1);
-        float2 a011 = __ldg(v + c.z1 * sz + c.y1 * sy + c.x0), a111 = __ldg(v + c.z1 * sz + c.y1 * sy + c.x1);
-        float c00 = fmaf(tx, a100.x - a000.x, a000.x), c10 = fmaf(tx, a110.x - a010.x, a010.x);
-        float c01 = fmaf(tx, a101.x - a001.x, a001.x), c11 = fmaf(tx, a111.x - a011.x, a011.x);
+        const float4* v = sc.dt4 + x0;
+        const float4 r00 = __ldg(v + z0 * sz + y0 * sy), r10 = __ldg(v + z0 * sz + y1 * sy);
+        const float4 r01 = __ldg(v + z1 * sz + y0 * sy), r11 = __ldg(v + z1 * sz + y1 * sy);
+        float c00 = fmaf(tx, r00.z - r00.x, r00.x), c10 = fmaf(tx, r10.z - r10.x, r10.x);
+        float c01 = fmaf(tx, r01.z - r01.x, r01.x), c11 = fmaf(tx, r11.z - r11.x, r11.x);
         float e0 = fmaf(ty, c10 - c00, c00), e1 = fmaf(ty, c11 - c01, c01);
         rho = fmaf(tz, e1 - e0, e0);
-        c00 = fmaf(tx, a100.y - a000.y, a000.y);
-        c10 = fmaf(tx, a110.y - a010.y, a010.y);
-        c01 = fmaf(tx, a101.y - a001.y, a001.y);
-        c11 = fmaf(tx, a111.y - a011.y, a011.y);
+        c00 = fmaf(tx, r00.w - r00.y, r00.y);
+        c10 = fmaf(tx, r10.w - r10.y, r10.y);
+        c01 = fmaf(tx, r01.w - r01.y, r01.y);
+        c11 = fmaf(tx, r11.w - r11.y, r11.y);
         e0 = fmaf(ty, c10 - c00, c00);
         e1 = fmaf(ty, c11 - c01, c01);
         tr = fmaf(tz, e1 - e0, e0);
@@ -175,23 +183,58 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
         ph = 1.0f;  // diffuse centre point (src/feature_pipeline.cpp:163-164)
         return;
     }
-    const float dist = sqrtf(dd);
-    const float capf = float(cap);
-    const float half = capf >= dist ? float(kPi) : asinf(capf / dist);
-    const float inv = 1.0f / dist;
+    const float inv = rsqrtf(dd);
     const float ax = dx * inv, ay = dy * inv, az = dz * inv;
     const float aa = ax * ax + ay * ay + az * az;
-    float cw = (q.wf[0] * ax + q.wf[1] * ay + q.wf[2] * az) * rsqrtf(q.ww * aa);
-    float cl = (q.lf[0] * ax + q.lf[1] * ay + q.lf[2] * az) * rsqrtf(q.ll * aa);
+    const float cw = (q.wf[0] * ax + q.wf[1] * ay + q.wf[2] * az) * rsqrtf(q.ww * aa);
     const float aw = acosf(fminf(fmaxf(cw, -1.0f), 1.0f));
-    const float al = acosf(fminf(fmaxf(cl, -1.0f), 1.0f));
-    float fw = 0.0f, fl = 0.0f;
-    for (int k = 0; k < d.n_planes; ++k) {
-        const float* pl = planes + k * d.A * d.H;
-        fw = fmaf(d.w[k], plane_lookup(pl, d.A, d.H, aw, half), fw);
-        fl = fmaf(d.w[k], plane_lookup(pl, d.A, d.H, al, half), fl);
+    float half, fl;
+    if (use_pre && i < npts0) {
+        const float2 pr = pre[i];  // translation-invariant diffuse aperture and light side
+        half = pr.x;
+        fl = pr.y;
+    } else {
+        const float capf = float(cap), dist = dd * inv;
+        half = capf >= dist ? float(kPi) : asinf(capf / dist);
+        const float cl = (q.lf[0] * ax + q.lf[1] * ay + q.lf[2] * az) * rsqrtf(q.ll * aa);
+        fl = cap_phase(planes, d.n_planes, d.w, d.A, d.H, acosf(fminf(fmaxf(cl, -1.0f), 1.0f)), half);
     }
-    ph = fw * fl;
+    ph = cap_phase(planes, d.n_planes, d.w, d.A, d.H, aw, half) * fl;
+}
+
+// pre[i] = {half angle, light-side cap integral} of diffuse point i for the light of
+// query 0 (axis = q_i/|q_i| and aperture asin(cap/|q_i ts|) do not depend on p).
+__global__ void k_diffuse_light(SceneDev sc, TemplateDev dt, SortDesc d, const float2* __restrict__ planes,
+                                const double* __restrict__ queries, float2* __restrict__ pre) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= dt.total) return;
+    const double* qq = dt.pts + 3 * i;
+    const double ts = sc.template_scale;
+    const float dx = float(qq[0] * ts), dy = float(qq[1] * ts), dz = float(qq[2] * ts);
+    const float dd = dx * dx + dy * dy + dz * dz;
+    if (dd <= 0.0f) {
+        pre[i] = make_float2(float(kPi), 1.0f);
+        return;
+    }
+    const float inv = rsqrtf(dd), dist = dd * inv;
+    const float ax = dx * inv, ay = dy * inv, az = dz * inv;
+    const float aa = ax * ax + ay * ay + az * az;
+    const float capf = float(dt.caps[i] * ts);
+    const float half = capf >= dist ? float(kPi) : asinf(capf / dist);
+    const float lx = float(queries[6]), ly = float(queries[7]), lz = float(queries[8]);
+    const float ll = lx * lx + ly * ly + lz * lz;
+    const float cl = (lx * ax + ly * ay + lz * az) * rsqrtf(ll * aa);
+    pre[i] = make_float2(half, cap_phase(planes, d.n_planes, d.w, d.A, d.H,
+                                         acosf(fminf(fmaxf(cl, -1.0f), 1.0f)), half));
+}
+
+__global__ void k_xpair(const float2* __restrict__ v, int nx, int ny, int nz, float4* __restrict__ out) {
+    const size_t n = size_t(nx) * ny * nz;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const int x = int(i % nx);
+        const float2 a = v[i], b = v[x + 1 < nx ? i + 1 : i];
+        out[i] = make_float4(a.x, a.y, b.x, b.y);
+    }
 }
 
 // Descending bitonic network on P (power of two) register values; all indices are
@@ -248,12 +291,17 @@ __device__ __forceinline__ void sort_segment(float* seg, int cnt, float& mean, f
 //  phase 3: the 8 rows of every 16-byte operand chunk are 128 contiguous bytes of
 //           the canonical layout, so each warp store is fully coalesced.
 __global__ void __launch_bounds__(kWarps * 32, 3)
-    k_sample_sort(SceneDev sc, TemplateDev dt, TemplateDev ht, SortDesc d, const float* __restrict__ planes_g,
-                  int64_t n, const double* __restrict__ queries, const float* __restrict__ feats,
-                  uint8_t* __restrict__ ops, float* __restrict__ mms, int* err) {
+    k_sample_sort(SceneDev sc, TemplateDev dt, TemplateDev ht, SortDesc d, const float2* __restrict__ planes_g,
+                  const float2* __restrict__ pre, int64_t n, const double* __restrict__ queries,
+                  const float* __restrict__ feats, uint8_t* __restrict__ ops, float* __restrict__ mms, int* err) {
     extern __shared__ __align__(16) float sm[];
-    const int plane_floats = d.n_planes * d.A * d.H;
-    for (int i = threadIdx.x; i < plane_floats; i += blockDim.x) sm[i] = planes_g[i];
+    const int plane_floats = 2 * d.n_planes * d.A * d.H;
+    float2* planes = reinterpret_cast<float2*>(sm);
+    for (int i = threadIdx.x; i < plane_floats / 2; i += blockDim.x) planes[i] = planes_g[i];
+    // light of query 0: diffuse light sides in `pre` are valid for queries with that light
+    double l_ref[3] = {0, 0, 0};
+    if (queries != nullptr && n > 0)
+        for (int c = 0; c < 3; ++c) l_ref[c] = queries[6 + c];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* scr_all = sm + plane_floats;                        // [8][scr_floats]
     float* pools = scr_all + kWarps * d.scr_floats;            // [8][n_segs][2]
@@ -271,11 +319,13 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
                 for (int i = lane; i < 3 * d.ntot; i += 32) scr[i] = 0.0f;
             } else if (feats == nullptr) {
                 QueryCtx qc;
-                query_ctx(sc, ht, queries + 9 * q, qc);
+                const double* qr = queries + 9 * q;
+                query_ctx(sc, ht, qr, qc);
                 if (!qc.ok && lane == 0) atomicExch(err, 1);
+                const bool use_pre = pre != nullptr && qr[6] == l_ref[0] && qr[7] == l_ref[1] && qr[8] == l_ref[2];
                 for (int i = lane; i < d.ntot; i += 32) {
                     float rho, tr, ph;
-                    point_features(sc, dt, ht, qc, i, d.npts0, sm, d, rho, tr, ph);
+                    point_features(sc, dt, ht, qc, i, d.npts0, planes, pre, use_pre, d, rho, tr, ph);
                     scr[i] = rho;
                     scr[d.ntot + i] = tr;
                     scr[2 * d.ntot + i] = ph;
@@ -337,35 +387,24 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
 }
 
 __global__ void k_blend_planes(const float* __restrict__ T, int G, int A, int H, int n_planes, double g0, double g1,
-                               double g2, float* __restrict__ out) {
-    int total = n_planes * A * H;
+                               double g2, float2* __restrict__ out) {
+    const int total = n_planes * A * H;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-        int k = idx / (A * H), ah = idx % (A * H);
-        double g = k == 0 ? g0 : (k == 1 ? g1 : g2);
+        const int k = idx / (A * H), ah = idx % (A * H), h = ah % H;
+        const double g = k == 0 ? g0 : (k == 1 ? g1 : g2);
         int gi;
         double gt;
-        table_coord(g, -0.99, 0.99, G, gi, gt);
-        out[idx] = float((1.0 - gt) * double(T[size_t(gi) * A * H + ah]) + gt * double(T[size_t(gi + 1) * A * H + ah]));
+        table_coord(g, -0.99, 0.99, G, gi, gt);  // PhaseTable::lookup_hg's g axis (src/phase.cpp:196-205)
+        const float* t0 = T + size_t(gi) * A * H + ah;
+        const float* t1 = t0 + size_t(A) * H;
+        const int dh = h + 1 < H ? 1 : 0;
+        const float v0 = float((1.0 - gt) * double(t0[0]) + gt * double(t1[0]));
+        const float v1 = float((1.0 - gt) * double(t0[dh]) + gt * double(t1[dh]));
+        out[idx] = make_float2(v0, v1);
     }
 }
 
-}  // namespace
-
-void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float* planes, cudaStream_t s) {
-    int n_planes = m.kind == SF_PHASE_ISOTROPIC ? 1 : m.n_lobes;
-    double g[3] = {0, 0, 0};
-    if (m.kind != SF_PHASE_ISOTROPIC)
-        for (int k = 0; k < n_planes; ++k) g[k] = m.g[k];
-    int total = n_planes * t.a * t.h;
-    k_blend_planes<<<(total + 255) / 256, 256, 0, s>>>(t.d, t.g, t.a, t.h, n_planes, g[0], g[1], g[2], planes);
-    SFB_CUDA(cudaGetLastError());
-    count_launch();
-}
-
-void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht, const float* planes,
-                        int n_planes, const SortLayout& L, int64_t n, const double* queries, const float* feats,
-                        uint8_t* ops, float* mms, int* err, cudaStream_t s) {
-    if (n <= 0) return;
+SortDesc make_desc(const SceneDev* sc, int n_planes, const SortLayout& L, int64_t n) {
     SortDesc d{};
     d.npts0 = L.npts[0];
     d.ntot = L.npts[0] + L.npts[1];
@@ -402,16 +441,55 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
             }
     d.n_segs = segs;
     d.n_chunks = chunks;
-    {
-        auto net = [](int c) { return c <= 8 ? 8 : c <= 16 ? 16 : c <= 32 ? 32 : 64; };
-        int t = 0;
-        for (int p : {64, 32, 16, 8})
-            for (int s2 = 0; s2 < segs; ++s2)
-                if (net(d.seg_n[s2]) == p) d.task_seg[t++] = uint8_t(s2);
-    }
-    d.scr_floats = (3 * d.ntot + 3) / 4 * 4;
-    const size_t smem =
-        size_t(d.n_planes * d.A * d.H + kWarps * d.scr_floats + kWarps * segs * 2) * sizeof(float);
+    auto net = [](int c) { return c <= 8 ? 8 : c <= 16 ? 16 : c <= 32 ? 32 : 64; };
+    int t = 0;
+    for (int p : {64, 32, 16, 8})
+        for (int s2 = 0; s2 < segs; ++s2)
+            if (net(d.seg_n[s2]) == p) d.task_seg[t++] = uint8_t(s2);
+    // odd row stride: the 8 query rows of a sort task group hit 8 different banks
+    d.scr_floats = (3 * d.ntot) | 1;
+    return d;
+}
+
+}  // namespace
+
+void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float* planes, cudaStream_t s) {
+    int n_planes = m.kind == SF_PHASE_ISOTROPIC ? 1 : m.n_lobes;
+    double g[3] = {0, 0, 0};
+    if (m.kind != SF_PHASE_ISOTROPIC)
+        for (int k = 0; k < n_planes; ++k) g[k] = m.g[k];
+    int total = n_planes * t.a * t.h;
+    k_blend_planes<<<(total + 255) / 256, 256, 0, s>>>(t.d, t.g, t.a, t.h, n_planes, g[0], g[1], g[2],
+                                                        reinterpret_cast<float2*>(planes));
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStream_t s) {
+    const size_t n = size_t(nx) * ny * nz;
+    k_xpair<<<unsigned(std::min<size_t>((n + 255) / 256, size_t(sm_count()) * 32)), 256, 0, s>>>(dt, nx, ny, nz,
+                                                                                                 out);
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float* planes, int n_planes,
+                          const double* queries, float2* pre, cudaStream_t s) {
+    SortLayout L{};
+    SortDesc d = make_desc(&sc, n_planes, L, 1);
+    k_diffuse_light<<<(dt.total + 127) / 128, 128, 0, s>>>(sc, dt, d, reinterpret_cast<const float2*>(planes),
+                                                           queries, pre);
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht, const float* planes,
+                        int n_planes, const float2* pre, const SortLayout& L, int64_t n, const double* queries,
+                        const float* feats, uint8_t* ops, float* mms, int* err, cudaStream_t s) {
+    if (n <= 0) return;
+    SortDesc d = make_desc(sc, n_planes, L, n);
+    const size_t smem = size_t(2 * d.n_planes * d.A * d.H + kWarps * d.scr_floats + kWarps * d.n_segs * 2 + 2) *
+                        sizeof(float);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         SFB_CUDA(cudaFuncSetAttribute(k_sample_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -424,8 +502,9 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
     SceneDev scd = sc ? *sc : SceneDev{};
     TemplateDev dtd = dt ? *dt : TemplateDev{};
     TemplateDev htd = ht ? *ht : TemplateDev{1, 0, nullptr, nullptr, 1.0};
-    k_sample_sort<<<unsigned(blocks), kWarps * 32, smem, s>>>(scd, dtd, htd, d, planes, n, queries, feats, ops,
-                                                              mms, err);
+    k_sample_sort<<<unsigned(blocks), kWarps * 32, smem, s>>>(scd, dtd, htd, d,
+                                                              reinterpret_cast<const float2*>(planes), pre, n,
+                                                              queries, feats, ops, mms, err);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }

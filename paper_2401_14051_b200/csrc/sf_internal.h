@@ -106,8 +106,10 @@ struct sf_scene {
     const sf_phase_table* table = nullptr;
     double template_scale = 1.0;
     float2* d_dt = nullptr;  // interleaved {density, transmittance} level-0 volume
-    float* d_planes = nullptr;  // phase table pre-blended at each lobe's g [n_planes][A][H]
+    float* d_planes = nullptr;  // phase table pre-blended at each lobe's g, [n_planes][A][H] float2 pairs
     int n_planes = 0;
+    float4* d_dt4 = nullptr;    // x-pair records of the {density, transmittance} volume
+    float2* d_pre = nullptr;    // per diffuse point {half angle, light-side cap integral}
 };
 
 // ---- launchers (defined in the .cu files) --------------------------------------
@@ -135,6 +137,7 @@ void launch_place_template(const sf_template& t, int64_t n, const double* p,
 struct SceneDev {
     GridDev grid;          // density geometry (v = density)
     const float2* dt;      // interleaved {density, tvol}
+    const float4* dt4;     // x-pair records {rho(x), T(x), rho(x+1), T(x+1)} (fused path)
     const float* tvol;     // plain tvol (when dt == nullptr)
     PhaseDev phase;
     double template_scale;
@@ -189,9 +192,14 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
 // Fused feature sampling + per-layer sort/pool + bf16 operand packing (K5+K6).
 // Samples the scene when `feats` is null, else sorts the given feature rows.
 void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht,
-                        const float* planes, int n_planes, const SortLayout& L, int64_t n,
-                        const double* queries, const float* feats, uint8_t* ops, float* mms,
+                        const float* planes, int n_planes, const float2* pre, const SortLayout& L,
+                        int64_t n, const double* queries, const float* feats, uint8_t* ops, float* mms,
                         int* err, cudaStream_t s);
+// Light-side phase of every diffuse point for the light of query 0 (diffuse
+// placement is a pure translation, so axis and aperture do not depend on p).
+void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float* planes, int n_planes,
+                          const double* queries, float2* pre, cudaStream_t s);
+void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStream_t s);
 // Pre-blended phase planes: for each lobe, the table interpolated at that lobe's g
 // (PhaseTable::lookup_hg's g axis, src/phase.cpp:191-219), [n_lobes][angle][aperture].
 void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float* planes,
