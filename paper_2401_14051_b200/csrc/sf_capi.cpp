@@ -948,7 +948,7 @@ int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_templa
         try {
             SFB_CUDA(cudaMalloc(&s->d_dt, density->count() * sizeof(float2)));
             SFB_CUDA(cudaMalloc(&s->d_dt4, density->count() * sizeof(float4)));
-            SFB_CUDA(cudaMalloc(&s->d_planes, size_t(s->n_planes) * table->a * table->h * sizeof(float2)));
+            SFB_CUDA(cudaMalloc(&s->d_planes, size_t(s->n_planes) * table->a * (table->h + 1) * sizeof(float2)));
             SFB_CUDA(cudaMalloc(&s->d_pre, std::max<size_t>(1, size_t(dt->total)) * sizeof(float2)));
             sfb::launch_interleave(density->d, tv.d, s->d_dt, density->count(), nullptr);
             sfb::launch_xpair(s->d_dt, density->nx, density->ny, density->nz, s->d_dt4, nullptr);

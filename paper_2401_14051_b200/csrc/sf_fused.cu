@@ -59,8 +59,8 @@ __device__ __forceinline__ float plane_lookup(const float2* pl, int A, int H, fl
     float v = fminf(fmaxf(half, 0.0f), float(kPi)) * (float(H - 1) / float(kPi));
     int j0 = min(int(v), H - 2);
     float s = v - float(j0);
-    const float2 r0 = pl[i0 * H + j0];
-    const float2 r1 = pl[(i0 + 1) * H + j0];
+    const float2 r0 = pl[i0 * (H + 1) + j0];  // rows padded to H+1 pairs: no bank aliasing
+    const float2 r1 = pl[(i0 + 1) * (H + 1) + j0];
     float a = fmaf(s, r0.y - r0.x, r0.x);
     float b = fmaf(s, r1.y - r1.x, r1.x);
     return fmaf(t, b - a, a);
@@ -69,7 +69,7 @@ __device__ __forceinline__ float plane_lookup(const float2* pl, int A, int H, fl
 __device__ __forceinline__ float cap_phase(const float2* planes, int n_planes, const float* w, int A, int H,
                                            float angle, float half) {
     float f = 0.0f;
-    for (int k = 0; k < n_planes; ++k) f = fmaf(w[k], plane_lookup(planes + k * A * H, A, H, angle, half), f);
+    for (int k = 0; k < n_planes; ++k) f = fmaf(w[k], plane_lookup(planes + k * A * (H + 1), A, H, angle, half), f);
     return f;
 }
 
@@ -295,9 +295,25 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
                   const float2* __restrict__ pre, int64_t n, const double* __restrict__ queries,
                   const float* __restrict__ feats, uint8_t* __restrict__ ops, float* __restrict__ mms, int* err) {
     extern __shared__ __align__(16) float sm[];
-    const int plane_floats = 2 * d.n_planes * d.A * d.H;
+    const int plane_floats = 2 * d.n_planes * d.A * (d.H + 1);
     float2* planes = reinterpret_cast<float2*>(sm);
     for (int i = threadIdx.x; i < plane_floats / 2; i += blockDim.x) planes[i] = planes_g[i];
+    // segment / chunk tables in shared memory (lane-divergent indices would serialize
+    // constant-bank loads)
+    __shared__ int s_scr[kMaxSegs], s_n[kMaxSegs], s_kf[kMaxSegs];
+    __shared__ int64_t s_prefix[kMaxSegs];
+    __shared__ uint8_t s_cseg[kMaxChunks], s_cj[kMaxChunks], s_task[kMaxSegs];
+    for (int i = threadIdx.x; i < d.n_segs; i += blockDim.x) {
+        s_scr[i] = d.seg_scr[i];
+        s_n[i] = d.seg_n[i];
+        s_kf[i] = d.seg_kf[i];
+        s_prefix[i] = d.seg_prefix[i];
+        s_task[i] = d.task_seg[i];
+    }
+    for (int i = threadIdx.x; i < d.n_chunks; i += blockDim.x) {
+        s_cseg[i] = d.chunk_seg[i];
+        s_cj[i] = d.chunk_j[i];
+    }
     // light of query 0: diffuse light sides in `pre` are valid for queries with that light
     double l_ref[3] = {0, 0, 0};
     if (queries != nullptr && n > 0)
@@ -341,9 +357,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
         __syncthreads();
         // ---- phase 2: per-(query, segment) register sorts + pools
         for (int t = threadIdx.x; t < d.n_segs * kWarps; t += blockDim.x) {
-            const int s = d.task_seg[t / kWarps], w = t % kWarps;
-            float* seg = scr_all + w * d.scr_floats + d.seg_scr[s];
-            const int cnt = d.seg_n[s];
+            const int s = s_task[t / kWarps], w = t % kWarps;
+            float* seg = scr_all + w * d.scr_floats + s_scr[s];
+            const int cnt = s_n[s];
             float mean, mx;
             if (cnt <= 8)
                 sort_segment<8>(seg, cnt, mean, mx);
@@ -362,17 +378,17 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
         const int row0 = int(q0 % kUmmaM);
         for (int t = threadIdx.x; t < d.n_chunks * kWarps; t += blockDim.x) {
             const int c = t / kWarps, w = t % kWarps;
-            const int s = d.chunk_seg[c], j = d.chunk_j[c];
-            const float* seg = scr_all + w * d.scr_floats + d.seg_scr[s];
+            const int s = s_cseg[c], j = s_cj[c];
+            const float* seg = scr_all + w * d.scr_floats + s_scr[s];
             const float* pl = pools + (w * d.n_segs + s) * 2;
-            const int cnt = d.seg_n[s], kf = d.seg_kf[s];
+            const int cnt = s_n[s], kf = s_kf[s];
             float v8[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 const int idx = 8 * j + e;
                 v8[e] = idx < cnt ? seg[idx] : (idx == cnt ? pl[0] : (idx == cnt + 1 ? pl[1] : 0.0f));
             }
-            uint8_t* blk = ops + d.seg_prefix[s] * d.n_tiles + tile * (int64_t(kUmmaM) * kf * 2);
+            uint8_t* blk = ops + s_prefix[s] * d.n_tiles + tile * (int64_t(kUmmaM) * kf * 2);
             store_chunk(blk, row0 + w, j, kf, v8);
         }
         for (int t = threadIdx.x; t < d.n_layers * kWarps; t += blockDim.x) {
@@ -390,7 +406,7 @@ __global__ void k_blend_planes(const float* __restrict__ T, int G, int A, int H,
                                double g2, float2* __restrict__ out) {
     const int total = n_planes * A * H;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-        const int k = idx / (A * H), ah = idx % (A * H), h = ah % H;
+        const int k = idx / (A * H), ah = idx % (A * H), h = ah % H, a = ah / H;
         const double g = k == 0 ? g0 : (k == 1 ? g1 : g2);
         int gi;
         double gt;
@@ -400,7 +416,7 @@ __global__ void k_blend_planes(const float* __restrict__ T, int G, int A, int H,
         const int dh = h + 1 < H ? 1 : 0;
         const float v0 = float((1.0 - gt) * double(t0[0]) + gt * double(t1[0]));
         const float v1 = float((1.0 - gt) * double(t0[dh]) + gt * double(t1[dh]));
-        out[idx] = make_float2(v0, v1);
+        out[(k * A + a) * (H + 1) + h] = make_float2(v0, v1);
     }
 }
 
@@ -488,7 +504,7 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
                         const float* feats, uint8_t* ops, float* mms, int* err, cudaStream_t s) {
     if (n <= 0) return;
     SortDesc d = make_desc(sc, n_planes, L, n);
-    const size_t smem = size_t(2 * d.n_planes * d.A * d.H + kWarps * d.scr_floats + kWarps * d.n_segs * 2 + 2) *
+    const size_t smem = size_t(2 * d.n_planes * d.A * (d.H + 1) + kWarps * d.scr_floats + kWarps * d.n_segs * 2 + 2) *
                         sizeof(float);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
