@@ -758,7 +758,13 @@ int sf_template_create(int kind, int n_layers, const int* counts, const double* 
         size_t np = std::max<size_t>(1, size_t(t->total));
         SFB_CUDA(cudaMalloc(&t->d_points, np * 3 * sizeof(double)));
         SFB_CUDA(cudaMalloc(&t->d_caps, np * sizeof(double)));
+        SFB_CUDA(cudaMalloc(&t->d_pts4, np * sizeof(float4)));
         if (t->total) {
+            std::vector<float4> p4(size_t(t->total));
+            for (int i = 0; i < t->total; ++i)
+                p4[size_t(i)] = make_float4(float(t->points[3 * size_t(i)]), float(t->points[3 * size_t(i) + 1]),
+                                            float(t->points[3 * size_t(i) + 2]), float(pc[size_t(i)]));
+            SFB_CUDA(cudaMemcpy(t->d_pts4, p4.data(), p4.size() * sizeof(float4), cudaMemcpyHostToDevice));
             SFB_CUDA(cudaMemcpy(t->d_points, t->points.data(), t->points.size() * sizeof(double),
                                 cudaMemcpyHostToDevice));
             SFB_CUDA(cudaMemcpy(t->d_caps, pc.data(), pc.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -793,6 +799,7 @@ void sf_template_destroy(sf_template* t) {
     if (!t) return;
     cudaFree(t->d_points);
     cudaFree(t->d_caps);
+    cudaFree(t->d_pts4);
     delete t;
 }
 
@@ -873,7 +880,7 @@ void check_precision(const sf_backbone& b, int precision, cudaStream_t s) {
 // bf16 path over one chunk: fused sample+sort (or sort of given features) -> tcgen05 backbone.
 void run_bf16_chunk(const sf_backbone& b, const sfb::SortLayout& L, const sfb::SceneDev* sc,
                     const sfb::TemplateDev* dt, const sfb::TemplateDev* ht, const float* planes, int n_planes,
-                    const float2* pre, int64_t m, const double* queries, const float* feats, const double* cfg8,
+                    const float4* pre, int64_t m, const double* queries, const float* feats, const double* cfg8,
                     uint8_t* ops, float* mms, int* err, float* y, double* F, cudaStream_t s) {
     {
         StageScope st(SF_STAGE_SAMPLE_SORT, s);
@@ -949,7 +956,7 @@ int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_templa
             SFB_CUDA(cudaMalloc(&s->d_dt, density->count() * sizeof(float2)));
             SFB_CUDA(cudaMalloc(&s->d_dt4, density->count() * sizeof(float4)));
             SFB_CUDA(cudaMalloc(&s->d_planes, size_t(s->n_planes) * table->a * (table->h + 1) * sizeof(float2)));
-            SFB_CUDA(cudaMalloc(&s->d_pre, std::max<size_t>(1, size_t(dt->total)) * sizeof(float2)));
+            SFB_CUDA(cudaMalloc(&s->d_pre, std::max<size_t>(1, size_t(dt->total)) * 2 * sizeof(float4)));
             sfb::launch_interleave(density->d, tv.d, s->d_dt, density->count(), nullptr);
             sfb::launch_xpair(s->d_dt, density->nx, density->ny, density->nz, s->d_dt4, nullptr);
             sfb::launch_blend_planes(*table, *model, s->d_planes, nullptr);

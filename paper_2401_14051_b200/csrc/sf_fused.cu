@@ -2,23 +2,30 @@
 // the 266 template features, sort/pool every (layer, feature type) and emit the
 // tensor-core operands directly (K5 + K6 fused; features never reach HBM).
 //
-// One warp per query. Lanes evaluate template points (density + transmittance
-// from the interleaved float2 volume, the Eq. 8 phase feature from pre-blended
-// phase planes held in shared memory), the warp then sorts each layer segment
-// descending with a 64-wide bitonic network over shuffles, sums it in sorted order
-// (one lane per segment, so mean = sequential float sum / n exactly as
-// src/predictor.cpp:176-185), and writes
-//   * the bf16 FC-1 feature operand rows [sorted_tau, mean_tau, max_tau, 0...] of
-//     every (kind, layer, tau) straight into the UMMA canonical layout of its
-//     128-query tile, and
-//   * the fp32 {mean, max} x 3 types row of every (kind, layer) for the attention.
+// Block = 8 consecutive queries (one 8-row group of a 128-row UMMA tile):
+//  phase 1  warp w samples the template points of query q0 + w, point-parallel so a
+//           warp's gathers stay inside one template footprint. Density and
+//           transmittance come from x-pair records {rho, T}(x0), {rho, T}(x0 + 1)
+//           (one 16-byte load per (y, z) corner row); the Eq. 8 phase feature from
+//           phase planes pre-blended at each lobe's g, held in shared memory.
+//  phase 2  thread-per-(query, segment) register bitonic sorts (a 48-point layer is
+//           split over a lane pair), sequential float sum in sorted order
+//           (src/predictor.cpp:176-185) and max;
+//  phase 3  every 16-byte chunk of the bf16 FC-1 feature operand rows
+//           [sorted_tau, mean_tau, max_tau, 0...] goes straight into the UMMA
+//           canonical layout (the 8 rows of a chunk are 128 contiguous bytes), plus
+//           the fp32 {mean, max} x 3 types row of every (kind, layer) for attention.
 //
 // Numerics (bf16 production path only; the FP32 parity path keeps the exact
-// kernels of sf_query.cu): positions, voxel coordinates and cell selection in
-// FP64 as the reference, interpolation weights and lerps in FP32, phase angles and
-// the phase-table bilinear in FP32 (survey: <= 3.2e-6 relative), all far inside
-// the bf16 rounding (3.9e-3) the operands undergo.
+// kernels of sf_query.cu): the query base point and highlight entry are placed in
+// voxel space in FP64 and split into an integer cell plus an FP32 fraction; template
+// offsets, interpolation weights, lerps, phase angles and the phase bilinear are
+// FP32 (relative errors ~1e-6, far inside the 3.9e-3 bf16 rounding the operands
+// then undergo). Diffuse placement is a pure translation, so each diffuse point's
+// voxel offset, unit axis, aperture and light-side cap integral are per-scene
+// constants (k_diffuse_prep).
 #include <algorithm>
+#include <cstdlib>
 
 #include "sf_internal.h"
 #include "sf_umma.cuh"
@@ -33,25 +40,24 @@ constexpr int kMaxChunks = 512;
 
 struct SortDesc {
     int npts0, ntot;
-    int n_segs, n_layers, n_chunks;
+    int n_segs, n_layers, n_chunks, n_tasks;
     int n_tiles;
     int64_t feat_stride;
     int A, H, n_planes;
     float w[3];
     int scr_floats;
-    // per segment (kind, layer, tau)
-    int seg_scr[kMaxSegs];  // offset of the segment in the warp scratch
+    int seg_scr[kMaxSegs];  // offset of the segment in the query scratch row
     int seg_n[kMaxSegs];
     int seg_kf[kMaxSegs];
     int64_t seg_prefix[kMaxSegs];
-    // per output chunk (16 B = 8 bf16 of one row)
     uint8_t chunk_seg[kMaxChunks];
     uint8_t chunk_j[kMaxChunks];
-    uint8_t task_seg[kMaxSegs];  // segments ordered by sorting-network size
+    uint8_t task_seg[2 * kMaxSegs];  // sort tasks by network size; bit 7 = upper half of a 64-wide pair
+    int debug;                       // SF_DEBUG_SAMPLE_SORT: 1 skip sampling, 2 skip sort, 4 skip stores
 };
 
 // Bilinear lookup in a pre-blended phase plane stored as aperture pairs
-// pl[a][h] = {P(a,h), P(a,h+1)}: two 8-byte shared loads per lookup.
+// pl[a][h] = {P(a,h), P(a,h+1)}, rows padded to H+1 pairs (no bank aliasing).
 __device__ __forceinline__ float plane_lookup(const float2* pl, int A, int H, float angle, float half) {
     float u = fminf(fmaxf(angle, 0.0f), float(kPi)) * (float(A - 1) / float(kPi));
     int i0 = min(int(u), A - 2);
@@ -59,173 +65,196 @@ __device__ __forceinline__ float plane_lookup(const float2* pl, int A, int H, fl
     float v = fminf(fmaxf(half, 0.0f), float(kPi)) * (float(H - 1) / float(kPi));
     int j0 = min(int(v), H - 2);
     float s = v - float(j0);
-    const float2 r0 = pl[i0 * (H + 1) + j0];  // rows padded to H+1 pairs: no bank aliasing
+    const float2 r0 = pl[i0 * (H + 1) + j0];
     const float2 r1 = pl[(i0 + 1) * (H + 1) + j0];
     float a = fmaf(s, r0.y - r0.x, r0.x);
     float b = fmaf(s, r1.y - r1.x, r1.x);
     return fmaf(t, b - a, a);
 }
 
-__device__ __forceinline__ float cap_phase(const float2* planes, int n_planes, const float* w, int A, int H,
-                                           float angle, float half) {
+// PhaseTable::lookup (src/phase.cpp:221-230) on the pre-blended planes.
+__device__ __forceinline__ float cap_phase(const float2* planes, const SortDesc& d, float cosine, float half) {
+    const float angle = acosf(fminf(fmaxf(cosine, -1.0f), 1.0f));
     float f = 0.0f;
-    for (int k = 0; k < n_planes; ++k) f = fmaf(w[k], plane_lookup(planes + k * A * (H + 1), A, H, angle, half), f);
+    for (int k = 0; k < d.n_planes; ++k)
+        f = fmaf(d.w[k], plane_lookup(planes + k * d.A * (d.H + 1), d.A, d.H, angle, half), f);
     return f;
 }
 
+// voxel-space coordinate (s - o)/vs - 0.5 split into an integer cell base and an FP32 fraction
+__device__ __forceinline__ void voxel_split(const GridDev& g, const double* s, int* base, float* frac) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double o = c == 0 ? g.ox : (c == 1 ? g.oy : g.oz);
+        const double f = g.ivs != 0.0 ? (s[c] - o) * g.ivs - 0.5 : (s[c] - o) / g.vs - 0.5;
+        const double fl = floor(f);
+        base[c] = int(fl);
+        frac[c] = float(f - fl);
+    }
+}
+
 struct QueryCtx {
-    double p[3], entry[3], axis[3], t[3], b[3];
-    double hscale;
-    float wf[3], lf[3];
-    float ww, ll;
+    int pb[3];               // query base cell
+    float pf[3];             // query base fraction
+    int eb[3];               // highlight entry cell
+    float ef[3];             // highlight entry fraction
+    float dpe[3];            // (entry - p) in voxels
+    float t[3], b[3], a[3];  // highlight frame
+    float hs;                // highlight scale in voxels per template unit
+    float wf[3], iw;         // omega and 1/|omega|
+    float lf[3], il;         // light and 1/|light|
     bool ok;
 };
 
 __device__ __forceinline__ void query_ctx(const SceneDev& sc, const TemplateDev& ht, const double* c, QueryCtx& q) {
     const double p[3] = {c[0], c[1], c[2]}, omega[3] = {c[3], c[4], c[5]}, light[3] = {c[6], c[7], c[8]};
+    const GridDev& g = sc.grid;
+    voxel_split(g, p, q.pb, q.pf);
     for (int i = 0; i < 3; ++i) {
-        q.p[i] = p[i];
         q.wf[i] = float(omega[i]);
         q.lf[i] = float(light[i]);
     }
-    q.ww = q.wf[0] * q.wf[0] + q.wf[1] * q.wf[1] + q.wf[2] * q.wf[2];
-    q.ll = q.lf[0] * q.lf[0] + q.lf[1] * q.lf[1] + q.lf[2] * q.lf[2];
+    q.iw = rsqrtf(q.wf[0] * q.wf[0] + q.wf[1] * q.wf[1] + q.wf[2] * q.wf[2]);
+    q.il = rsqrtf(q.lf[0] * q.lf[0] + q.lf[1] * q.lf[1] + q.lf[2] * q.lf[2]);
     // light entry + highlight frame (src/feature_pipeline.cpp:130-137, src/templates.cpp:220-239)
-    const double lo[3] = {sc.grid.ox, sc.grid.oy, sc.grid.oz};
-    const double hi[3] = {sc.grid.hx, sc.grid.hy, sc.grid.hz};
-    light_entry(lo, hi, p, light, q.entry);
-    double span[3] = {p[0] - q.entry[0], p[1] - q.entry[1], p[2] - q.entry[2]};
-    double len = sqrt(dot3(span, span));
+    const double lo[3] = {g.ox, g.oy, g.oz}, hi[3] = {g.hx, g.hy, g.hz};
+    double entry[3];
+    light_entry(lo, hi, p, light, entry);
+    voxel_split(g, entry, q.eb, q.ef);
+    double span[3] = {p[0] - entry[0], p[1] - entry[1], p[2] - entry[2]};
+    const double len = sqrt(dot3(span, span));
     q.ok = len > 0.0;
-    double il = 1.0 / len;
-    for (int i = 0; i < 3; ++i) q.axis[i] = span[i] * il;
-    double od = dot3(omega, q.axis);
-    double t[3] = {omega[0] - q.axis[0] * od, omega[1] - q.axis[1] * od, omega[2] - q.axis[2] * od};
-    double tl = sqrt(dot3(t, t));
+    const double il = 1.0 / len;
+    double axis[3] = {span[0] * il, span[1] * il, span[2] * il};
+    const double od = dot3(omega, axis);
+    double t[3] = {omega[0] - axis[0] * od, omega[1] - axis[1] * od, omega[2] - axis[2] * od};
+    const double tl = sqrt(dot3(t, t));
+    double b[3];
     if (tl > 1e-9) {
-        double it = 1.0 / tl;
-        for (int i = 0; i < 3; ++i) q.t[i] = t[i] * it;
-        q.b[0] = q.axis[1] * q.t[2] - q.axis[2] * q.t[1];
-        q.b[1] = q.axis[2] * q.t[0] - q.axis[0] * q.t[2];
-        q.b[2] = q.axis[0] * q.t[1] - q.axis[1] * q.t[0];
+        const double it = 1.0 / tl;
+        for (int i = 0; i < 3; ++i) t[i] *= it;
+        b[0] = axis[1] * t[2] - axis[2] * t[1];
+        b[1] = axis[2] * t[0] - axis[0] * t[2];
+        b[2] = axis[0] * t[1] - axis[1] * t[0];
     } else {
-        orthonormal_basis(q.axis, q.t, q.b);
+        orthonormal_basis(axis, t, b);
     }
-    q.hscale = len / ht.gen_distance;
+    const double ivs = g.ivs != 0.0 ? g.ivs : 1.0 / g.vs;
+    for (int i = 0; i < 3; ++i) {
+        q.t[i] = float(t[i]);
+        q.b[i] = float(b[i]);
+        q.a[i] = float(axis[i]);
+        q.dpe[i] = float(q.eb[i] - q.pb[i]) + (q.ef[i] - q.pf[i]);
+    }
+    q.hs = float(len / ht.gen_distance * ivs);
 }
 
-// density, transmittance and phase feature of template point i (0..ntot)
-__device__ __forceinline__ void point_features(const SceneDev& sc, const TemplateDev& dt, const TemplateDev& ht,
-                                               const QueryCtx& q, int i, int npts0, const float2* planes,
-                                               const float2* pre, bool use_pre, const SortDesc& d, float& rho,
-                                               float& tr, float& ph) {
-    double s[3];
-    double cap;
-    if (i < npts0) {
-        const double* qq = dt.pts + 3 * i;
-        for (int c = 0; c < 3; ++c) s[c] = q.p[c] + qq[c] * sc.template_scale;
-        cap = dt.caps[i] * sc.template_scale;
-    } else {
-        const int li = i - npts0;
-        const double* qq = ht.pts + 3 * li;
-        for (int c = 0; c < 3; ++c) {
-            double v = q.t[c] * qq[0] + q.b[c] * qq[1];
-            v = v + q.axis[c] * qq[2];
-            s[c] = q.entry[c] + v * q.hscale;
-        }
-        cap = ht.caps[li] * q.hscale;
-    }
+// {density, transmittance} at voxel coordinate base + frac: 0 / 1 outside the box
+// (sample_trilinear + TransmittanceFeatureVolume::sample), else trilinear over
+// x-pair records with the clamp-to-edge cell of src/volume_grid.cpp:45-56.
+__device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, const float* f, float& rho,
+                                          float& tr) {
     const GridDev& g = sc.grid;
-    if (!in_box(g, s[0], s[1], s[2])) {
+    const int n[3] = {g.nx, g.ny, g.nz};
+    bool inside = true;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        inside &= (f[c] >= -0.5f - float(base[c])) && (f[c] <= float(n[c] - base[c]) - 0.5f);
+    if (!inside) {
         rho = 0.0f;
         tr = 1.0f;
-    } else {
-        // FP64 cell selection exactly as sample_trilinear; FP32 weights and lerps.
-        // x-pair records hold {rho, T} at x0 and clamp(x0 + 1): one 16-byte load per
-        // (y, z) corner row; a cell clamped at the low x edge has tx forced to 0.
-        double fx, fy, fz;
-        if (g.ivs != 0.0) {
-            fx = (s[0] - g.ox) * g.ivs - 0.5;
-            fy = (s[1] - g.oy) * g.ivs - 0.5;
-            fz = (s[2] - g.oz) * g.ivs - 0.5;
-        } else {
-            fx = (s[0] - g.ox) / g.vs - 0.5;
-            fy = (s[1] - g.oy) / g.vs - 0.5;
-            fz = (s[2] - g.oz) / g.vs - 0.5;
-        }
-        const double flx = floor(fx), fly = floor(fy), flz = floor(fz);
-        int x0 = int(flx), y0 = int(fly), z0 = int(flz);
-        float tx = float(fx - flx), ty = float(fy - fly), tz = float(fz - flz);
-        if (x0 < 0) tx = 0.0f;
-        const int y1 = clampi(y0 + 1, 0, g.ny - 1), z1 = clampi(z0 + 1, 0, g.nz - 1);
-        x0 = clampi(x0, 0, g.nx - 1);
-        y0 = clampi(y0, 0, g.ny - 1);
-        z0 = clampi(z0, 0, g.nz - 1);
-        const size_t sy = size_t(g.nx), sz = size_t(g.nx) * g.ny;
-        const float4* v = sc.dt4 + x0;
-        const float4 r00 = __ldg(v + z0 * sz + y0 * sy), r10 = __ldg(v + z0 * sz + y1 * sy);
-        const float4 r01 = __ldg(v + z1 * sz + y0 * sy), r11 = __ldg(v + z1 * sz + y1 * sy);
-        float c00 = fmaf(tx, r00.z - r00.x, r00.x), c10 = fmaf(tx, r10.z - r10.x, r10.x);
-        float c01 = fmaf(tx, r01.z - r01.x, r01.x), c11 = fmaf(tx, r11.z - r11.x, r11.x);
-        float e0 = fmaf(ty, c10 - c00, c00), e1 = fmaf(ty, c11 - c01, c01);
-        rho = fmaf(tz, e1 - e0, e0);
-        c00 = fmaf(tx, r00.w - r00.y, r00.y);
-        c10 = fmaf(tx, r10.w - r10.y, r10.y);
-        c01 = fmaf(tx, r01.w - r01.y, r01.y);
-        c11 = fmaf(tx, r11.w - r11.y, r11.y);
-        e0 = fmaf(ty, c10 - c00, c00);
-        e1 = fmaf(ty, c11 - c01, c01);
-        tr = fmaf(tz, e1 - e0, e0);
+        return;
     }
-    const float dx = float(s[0] - q.p[0]), dy = float(s[1] - q.p[1]), dz = float(s[2] - q.p[2]);
+    int i0[3];
+    float t[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float fl = floorf(f[c]);
+        i0[c] = base[c] + int(fl);
+        t[c] = f[c] - fl;
+    }
+    if (i0[0] < 0) t[0] = 0.0f;
+    const int y1 = clampi(i0[1] + 1, 0, g.ny - 1), z1 = clampi(i0[2] + 1, 0, g.nz - 1);
+    const int x0 = clampi(i0[0], 0, g.nx - 1), y0 = clampi(i0[1], 0, g.ny - 1), z0 = clampi(i0[2], 0, g.nz - 1);
+    const size_t sy = size_t(g.nx), sz = size_t(g.nx) * g.ny;
+    const float4* v = sc.dt4 + x0;
+    const float4 r00 = __ldg(v + z0 * sz + y0 * sy), r10 = __ldg(v + z0 * sz + y1 * sy);
+    const float4 r01 = __ldg(v + z1 * sz + y0 * sy), r11 = __ldg(v + z1 * sz + y1 * sy);
+    float c00 = fmaf(t[0], r00.z - r00.x, r00.x), c10 = fmaf(t[0], r10.z - r10.x, r10.x);
+    float c01 = fmaf(t[0], r01.z - r01.x, r01.x), c11 = fmaf(t[0], r11.z - r11.x, r11.x);
+    float e0 = fmaf(t[1], c10 - c00, c00), e1 = fmaf(t[1], c11 - c01, c01);
+    rho = fmaf(t[2], e1 - e0, e0);
+    c00 = fmaf(t[0], r00.w - r00.y, r00.y);
+    c10 = fmaf(t[0], r10.w - r10.y, r10.y);
+    c01 = fmaf(t[0], r01.w - r01.y, r01.y);
+    c11 = fmaf(t[0], r11.w - r11.y, r11.y);
+    e0 = fmaf(t[1], c10 - c00, c00);
+    e1 = fmaf(t[1], c11 - c01, c01);
+    tr = fmaf(t[2], e1 - e0, e0);
+}
+
+// Features of template point i (diffuse 0..npts0-1, then highlight).
+__device__ __forceinline__ void point_features(const SceneDev& sc, const TemplateDev& ht, const QueryCtx& q, int i,
+                                               const SortDesc& d, const float2* planes, const float4* __restrict__ pre,
+                                               bool same_light, float& rho, float& tr, float& ph) {
+    if (i < d.npts0) {
+        const float4 p0 = __ldg(pre + 2 * i), p1 = __ldg(pre + 2 * i + 1);  // {offset, half}, {axis, light side}
+        const float f[3] = {q.pf[0] + p0.x, q.pf[1] + p0.y, q.pf[2] + p0.z};
+        sample_rt(sc, q.pb, f, rho, tr);
+        if (p0.w < 0.0f) {
+            ph = 1.0f;  // diffuse centre point (src/feature_pipeline.cpp:163-164)
+            return;
+        }
+        const float fw = cap_phase(planes, d, (q.wf[0] * p1.x + q.wf[1] * p1.y + q.wf[2] * p1.z) * q.iw, p0.w);
+        const float fl = same_light
+                             ? p1.w
+                             : cap_phase(planes, d, (q.lf[0] * p1.x + q.lf[1] * p1.y + q.lf[2] * p1.z) * q.il, p0.w);
+        ph = fw * fl;
+        return;
+    }
+    const float4 tq = __ldg(ht.pts4 + (i - d.npts0));  // {x, y, z, cap}
+    float h[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) h[c] = fmaf(q.a[c], tq.z, fmaf(q.b[c], tq.y, q.t[c] * tq.x)) * q.hs;
+    const float f[3] = {q.ef[0] + h[0], q.ef[1] + h[1], q.ef[2] + h[2]};
+    sample_rt(sc, q.eb, f, rho, tr);
+    const float dx = q.dpe[0] + h[0], dy = q.dpe[1] + h[1], dz = q.dpe[2] + h[2];
     const float dd = dx * dx + dy * dy + dz * dz;
     if (dd <= 0.0f) {
-        ph = 1.0f;  // diffuse centre point (src/feature_pipeline.cpp:163-164)
+        ph = 1.0f;
         return;
     }
     const float inv = rsqrtf(dd);
+    const float r = tq.w * q.hs * inv;  // cap / dist, both in voxels
+    const float half = r >= 1.0f ? float(kPi) : asinf(r);
     const float ax = dx * inv, ay = dy * inv, az = dz * inv;
-    const float aa = ax * ax + ay * ay + az * az;
-    const float cw = (q.wf[0] * ax + q.wf[1] * ay + q.wf[2] * az) * rsqrtf(q.ww * aa);
-    const float aw = acosf(fminf(fmaxf(cw, -1.0f), 1.0f));
-    float half, fl;
-    if (use_pre && i < npts0) {
-        const float2 pr = pre[i];  // translation-invariant diffuse aperture and light side
-        half = pr.x;
-        fl = pr.y;
-    } else {
-        const float capf = float(cap), dist = dd * inv;
-        half = capf >= dist ? float(kPi) : asinf(capf / dist);
-        const float cl = (q.lf[0] * ax + q.lf[1] * ay + q.lf[2] * az) * rsqrtf(q.ll * aa);
-        fl = cap_phase(planes, d.n_planes, d.w, d.A, d.H, acosf(fminf(fmaxf(cl, -1.0f), 1.0f)), half);
-    }
-    ph = cap_phase(planes, d.n_planes, d.w, d.A, d.H, aw, half) * fl;
+    ph = cap_phase(planes, d, (q.wf[0] * ax + q.wf[1] * ay + q.wf[2] * az) * q.iw, half) *
+         cap_phase(planes, d, (q.lf[0] * ax + q.lf[1] * ay + q.lf[2] * az) * q.il, half);
 }
 
-// pre[i] = {half angle, light-side cap integral} of diffuse point i for the light of
-// query 0 (axis = q_i/|q_i| and aperture asin(cap/|q_i ts|) do not depend on p).
-__global__ void k_diffuse_light(SceneDev sc, TemplateDev dt, SortDesc d, const float2* __restrict__ planes,
-                                const double* __restrict__ queries, float2* __restrict__ pre) {
+// Per-scene diffuse constants: pre[2i] = {offset (voxels), half angle or -1 at the
+// centre}, pre[2i+1] = {unit axis, light-side cap integral for the light of query 0}.
+__global__ void k_diffuse_prep(SceneDev sc, TemplateDev dt, SortDesc d, const float2* __restrict__ planes,
+                               const double* __restrict__ queries, float4* __restrict__ pre) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= dt.total) return;
     const double* qq = dt.pts + 3 * i;
     const double ts = sc.template_scale;
-    const float dx = float(qq[0] * ts), dy = float(qq[1] * ts), dz = float(qq[2] * ts);
-    const float dd = dx * dx + dy * dy + dz * dz;
-    if (dd <= 0.0f) {
-        pre[i] = make_float2(float(kPi), 1.0f);
+    const double ivs = sc.grid.ivs != 0.0 ? sc.grid.ivs : 1.0 / sc.grid.vs;
+    const double ox = qq[0] * ts, oy = qq[1] * ts, oz = qq[2] * ts;
+    const double dd = ox * ox + oy * oy + oz * oz;
+    if (dd <= 0.0) {
+        pre[2 * i] = make_float4(0.0f, 0.0f, 0.0f, -1.0f);
+        pre[2 * i + 1] = make_float4(0.0f, 0.0f, 0.0f, 1.0f);
         return;
     }
-    const float inv = rsqrtf(dd), dist = dd * inv;
-    const float ax = dx * inv, ay = dy * inv, az = dz * inv;
-    const float aa = ax * ax + ay * ay + az * az;
-    const float capf = float(dt.caps[i] * ts);
-    const float half = capf >= dist ? float(kPi) : asinf(capf / dist);
+    const double dist = sqrt(dd), cap = dt.caps[i] * ts;
+    const float half = float(cap >= dist ? kPi : asin(cap / dist));
+    const float ax = float(ox / dist), ay = float(oy / dist), az = float(oz / dist);
     const float lx = float(queries[6]), ly = float(queries[7]), lz = float(queries[8]);
-    const float ll = lx * lx + ly * ly + lz * lz;
-    const float cl = (lx * ax + ly * ay + lz * az) * rsqrtf(ll * aa);
-    pre[i] = make_float2(half, cap_phase(planes, d.n_planes, d.w, d.A, d.H,
-                                         acosf(fminf(fmaxf(cl, -1.0f), 1.0f)), half));
+    const float cl = (lx * ax + ly * ay + lz * az) * rsqrtf(lx * lx + ly * ly + lz * lz);
+    pre[2 * i] = make_float4(float(ox * ivs), float(oy * ivs), float(oz * ivs), half);
+    pre[2 * i + 1] = make_float4(ax, ay, az, cap_phase(planes, d, cl, half));
 }
 
 __global__ void k_xpair(const float2* __restrict__ v, int nx, int ny, int nz, float4* __restrict__ out) {
@@ -237,10 +266,9 @@ __global__ void k_xpair(const float2* __restrict__ v, int nx, int ny, int nz, fl
     }
 }
 
-// Descending bitonic network on P (power of two) register values; all indices are
-// compile-time so the segment never leaves registers.
+// Compile-time bitonic sort of P register values, descending if `desc`.
 template <int P>
-__device__ __forceinline__ void bitonic_desc(float* v) {
+__device__ __forceinline__ void bitonic(float* v, bool desc) {
 #pragma unroll
     for (int k = 2; k <= P; k <<= 1) {
 #pragma unroll
@@ -251,7 +279,7 @@ __device__ __forceinline__ void bitonic_desc(float* v) {
                 if (l > i) {
                     const float a = v[i], b = v[l];
                     const float hi = fmaxf(a, b), lo = fminf(a, b);
-                    if ((i & k) == 0) {
+                    if (((i & k) == 0) == desc) {
                         v[i] = hi;
                         v[l] = lo;
                     } else {
@@ -264,14 +292,31 @@ __device__ __forceinline__ void bitonic_desc(float* v) {
     }
 }
 
-// Sort one segment (cnt <= P values at seg) in registers, write it back sorted and
-// return mean (sequential float sum in sorted order / cnt) and max.
+// Descending bitonic merge of a bitonic sequence of P values.
+template <int P>
+__device__ __forceinline__ void merge_desc(float* v) {
+#pragma unroll
+    for (int j = P >> 1; j > 0; j >>= 1) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const int l = i ^ j;
+            if (l > i) {
+                const float a = v[i], b = v[l];
+                v[i] = fmaxf(a, b);
+                v[l] = fminf(a, b);
+            }
+        }
+    }
+}
+
+// One thread sorts a segment of cnt <= P values in place; returns mean (sequential
+// float sum in sorted order / cnt) and max.
 template <int P>
 __device__ __forceinline__ void sort_segment(float* seg, int cnt, float& mean, float& mx) {
     float v[P];
 #pragma unroll
     for (int j = 0; j < P; ++j) v[j] = j < cnt ? seg[j] : -INFINITY;
-    bitonic_desc<P>(v);
+    bitonic<P>(v, true);
     float acc = 0.0f;
 #pragma unroll
     for (int j = 0; j < P; ++j)
@@ -283,65 +328,89 @@ __device__ __forceinline__ void sort_segment(float* seg, int cnt, float& mean, f
     mx = v[0];
 }
 
-// Block = 8 consecutive queries (one 8-row group of a UMMA tile).
-//  phase 1: warp w samples the 266 template points of query q0 + w (point-parallel,
-//           so a warp's gathers stay inside one template's footprint);
-//  phase 2: thread-per-(query, segment) register sorts, tasks ordered by network
-//           size so a warp runs one network;
-//  phase 3: the 8 rows of every 16-byte operand chunk are 128 contiguous bytes of
-//           the canonical layout, so each warp store is fully coalesced.
+// A lane pair sorts a 33..64-value segment: each lane sorts 32 (the upper lane
+// ascending, making the 64 bitonic), one cross-lane compare-exchange, a descending
+// merge per lane; the lower lane's running sum continues on the upper lane, so the
+// sum is exactly sequential in sorted order.
+__device__ __forceinline__ void sort_segment_pair(float* seg, int cnt, bool upper, float& mean, float& mx) {
+    float v[32];
+    const int base = upper ? 32 : 0;
+    const unsigned mask = __activemask();  // pair partners always run this branch together
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = base + j < cnt ? seg[base + j] : -INFINITY;
+    bitonic<32>(v, !upper);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const float o = __shfl_xor_sync(mask, v[j], 1);
+        v[j] = upper ? fminf(v[j], o) : fmaxf(v[j], o);
+    }
+    merge_desc<32>(v);
+    float acc = 0.0f;
+    if (!upper)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc += v[j];
+    acc = __shfl_xor_sync(mask, acc, 1);
+    mx = __shfl_xor_sync(mask, v[0], 1);
+    if (upper) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (32 + j < cnt) acc += v[j];
+        mean = acc / float(cnt);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        if (base + j < cnt) seg[base + j] = v[j];
+}
+
 __global__ void __launch_bounds__(kWarps * 32, 3)
-    k_sample_sort(SceneDev sc, TemplateDev dt, TemplateDev ht, SortDesc d, const float2* __restrict__ planes_g,
-                  const float2* __restrict__ pre, int64_t n, const double* __restrict__ queries,
+    k_sample_sort(SceneDev sc, TemplateDev ht, SortDesc d, const float2* __restrict__ planes_g,
+                  const float4* __restrict__ pre, int64_t n, const double* __restrict__ queries,
                   const float* __restrict__ feats, uint8_t* __restrict__ ops, float* __restrict__ mms, int* err) {
     extern __shared__ __align__(16) float sm[];
     const int plane_floats = 2 * d.n_planes * d.A * (d.H + 1);
     float2* planes = reinterpret_cast<float2*>(sm);
     for (int i = threadIdx.x; i < plane_floats / 2; i += blockDim.x) planes[i] = planes_g[i];
-    // segment / chunk tables in shared memory (lane-divergent indices would serialize
-    // constant-bank loads)
     __shared__ int s_scr[kMaxSegs], s_n[kMaxSegs], s_kf[kMaxSegs];
     __shared__ int64_t s_prefix[kMaxSegs];
-    __shared__ uint8_t s_cseg[kMaxChunks], s_cj[kMaxChunks], s_task[kMaxSegs];
+    __shared__ uint8_t s_cseg[kMaxChunks], s_cj[kMaxChunks], s_task[2 * kMaxSegs];
     for (int i = threadIdx.x; i < d.n_segs; i += blockDim.x) {
         s_scr[i] = d.seg_scr[i];
         s_n[i] = d.seg_n[i];
         s_kf[i] = d.seg_kf[i];
         s_prefix[i] = d.seg_prefix[i];
-        s_task[i] = d.task_seg[i];
     }
+    for (int i = threadIdx.x; i < d.n_tasks; i += blockDim.x) s_task[i] = d.task_seg[i];
     for (int i = threadIdx.x; i < d.n_chunks; i += blockDim.x) {
         s_cseg[i] = d.chunk_seg[i];
         s_cj[i] = d.chunk_j[i];
     }
-    // light of query 0: diffuse light sides in `pre` are valid for queries with that light
-    double l_ref[3] = {0, 0, 0};
+    double l_ref[3] = {0, 0, 0};  // the light `pre` was prepared for (query 0)
     if (queries != nullptr && n > 0)
         for (int c = 0; c < 3; ++c) l_ref[c] = queries[6 + c];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* scr_all = sm + plane_floats;                        // [8][scr_floats]
-    float* pools = scr_all + kWarps * d.scr_floats;            // [8][n_segs][2]
+    float* scr_all = sm + plane_floats;              // [8][scr_floats]
+    float* pools = scr_all + kWarps * d.scr_floats;  // [8][n_segs][2]
     const int64_t q_pad = int64_t(d.n_tiles) * kUmmaM;
     const int64_t n_groups = q_pad / kWarps;
     __syncthreads();
 
     for (int64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
         const int64_t q0 = grp * kWarps;
-        // ---- phase 1: features
+        // ---- phase 1: features of query q0 + warp
         {
             float* scr = scr_all + warp * d.scr_floats;
             const int64_t q = q0 + warp;
-            if (q >= n) {
+            if (q >= n || (d.debug & 1)) {
                 for (int i = lane; i < 3 * d.ntot; i += 32) scr[i] = 0.0f;
             } else if (feats == nullptr) {
                 QueryCtx qc;
                 const double* qr = queries + 9 * q;
                 query_ctx(sc, ht, qr, qc);
                 if (!qc.ok && lane == 0) atomicExch(err, 1);
-                const bool use_pre = pre != nullptr && qr[6] == l_ref[0] && qr[7] == l_ref[1] && qr[8] == l_ref[2];
+                const bool same_light = qr[6] == l_ref[0] && qr[7] == l_ref[1] && qr[8] == l_ref[2];
                 for (int i = lane; i < d.ntot; i += 32) {
                     float rho, tr, ph;
-                    point_features(sc, dt, ht, qc, i, d.npts0, planes, pre, use_pre, d, rho, tr, ph);
+                    point_features(sc, ht, qc, i, d, planes, pre, same_light, rho, tr, ph);
                     scr[i] = rho;
                     scr[d.ntot + i] = tr;
                     scr[2 * d.ntot + i] = ph;
@@ -355,28 +424,40 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
             }
         }
         __syncthreads();
-        // ---- phase 2: per-(query, segment) register sorts + pools
-        for (int t = threadIdx.x; t < d.n_segs * kWarps; t += blockDim.x) {
-            const int s = s_task[t / kWarps], w = t % kWarps;
-            float* seg = scr_all + w * d.scr_floats + s_scr[s];
+        // ---- phase 2: register sorts + pools, tasks ordered by network size
+        for (int t = threadIdx.x; t < ((d.debug & 2) ? 0 : d.n_tasks * kWarps); t += blockDim.x) {
+            const int task = s_task[t / kWarps];
+            const int s = task & 0x7f;
             const int cnt = s_n[s];
-            float mean, mx;
-            if (cnt <= 8)
-                sort_segment<8>(seg, cnt, mean, mx);
-            else if (cnt <= 16)
-                sort_segment<16>(seg, cnt, mean, mx);
-            else if (cnt <= 32)
-                sort_segment<32>(seg, cnt, mean, mx);
-            else
-                sort_segment<64>(seg, cnt, mean, mx);
-            pools[(w * d.n_segs + s) * 2] = mean;
-            pools[(w * d.n_segs + s) * 2 + 1] = mx;
+            float mean = 0.0f, mx = 0.0f;
+            if (cnt > 32) {
+                // a 64-wide segment owns two task slots = 16 threads: (query w, half) = (t%16 / 2, t & 1)
+                const int w = (t % (2 * kWarps)) >> 1;
+                const bool upper = t & 1;
+                float* seg = scr_all + w * d.scr_floats + s_scr[s];
+                sort_segment_pair(seg, cnt, upper, mean, mx);
+                if (upper) {
+                    pools[(w * d.n_segs + s) * 2] = mean;
+                    pools[(w * d.n_segs + s) * 2 + 1] = mx;
+                }
+            } else {
+                const int w = t % kWarps;
+                float* seg = scr_all + w * d.scr_floats + s_scr[s];
+                if (cnt <= 8)
+                    sort_segment<8>(seg, cnt, mean, mx);
+                else if (cnt <= 16)
+                    sort_segment<16>(seg, cnt, mean, mx);
+                else
+                    sort_segment<32>(seg, cnt, mean, mx);
+                pools[(w * d.n_segs + s) * 2] = mean;
+                pools[(w * d.n_segs + s) * 2 + 1] = mx;
+            }
         }
         __syncthreads();
-        // ---- phase 3: outputs
+        // ---- phase 3: operand chunks (8 rows = 128 contiguous bytes) and pools
         const int64_t tile = q0 / kUmmaM;
         const int row0 = int(q0 % kUmmaM);
-        for (int t = threadIdx.x; t < d.n_chunks * kWarps; t += blockDim.x) {
+        for (int t = threadIdx.x; t < ((d.debug & 4) ? 0 : d.n_chunks * kWarps); t += blockDim.x) {
             const int c = t / kWarps, w = t % kWarps;
             const int s = s_cseg[c], j = s_cj[c];
             const float* seg = scr_all + w * d.scr_floats + s_scr[s];
@@ -457,13 +538,21 @@ SortDesc make_desc(const SceneDev* sc, int n_planes, const SortLayout& L, int64_
             }
     d.n_segs = segs;
     d.n_chunks = chunks;
+    // Sort tasks: 64-wide segments first as lane pairs (2 task slots = 16 threads),
+    // then 32/16/8-wide, so each warp runs (mostly) one network size.
     auto net = [](int c) { return c <= 8 ? 8 : c <= 16 ? 16 : c <= 32 ? 32 : 64; };
     int t = 0;
-    for (int p : {64, 32, 16, 8})
+    for (int s2 = 0; s2 < segs; ++s2)
+        if (net(d.seg_n[s2]) == 64) {
+            d.task_seg[t++] = uint8_t(s2);
+            d.task_seg[t++] = uint8_t(s2 | 0x80);
+        }
+    for (int p : {32, 16, 8})
         for (int s2 = 0; s2 < segs; ++s2)
             if (net(d.seg_n[s2]) == p) d.task_seg[t++] = uint8_t(s2);
-    // odd row stride: the 8 query rows of a sort task group hit 8 different banks
-    d.scr_floats = (3 * d.ntot) | 1;
+    d.n_tasks = t;
+    d.scr_floats = (3 * d.ntot) | 1;  // odd row stride: 8 query rows hit 8 banks
+    if (const char* e = std::getenv("SF_DEBUG_SAMPLE_SORT")) d.debug = std::atoi(e);
     return d;
 }
 
@@ -490,22 +579,23 @@ void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStr
 }
 
 void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float* planes, int n_planes,
-                          const double* queries, float2* pre, cudaStream_t s) {
+                          const double* queries, float4* pre, cudaStream_t s) {
     SortLayout L{};
     SortDesc d = make_desc(&sc, n_planes, L, 1);
-    k_diffuse_light<<<(dt.total + 127) / 128, 128, 0, s>>>(sc, dt, d, reinterpret_cast<const float2*>(planes),
-                                                           queries, pre);
+    k_diffuse_prep<<<(dt.total + 127) / 128, 128, 0, s>>>(sc, dt, d, reinterpret_cast<const float2*>(planes),
+                                                          queries, pre);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
 
 void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht, const float* planes,
-                        int n_planes, const float2* pre, const SortLayout& L, int64_t n, const double* queries,
+                        int n_planes, const float4* pre, const SortLayout& L, int64_t n, const double* queries,
                         const float* feats, uint8_t* ops, float* mms, int* err, cudaStream_t s) {
+    (void)dt;  // diffuse placement comes from `pre` (k_diffuse_prep)
     if (n <= 0) return;
     SortDesc d = make_desc(sc, n_planes, L, n);
-    const size_t smem = size_t(2 * d.n_planes * d.A * (d.H + 1) + kWarps * d.scr_floats + kWarps * d.n_segs * 2 + 2) *
-                        sizeof(float);
+    const size_t smem =
+        size_t(2 * d.n_planes * d.A * (d.H + 1) + kWarps * d.scr_floats + kWarps * d.n_segs * 2 + 2) * sizeof(float);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         SFB_CUDA(cudaFuncSetAttribute(k_sample_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -516,11 +606,9 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
     int64_t cap = int64_t(sm_count()) * 3;
     if (blocks > cap) blocks = cap;
     SceneDev scd = sc ? *sc : SceneDev{};
-    TemplateDev dtd = dt ? *dt : TemplateDev{};
-    TemplateDev htd = ht ? *ht : TemplateDev{1, 0, nullptr, nullptr, 1.0};
-    k_sample_sort<<<unsigned(blocks), kWarps * 32, smem, s>>>(scd, dtd, htd, d,
-                                                              reinterpret_cast<const float2*>(planes), pre, n,
-                                                              queries, feats, ops, mms, err);
+    TemplateDev htd = ht ? *ht : TemplateDev{1, 0, nullptr, nullptr, 1.0, nullptr};
+    k_sample_sort<<<unsigned(blocks), kWarps * 32, smem, s>>>(scd, htd, d, reinterpret_cast<const float2*>(planes),
+                                                              pre, n, queries, feats, ops, mms, err);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }

@@ -78,6 +78,7 @@ struct sf_template {
     double gen_distance = 0.0, cone_half_angle = 0.0;
     double* d_points = nullptr;  // [total][3]
     double* d_caps = nullptr;    // [total] per-point layer cap radius (unscaled)
+    float4* d_pts4 = nullptr;    // [total] {x, y, z, cap} as float
 };
 
 // Parameter layout of one stack and of the whole net, in walk_params order
@@ -109,7 +110,7 @@ struct sf_scene {
     float* d_planes = nullptr;  // phase table pre-blended at each lobe's g, [n_planes][A][H] float2 pairs
     int n_planes = 0;
     float4* d_dt4 = nullptr;    // x-pair records of the {density, transmittance} volume
-    float2* d_pre = nullptr;    // per diffuse point {half angle, light-side cap integral}
+    float4* d_pre = nullptr;    // per diffuse point {offset (voxels), half angle}, {unit axis, light side}
 };
 
 // ---- launchers (defined in the .cu files) --------------------------------------
@@ -148,6 +149,7 @@ struct TemplateDev {
     const double* pts;
     const double* caps;
     double gen_distance;
+    const float4* pts4;  // {x, y, z, layer cap radius} in float (fused path)
 };
 SceneDev scene_dev(const sf_grid& density, const sf_grid& tvol, const float2* dt,
                    const sf_phase_model& m, const sf_phase_table& t, double ts);
@@ -192,13 +194,13 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
 // Fused feature sampling + per-layer sort/pool + bf16 operand packing (K5+K6).
 // Samples the scene when `feats` is null, else sorts the given feature rows.
 void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht,
-                        const float* planes, int n_planes, const float2* pre, const SortLayout& L,
+                        const float* planes, int n_planes, const float4* pre, const SortLayout& L,
                         int64_t n, const double* queries, const float* feats, uint8_t* ops, float* mms,
                         int* err, cudaStream_t s);
 // Light-side phase of every diffuse point for the light of query 0 (diffuse
 // placement is a pure translation, so axis and aperture do not depend on p).
 void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float* planes, int n_planes,
-                          const double* queries, float2* pre, cudaStream_t s);
+                          const double* queries, float4* pre, cudaStream_t s);
 void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStream_t s);
 // Pre-blended phase planes: for each lobe, the table interpolated at that lobe's g
 // (PhaseTable::lookup_hg's g axis, src/phase.cpp:191-219), [n_lobes][angle][aperture].

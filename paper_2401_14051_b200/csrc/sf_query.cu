@@ -400,7 +400,7 @@ SceneDev scene_dev(const sf_grid& density, const sf_grid& tvol, const float2* dt
 }
 
 TemplateDev template_dev(const sf_template& t) {
-    return TemplateDev{t.kind, t.total, t.d_points, t.d_caps, t.gen_distance};
+    return TemplateDev{t.kind, t.total, t.d_points, t.d_caps, t.gen_distance, t.d_pts4};
 }
 
 void launch_sample_features(const SceneDev& sc, const TemplateDev& td, int64_t n,
