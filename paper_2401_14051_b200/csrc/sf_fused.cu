@@ -75,6 +75,7 @@ __device__ __forceinline__ float plane_lookup(const float2* pl, int A, int H, fl
 // PhaseTable::lookup (src/phase.cpp:221-230) on the pre-blended planes.
 __device__ __forceinline__ float cap_phase(const float2* planes, const SortDesc& d, float cosine, float half) {
     const float angle = acosf(fminf(fmaxf(cosine, -1.0f), 1.0f));
+    if (d.n_planes == 1) return d.w[0] * plane_lookup(planes, d.A, d.H, angle, half);  // single lobe / isotropic
     float f = 0.0f;
     for (int k = 0; k < d.n_planes; ++k)
         f = fmaf(d.w[k], plane_lookup(planes + k * d.A * (d.H + 1), d.A, d.H, angle, half), f);
@@ -103,8 +104,18 @@ struct QueryCtx {
     float hs;                // highlight scale in voxels per template unit
     float wf[3], iw;         // omega and 1/|omega|
     float lf[3], il;         // light and 1/|light|
+    float pbox[6], ebox[6];  // in-box fraction bounds relative to pb / eb
     bool ok;
 };
+
+__device__ __forceinline__ void box_bounds(const GridDev& g, const int* base, float* box) {
+    const int n[3] = {g.nx, g.ny, g.nz};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        box[2 * c] = -0.5f - float(base[c]);
+        box[2 * c + 1] = float(n[c] - base[c]) - 0.5f;
+    }
+}
 
 __device__ __forceinline__ void query_ctx(const SceneDev& sc, const TemplateDev& ht, const double* c, QueryCtx& q) {
     const double p[3] = {c[0], c[1], c[2]}, omega[3] = {c[3], c[4], c[5]}, light[3] = {c[6], c[7], c[8]};
@@ -147,20 +158,20 @@ __device__ __forceinline__ void query_ctx(const SceneDev& sc, const TemplateDev&
         q.dpe[i] = float(q.eb[i] - q.pb[i]) + (q.ef[i] - q.pf[i]);
     }
     q.hs = float(len / ht.gen_distance * ivs);
+    box_bounds(g, q.pb, q.pbox);
+    box_bounds(g, q.eb, q.ebox);
 }
 
 // {density, transmittance} at voxel coordinate base + frac: 0 / 1 outside the box
 // (sample_trilinear + TransmittanceFeatureVolume::sample), else trilinear over
 // x-pair records with the clamp-to-edge cell of src/volume_grid.cpp:45-56.
-__device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, const float* f, float& rho,
-                                          float& tr) {
+// `box` = per-base {lo, hi} fraction bounds of the closed grid box: inside iff
+// lo_c <= f_c <= hi_c (lo = -0.5 - base, hi = n - 0.5 - base).
+__device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, const float* box, const float* f,
+                                          float& rho, float& tr) {
     const GridDev& g = sc.grid;
-    const int n[3] = {g.nx, g.ny, g.nz};
-    bool inside = true;
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-        inside &= (f[c] >= -0.5f - float(base[c])) && (f[c] <= float(n[c] - base[c]) - 0.5f);
-    if (!inside) {
+    if (!(f[0] >= box[0] && f[0] <= box[1] && f[1] >= box[2] && f[1] <= box[3] && f[2] >= box[4] &&
+          f[2] <= box[5])) {
         rho = 0.0f;
         tr = 1.0f;
         return;
@@ -174,12 +185,14 @@ __device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, c
         t[c] = f[c] - fl;
     }
     if (i0[0] < 0) t[0] = 0.0f;
-    const int y1 = clampi(i0[1] + 1, 0, g.ny - 1), z1 = clampi(i0[2] + 1, 0, g.nz - 1);
-    const int x0 = clampi(i0[0], 0, g.nx - 1), y0 = clampi(i0[1], 0, g.ny - 1), z0 = clampi(i0[2], 0, g.nz - 1);
-    const size_t sy = size_t(g.nx), sz = size_t(g.nx) * g.ny;
-    const float4* v = sc.dt4 + x0;
-    const float4 r00 = __ldg(v + z0 * sz + y0 * sy), r10 = __ldg(v + z0 * sz + y1 * sy);
-    const float4 r01 = __ldg(v + z1 * sz + y0 * sy), r11 = __ldg(v + z1 * sz + y1 * sy);
+    // 32-bit voxel indices (grids up to 2^31 voxels)
+    const int y1 = min(i0[1] + 1, g.ny - 1), z1 = min(i0[2] + 1, g.nz - 1);
+    const int x0 = max(i0[0], 0), y0 = max(i0[1], 0), z0 = max(i0[2], 0);
+    const int sy = g.nx, sz = g.nx * g.ny;
+    const int i00 = z0 * sz + y0 * sy + x0, dy = (max(y1, 0) - y0) * sy, dz = (max(z1, 0) - z0) * sz;
+    const float4* v = sc.dt4;
+    const float4 r00 = __ldg(v + i00), r10 = __ldg(v + i00 + dy);
+    const float4 r01 = __ldg(v + i00 + dz), r11 = __ldg(v + i00 + dz + dy);
     float c00 = fmaf(t[0], r00.z - r00.x, r00.x), c10 = fmaf(t[0], r10.z - r10.x, r10.x);
     float c01 = fmaf(t[0], r01.z - r01.x, r01.x), c11 = fmaf(t[0], r11.z - r11.x, r11.x);
     float e0 = fmaf(t[1], c10 - c00, c00), e1 = fmaf(t[1], c11 - c01, c01);
@@ -200,7 +213,7 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
     if (i < d.npts0) {
         const float4 p0 = __ldg(pre + 2 * i), p1 = __ldg(pre + 2 * i + 1);  // {offset, half}, {axis, light side}
         const float f[3] = {q.pf[0] + p0.x, q.pf[1] + p0.y, q.pf[2] + p0.z};
-        sample_rt(sc, q.pb, f, rho, tr);
+        sample_rt(sc, q.pb, q.pbox, f, rho, tr);
         if (p0.w < 0.0f) {
             ph = 1.0f;  // diffuse centre point (src/feature_pipeline.cpp:163-164)
             return;
@@ -217,7 +230,7 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
 #pragma unroll
     for (int c = 0; c < 3; ++c) h[c] = fmaf(q.a[c], tq.z, fmaf(q.b[c], tq.y, q.t[c] * tq.x)) * q.hs;
     const float f[3] = {q.ef[0] + h[0], q.ef[1] + h[1], q.ef[2] + h[2]};
-    sample_rt(sc, q.eb, f, rho, tr);
+    sample_rt(sc, q.eb, q.ebox, f, rho, tr);
     const float dx = q.dpe[0] + h[0], dy = q.dpe[1] + h[1], dz = q.dpe[2] + h[2];
     const float dd = dx * dx + dy * dy + dz * dz;
     if (dd <= 0.0f) {
