@@ -227,6 +227,11 @@ int sf_profile_enable(int on);
 int sf_profile_read(double stage_ms[SF_STAGE_COUNT], int64_t stage_launches[SF_STAGE_COUNT]);
 /* Number of kernels this library has launched since load (all entry points). */
 int64_t sf_launch_count(void);
+/* Diagnostics: with SF_DEBUG_TC set in the environment, CTA 0 of the tensor-core
+ * backbone accumulates clock64 cycles per phase (0 bundle wait FC-1, 1 attention,
+ * 2 FC-1 MMA, 3 FC-1 epilogue, 4 bundle wait FC-2, 5 FC-2 MMA, 6 FC-2 epilogue,
+ * 7 other, 8 total); reading resets them. */
+int sf_debug_tc_profile(uint64_t out[16]);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,7 @@ _SIGS = {
     "sf_profile_enable": (I, [I]),
     "sf_profile_read": (I, [P, P]),
     "sf_launch_count": (I64, []),
+    "sf_debug_tc_profile": (I, [P]),
 }
 
 STAGES = ("config", "features_diffuse", "features_highlight", "slice", "backbone", "sample_sort")

@@ -1118,6 +1118,14 @@ int sf_profile_read(double stage_ms[SF_STAGE_COUNT], int64_t stage_launches[SF_S
 
 int64_t sf_launch_count(void) { return g_launches.load(); }
 
+int sf_debug_tc_profile(uint64_t out[16]) {
+    return guard([&] {
+        unsigned long long v[16];
+        sfb::tc_read_prof(v);
+        for (int i = 0; i < 16; ++i) out[i] = v[i];
+    });
+}
+
 }  // extern "C"
 
 extern "C" void sf_backbone_destroy(sf_backbone* b) {

@@ -188,6 +188,7 @@ SortLayout sort_layout(const sf_backbone_config& c);
 bool tc_supported(const sf_backbone_config& c);
 void tc_prepare(sf_backbone& b, cudaStream_t s);
 void tc_release(sf_backbone& b);
+void tc_read_prof(unsigned long long* out);
 void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, const float* mms,
                         const double* cfg8, float* y, double* F, cudaStream_t s);
 
