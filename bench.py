@@ -65,6 +65,18 @@ def peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def ncu_traffic():
+    """Per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of each kernel from the
+    committed ncu --set full summary (profiles/ncu_traffic.json, written from a capture of
+    tools/profile_step.py at this workload)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        j = json.load(f)
+    return {k: v.get("dram_bytes") for k, v in j.get("kernels", {}).items()}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -96,7 +108,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
             return
@@ -306,25 +318,36 @@ def run_b200(args):
     stage_launch = {k: v[1] / p_steps for k, v in stages.items()}
 
     hbm, bf16, bf16_sus, peak_kind = peaks()
-    # Algorithmic bytes per query for sampling: 8 corners x 8 B
-    # {rho,T} per template point + 2 phase lookups x 8 corners x 4 B x n_lobes
-    # per non-centre point.
-    bytes_d = 194 * 64 + 193 * 2 * 8 * 4
-    bytes_h = 72 * 64 + 72 * 2 * 8 * 4
-    flop_q = 274912  # 2 x 137,456 weight MACs per query (walk_params shapes)
+    # Algorithmic work per query:
+    #  * sampling: logical gather bytes = 266 points x 8 corners x 8 B {rho, T}
+    #    + 265 non-centre points x 2 phase lookups x 8 corners x 4 B (1 lobe)
+    #    = 17,024 + 16,960 = 33,984 B/query (diffuse 194 + highlight 72 points);
+    #  * network: 274,912 FLOP/query (2 x 137,456 weight MACs from walk_params shapes).
+    bytes_q = {"sample_sort": 266 * 64 + 265 * 64, "features_diffuse": 194 * 64 + 193 * 64,
+               "features_highlight": 72 * 64 + 72 * 64, "slice": 2 * 3 * 266 * 4}
+    flop_q = 274912
+    traffic = ncu_traffic()
     dom = max(stage_ms, key=stage_ms.get)
+    kname = {"sample_sort": "k_sample_sort", "backbone": "k_backbone_tc" if precision == sf.BF16 else
+             "k_backbone_fp32", "features_diffuse": "k_sample_features", "features_highlight": "k_sample_features",
+             "slice": "k_slice", "config": "k_make_cfg8"}[dom]
     if dom == "backbone":
         achieved = flop_q * n / (stage_ms[dom] * 1e-3) / 1e12
-        roof = {"bound": "tensor", "kernel": "backbone", "achieved": achieved, "peak": bf16_sus,
-                "unit": "TFLOP/s", "frac": achieved / bf16_sus, "traffic": None,
-                "peak_kind": f"{peak_kind} bf16 sustained",
+        roof = {"bound": "tensor", "kernel": kname, "achieved": achieved, "peak": bf16_sus,
+                "unit": "TFLOP/s", "frac": achieved / bf16_sus, "traffic": traffic.get(kname),
+                "peak_kind": f"{peak_kind} bf16 sustained (cuBLAS)",
                 "algorithmic": f"{flop_q} FLOP/query x {n} queries per launch"}
     else:
-        bq = bytes_d if dom == "features_diffuse" else bytes_h if dom == "features_highlight" else bytes_d
+        bq = bytes_q.get(dom, bytes_q["sample_sort"])
         achieved = bq * n / (stage_ms[dom] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "peak_kind": f"{peak_kind} HBM copy",
-                "algorithmic": f"{bq} B/query gathered x {n} queries per launch"}
+        roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic.get(kname), "peak_kind": f"{peak_kind} HBM copy",
+                "algorithmic": f"{bq} B/query logical gathers x {n} queries per launch"}
+    net_ms = stage_ms.get("backbone", 0.0)
+    roof["network"] = {"kernel": kname if dom == "backbone" else
+                       ("k_backbone_tc" if precision == sf.BF16 else "k_backbone_fp32"),
+                       "ms": net_ms, "tflops": flop_q * n / max(net_ms * 1e-3, 1e-12) / 1e12,
+                       "frac_of_bf16_sustained": flop_q * n / max(net_ms * 1e-3, 1e-12) / 1e12 / bf16_sus}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -365,7 +388,7 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "bf16"])
