@@ -1,0 +1,75 @@
+"""Multi-GPU sharding of shading-point queries.
+
+Every query is independent given the replicated inputs (density volume,
+transmittance feature volume, phase table, templates, network weights), so the
+image is split into square tiles dealt round-robin to the ranks (one process per
+GPU); each rank runs the fused query on its tiles and the per-tile radiance is
+gathered once per frame — the only exchange of the path. No collective touches
+the data path itself (weak scaling when every rank owns a fixed number of tiles).
+
+Works with any torch.distributed backend: NCCL over NVLink on the B200 box, gloo
+for the CPU tests (tests/test_sharding_gloo.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def tile_ids(width: int, height: int, tile: int):
+    """Row-major tile grid; returns (n_tiles_x, n_tiles_y)."""
+    return (width + tile - 1) // tile, (height + tile - 1) // tile
+
+
+def rank_pixels(width: int, height: int, tile: int, rank: int, world: int) -> np.ndarray:
+    """Pixel indices (row-major, y * width + x) owned by `rank`: tiles t with t % world == rank,
+    each tile's pixels in row-major order, tiles in increasing order."""
+    ntx, nty = tile_ids(width, height, tile)
+    out = []
+    for t in range(rank, ntx * nty, world):
+        ty, tx = divmod(t, ntx)
+        y0, x0 = ty * tile, tx * tile
+        ys = np.arange(y0, min(y0 + tile, height))
+        xs = np.arange(x0, min(x0 + tile, width))
+        out.append((ys[:, None] * width + xs[None, :]).reshape(-1))
+    return np.concatenate(out) if out else np.zeros(0, np.int64)
+
+
+def shard_sizes(width: int, height: int, tile: int, world: int):
+    return [len(rank_pixels(width, height, tile, r, world)) for r in range(world)]
+
+
+def gather_radiance(local, width: int, height: int, tile: int, rank: int, world: int, group=None):
+    """Assemble the full [height*width, 3] radiance on every rank from per-rank tiles.
+
+    `local` is a torch tensor [n_local, 3] (CUDA with NCCL, CPU with gloo) in the
+    pixel order of rank_pixels(..., rank, world). Ranks own different pixel counts
+    at the image border, so shards are padded to the largest before all_gather.
+    """
+    import torch
+    import torch.distributed as dist
+
+    sizes = shard_sizes(width, height, tile, world)
+    pad = max(sizes)
+    buf = torch.zeros((pad, local.shape[1]), dtype=local.dtype, device=local.device)
+    buf[: local.shape[0]] = local
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    full = torch.empty((width * height, local.shape[1]), dtype=local.dtype, device=local.device)
+    for r in range(world):
+        idx = torch.as_tensor(rank_pixels(width, height, tile, r, world), device=local.device)
+        full[idx] = parts[r][: sizes[r]]
+    return full
+
+
+def query_image(eval_fn, queries, width: int, height: int, tile: int, rank: int, world: int, group=None):
+    """Run `eval_fn(rows) -> [n, 3]` on this rank's tiles of the per-pixel query rows
+    ([height*width, 9]) and gather the image. `eval_fn` is the fused GPU query
+    (paper_2401_14051_b200.query bound to a scene/net) in production, anything with the
+    same contract in tests."""
+    import torch
+
+    mine = rank_pixels(width, height, tile, rank, world)
+    local = eval_fn(queries[mine])
+    if not isinstance(local, torch.Tensor):
+        local = torch.as_tensor(np.ascontiguousarray(local))
+    return gather_radiance(local, width, height, tile, rank, world, group)
