@@ -880,11 +880,11 @@ void check_precision(const sf_backbone& b, int precision, cudaStream_t s) {
 // bf16 path over one chunk: fused sample+sort (or sort of given features) -> tcgen05 backbone.
 void run_bf16_chunk(const sf_backbone& b, const sfb::SortLayout& L, const sfb::SceneDev* sc,
                     const sfb::TemplateDev* dt, const sfb::TemplateDev* ht, const float* planes, int n_planes,
-                    const float4* pre, int64_t m, const double* queries, const float* feats, const double* cfg8,
+                    const float4* pre, int64_t m, const void* recs, const float* feats, const double* cfg8,
                     uint8_t* ops, float* mms, int* err, float* y, double* F, cudaStream_t s) {
     {
         StageScope st(SF_STAGE_SAMPLE_SORT, s);
-        sfb::launch_sample_sort(sc, dt, ht, planes, n_planes, pre, L, m, queries, feats, ops, mms, err, s);
+        sfb::launch_sample_sort(sc, dt, ht, planes, n_planes, pre, L, m, recs, feats, ops, mms, err, s);
     }
     {
         StageScope st(SF_STAGE_BACKBONE, s);
@@ -1004,6 +1004,7 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
             Scratch<uint8_t> ops(size_t(tiles) * L.tile_bytes, stream);
             Scratch<float> mms(size_t(L.n_layers) * tiles * sfb::kUmmaM * 8, stream);
             Scratch<double> cfg8(size_t(chunk) * 8, stream);
+            Scratch<uint8_t> recs(size_t(chunk) * sfb::query_rec_bytes(), stream);
             Scratch<int> err(1, stream);
             SFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
             sfb::SceneDev sc = sfb::scene_dev(*s->density, *s->tvol->values, s->d_dt, s->model, *s->table,
@@ -1019,9 +1020,9 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
                 const double* qd = iq.d + 9 * q0;
                 {
                     StageScope st(SF_STAGE_CONFIG, stream);
-                    sfb::launch_make_cfg8(*medium, m, qd, cfg8.p, stream);
+                    sfb::launch_query_prep(sc, ht, *medium, m, qd, cfg8.p, recs.p, stream);
                 }
-                run_bf16_chunk(*b, L, &sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, m, qd, nullptr, cfg8.p,
+                run_bf16_chunk(*b, L, &sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, m, recs.p, nullptr, cfg8.p,
                                ops.p, mms.p, err.p, oy.d ? oy.d + 3 * q0 : nullptr, oF.d ? oF.d + 3 * q0 : nullptr,
                                stream);
             }

@@ -94,7 +94,9 @@ __device__ __forceinline__ void voxel_split(const GridDev& g, const double* s, i
     }
 }
 
-struct QueryCtx {
+// Per-query context, computed once per query by k_query_prep (one thread per
+// query) instead of redundantly by the 32 lanes of the sampling warp.
+struct __align__(16) QueryCtx {
     int pb[3];               // query base cell
     float pf[3];             // query base fraction
     int eb[3];               // highlight entry cell
@@ -105,7 +107,9 @@ struct QueryCtx {
     float wf[3], iw;         // omega and 1/|omega|
     float lf[3], il;         // light and 1/|light|
     float pbox[6], ebox[6];  // in-box fraction bounds relative to pb / eb
-    bool ok;
+    int ok;                  // highlight entry != p
+    int same_light;          // light equals query 0's (diffuse light side precomputed)
+    int pad_;
 };
 
 __device__ __forceinline__ void box_bounds(const GridDev& g, const int* base, float* box) {
@@ -134,7 +138,7 @@ __device__ __forceinline__ void query_ctx(const SceneDev& sc, const TemplateDev&
     voxel_split(g, entry, q.eb, q.ef);
     double span[3] = {p[0] - entry[0], p[1] - entry[1], p[2] - entry[2]};
     const double len = sqrt(dot3(span, span));
-    q.ok = len > 0.0;
+    q.ok = len > 0.0 ? 1 : 0;
     const double il = 1.0 / len;
     double axis[3] = {span[0] * il, span[1] * il, span[2] * il};
     const double od = dot3(omega, axis);
@@ -270,6 +274,31 @@ __global__ void k_diffuse_prep(SceneDev sc, TemplateDev dt, SortDesc d, const fl
     pre[2 * i + 1] = make_float4(ax, ay, az, cap_phase(planes, d, cl, half));
 }
 
+// Per-query preparation for the production path: make_config rows
+// (src/predictor.cpp:261-274, alpha = angle_between(omega, l)) and the sampling
+// context (voxel-space bases, highlight frame, in-box bounds).
+__global__ void k_query_prep(SceneDev sc, TemplateDev ht, sf_medium_params m, int64_t n,
+                             const double* __restrict__ queries, double* __restrict__ cfg8,
+                             QueryCtx* __restrict__ recs) {
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
+        const double* c = queries + 9 * q;
+        QueryCtx qc;
+        query_ctx(sc, ht, c, qc);
+        qc.same_light = (c[6] == queries[6] && c[7] == queries[7] && c[8] == queries[8]) ? 1 : 0;
+        qc.pad_ = 0;
+        recs[q] = qc;
+        double* o = cfg8 + 8 * q;
+        o[0] = m.n_g;
+        o[1] = m.n_g > 0 ? m.g[0] : 0.0;
+        o[2] = m.n_g > 1 ? m.g[1] : 0.0;
+        o[3] = m.n_g > 2 ? m.g[2] : 0.0;
+        o[4] = m.albedo[0];
+        o[5] = m.albedo[1];
+        o[6] = m.albedo[2];
+        o[7] = angle_between(c + 3, c + 6);
+    }
+}
+
 __global__ void k_xpair(const float2* __restrict__ v, int nx, int ny, int nz, float4* __restrict__ out) {
     const size_t n = size_t(nx) * ny * nz;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
@@ -377,7 +406,7 @@ __device__ __forceinline__ void sort_segment_pair(float* seg, int cnt, bool uppe
 
 __global__ void __launch_bounds__(kWarps * 32, 3)
     k_sample_sort(SceneDev sc, TemplateDev ht, SortDesc d, const float2* __restrict__ planes_g,
-                  const float4* __restrict__ pre, int64_t n, const double* __restrict__ queries,
+                  const float4* __restrict__ pre, int64_t n, const QueryCtx* __restrict__ recs,
                   const float* __restrict__ feats, uint8_t* __restrict__ ops, float* __restrict__ mms, int* err) {
     extern __shared__ __align__(16) float sm[];
     const int plane_floats = 2 * d.n_planes * d.A * (d.H + 1);
@@ -397,9 +426,6 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
         s_cseg[i] = d.chunk_seg[i];
         s_cj[i] = d.chunk_j[i];
     }
-    double l_ref[3] = {0, 0, 0};  // the light `pre` was prepared for (query 0)
-    if (queries != nullptr && n > 0)
-        for (int c = 0; c < 3; ++c) l_ref[c] = queries[6 + c];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* scr_all = sm + plane_floats;              // [8][scr_floats]
     float* pools = scr_all + kWarps * d.scr_floats;  // [8][n_segs][2]
@@ -415,12 +441,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
             const int64_t q = q0 + warp;
             if (q >= n || (d.debug & 1)) {
                 for (int i = lane; i < 3 * d.ntot; i += 32) scr[i] = 0.0f;
-            } else if (feats == nullptr) {
-                QueryCtx qc;
-                const double* qr = queries + 9 * q;
-                query_ctx(sc, ht, qr, qc);
+            } else if (recs != nullptr) {
+                const QueryCtx qc = recs[q];
                 if (!qc.ok && lane == 0) atomicExch(err, 1);
-                const bool same_light = qr[6] == l_ref[0] && qr[7] == l_ref[1] && qr[8] == l_ref[2];
+                const bool same_light = qc.same_light != 0;
                 for (int i = lane; i < d.ntot; i += 32) {
                     float rho, tr, ph;
                     point_features(sc, ht, qc, i, d, planes, pre, same_light, rho, tr, ph);
@@ -601,8 +625,19 @@ void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float
     count_launch();
 }
 
+size_t query_rec_bytes() { return sizeof(QueryCtx); }
+
+void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_medium_params& m, int64_t n,
+                       const double* queries, double* cfg8, void* recs, cudaStream_t s) {
+    if (n <= 0) return;
+    const int64_t blocks = std::min<int64_t>((n + 127) / 128, int64_t(sm_count()) * 16);
+    k_query_prep<<<unsigned(blocks), 128, 0, s>>>(sc, ht, m, n, queries, cfg8, static_cast<QueryCtx*>(recs));
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+}
+
 void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht, const float* planes,
-                        int n_planes, const float4* pre, const SortLayout& L, int64_t n, const double* queries,
+                        int n_planes, const float4* pre, const SortLayout& L, int64_t n, const void* recs,
                         const float* feats, uint8_t* ops, float* mms, int* err, cudaStream_t s) {
     (void)dt;  // diffuse placement comes from `pre` (k_diffuse_prep)
     if (n <= 0) return;
@@ -621,7 +656,8 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
     SceneDev scd = sc ? *sc : SceneDev{};
     TemplateDev htd = ht ? *ht : TemplateDev{1, 0, nullptr, nullptr, 1.0, nullptr};
     k_sample_sort<<<unsigned(blocks), kWarps * 32, smem, s>>>(scd, htd, d, reinterpret_cast<const float2*>(planes),
-                                                              pre, n, queries, feats, ops, mms, err);
+                                                              pre, n, static_cast<const QueryCtx*>(recs), feats,
+                                                              ops, mms, err);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }

@@ -196,8 +196,12 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
 // Samples the scene when `feats` is null, else sorts the given feature rows.
 void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht,
                         const float* planes, int n_planes, const float4* pre, const SortLayout& L,
-                        int64_t n, const double* queries, const float* feats, uint8_t* ops, float* mms,
+                        int64_t n, const void* recs, const float* feats, uint8_t* ops, float* mms,
                         int* err, cudaStream_t s);
+// Per-query context records (sampling bases, highlight frame) + make_config rows.
+size_t query_rec_bytes();
+void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_medium_params& m, int64_t n,
+                       const double* queries, double* cfg8, void* recs, cudaStream_t s);
 // Light-side phase of every diffuse point for the light of query 0 (diffuse
 // placement is a pure translation, so axis and aperture do not depend on p).
 void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float* planes, int n_planes,
