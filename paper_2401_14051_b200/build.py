@@ -31,7 +31,8 @@ def _compile(src: str, verbose: bool) -> str:
     deps.append(os.path.join(HERE, "..", "include", "scatterfield_b200.h"))
     if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
         return out
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", path, "-o", out]
+    extra = os.environ.get("SF_NVCC_EXTRA", "").split()  # debug defines, e.g. -DSF_TC_WATCHDOG
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", path, "-o", out]
     if verbose and src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -22,6 +22,7 @@
 //
 // Precision: bf16 GEMM operands (weights, o_att, features, u, merges), fp32
 // accumulation, fp32 bias / activation / residual / attention (tests/bf16_emulation.py).
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -34,16 +35,21 @@ namespace sfb {
 
 namespace {
 
-constexpr int kThreads = 128;   // one thread per query row / TMEM lane
+constexpr int kConsumers = 128;             // one thread per query row / TMEM lane
+constexpr int kThreads = kConsumers + 32;    // + one producer warp issuing the bundle copies
 constexpr int kTmemCols = 256;  // fc1 [0,32) fc2 [32,64) merge/head [64,128) cross [128,192)
 constexpr int kSlots = 3;
-constexpr int kSlotBytes = 28672;
-// FC-1 bundle layout
-constexpr int kSlotW1a = 0, kSlotW1b = 2048, kSlotFeat = 6144, kSlotMM = 22528;
-constexpr int kSlotAtt = 26624;   // [52] attention W1 b1 W2 b2 (+pad), [32] FC-1 bias
-constexpr int kSlotInit = 27136;  // [224] conditioning W, [32] b (first layer of a stack)
-// 64-wide bundles: weights at 0, bias at 8192, head2 W/b at 8448 (head-1 bundle)
-constexpr int kSlotBias = 8192, kSlotHead2 = 8448;
+constexpr int kSlotBytes = 23552;
+// FC-1 bundle: W1[:, :32], W1[:, 32:], the tile's sorted-feature block, FC-1 bias
+constexpr int kSlotW1a = 0, kSlotW1b = 2048, kSlotFeat = 6144, kSlotB1 = 22528;
+// FC-2 bundle: W2, bias. 64-wide bundles: weights, bias, head2 W/b (head-1 bundle)
+constexpr int kSlotB2 = 2048, kSlotBias = 8192, kSlotHead2 = 8448;
+constexpr int kSlotWmHi = 4096;  // merge bundle: W_m[:, 0:32] at 0, W_m[:, 32:64] here
+// Attention payload of the NEXT FC-1 step, carried by the bundle of the step before it so
+// the attention weight is computed while that step's MMA runs: the tile's mean/max block,
+// [52] attention W1 b1 W2 b2 (+pad), [224 + 32] conditioning W/b (first layer of a stack).
+constexpr int kPayMM = 9728, kPayAtt = 13824, kPayInit = 14080;
+static_assert(kPayInit + 1024 <= kSlotB1 && kSlotB1 + 128 <= kSlotBytes, "slot layout");
 constexpr int kMaxSteps = 96;
 constexpr int kMaxCopies = 6;
 
@@ -64,6 +70,8 @@ struct Step {
     Copy c[kMaxCopies];
 };
 
+static_assert(sizeof(Copy) == 32 && sizeof(Step) == 16 + 32 * kMaxCopies, "step program is read as int4 words");
+
 struct TcDesc {
     int nl[2];
     int counts[2][16];
@@ -71,7 +79,7 @@ struct TcDesc {
     double gamma;
     int n_steps;
     int prof;  // SF_DEBUG_TC: CTA 0 / thread 0 accumulates clock64 per phase into g_tc_prof
-    Step steps[kMaxSteps];
+    const Step* steps;  // step program in global memory (read through the L1 by the issuing thread)
 };
 
 __device__ unsigned long long g_tc_prof[16];
@@ -82,68 +90,105 @@ struct TcPack {
 };
 
 struct Ring {
-    uint8_t* slot[kSlots];
-    uint64_t* full;  // [kSlots]
-    uint64_t* mma;
-    uint32_t par[kSlots];
+    uint8_t* base;
+    uint64_t* full;   // [kSlots] bundle landed (producer expect_tx + bulk copies)
+    uint64_t* empty;  // [kSlots] bundle consumed (consumer thread 0)
+    uint64_t* mma;    // MMA completion (tcgen05.commit)
     uint32_t mpar;
-    int step;
 };
 
-__device__ __forceinline__ void issue_step(const Ring& r, const TcDesc& d, int j, const uint8_t* wpk,
+// Producer: the copies of one step into ring slot j % kSlots. The step program is in
+// global memory; the whole descriptor is fetched with independent loads (one L2 round
+// trip) before the producer waits for the slot, so only the copies remain to issue.
+struct StepRegs {
+    int4 w[1 + 2 * kMaxCopies];
+};
+
+__device__ __forceinline__ void load_step(const TcDesc& d, int j, StepRegs& sr) {
+    const int4* p = reinterpret_cast<const int4*>(d.steps + j);
+#pragma unroll
+    for (int k = 0; k < 1 + 2 * kMaxCopies; ++k) sr.w[k] = __ldg(p + k);
+}
+
+__device__ __forceinline__ void issue_step(const Ring& r, const StepRegs& sr, int j, const uint8_t* wpk,
                                            const uint8_t* ops, const uint8_t* mms, int tile, int n_tiles) {
-    if (j >= d.n_steps) return;
-    const Step& s = d.steps[j];
     const int slot = j % kSlots;
     uint64_t* bar = &r.full[slot];
-    mbar_expect_tx(bar, s.total);
-    for (int c = 0; c < s.ncopy; ++c) {
-        const Copy& cp = s.c[c];
+    mbar_expect_tx(bar, uint32_t(sr.w[0].y));
+#pragma unroll
+    for (int c = 0; c < kMaxCopies; ++c) {
+        if (c >= sr.w[0].x) break;
+        const int4 c0 = sr.w[1 + 2 * c], c1 = sr.w[2 + 2 * c];
+        const int kind = c0.x;
+        const uint32_t dst = uint32_t(c0.y), bytes = uint32_t(c0.z);
+        const int64_t a = (int64_t(uint32_t(c1.y)) << 32) | uint32_t(c1.x);
+        const int64_t stride = (int64_t(uint32_t(c1.w)) << 32) | uint32_t(c1.z);
         const uint8_t* src;
-        if (cp.kind == 0)
-            src = wpk + cp.a;
-        else if (cp.kind == 1)
-            src = ops + cp.a * n_tiles + int64_t(tile) * cp.stride;
+        if (kind == 0)
+            src = wpk + a;
+        else if (kind == 1)
+            src = ops + a * n_tiles + int64_t(tile) * stride;
         else
-            src = mms + cp.a * int64_t(n_tiles) * 4096 + int64_t(tile) * 4096;
-        bulk_g2s(r.slot[slot] + cp.dst, src, cp.bytes, bar);
+            src = mms + a * int64_t(n_tiles) * 4096 + int64_t(tile) * 4096;
+        bulk_g2s(r.base + slot * kSlotBytes + dst, src, bytes, bar);
     }
 }
 
-// Wait for the current step's bundle (all threads read parameters from it).
-__device__ __forceinline__ uint8_t* acquire(Ring& r) {
-    const int slot = r.step % kSlots;
-    mbar_wait(&r.full[slot], r.par[slot]);
-    r.par[slot] ^= 1;
-    return r.slot[slot];
+#ifdef SF_TC_WATCHDOG
+// Debug builds: a wait that has not completed after ~1 s records who waited on what in
+// g_tc_prof[14..15] and gives up, so a protocol deadlock ends the kernel with a diagnosis.
+__device__ void wd_wait(uint64_t* bar, uint32_t parity, int code, int j) {
+    const long long t0 = clock64();
+    while (true) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (ok) return;
+        if (clock64() - t0 > 2000000000ll) {
+            if (atomicCAS(&g_tc_prof[15], 0ull, 1ull + blockIdx.x) == 0ull)
+                g_tc_prof[14] = uint64_t(code) | (uint64_t(j) << 8) | (uint64_t(parity) << 24) |
+                                (uint64_t(threadIdx.x) << 32);
+            return;
+        }
+    }
+}
+#define SF_WAIT(bar, par, code, j) wd_wait(bar, par, code, j)
+#else
+#define SF_WAIT(bar, par, code, j) mbar_wait(bar, par)
+#endif
+
+__device__ __forceinline__ uint8_t* wait_full(const Ring& r, int j) {
+    const int slot = j % kSlots;
+    SF_WAIT(&r.full[slot], uint32_t(j / kSlots) & 1u, 1, j);
+    return r.base + slot * kSlotBytes;
 }
 
-// Issue the step's MMAs (thread 0) after prefetching bundle j+2, then wait.
-// a0/k0 x weights at w0, then optionally a1/k1 x weights at w1 into the same columns.
-__device__ __forceinline__ void run_mma(Ring& r, const TcDesc& d, const uint8_t* wpk, const uint8_t* ops,
-                                        const uint8_t* mms, int tile, int n_tiles, uint32_t tmem_d, int n,
-                                        uint32_t a0, int k0, uint32_t w0, uint32_t a1, int k1, uint32_t w1,
-                                        bool accumulate) {
+// Consumer thread 0: step j's bundle is no longer read (its MMA completed, epilogue done).
+__device__ __forceinline__ void release(const Ring& r, int j) {
+    if (j >= 0) mbar_arrive(&r.empty[j % kSlots]);
+}
+
+// Operands written by the consumer threads -> visible to the tensor core; then thread 0 issues.
+__device__ __forceinline__ void mma_sync() {
     fence_proxy_async();
     tc_fence_before();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        tc_fence_after();
-        // ring slot (j+2)%3 was last used by step j-1, whose MMA and readers are done
-        issue_step(r, d, r.step + kSlots - 1, wpk, ops, mms, tile, n_tiles);
-        const uint32_t id = idesc_bf16(n);
-        for (int k = 0; k < k0 / 16; ++k)
-            umma_bf16(tmem_d, smem_desc(a0 + k * 256, 128, k0 * 16), smem_desc(w0 + k * 256, 128, k0 * 16), id,
-                      (accumulate || k > 0) ? 1u : 0u);
-        for (int k = 0; k < k1 / 16; ++k)
-            umma_bf16(tmem_d, smem_desc(a1 + k * 256, 128, k1 * 16), smem_desc(w1 + k * 256, 128, k1 * 16), id,
-                      1u);
-        umma_commit(r.mma);
-    }
-    mbar_wait(r.mma, r.mpar);
-    r.mpar ^= 1;
-    r.step += 1;
+    consumer_bar_sync();
     tc_fence_after();
+}
+
+__device__ __forceinline__ void mma_wait(Ring& r) {
+    SF_WAIT(r.mma, r.mpar, 3, 0);
+    r.mpar ^= 1;
+    tc_fence_after();
+}
+
+// D[128 x n] (+)= A[128 x k] * W[n x k]^T, both K-major canonical; one UMMA per 16 K.
+__device__ __forceinline__ void issue_gemm(uint32_t tmem_d, int n, uint32_t a, int k, uint32_t w, bool accumulate) {
+    const uint32_t id = idesc_bf16(n);
+    const uint64_t da = smem_desc(a, 128, k * 16), dw = smem_desc(w, 128, k * 16);
+    for (int s = 0; s < k / 16; ++s)  // +256 B per K step = +16 in the start-address field
+        umma_bf16(tmem_d, da + 16u * s, dw + 16u * s, id, (accumulate || s > 0) ? 1u : 0u);
 }
 
 __device__ __forceinline__ float relu(float v) { return v > 0.0f ? v : 0.0f; }
@@ -160,13 +205,60 @@ __device__ __forceinline__ void dense_s(const float* W, const float* b, const fl
     }
 }
 
+struct RowCtx {
+    float cfgv[7];
+    float g_mean, alpha;
+    int literal;
+};
+
+// Channel attention weight of type tau (src/neural.cpp:473-491) from a bundle's payload.
+__device__ __forceinline__ float attention(const uint8_t* slot, int tau, const RowCtx& rc) {
+    const float4* mm = reinterpret_cast<const float4*>(slot + kPayMM) + threadIdx.x * 2;
+    const float4 m0 = mm[0], m1 = mm[1];
+    const float v[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, rc.g_mean, rc.alpha};
+    if (rc.literal) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc += relu(v[j]);
+        return 1.0f / (1.0f + __expf(-(acc / 8.0f)));
+    }
+    const float* prm = reinterpret_cast<const float*>(slot + kPayAtt);
+    float h[4], w3[3];
+    dense_s<4, 8>(prm, prm + 32, v, h);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = relu(h[j]);
+    dense_s<3, 4>(prm + 36, prm + 48, h, w3);
+    const float z = tau == 0 ? w3[0] : (tau == 1 ? w3[1] : w3[2]);
+    return 1.0f / (1.0f + __expf(-z));
+}
+
+// First layer of a stack: o = relu(W_init cfg + b) (src/predictor.cpp:206-212), o_att = w o.
+__device__ __forceinline__ void stack_start(const uint8_t* slot, int tau, const RowCtx& rc, float* oa) {
+    const float* ini = reinterpret_cast<const float*>(slot + kPayInit);
+    const float w = attention(slot, tau, rc);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {  // 8 outputs at a time: bounds the loads the compiler hoists
+        float o[8];
+        dense_s<8, 7>(ini + 56 * g, ini + 224 + 8 * g, rc.cfgv, o);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) oa[8 * g + j] = relu(o[j]) * w;
+        asm volatile("" ::: "memory");
+    }
+}
+
+__device__ __forceinline__ void store_row32(uint8_t* a, const float* v) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) store_chunk(a, threadIdx.x, c, 32, v + 8 * c);
+}
+
 __global__ void __launch_bounds__(kThreads, 2)
-    k_backbone_tc(const __grid_constant__ TcDesc d, const uint8_t* __restrict__ wpk, const uint8_t* __restrict__ ops,
+    k_backbone_tc(const TcDesc d, const uint8_t* __restrict__ wpk, const uint8_t* __restrict__ ops,
                   const uint8_t* __restrict__ mms, int n_tiles, int64_t n, const double* __restrict__ cfg8,
                   float* __restrict__ y_out, double* __restrict__ F_out) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    __shared__ uint64_t bars[kSlots + 1];
+    __shared__ uint64_t bars[2 * kSlots + 1];
     __shared__ uint32_t tmem_slot;
+    __shared__ int s_kf[2][16];
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -180,192 +272,220 @@ __global__ void __launch_bounds__(kThreads, 2)
         atomicAdd(&g_tc_prof[k], (unsigned long long)(t_now - t_last));     \
         t_last = t_now;                                                     \
     }
-    const int64_t q = int64_t(tile) * kUmmaM + tid;
-    const bool live = q < n;
 
     uintptr_t base = (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023);
-    uint8_t* a_att = reinterpret_cast<uint8_t*>(base);  // [128 x 32]
-    uint8_t* a2 = a_att + kUmmaM * 32 * 2;              // [128 x 64]
+    uint8_t* a_att = reinterpret_cast<uint8_t*>(base);  // [128 x 32] o_att operand of FC-1
+    uint8_t* a_od = a_att + kUmmaM * 32 * 2;            // [128 x 32] diffuse stack output (merge, K 0-31)
+    uint8_t* a2 = a_od + kUmmaM * 32 * 2;               // [128 x 64] FC-2 / merge (K 32-63) / cross / head
     Ring r;
-    r.slot[0] = a2 + kUmmaM * 64 * 2;
-    for (int s = 1; s < kSlots; ++s) r.slot[s] = r.slot[s - 1] + kSlotBytes;
+    r.base = a2 + kUmmaM * 64 * 2;
     r.full = bars;
-    r.mma = bars + kSlots;
-    for (int s = 0; s < kSlots; ++s) r.par[s] = 0;
+    r.empty = bars + kSlots;
+    r.mma = bars + 2 * kSlots;
     r.mpar = 0;
-    r.step = 0;
 
     if (warp == 0) tmem_alloc(&tmem_slot, kTmemCols);
     if (tid == 0) {
-        for (int s = 0; s <= kSlots; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < 2 * kSlots + 1; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (tid < 32) s_kf[tid >> 4][tid & 15] = (d.counts[tid >> 4][tid & 15] + 2 + 15) / 16 * 16;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+
+    if (warp == kConsumers / 32) {  // producer warp: keeps the ring full, off the critical path
+        if ((tid & 31) == 0) {
+            StepRegs cur, nxt;
+            load_step(d, 0, cur);
+            for (int j = 0; j < d.n_steps; ++j) {
+                if (j + 1 < d.n_steps) load_step(d, j + 1, nxt);  // in flight across the slot wait
+                if (j >= kSlots) SF_WAIT(&r.empty[j % kSlots], uint32_t(j / kSlots - 1) & 1u, 2, j);
+                issue_step(r, cur, j, wpk, ops, mms, tile, n_tiles);
+                cur = nxt;
+            }
+        }
+        return;
+    }
+
+    const int64_t q = int64_t(tile) * kUmmaM + tid;
+    const bool live = q < n;
     const uint32_t tmem = tmem_slot;
-    if (tid == 0)
-        for (int j = 0; j < kSlots - 1; ++j) issue_step(r, d, j, wpk, ops, mms, tile, n_tiles);
     const uint32_t lane = uint32_t(warp * 32) << 16;
-    const uint32_t s_att = smem_u32(a_att), s_a2 = smem_u32(a2);
+    const uint32_t s_att = smem_u32(a_att), s_od = smem_u32(a_od), s_a2 = smem_u32(a2);
 
     // conditioning (cfg_vector, src/predictor.cpp:193-202)
-    float cfgv[7] = {0, 0, 0, 0, 0, 0, 0};
-    float g_mean = 0.0f, alpha = 0.0f;
-    double alb[3] = {0.5, 0.5, 0.5};
+    RowCtx rc;
+    for (int i = 0; i < 7; ++i) rc.cfgv[i] = 0.0f;
+    rc.g_mean = 0.0f;
+    rc.alpha = 0.0f;
+    rc.literal = d.literal;
     if (live) {
         const double* c8 = cfg8 + 8 * q;
         int ng = int(c8[0]);
-        for (int i = 0; i < ng; ++i) g_mean += float(c8[1 + i]);
-        if (ng > 0) g_mean /= float(double(ng));
-        alpha = float(c8[7]);
-        for (int i = 0; i < ng && i < 3; ++i) cfgv[i] = float(c8[1 + i]);
-        for (int i = 0; i < 4; ++i) cfgv[3 + i] = float(c8[4 + i]);
-        alb[0] = c8[4];
-        alb[1] = c8[5];
-        alb[2] = c8[6];
+        for (int i = 0; i < ng; ++i) rc.g_mean += float(c8[1 + i]);
+        if (ng > 0) rc.g_mean /= float(double(ng));
+        rc.alpha = float(c8[7]);
+        for (int i = 0; i < ng && i < 3; ++i) rc.cfgv[i] = float(c8[1 + i]);
+        for (int i = 0; i < 4; ++i) rc.cfgv[3 + i] = float(c8[4 + i]);
     }
 
-    uint32_t od_pk[16];
+    float oa[32];  // o_att of the current layer (fp32 residual); its bf16 copy is a_att
+    // step 0: payload of the first FC-1 step
+    stack_start(wait_full(r, 0), 0, rc, oa);
+    store_row32(a_att, oa);
+    int j = 1;
     for (int tau = 0; tau < 3; ++tau) {
         for (int kind = 0; kind < 2; ++kind) {
-            float o[32];
-            for (int i = 0; i < d.nl[kind]; ++i) {
+            const int nl = kind == 0 ? d.nl[0] : d.nl[1];
+            for (int i = 0; i < nl; ++i) {
+                // FC-1 = [o_att | sorted_tau, mean, max] W1^T
                 PROF(7);
-                uint8_t* slot = acquire(r);
+                const uint8_t* s1 = wait_full(r, j);
                 PROF(0);
-                const uint32_t s_slot = smem_u32(slot);
-                const float* prm = reinterpret_cast<const float*>(slot + kSlotAtt);
-                if (i == 0) {  // conditioning layer o = relu(W_init cfg + b)
-                    const float* ini = reinterpret_cast<const float*>(slot + kSlotInit);
-                    dense_s<32, 7>(ini, ini + 224, cfgv, o);
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) o[j] = relu(o[j]);
+                mma_sync();
+                if (tid == 0) {
+                    const uint32_t b1s = smem_u32(s1);
+                    issue_gemm(tmem + 0, 32, s_att, 32, b1s + kSlotW1a, false);
+                    issue_gemm(tmem + 0, 32, b1s + kSlotFeat, s_kf[kind][i], b1s + kSlotW1b, true);
+                    umma_commit(r.mma);
+                    release(r, j - 1);
                 }
-                // channel attention (src/neural.cpp:473-491) from the tile's mean/max block
-                const float4* mm = reinterpret_cast<const float4*>(slot + kSlotMM) + tid * 2;
-                const float4 m0 = mm[0], m1 = mm[1];
-                const float v[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, g_mean, alpha};
-                float w;
-                if (d.literal) {
-                    float acc = 0.0f;
-                    for (int j = 0; j < 8; ++j) acc += relu(v[j]);
-                    w = 1.0f / (1.0f + __expf(-(acc / 8.0f)));
-                } else {
-                    float h[4], w3[3];
-                    dense_s<4, 8>(prm, prm + 32, v, h);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) h[j] = relu(h[j]);
-                    dense_s<3, 4>(prm + 36, prm + 48, h, w3);
-                    w = 1.0f / (1.0f + __expf(-w3[tau]));
-                }
-                float oa[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) oa[j] = o[j] * w;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) store_chunk(a_att, tid, c, 32, oa + 8 * c);
+                mma_wait(r);
                 PROF(1);
-                const int kf = d.steps[r.step].k2;
-                run_mma(r, d, wpk, ops, mms, tile, n_tiles, tmem + 0, 32, s_att, 32, s_slot + kSlotW1a,
-                        s_slot + kSlotFeat, kf, s_slot + kSlotW1b, false);
-                PROF(2);
                 // FC-1 epilogue: u = relu(acc + b1) -> bf16 operand of FC-2
-                const float* b1 = prm + 52;
-                float acc[32];
-                tmem_ld32(tmem + lane + 0, acc);
+                {
+                    const float* b1 = reinterpret_cast<const float*>(s1 + kSlotB1);
+                    float acc[32];
+                    tmem_ld32(tmem + lane + 0, acc);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    float v8[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) v8[e] = relu(acc[8 * c + e] + b1[8 * c + e]);
-                    store_chunk(a2, tid, c, 32, v8);
+                    for (int e = 0; e < 32; ++e) acc[e] = relu(acc[e] + b1[e]);
+                    store_row32(a2, acc);
                 }
+                PROF(2);
+                const uint8_t* s2 = wait_full(r, j + 1);
                 PROF(3);
-                uint8_t* slot2 = acquire(r);
+                mma_sync();
+                if (tid == 0) {
+                    issue_gemm(tmem + 32, 32, s_a2, 32, smem_u32(s2), false);
+                    umma_commit(r.mma);
+                    release(r, j);
+                }
                 PROF(4);
-                run_mma(r, d, wpk, ops, mms, tile, n_tiles, tmem + 32, 32, s_a2, 32, smem_u32(slot2), 0, 0, 0,
-                        false);
+                // while FC-2 runs: the next FC-1's attention weight (payload of this bundle)
+                const bool last = i == nl - 1;
+                float w_next = 0.0f;
+                if (!last) w_next = attention(s2, tau, rc);
                 PROF(5);
-                // FC-2 epilogue + residual: o = relu(acc + b2) + o_att (fp32)
-                const float* b2 = reinterpret_cast<const float*>(slot2 + 2048);
-                tmem_ld32(tmem + lane + 32, acc);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) o[j] = relu(acc[j] + b2[j]) + oa[j];
+                mma_wait(r);
                 PROF(6);
-            }
-            if (kind == 0) {
+                // FC-2 epilogue + residual: o = relu(acc + b2) + o_att (fp32)
+                float o[32];
+                {
+                    const float* b2 = reinterpret_cast<const float*>(s2 + kSlotB2);
+                    tmem_ld32(tmem + lane + 32, o);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) od_pk[j] = pack_bf16(o[2 * j], o[2 * j + 1]);
-            } else {
+                    for (int e = 0; e < 32; ++e) o[e] = relu(o[e] + b2[e]) + oa[e];
+                }
+                if (!last) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    *reinterpret_cast<uint4*>(a2 + canon_off(tid, 8 * c, 64)) =
-                        make_uint4(od_pk[4 * c], od_pk[4 * c + 1], od_pk[4 * c + 2], od_pk[4 * c + 3]);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) store_chunk(a2, tid, 4 + c, 64, o + 8 * c);
+                    for (int e = 0; e < 32; ++e) oa[e] = o[e] * w_next;
+                    store_row32(a_att, oa);
+                } else if (kind == 0) {  // od: K 0-31 of the merge input
+                    store_row32(a_od, o);
+                    stack_start(s2, tau, rc, oa);  // highlight stack (once per type: not overlapped)
+                    store_row32(a_att, oa);
+                } else {  // oh: K 32-63 of the merge input
+                    store_row32(a2, o);
+                }
+                j += 2;
             }
         }
         // merged_tau = relu(W_m [od; oh] + b)
-        uint8_t* slot = acquire(r);
-        run_mma(r, d, wpk, ops, mms, tile, n_tiles, tmem + 64, 64, s_a2, 64, smem_u32(slot), 0, 0, 0, false);
-        const float* bm = reinterpret_cast<const float*>(slot + kSlotBias);
-        for (int half = 0; half < 2; ++half) {
-            float acc[32];
-            tmem_ld32(tmem + lane + 64 + 32 * half, acc);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float v8[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v8[e] = relu(acc[8 * c + e] + bm[32 * half + 8 * c + e]);
-                store_chunk(a2, tid, half * 4 + c, 64, v8);
+        {
+            const uint8_t* sm = wait_full(r, j);
+            mma_sync();
+            if (tid == 0) {
+                issue_gemm(tmem + 64, 64, s_od, 32, smem_u32(sm), false);
+                issue_gemm(tmem + 64, 64, s_a2, 32, smem_u32(sm) + kSlotWmHi, true);
+                umma_commit(r.mma);
+                release(r, j - 1);
             }
+            mma_wait(r);
+            const float* bm = reinterpret_cast<const float*>(sm + kSlotBias);
+            for (int half = 0; half < 2; ++half) {
+                float acc[32];
+                tmem_ld32(tmem + lane + 64 + 32 * half, acc);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) acc[e] = relu(acc[e] + bm[32 * half + e]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) store_chunk(a2, tid, half * 4 + c, 64, acc + 8 * c);
+            }
+            ++j;
         }
         // cross += W_c[:, 64 tau : 64 tau + 64] merged_tau (accumulated in TMEM)
-        slot = acquire(r);
-        run_mma(r, d, wpk, ops, mms, tile, n_tiles, tmem + 128, 64, s_a2, 64, smem_u32(slot), 0, 0, 0, tau > 0);
-        if (tau == 2) {  // the last cross bundle carries the cross bias
-            const float* bc = reinterpret_cast<const float*>(slot + kSlotBias);
-            float h[32];
-            for (int half = 0; half < 2; ++half) {
-                tmem_ld32(tmem + lane + 128 + 32 * half, h);
+        {
+            const uint8_t* sc = wait_full(r, j);
+            mma_sync();
+            if (tid == 0) {
+                issue_gemm(tmem + 128, 64, s_a2, 64, smem_u32(sc), tau > 0);
+                umma_commit(r.mma);
+                release(r, j - 1);
+            }
+            if (tau < 2) {  // next type's first diffuse layer, while the cross MMA runs
+                stack_start(sc, tau + 1, rc, oa);
+                store_row32(a_att, oa);
+            }
+            mma_wait(r);
+            if (tau == 2) {  // the last cross bundle carries the cross bias
+                const float* bc = reinterpret_cast<const float*>(sc + kSlotBias);
+                for (int half = 0; half < 2; ++half) {
+                    float h[32];
+                    tmem_ld32(tmem + lane + 128 + 32 * half, h);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    float v8[8];
+                    for (int e = 0; e < 32; ++e) h[e] = relu(h[e] + bc[32 * half + e]);
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) v8[e] = relu(h[8 * c + e] + bc[32 * half + 8 * c + e]);
-                    store_chunk(a2, tid, half * 4 + c, 64, v8);
+                    for (int c = 0; c < 4; ++c) store_chunk(a2, tid, half * 4 + c, 64, h + 8 * c);
                 }
             }
+            ++j;
         }
     }
     // head 0 / 1 (64 -> 64, relu); head 2 (64 -> 3) SIMT from the head-1 bundle
-    float h[64];
     for (int l = 0; l < 2; ++l) {
-        uint8_t* slot = acquire(r);
-        run_mma(r, d, wpk, ops, mms, tile, n_tiles, tmem + 64, 64, s_a2, 64, smem_u32(slot), 0, 0, 0, false);
-        const float* bh = reinterpret_cast<const float*>(slot + kSlotBias);
+        const uint8_t* sh = wait_full(r, j);
+        mma_sync();
+        if (tid == 0) {
+            issue_gemm(tmem + 64, 64, s_a2, 64, smem_u32(sh), false);
+            umma_commit(r.mma);
+            release(r, j - 1);
+        }
+        mma_wait(r);
+        const float* bh = reinterpret_cast<const float*>(sh + kSlotBias);
+        float h[64];
         tmem_ld32(tmem + lane + 64, h);
         tmem_ld32(tmem + lane + 96, h + 32);
 #pragma unroll
-        for (int j = 0; j < 64; ++j) h[j] = relu(h[j] + bh[j]);
+        for (int e = 0; e < 64; ++e) h[e] = relu(h[e] + bh[e]);
         if (l == 0) {
 #pragma unroll
             for (int c = 0; c < 8; ++c) store_chunk(a2, tid, c, 64, h + 8 * c);
         } else {
-            const float* h2 = reinterpret_cast<const float*>(slot + kSlotHead2);
+            const float* h2 = reinterpret_cast<const float*>(sh + kSlotHead2);
             float y[3];
             dense_s<3, 64>(h2, h2 + 192, h, y);
             if (live) {
                 for (int c = 0; c < 3; ++c) {
                     float yc = fabsf(y[c]);
                     if (y_out) y_out[3 * q + c] = yc;
-                    if (F_out) F_out[3 * q + c] = pow(alb[c], d.gamma) * expm1(double(yc));  // decode_prediction
+                    if (F_out) F_out[3 * q + c] = pow(cfg8[8 * q + 4 + c], d.gamma) * expm1(double(yc));  // decode_prediction
                 }
             }
         }
+        ++j;
     }
     tc_fence_before();
-    __syncthreads();
+    consumer_bar_sync();
     if (warp == 0) tmem_dealloc(tmem, kTmemCols);
     if (prof) atomicAdd(&g_tc_prof[8], (unsigned long long)(clock64() - t_start));
 #undef PROF
@@ -408,7 +528,7 @@ std::vector<float> slice(const std::vector<float>& P, int64_t off, size_t n) {
 
 bool tc_supported(const sf_backbone_config& c) {
     if (c.width != 32 || c.merge_width != 64 || c.head_width != 64) return false;
-    if (c.n_diffuse_layers * 6 + c.n_highlight_layers * 6 + 3 * 2 + 2 > kMaxSteps) return false;
+    if (c.n_diffuse_layers * 6 + c.n_highlight_layers * 6 + 3 * 2 + 2 + 1 > kMaxSteps) return false;
     for (int i = 0; i < c.n_diffuse_layers; ++i)
         if (c.diffuse_counts[i] + 2 > 64) return false;
     for (int i = 0; i < c.n_highlight_layers; ++i)
@@ -460,39 +580,45 @@ void tc_prepare(sf_backbone& b, cudaStream_t s) {
         for (int k = 0; k < st.ncopy; ++k) st.total += st.c[k].bytes;
         steps.push_back(st);
     };
+    // Attention payload of an FC-1 step: appended to the bundle of the step before it.
+    auto add_payload = [&](int kind, int tau, int i, int64_t att_off, int64_t init_off) {
+        Step& prev = steps.back();
+        prev.c[prev.ncopy++] = Copy{2, uint32_t(kPayMM), uint32_t(kUmmaM * 8 * 4), 0, S.mm_layer[kind][i], 4096};
+        std::vector<float> att(52, 0.0f);  // [W1 32, b1 4, W2 12, b2 3, pad]
+        if (!c.literal_attention)
+            for (int k = 0; k < 51; ++k) att[size_t(k)] = P[size_t(att_off + k)];
+        prev.c[prev.ncopy++] = pcopy(pack_f32(buf, att), f32_bytes(att.size()), kPayAtt);
+        if (i == 0) {  // conditioning layer of the stack
+            std::vector<float> ini = slice(P, init_off, size_t(W * 7 + W));
+            prev.c[prev.ncopy++] = pcopy(pack_f32(buf, ini), f32_bytes(ini.size()), kPayInit);
+        }
+        (void)tau;
+    };
+    steps.push_back(Step{});  // step 0: payload of the first FC-1 step only
     for (int tau = 0; tau < 3; ++tau) {
         for (int kind = 0; kind < 2; ++kind) {
             const int64_t init_off = L.stack_off[kind][tau];
             int64_t off = init_off + W * 7 + W;
             for (int i = 0; i < S.nl[kind]; ++i) {
-                std::vector<float> simt(84, 0.0f);  // [W1 32, b1 4, W2 12, b2 3, pad] + FC-1 bias [32]
-                if (!c.literal_attention) {
-                    for (int k = 0; k < 51; ++k) simt[size_t(k)] = P[size_t(off + k)];
-                    off += 51;
-                }
+                const int64_t att_off = off;
+                if (!c.literal_attention) off += 51;
+                add_payload(kind, tau, i, att_off, init_off);
                 const int cnt = S.counts[kind][i];
                 const int K = W + cnt + 2, kf = S.kf[kind][i];
-                for (int k = 0; k < W; ++k) simt[size_t(52 + k)] = P[size_t(off + int64_t(W) * K + k)];
                 Step st{};
                 st.k2 = kf;
                 st.c[0] = pcopy(pack_blob(buf, P.data() + off, W, W, K, 0, W), W * W * 2, kSlotW1a);
                 st.c[1] = pcopy(pack_blob(buf, P.data() + off, W, cnt + 2, K, W, kf), uint32_t(W * kf * 2), kSlotW1b);
                 st.c[2] = Copy{1, uint32_t(kSlotFeat), uint32_t(kUmmaM * kf * 2), 0, S.seg_prefix[kind][i][tau],
                                int64_t(kUmmaM) * kf * 2};
-                st.c[3] = Copy{2, uint32_t(kSlotMM), uint32_t(kUmmaM * 8 * 4), 0, S.mm_layer[kind][i], 4096};
-                st.c[4] = pcopy(pack_f32(buf, simt), f32_bytes(simt.size()), kSlotAtt);
-                st.ncopy = 5;
-                if (i == 0) {  // conditioning layer of the stack
-                    std::vector<float> ini = slice(P, init_off, size_t(W * 7 + W));
-                    st.c[5] = pcopy(pack_f32(buf, ini), f32_bytes(ini.size()), kSlotInit);
-                    st.ncopy = 6;
-                }
+                st.c[3] = pcopy(pack_f32(buf, slice(P, off + int64_t(W) * K, W)), f32_bytes(W), kSlotB1);
+                st.ncopy = 4;
                 push(st);
                 off += int64_t(W) * K + W;
                 Step s2{};
                 s2.k2 = W;
                 s2.c[0] = pcopy(pack_blob(buf, P.data() + off, W, W, W, 0, W), W * W * 2, 0);
-                s2.c[1] = pcopy(pack_f32(buf, slice(P, off + W * W, W)), f32_bytes(W), 2048);
+                s2.c[1] = pcopy(pack_f32(buf, slice(P, off + W * W, W)), f32_bytes(W), kSlotB2);
                 s2.ncopy = 2;
                 push(s2);
                 off += W * W + W;
@@ -501,9 +627,10 @@ void tc_prepare(sf_backbone& b, cudaStream_t s) {
         const int64_t mo = L.merge_off + int64_t(tau) * (64 * 64 + 64);
         Step sm{};
         sm.k2 = 64;
-        sm.c[0] = pcopy(pack_blob(buf, P.data() + mo, 64, 64, 64, 0, 64), 8192, 0);
-        sm.c[1] = pcopy(pack_f32(buf, slice(P, mo + 64 * 64, 64)), f32_bytes(64), kSlotBias);
-        sm.ncopy = 2;
+        sm.c[0] = pcopy(pack_blob(buf, P.data() + mo, 64, 32, 64, 0, 32), 4096, 0);
+        sm.c[1] = pcopy(pack_blob(buf, P.data() + mo, 64, 32, 64, 32, 32), 4096, kSlotWmHi);
+        sm.c[2] = pcopy(pack_f32(buf, slice(P, mo + 64 * 64, 64)), f32_bytes(64), kSlotBias);
+        sm.ncopy = 3;
         push(sm);
         Step sc{};
         sc.k2 = 64;
@@ -529,6 +656,10 @@ void tc_prepare(sf_backbone& b, cudaStream_t s) {
         push(sh);
     }
     if (steps.size() > size_t(kMaxSteps)) fail(SF_ERR_INVALID_ARGUMENT, "tc backbone: too many layers");
+    for (Step& st : steps) {
+        st.total = 0;
+        for (int k = 0; k < st.ncopy; ++k) st.total += st.c[k].bytes;
+    }
     TcDesc& d = pk->desc;
     d.nl[0] = S.nl[0];
     d.nl[1] = S.nl[1];
@@ -537,10 +668,13 @@ void tc_prepare(sf_backbone& b, cudaStream_t s) {
     d.literal = c.literal_attention;
     d.gamma = c.gamma;
     d.n_steps = int(steps.size());
-    for (size_t j = 0; j < steps.size(); ++j) d.steps[j] = steps[j];
     d.prof = std::getenv("SF_DEBUG_TC") != nullptr;
+    const size_t blob_bytes = (buf.size() + 255) & ~size_t(255);
+    buf.resize(blob_bytes + steps.size() * sizeof(Step));
+    std::memcpy(buf.data() + blob_bytes, steps.data(), steps.size() * sizeof(Step));
     SFB_CUDA(cudaMalloc(&pk->d_blobs, buf.size()));
     SFB_CUDA(cudaMemcpy(pk->d_blobs, buf.data(), buf.size(), cudaMemcpyHostToDevice));
+    d.steps = reinterpret_cast<const Step*>(pk->d_blobs + blob_bytes);
     b.tc = pk.release();
 }
 
@@ -556,11 +690,17 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
                         float* y, double* F, cudaStream_t s) {
     if (n <= 0) return;
     auto pk = static_cast<const TcPack*>(b.tc);
-    const size_t smem = 1024 + kUmmaM * 32 * 2 + kUmmaM * 64 * 2 + size_t(kSlots) * kSlotBytes;
-    static bool attr_set = false;
-    if (!attr_set) {
+    size_t smem = 1024 + 2 * kUmmaM * 32 * 2 + kUmmaM * 64 * 2 + size_t(kSlots) * kSlotBytes;
+    static const bool solo = std::getenv("SF_DEBUG_TC") && std::atoi(std::getenv("SF_DEBUG_TC")) == 2;
+    if (solo) smem = 200 * 1024;  // one CTA per SM: uncontended chain latency
+    static size_t attr_set = 0;
+    if (attr_set != smem) {
         SFB_CUDA(cudaFuncSetAttribute(k_backbone_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        attr_set = true;
+        attr_set = smem;
+        int per_sm = 0;  // the design assumes two co-resident tiles per SM (registers, smem, 2 x 256 TMEM cols)
+        SFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backbone_tc, kThreads, smem));
+        if (per_sm < 2 && !std::getenv("SF_DEBUG_TC"))
+            std::fprintf(stderr, "libsf_b200: k_backbone_tc occupancy %d CTA/SM (expected 2)\n", per_sm);
     }
     const int n_tiles = int((n + kUmmaM - 1) / kUmmaM);
     k_backbone_tc<<<n_tiles, kThreads, smem, s>>>(pk->desc, pk->d_blobs, ops, reinterpret_cast<const uint8_t*>(mms),

@@ -1,6 +1,6 @@
 """Per-phase cycle breakdown of tensor-core backbone CTA 0 (SF_DEBUG_TC=1)."""
 import ctypes, os, sys
-os.environ["SF_DEBUG_TC"] = "1"
+os.environ["SF_DEBUG_TC"] = sys.argv[1] if len(sys.argv) > 1 else "1"
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
 import paper_2401_14051_b200 as sf
@@ -20,6 +20,8 @@ sf.lib.sf_debug_tc_profile(buf)
 for _ in range(5): sf.query(sc, net, med, c, sf.BF16, F_out=F)
 torch.cuda.synchronize()
 sf.lib.sf_debug_tc_profile(buf)
-names = ["acq_fc1", "attention", "mma_fc1", "epi_fc1", "acq_fc2", "mma_fc2", "epi_fc2", "loop_other", "total"]
-v = [buf[i] / 5 for i in range(9)]
+names = ["wait_full1", "mma_fc1", "epi_fc1", "wait_full2", "issue_fc2", "attention", "wait_fc2", "epi_fc2+loop", "total"]
+v = [buf[i] / 5 for i in range(16)]
 print({n: int(x) for n, x in zip(names, v)}, "per-layer-step avg (36 layers):", {n: int(x / 36) for n, x in zip(names[:7], v[:7])})
+n_mma = max(v[13], 1)
+print("run_mma per call (cycles):", {k: int(v[i] / n_mma) for k, i in (("sync", 9), ("prefetch", 10), ("issue", 11), ("wait", 12))}, "calls", n_mma)
