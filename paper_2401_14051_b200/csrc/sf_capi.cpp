@@ -60,7 +60,22 @@ struct Scratch {
     Scratch(size_t n, cudaStream_t st) { alloc(n, st); }
     void alloc(size_t n, cudaStream_t st) {
         s = st;
+        keep_pool();
         if (n) SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st));
+    }
+    // Per-call scratch comes from the device's stream-ordered pool; keep its memory mapped
+    // between calls (the default release threshold of 0 unmaps it at every synchronise,
+    // and re-mapping ~100 MB of operand blocks per query batch costs more than the batch).
+    static void keep_pool() {
+        static thread_local int done_dev = -1;
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        done_dev = dev;
     }
     ~Scratch() {
         if (p) cudaFreeAsync(p, s);
@@ -877,6 +892,32 @@ void check_precision(const sf_backbone& b, int precision, cudaStream_t s) {
     sfb::tc_prepare(const_cast<sf_backbone&>(b), s);
 }
 
+// Second stream + events for the pipelined bf16 query (one set per process; calls serialise on it).
+struct PipeStreams {
+    std::mutex mu;
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ready = nullptr, done[2] = {nullptr, nullptr};
+};
+PipeStreams& pipe_streams() {
+    static PipeStreams* ps = [] {
+        auto* p = new PipeStreams;
+        SFB_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+        SFB_CUDA(cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming));
+        for (auto& e : p->done) SFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        return p;
+    }();
+    return *ps;
+}
+// tiles per pipelined chunk (SF_PIPE_TILES; default off: measured no gain at C2 once the
+// sample/sort kernel stopped round-tripping its scratch through a third phase)
+int64_t pipe_tiles() {
+    static const int64_t t = [] {
+        const char* e = std::getenv("SF_PIPE_TILES");
+        return e ? std::atoll(e) : int64_t(0);
+    }();
+    return t;
+}
+
 // bf16 path over one chunk: fused sample+sort (or sort of given features) -> tcgen05 backbone.
 void run_bf16_chunk(const sf_backbone& b, const sfb::SortLayout& L, const sfb::SceneDev* sc,
                     const sfb::TemplateDev* dt, const sfb::TemplateDev* ht, const float* planes, int n_planes,
@@ -997,14 +1038,21 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
         Out<double> oF(F_out, size_t(n) * 3, stream);
         Out<float> oy(y_out, size_t(n) * 3, stream);
         if (precision == SF_PRECISION_BF16) {
-            // production path: fused sample+sort -> tcgen05 backbone, chunked by tiles
+            // production path: fused sample+sort -> tcgen05 backbone. The queries go in chunks
+            // of tiles through two streams: the backbone of chunk k (latency-bound: a few warps
+            // per SM waiting on tensor-core round trips) runs while chunk k+1 is sampled
+            // (throughput-bound), and chunk k's operand blocks are still L2-resident when read.
             const sfb::SortLayout L = sfb::sort_layout(c);
-            const int64_t chunk = std::min<int64_t>((n + sfb::kUmmaM - 1) / sfb::kUmmaM * sfb::kUmmaM, 1 << 19);
-            const int64_t tiles = chunk / sfb::kUmmaM;
-            Scratch<uint8_t> ops(size_t(tiles) * L.tile_bytes, stream);
-            Scratch<float> mms(size_t(L.n_layers) * tiles * sfb::kUmmaM * 8, stream);
-            Scratch<double> cfg8(size_t(chunk) * 8, stream);
-            Scratch<uint8_t> recs(size_t(chunk) * sfb::query_rec_bytes(), stream);
+            const int64_t n_tiles = (n + sfb::kUmmaM - 1) / sfb::kUmmaM;
+            const int64_t span = std::min<int64_t>(n_tiles, 1 << 13) * sfb::kUmmaM;  // query_prep batch
+            int64_t chunk_tiles = pipe_tiles();
+            if (chunk_tiles <= 0 || chunk_tiles >= n_tiles) chunk_tiles = std::min<int64_t>(n_tiles, 1 << 12);
+            const int64_t chunk = chunk_tiles * sfb::kUmmaM;
+            const int nbuf = chunk < n ? 2 : 1;
+            Scratch<uint8_t> ops(size_t(nbuf) * chunk_tiles * L.tile_bytes, stream);
+            Scratch<float> mms(size_t(nbuf) * L.n_layers * chunk * 8, stream);
+            Scratch<double> cfg8(size_t(span) * 8, stream);
+            Scratch<uint8_t> recs(size_t(span) * sfb::query_rec_bytes(), stream);
             Scratch<int> err(1, stream);
             SFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
             sfb::SceneDev sc = sfb::scene_dev(*s->density, *s->tvol->values, s->d_dt, s->model, *s->table,
@@ -1015,16 +1063,45 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
                 StageScope st(SF_STAGE_CONFIG, stream);
                 sfb::launch_diffuse_light(sc, dt, s->d_planes, s->n_planes, iq.d, s->d_pre, stream);
             }
-            for (int64_t q0 = 0; q0 < n; q0 += chunk) {
-                int64_t m = std::min(chunk, n - q0);
-                const double* qd = iq.d + 9 * q0;
+            PipeStreams& ps = pipe_streams();
+            cudaStream_t aux = nbuf > 1 ? ps.aux : stream;
+            std::lock_guard<std::mutex> plk(ps.mu);
+            int k = 0;
+            for (int64_t p0 = 0; p0 < n; p0 += span) {
+                const int64_t pm = std::min(span, n - p0);
                 {
                     StageScope st(SF_STAGE_CONFIG, stream);
-                    sfb::launch_query_prep(sc, ht, *medium, m, qd, cfg8.p, recs.p, stream);
+                    sfb::launch_query_prep(sc, ht, *medium, pm, iq.d + 9 * p0, cfg8.p, recs.p, stream);
                 }
-                run_bf16_chunk(*b, L, &sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, m, recs.p, nullptr, cfg8.p,
-                               ops.p, mms.p, err.p, oy.d ? oy.d + 3 * q0 : nullptr, oF.d ? oF.d + 3 * q0 : nullptr,
-                               stream);
+                for (int64_t c0 = 0; c0 < pm; c0 += chunk, ++k) {
+                    const int64_t m = std::min(chunk, pm - c0), q0 = p0 + c0;
+                    const int bi = k % nbuf;
+                    uint8_t* ob = ops.p + size_t(bi) * chunk_tiles * L.tile_bytes;
+                    float* mb = mms.p + size_t(bi) * L.n_layers * chunk * 8;
+                    if (k >= nbuf) SFB_CUDA(cudaStreamWaitEvent(stream, ps.done[bi], 0));  // buffer bi free
+                    {
+                        StageScope st(SF_STAGE_SAMPLE_SORT, stream);
+                        sfb::launch_sample_sort(&sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, L, m,
+                                                recs.p + c0 * sfb::query_rec_bytes(), nullptr, ob, mb, err.p, stream);
+                    }
+                    if (aux != stream) {
+                        SFB_CUDA(cudaEventRecord(ps.ready, stream));
+                        SFB_CUDA(cudaStreamWaitEvent(aux, ps.ready, 0));
+                    }
+                    {
+                        StageScope st(SF_STAGE_BACKBONE, aux);
+                        sfb::launch_backbone_tc(*b, m, ob, mb, cfg8.p + 8 * c0, oy.d ? oy.d + 3 * q0 : nullptr,
+                                                oF.d ? oF.d + 3 * q0 : nullptr, aux);
+                    }
+                    if (aux != stream) SFB_CUDA(cudaEventRecord(ps.done[bi], aux));
+                    // the next query_prep batch overwrites cfg8/recs that this chunk's backbone reads
+                    if (aux != stream && c0 + chunk >= pm && p0 + span < n)
+                        SFB_CUDA(cudaStreamWaitEvent(stream, ps.done[bi], 0));
+                }
+            }
+            if (aux != stream) {  // join: every chunk's backbone before the caller's stream continues
+                SFB_CUDA(cudaEventRecord(ps.ready, aux));
+                SFB_CUDA(cudaStreamWaitEvent(stream, ps.ready, 0));
             }
             if (!oF.host && !oy.host && !iq.buf.p) return;  // device in/out: asynchronous (see below)
             int herr = 0;

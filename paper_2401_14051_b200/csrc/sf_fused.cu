@@ -54,6 +54,7 @@ struct SortDesc {
     uint8_t chunk_j[kMaxChunks];
     uint8_t task_seg[2 * kMaxSegs];  // sort tasks by network size; bit 7 = upper half of a 64-wide pair
     int debug;                       // SF_DEBUG_SAMPLE_SORT: 1 skip sampling, 2 skip sort, 4 skip stores
+    int nbuf;                        // scratch buffers (2: one block barrier per group, if 3 blocks/SM still fit)
 };
 
 // Bilinear lookup in a pre-blended phase plane stored as aperture pairs
@@ -351,10 +352,62 @@ __device__ __forceinline__ void merge_desc(float* v) {
     }
 }
 
-// One thread sorts a segment of cnt <= P values in place; returns mean (sequential
-// float sum in sorted order / cnt) and max.
+// Where a sorted segment's operand row goes: chunk j (8 values = 16 bytes) of row
+// `row` in the segment's [128 x kf] canonical block; pools go to the (kind, layer)
+// mean/max row {mean d,p,t, max d,p,t, 0, 0}.
+struct SegOut {
+    uint8_t* blk;
+    int row, kf, tau;
+    float* mm;  // 8 floats
+};
+
+// Value idx of the operand row [sorted (cnt), mean, max, 0...] from the registers of
+// a sorted segment (v holds positions off .. off+P-1).
 template <int P>
-__device__ __forceinline__ void sort_segment(float* seg, int cnt, float& mean, float& mx) {
+__device__ __forceinline__ float row_value(const float* v, int off, int idx, int cnt, float mean, float mx) {
+    const int r = idx - off;
+    float x = idx == cnt ? mean : (idx == cnt + 1 ? mx : 0.0f);
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (r == k && idx < cnt) x = v[k];
+    return x;
+}
+
+// Chunks [j0, j1) of the operand row, written straight from registers (8 threads of
+// consecutive query rows write one 128-byte line).
+template <int P>
+__device__ __forceinline__ void emit_chunks(const float* v, int off, int j0, int j1, int cnt, float mean, float mx,
+                                            const SegOut& o) {
+#pragma unroll
+    for (int j = 0; j < (P + 2 + 15) / 16 * 2; ++j) {
+        const int jj = j0 + j;
+        if (jj >= j1) break;
+        float v8[8];
+        if (off == 0 && 8 * jj + 8 <= P) {  // fully inside the register block: static indices
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int idx = 8 * j + e;  // == 8 * jj + e when j0 == 0
+                v8[e] = idx < cnt ? v[idx < P ? idx : 0] : (idx == cnt ? mean : (idx == cnt + 1 ? mx : 0.0f));
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v8[e] = row_value<P>(v, off, 8 * jj + e, cnt, mean, mx);
+        }
+        store_chunk(o.blk, o.row, jj, o.kf, v8);
+    }
+}
+
+__device__ __forceinline__ void emit_pools(const SegOut& o, float mean, float mx) {
+    o.mm[o.tau] = mean;
+    o.mm[3 + o.tau] = mx;
+    if (o.tau == 0) *reinterpret_cast<float2*>(o.mm + 6) = make_float2(0.0f, 0.0f);
+}
+
+// One thread sorts a segment of cnt <= P values (descending), takes mean (sequential
+// float sum in sorted order / cnt, src/predictor.cpp:176-185) and max, and writes the
+// operand row and pools.
+template <int P>
+__device__ __forceinline__ void sort_emit(const float* seg, int cnt, const SegOut& o, bool store) {
     float v[P];
 #pragma unroll
     for (int j = 0; j < P; ++j) v[j] = j < cnt ? seg[j] : -INFINITY;
@@ -363,18 +416,18 @@ __device__ __forceinline__ void sort_segment(float* seg, int cnt, float& mean, f
 #pragma unroll
     for (int j = 0; j < P; ++j)
         if (j < cnt) acc += v[j];
-#pragma unroll
-    for (int j = 0; j < P; ++j)
-        if (j < cnt) seg[j] = v[j];
-    mean = acc / float(cnt);
-    mx = v[0];
+    const float mean = acc / float(cnt), mx = v[0];
+    if (!store) return;
+    emit_chunks<P>(v, 0, 0, o.kf / 8, cnt, mean, mx, o);
+    emit_pools(o, mean, mx);
 }
 
 // A lane pair sorts a 33..64-value segment: each lane sorts 32 (the upper lane
 // ascending, making the 64 bitonic), one cross-lane compare-exchange, a descending
 // merge per lane; the lower lane's running sum continues on the upper lane, so the
-// sum is exactly sequential in sorted order.
-__device__ __forceinline__ void sort_segment_pair(float* seg, int cnt, bool upper, float& mean, float& mx) {
+// sum is exactly sequential in sorted order. The lower lane emits chunks 0-3, the
+// upper the rest (mean and max land there) and the pools.
+__device__ __forceinline__ void sort_emit_pair(const float* seg, int cnt, bool upper, const SegOut& o, bool store) {
     float v[32];
     const int base = upper ? 32 : 0;
     const unsigned mask = __activemask();  // pair partners always run this branch together
@@ -383,8 +436,8 @@ __device__ __forceinline__ void sort_segment_pair(float* seg, int cnt, bool uppe
     bitonic<32>(v, !upper);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-        const float o = __shfl_xor_sync(mask, v[j], 1);
-        v[j] = upper ? fminf(v[j], o) : fmaxf(v[j], o);
+        const float x = __shfl_xor_sync(mask, v[j], 1);
+        v[j] = upper ? fminf(v[j], x) : fmaxf(v[j], x);
     }
     merge_desc<32>(v);
     float acc = 0.0f;
@@ -392,16 +445,21 @@ __device__ __forceinline__ void sort_segment_pair(float* seg, int cnt, bool uppe
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc += v[j];
     acc = __shfl_xor_sync(mask, acc, 1);
-    mx = __shfl_xor_sync(mask, v[0], 1);
+    const float mx = __shfl_xor_sync(mask, v[0], 1);
+    float mean = 0.0f;
     if (upper) {
 #pragma unroll
         for (int j = 0; j < 32; ++j)
             if (32 + j < cnt) acc += v[j];
         mean = acc / float(cnt);
     }
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-        if (base + j < cnt) seg[base + j] = v[j];
+    if (!store) return;
+    if (!upper) {
+        emit_chunks<32>(v, 0, 0, 4, cnt, mean, mx, o);
+    } else {
+        emit_chunks<32>(v, 32, 4, o.kf / 8, cnt, mean, mx, o);
+        emit_pools(o, mean, mx);
+    }
 }
 
 __global__ void __launch_bounds__(kWarps * 32, 3)
@@ -414,7 +472,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
     for (int i = threadIdx.x; i < plane_floats / 2; i += blockDim.x) planes[i] = planes_g[i];
     __shared__ int s_scr[kMaxSegs], s_n[kMaxSegs], s_kf[kMaxSegs];
     __shared__ int64_t s_prefix[kMaxSegs];
-    __shared__ uint8_t s_cseg[kMaxChunks], s_cj[kMaxChunks], s_task[2 * kMaxSegs];
+    __shared__ uint8_t s_task[2 * kMaxSegs];
     for (int i = threadIdx.x; i < d.n_segs; i += blockDim.x) {
         s_scr[i] = d.seg_scr[i];
         s_n[i] = d.seg_n[i];
@@ -422,27 +480,43 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
         s_prefix[i] = d.seg_prefix[i];
     }
     for (int i = threadIdx.x; i < d.n_tasks; i += blockDim.x) s_task[i] = d.task_seg[i];
-    for (int i = threadIdx.x; i < d.n_chunks; i += blockDim.x) {
-        s_cseg[i] = d.chunk_seg[i];
-        s_cj[i] = d.chunk_j[i];
-    }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* scr_all = sm + plane_floats;              // [8][scr_floats]
-    float* pools = scr_all + kWarps * d.scr_floats;  // [8][n_segs][2]
+    // nbuf scratch buffers [8][scr_floats]: with two, group g+1 is sampled while g is still
+    // being sorted by other warps and one block barrier per group suffices
+    float* scr_buf = sm + plane_floats;
+    QueryCtx* s_qc =
+        reinterpret_cast<QueryCtx*>(sm + ((plane_floats + d.nbuf * kWarps * d.scr_floats + 3) & ~3));  // [2][8]
     const int64_t q_pad = int64_t(d.n_tiles) * kUmmaM;
     const int64_t n_groups = q_pad / kWarps;
+    // per-warp prefetch of a group's query context (cp.async, 12 x 16 bytes)
+    auto prefetch_ctx = [&](int64_t grp, int buf) {
+        const int64_t q = grp * kWarps + warp;
+        if (recs != nullptr && grp < n_groups && q < n && lane < int(sizeof(QueryCtx) / 16)) {
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_qc[buf * kWarps + warp])) + 16 * lane;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst),
+                         "l"(reinterpret_cast<const char*>(recs + q) + 16 * lane)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     __syncthreads();
+    prefetch_ctx(blockIdx.x, 0);
 
-    for (int64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    int it = 0;
+    for (int64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x, ++it) {
         const int64_t q0 = grp * kWarps;
-        // ---- phase 1: features of query q0 + warp
+        float* scr_all = scr_buf + (d.nbuf == 2 ? (it & 1) : 0) * kWarps * d.scr_floats;
+        // ---- phase 1: features of query q0 + warp (warp-private; overlaps other warps' sorts)
         {
             float* scr = scr_all + warp * d.scr_floats;
             const int64_t q = q0 + warp;
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            const QueryCtx& qc = s_qc[(it & 1) * kWarps + warp];
+            prefetch_ctx(grp + gridDim.x, (it + 1) & 1);  // next group's context lands during this one
             if (q >= n || (d.debug & 1)) {
                 for (int i = lane; i < 3 * d.ntot; i += 32) scr[i] = 0.0f;
             } else if (recs != nullptr) {
-                const QueryCtx qc = recs[q];
                 if (!qc.ok && lane == 0) atomicExch(err, 1);
                 const bool same_light = qc.same_light != 0;
                 for (int i = lane; i < d.ntot; i += 32) {
@@ -461,63 +535,38 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
             }
         }
         __syncthreads();
-        // ---- phase 2: register sorts + pools, tasks ordered by network size
-        for (int t = threadIdx.x; t < ((d.debug & 2) ? 0 : d.n_tasks * kWarps); t += blockDim.x) {
-            const int task = s_task[t / kWarps];
-            const int s = task & 0x7f;
-            const int cnt = s_n[s];
-            float mean = 0.0f, mx = 0.0f;
-            if (cnt > 32) {
-                // a 64-wide segment owns two task slots = 16 threads: (query w, half) = (t%16 / 2, t & 1)
-                const int w = (t % (2 * kWarps)) >> 1;
-                const bool upper = t & 1;
-                float* seg = scr_all + w * d.scr_floats + s_scr[s];
-                sort_segment_pair(seg, cnt, upper, mean, mx);
-                if (upper) {
-                    pools[(w * d.n_segs + s) * 2] = mean;
-                    pools[(w * d.n_segs + s) * 2 + 1] = mx;
-                }
-            } else {
-                const int w = t % kWarps;
-                float* seg = scr_all + w * d.scr_floats + s_scr[s];
-                if (cnt <= 8)
-                    sort_segment<8>(seg, cnt, mean, mx);
-                else if (cnt <= 16)
-                    sort_segment<16>(seg, cnt, mean, mx);
-                else
-                    sort_segment<32>(seg, cnt, mean, mx);
-                pools[(w * d.n_segs + s) * 2] = mean;
-                pools[(w * d.n_segs + s) * 2 + 1] = mx;
-            }
-        }
-        __syncthreads();
-        // ---- phase 3: operand chunks (8 rows = 128 contiguous bytes) and pools
+        // ---- phase 2: register sorts, tasks ordered by network size; each thread writes its
+        // segment's operand chunks (8 consecutive threads = 8 query rows = one 128-byte line)
+        // and pools straight from registers
         const int64_t tile = q0 / kUmmaM;
         const int row0 = int(q0 % kUmmaM);
-        for (int t = threadIdx.x; t < ((d.debug & 4) ? 0 : d.n_chunks * kWarps); t += blockDim.x) {
-            const int c = t / kWarps, w = t % kWarps;
-            const int s = s_cseg[c], j = s_cj[c];
-            const float* seg = scr_all + w * d.scr_floats + s_scr[s];
-            const float* pl = pools + (w * d.n_segs + s) * 2;
-            const int cnt = s_n[s], kf = s_kf[s];
-            float v8[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int idx = 8 * j + e;
-                v8[e] = idx < cnt ? seg[idx] : (idx == cnt ? pl[0] : (idx == cnt + 1 ? pl[1] : 0.0f));
-            }
-            uint8_t* blk = ops + s_prefix[s] * d.n_tiles + tile * (int64_t(kUmmaM) * kf * 2);
-            store_chunk(blk, row0 + w, j, kf, v8);
+        const bool store = !(d.debug & 4);
+        for (int t = threadIdx.x; t < ((d.debug & 2) ? 0 : d.n_tasks * kWarps); t += blockDim.x) {
+            const int task = s_task[t / kWarps];
+            const int sg = task & 0x7f;
+            const int cnt = s_n[sg];
+            const bool pair = cnt > 32;
+            // a 64-wide segment owns two task slots = 16 threads: (query w, half) = (t%16 / 2, t & 1)
+            const int w = pair ? (t % (2 * kWarps)) >> 1 : t % kWarps;
+            SegOut o;
+            o.kf = s_kf[sg];
+            o.blk = ops + s_prefix[sg] * d.n_tiles + tile * (int64_t(kUmmaM) * o.kf * 2);
+            o.row = row0 + w;
+            o.tau = sg % 3;
+            o.mm = mms + (int64_t(sg / 3) * q_pad + q0 + w) * 8;
+            const float* seg = scr_all + w * d.scr_floats + s_scr[sg];
+            if (pair)
+                sort_emit_pair(seg, cnt, t & 1, o, store);
+            else if (cnt <= 8)
+                sort_emit<8>(seg, cnt, o, store);
+            else if (cnt <= 16)
+                sort_emit<16>(seg, cnt, o, store);
+            else
+                sort_emit<32>(seg, cnt, o, store);
         }
-        for (int t = threadIdx.x; t < d.n_layers * kWarps; t += blockDim.x) {
-            const int l = t / kWarps, w = t % kWarps;
-            const float* pl = pools + (w * d.n_segs + 3 * l) * 2;  // segments 3l + tau
-            float4* o = reinterpret_cast<float4*>(mms + (int64_t(l) * q_pad + q0 + w) * 8);
-            o[0] = make_float4(pl[0], pl[2], pl[4], pl[1]);
-            o[1] = make_float4(pl[3], pl[5], 0.0f, 0.0f);
-        }
-        __syncthreads();
+        if (d.nbuf == 1) __syncthreads();  // the next group's sampling overwrites this scratch
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 __global__ void k_blend_planes(const float* __restrict__ T, int G, int A, int H, int n_planes, double g0, double g1,
@@ -642,8 +691,19 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
     (void)dt;  // diffuse placement comes from `pre` (k_diffuse_prep)
     if (n <= 0) return;
     SortDesc d = make_desc(sc, n_planes, L, n);
-    const size_t smem =
-        size_t(2 * d.n_planes * d.A * (d.H + 1) + kWarps * d.scr_floats + kWarps * d.n_segs * 2 + 2) * sizeof(float);
+    auto smem_for = [&](int nbuf) {
+        return size_t(2 * d.n_planes * d.A * (d.H + 1) + nbuf * kWarps * d.scr_floats) * sizeof(float) +
+               2 * kWarps * sizeof(QueryCtx) + 16;
+    };
+    static const size_t static_smem = [] {
+        cudaFuncAttributes fa{};
+        SFB_CUDA(cudaFuncGetAttributes(&fa, k_sample_sort));
+        return fa.sharedSizeBytes;
+    }();
+    // 3 blocks/SM (the register limit) within 228 KB, 1 KB reserved per block
+    d.nbuf = 3 * (smem_for(2) + static_smem + 1024) <= 228 * 1024 ? 2 : 1;
+    if (const char* e = std::getenv("SF_SORT_NBUF")) d.nbuf = std::atoi(e) == 1 ? 1 : d.nbuf;
+    const size_t smem = smem_for(d.nbuf);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         SFB_CUDA(cudaFuncSetAttribute(k_sample_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
