@@ -260,6 +260,25 @@ def build_transmittance_volume(pyramid: DensityPyramid, light, weights: Combiner
     return TransmittanceFeatureVolume(h, _normalize(light), weights)
 
 
+def build_transmittance_slab(pyramid: DensityPyramid, light, z0: int, z1: int, weights: CombinerWeights = None,
+                             cfg: FeatureConfig = None, out=None, stream=None):
+    """Level-0 rows [z0, z1) of build_transmittance_volume, bit-identical to the full build's
+    rows (the per-light build sharded by z-slab). `out`: a CUDA tensor
+    [(z1-z0), ny, nx] float32 to fill in place (stays on the device), else returns numpy."""
+    cfg = cfg or FeatureConfig()
+    weights = weights or CombinerWeights.identity(pyramid.level_count())
+    if weights.level_count() != pyramid.level_count():
+        raise ScatterfieldError(7, "combine_transmittance: weight/level mismatch")
+    k = np.ascontiguousarray(weights.kernels, np.float32)
+    s = np.ascontiguousarray(weights.scales, np.float32)
+    g0 = pyramid.level(0)
+    nx, ny, _ = g0.dims
+    dst = out if out is not None else np.empty((max(z1 - z0, 0), ny, nx), np.float32)
+    check(lib.sf_build_transmittance_slab(pyramid._h, dvec(light), ptr(k), ptr(s), float(cfg.lambda_),
+                                          float(cfg.step_scale), int(z0), int(z1), ptr(dst), stream_ptr(stream)))
+    return dst
+
+
 def light_entry_point(bounds, p, light):
     """light_entry_point (src/feature_pipeline.cpp:130-137)."""
     out = (C.c_double * 3)()

@@ -49,21 +49,65 @@ __global__ void k_pyramid_down(const float* __restrict__ src, int sx, int sy, in
     }
 }
 
+// Per-level x-pair copy of a density level in FP64: {double(v(x)), double(v(min(x+1, nx-1)))}.
+// The march below then reads the 8 corners of a trilinear cell as 4 16-byte loads with the
+// float->double conversions done once per voxel instead of once per sample.
+__global__ void k_xpair_f64(const float* __restrict__ v, int nx, int ny, int nz, double2* __restrict__ out) {
+    const int n = nx * ny * nz;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int x = i % nx;
+        out[i] = make_double2(double(v[i]), double(v[x + 1 < nx ? i + 1 : i]));
+    }
+}
+
+// DensityGrid::sample_trilinear (src/volume_grid.cpp:40-62) on the x-pair copy: the same FP64
+// operations in the same order as sf_device.cuh trilinear(). At x0 = -1 the reference lerps
+// v(0) with itself; the pair at 0 is {v(0), v(1)}, so tx = 0 gives v(0) + 0 * (v(1) - v(0)) =
+// v(0) exactly. At x0 = nx-1 the pair is {v(nx-1), v(nx-1)} as in the reference.
+__device__ __forceinline__ double trilinear_xp(const GridDev& g, const double2* __restrict__ xp, double px,
+                                               double py, double pz) {
+    if (!in_box(g, px, py, pz)) return 0.0;
+    double fx, fy, fz;
+    if (g.ivs != 0.0) {
+        fx = (px - g.ox) * g.ivs - 0.5;
+        fy = (py - g.oy) * g.ivs - 0.5;
+        fz = (pz - g.oz) * g.ivs - 0.5;
+    } else {
+        fx = (px - g.ox) / g.vs - 0.5;
+        fy = (py - g.oy) / g.vs - 0.5;
+        fz = (pz - g.oz) / g.vs - 0.5;
+    }
+    const double flx = floor(fx), fly = floor(fy), flz = floor(fz);
+    const int x0 = int(flx), y0 = int(fly), z0 = int(flz);
+    double tx = fx - flx;
+    const double ty = fy - fly, tz = fz - flz;
+    if (x0 < 0) tx = 0.0;
+    const int xc = x0 < 0 ? 0 : x0;
+    const int ya = clampi(y0, 0, g.ny - 1), yb = clampi(y0 + 1, 0, g.ny - 1);
+    const int za = clampi(z0, 0, g.nz - 1), zb = clampi(z0 + 1, 0, g.nz - 1);
+    const double2 r00 = __ldg(xp + (za * g.ny + ya) * g.nx + xc), r10 = __ldg(xp + (za * g.ny + yb) * g.nx + xc);
+    const double2 r01 = __ldg(xp + (zb * g.ny + ya) * g.nx + xc), r11 = __ldg(xp + (zb * g.ny + yb) * g.nx + xc);
+    const double c00 = lerp1(r00.x, r00.y, tx), c10 = lerp1(r10.x, r10.y, tx);
+    const double c01 = lerp1(r01.x, r01.y, tx), c11 = lerp1(r11.x, r11.y, tx);
+    return lerp1(lerp1(c00, c10, ty), lerp1(c01, c11, ty), tz);
+}
+
 // K2: graded transmittance of one level (src/feature_pipeline.cpp:37-68) with the
-// midpoint-rule optical depth (src/volume_grid.cpp:64-78). One thread per voxel;
-// neighbouring threads march neighbouring parallel rays, so the trilinear
-// gathers of a warp stay within a few cache lines.
-__global__ void k_graded(GridDev g, double tsx, double tsy, double tsz, double coeff,
-                         double step, float* __restrict__ out) {
-    size_t n = size_t(g.nx) * g.ny * g.nz;
+// midpoint-rule optical depth (src/volume_grid.cpp:64-78), for voxel rows z in [zlo, zhi)
+// (a z-slab when the build is sharded over GPUs). One thread per voxel; neighbouring
+// threads march neighbouring parallel rays, so a warp's gathers stay within a few lines.
+// FP64 throughout, as the reference: the kernel is FP64-pipe bound.
+__global__ void k_graded(GridDev g, const double2* __restrict__ xp, double tsx, double tsy, double tsz,
+                         double coeff, double step, int zlo, int zhi, float* __restrict__ out) {
+    const int plane = g.nx * g.ny;
+    const int i0 = zlo * plane, i1 = zhi * plane;
     const double lo[3] = {g.ox, g.oy, g.oz};
     const double hi[3] = {g.hx, g.hy, g.hz};
     const double ts[3] = {tsx, tsy, tsz};
-    for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < n;
-         idx += size_t(gridDim.x) * blockDim.x) {
-        int x = int(idx % g.nx);
-        int y = int((idx / g.nx) % g.ny);
-        int z = int(idx / (size_t(g.nx) * g.ny));
+    for (int idx = i0 + blockIdx.x * blockDim.x + threadIdx.x; idx < i1; idx += gridDim.x * blockDim.x) {
+        const int x = idx % g.nx;
+        const int y = (idx / g.nx) % g.ny;
+        const int z = idx / plane;
         double p[3] = {g.ox + (x + 0.5) * g.vs, g.oy + (y + 0.5) * g.vs, g.oz + (z + 0.5) * g.vs};
         double t0, t1, tau = 0.0;
         if (intersect_box(lo, hi, p, ts, t0, t1) && t1 > 0.0) {
@@ -79,7 +123,7 @@ __global__ void k_graded(GridDev g, double tsx, double tsy, double tsz, double c
                 double sum = 0.0;
                 for (int i = 0; i < ns; ++i) {
                     double s = (i + 0.5) * h;
-                    sum += trilinear(g, p[0] + dir[0] * s, p[1] + dir[1] * s, p[2] + dir[2] * s);
+                    sum += trilinear_xp(g, xp, p[0] + dir[0] * s, p[1] + dir[1] * s, p[2] + dir[2] * s);
                 }
                 tau = sum * h;
             }
@@ -94,10 +138,10 @@ struct Kernel27 {
 
 // K3a: conv3_replicate (src/feature_pipeline.cpp:70-92); FP64 accumulation in
 // tap order dz, dy, dx.
-__global__ void k_conv3(const float* __restrict__ in, int nx, int ny, int nz, Kernel27 k,
+__global__ void k_conv3(const float* __restrict__ in, int nx, int ny, int nz, Kernel27 k, int zlo, int zhi,
                         float* __restrict__ out) {
-    size_t n = size_t(nx) * ny * nz;
-    for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < n;
+    const size_t n = size_t(nx) * ny * zhi;
+    for (size_t idx = size_t(nx) * ny * zlo + blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < n;
          idx += size_t(gridDim.x) * blockDim.x) {
         int x = int(idx % nx);
         int y = int((idx / nx) % ny);
@@ -130,9 +174,10 @@ struct Levels {
 // level-0 voxel centre, FP64 trilinear of each convolved level, scaled, then
 // accumulated in float in level order. One pass over all levels per voxel keeps
 // the float accumulation order of the reference while writing the output once.
-__global__ void k_combine(Levels lv, GridDev base, float* __restrict__ out) {
-    size_t n = size_t(base.nx) * base.ny * base.nz;
-    for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < n;
+__global__ void k_combine(Levels lv, GridDev base, int zlo, int zhi, float* __restrict__ out) {
+    const size_t off = size_t(base.nx) * base.ny * zlo;
+    const size_t n = size_t(base.nx) * base.ny * zhi;
+    for (size_t idx = off + blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < n;
          idx += size_t(gridDim.x) * blockDim.x) {
         int x = int(idx % base.nx);
         int y = int((idx / base.nx) % base.ny);
@@ -144,7 +189,7 @@ __global__ void k_combine(Levels lv, GridDev base, float* __restrict__ out) {
             double v = trilinear(lv.g[li], c[0], c[1], c[2]);
             acc += float(lv.scale[li] * v);
         }
-        out[idx] = acc;
+        out[idx - off] = acc;
     }
 }
 
@@ -230,24 +275,34 @@ void launch_pyramid_down(const sf_grid& src, sf_grid& dst, cudaStream_t s) {
     count_launch();
 }
 
-void launch_graded(const sf_grid& level, const double ts[3], double coeff, double step,
+void launch_graded(const sf_grid& level, const double ts[3], double coeff, double step, int zlo, int zhi,
                    float* out, cudaStream_t s) {
-    k_graded<<<grid_for(level.count(), 128), 128, 0, s>>>(level.dev(), ts[0], ts[1], ts[2],
-                                                          coeff, step, out);
+    if (zhi <= zlo) return;
+    double2* xp = nullptr;
+    SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xp), level.count() * sizeof(double2), s));
+    k_xpair_f64<<<grid_for(level.count()), kBlock, 0, s>>>(level.d, level.nx, level.ny, level.nz, xp);
     SFB_CUDA(cudaGetLastError());
     count_launch();
+    const size_t rows = size_t(level.nx) * level.ny * size_t(zhi - zlo);
+    k_graded<<<grid_for(rows, 128), 128, 0, s>>>(level.dev(), xp, ts[0], ts[1], ts[2], coeff, step, zlo, zhi, out);
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+    SFB_CUDA(cudaFreeAsync(xp, s));
 }
 
-void launch_conv3(const sf_grid& in, const float k27[27], float* out, cudaStream_t s) {
+void launch_conv3(const sf_grid& in, const float k27[27], int zlo, int zhi, float* out, cudaStream_t s) {
+    if (zhi <= zlo) return;
     Kernel27 k;
     for (int i = 0; i < 27; ++i) k.k[i] = k27[i];
-    k_conv3<<<grid_for(in.count()), kBlock, 0, s>>>(in.d, in.nx, in.ny, in.nz, k, out);
+    k_conv3<<<grid_for(size_t(in.nx) * in.ny * size_t(zhi - zlo)), kBlock, 0, s>>>(in.d, in.nx, in.ny, in.nz, k, zlo,
+                                                                                   zhi, out);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
 
 void launch_combine(const std::vector<const sf_grid*>& conv, const std::vector<float>& scales,
-                    const sf_grid& base, float* out, cudaStream_t s) {
+                    const sf_grid& base, int zlo, int zhi, float* out, cudaStream_t s) {
+    if (zhi <= zlo) return;
     if (conv.size() > size_t(kMaxLevels)) fail(SF_ERR_INVALID_ARGUMENT, "combine: too many levels");
     Levels lv{};
     lv.n = int(conv.size());
@@ -255,7 +310,8 @@ void launch_combine(const std::vector<const sf_grid*>& conv, const std::vector<f
         lv.g[i] = conv[size_t(i)]->dev();
         lv.scale[i] = double(scales[size_t(i)]);
     }
-    k_combine<<<grid_for(base.count()), kBlock, 0, s>>>(lv, base.dev(), out);
+    k_combine<<<grid_for(size_t(base.nx) * base.ny * size_t(zhi - zlo)), kBlock, 0, s>>>(lv, base.dev(), zlo, zhi,
+                                                                                         out);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }

@@ -145,8 +145,32 @@ sf_grid* new_grid(int nx, int ny, int nz, double vs, const double o[3]) {
 
 void free_grid(sf_grid* g) {
     if (!g) return;
-    if (g->owned && g->d) cudaFree(g->d);
+    if (g->owned && g->d) {
+        if (g->pooled)
+            cudaFreeAsync(g->d, g->pool_stream);
+        else
+            cudaFree(g->d);
+    }
     delete g;
+}
+
+// Intermediate grid of a build (graded fields, conv outputs): stream-ordered pool memory,
+// so allocating and freeing it never synchronises the device.
+sf_grid* new_scratch_grid(int nx, int ny, int nz, double vs, const double o[3], cudaStream_t s) {
+    auto g = std::make_unique<sf_grid>();
+    g->nx = nx;
+    g->ny = ny;
+    g->nz = nz;
+    g->vs = vs;
+    for (int i = 0; i < 3; ++i) {
+        g->origin[i] = o[i];
+        g->hi[i] = o[i] + (i == 0 ? nx : i == 1 ? ny : nz) * vs;
+    }
+    Scratch<float>::keep_pool();
+    SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g->d), g->count() * sizeof(float), s));
+    g->pooled = true;
+    g->pool_stream = s;
+    return g.release();
 }
 
 bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
@@ -451,19 +475,43 @@ int sf_pyramid_build(const sf_grid* finest, sf_pyramid** out, sf_stream stream) 
         auto cleanup = [&] {
             for (sf_grid* l : p->levels) free_grid(l);
             p->levels.clear();
+            if (p->block) cudaFree(p->block);
+            p->block = nullptr;
         };
         try {
-            sf_grid* l0 = new_grid(finest->nx, finest->ny, finest->nz, finest->vs, finest->origin);
-            p->levels.push_back(l0);
-            SFB_CUDA(cudaMemcpyAsync(l0->d, finest->d, l0->count() * sizeof(float),
-                                     cudaMemcpyDeviceToDevice, stream));
-            while (std::max({p->levels.back()->nx, p->levels.back()->ny, p->levels.back()->nz}) > 1) {
-                const sf_grid* src = p->levels.back();
-                sf_grid* dst = new_grid(std::max(1, src->nx / 2), std::max(1, src->ny / 2),
-                                        std::max(1, src->nz / 2), src->vs * 2.0, src->origin);
-                p->levels.push_back(dst);
-                sfb::launch_pyramid_down(*src, *dst, stream);
+            // level dims (build_pyramid, src/volume_grid.cpp:91-130: halve until max dim 1)
+            std::vector<int> dims{finest->nx, finest->ny, finest->nz};
+            size_t total = 0;
+            for (int nx = finest->nx, ny = finest->ny, nz = finest->nz;;) {
+                total += size_t(nx) * ny * nz;
+                if (std::max({nx, ny, nz}) <= 1) break;
+                nx = std::max(1, nx / 2);
+                ny = std::max(1, ny / 2);
+                nz = std::max(1, nz / 2);
+                dims.insert(dims.end(), {nx, ny, nz});
             }
+            SFB_CUDA(cudaMalloc(&p->block, total * sizeof(float)));
+            size_t off = 0;
+            double vs = finest->vs;
+            for (size_t l = 0; l < dims.size() / 3; ++l, vs *= 2.0) {
+                auto g = std::make_unique<sf_grid>();
+                g->nx = dims[3 * l];
+                g->ny = dims[3 * l + 1];
+                g->nz = dims[3 * l + 2];
+                g->vs = vs;
+                for (int i = 0; i < 3; ++i) {
+                    g->origin[i] = finest->origin[i];
+                    g->hi[i] = finest->origin[i] + (i == 0 ? g->nx : i == 1 ? g->ny : g->nz) * vs;
+                }
+                g->d = p->block + off;
+                g->owned = false;
+                off += g->count();
+                p->levels.push_back(g.release());
+            }
+            SFB_CUDA(cudaMemcpyAsync(p->levels[0]->d, finest->d, finest->count() * sizeof(float),
+                                     cudaMemcpyDeviceToDevice, stream));
+            for (size_t l = 1; l < p->levels.size(); ++l)
+                sfb::launch_pyramid_down(*p->levels[l - 1], *p->levels[l], stream);
             sync(stream);
         } catch (...) {
             cleanup();
@@ -483,6 +531,7 @@ const sf_grid* sf_pyramid_level(const sf_pyramid* p, int level) {
 void sf_pyramid_destroy(sf_pyramid* p) {
     if (!p) return;
     for (sf_grid* l : p->levels) free_grid(l);
+    if (p->block) cudaFree(p->block);
     delete p;
 }
 
@@ -496,7 +545,7 @@ void normalize3(const double l[3], double o[3]) {
 }
 
 sf_grid* graded_level(const sf_pyramid* p, int level, const double light[3], double lambda,
-                      double step, cudaStream_t s) {
+                      double step, cudaStream_t s, bool scratch = false, int zlo = 0, int zhi = -1) {
     if (level < 0 || level >= int(p->levels.size()))
         fail(SF_ERR_INVALID_ARGUMENT, "graded_transmittance: invalid level");
     if (!(lambda > 0.0 && lambda < 1.0))
@@ -507,9 +556,10 @@ sf_grid* graded_level(const sf_pyramid* p, int level, const double light[3], dou
     normalize3(light, ld);
     double ts[3] = {-ld[0], -ld[1], -ld[2]};
     double coeff = std::pow(lambda, level + 1);
-    sf_grid* out = new_grid(rho->nx, rho->ny, rho->nz, rho->vs, rho->origin);
+    sf_grid* out = scratch ? new_scratch_grid(rho->nx, rho->ny, rho->nz, rho->vs, rho->origin, s)
+                           : new_grid(rho->nx, rho->ny, rho->nz, rho->vs, rho->origin);
     try {
-        sfb::launch_graded(*rho, ts, coeff, step, out->d, s);
+        sfb::launch_graded(*rho, ts, coeff, step, zlo, zhi < 0 ? rho->nz : zhi, out->d, s);
     } catch (...) {
         free_grid(out);
         throw;
@@ -517,12 +567,9 @@ sf_grid* graded_level(const sf_pyramid* p, int level, const double light[3], dou
     return out;
 }
 
-sf_tvol* combine(const std::vector<const sf_grid*>& fields, const float* kernels,
-                 const float* scales, const double light[3], cudaStream_t s) {
-    if (fields.empty()) fail(SF_ERR_INVALID_ARGUMENT, "combine_transmittance: no fields");
-    const sf_grid& base = *fields[0];
-    int L = int(fields.size());
-    std::vector<float> K(size_t(L) * 27, 0.0f), S(static_cast<size_t>(L), 0.0f);
+void combiner_weights(int L, const float* kernels, const float* scales, std::vector<float>& K, std::vector<float>& S) {
+    K.assign(size_t(L) * 27, 0.0f);
+    S.assign(size_t(L), 0.0f);
     if (kernels) {
         std::memcpy(K.data(), kernels, K.size() * sizeof(float));
         std::memcpy(S.data(), scales, S.size() * sizeof(float));
@@ -532,28 +579,46 @@ sf_tvol* combine(const std::vector<const sf_grid*>& fields, const float* kernels
             S[size_t(l)] = float(1.0 / L);
         }
     }
-    auto t = std::make_unique<sf_tvol>();
-    normalize3(light, t->light);
-    t->kernels = K;
-    t->scales = S;
+}
+
+// conv3 of every level (level 0 over rows [c0, c1) only) then the combine of level-0 rows
+// [z0, z1) into out.
+void conv_combine(const std::vector<const sf_grid*>& fields, const std::vector<float>& K,
+                  const std::vector<float>& S, int c0, int c1, int z0, int z1, float* out, cudaStream_t s) {
+    const sf_grid& base = *fields[0];
     std::vector<sf_grid*> conv;
     try {
-        for (int l = 0; l < L; ++l) {
-            const sf_grid& f = *fields[size_t(l)];
-            sf_grid* c = new_grid(f.nx, f.ny, f.nz, f.vs, f.origin);
+        for (size_t l = 0; l < fields.size(); ++l) {
+            const sf_grid& f = *fields[l];
+            sf_grid* c = new_scratch_grid(f.nx, f.ny, f.nz, f.vs, f.origin, s);
             conv.push_back(c);
-            sfb::launch_conv3(f, &K[size_t(l) * 27], c->d, s);
+            sfb::launch_conv3(f, &K[l * 27], l == 0 ? c0 : 0, l == 0 ? c1 : f.nz, c->d, s);
         }
-        t->values = new_grid(base.nx, base.ny, base.nz, base.vs, base.origin);
         std::vector<const sf_grid*> cv(conv.begin(), conv.end());
-        sfb::launch_combine(cv, S, base, t->values->d, s);
+        sfb::launch_combine(cv, S, base, z0, z1, out, s);
         sync(s);
     } catch (...) {
         for (sf_grid* c : conv) free_grid(c);
-        if (t->values) free_grid(t->values);
         throw;
     }
     for (sf_grid* c : conv) free_grid(c);
+}
+
+sf_tvol* combine(const std::vector<const sf_grid*>& fields, const float* kernels,
+                 const float* scales, const double light[3], cudaStream_t s) {
+    if (fields.empty()) fail(SF_ERR_INVALID_ARGUMENT, "combine_transmittance: no fields");
+    const sf_grid& base = *fields[0];
+    const int L = int(fields.size());
+    auto t = std::make_unique<sf_tvol>();
+    normalize3(light, t->light);
+    combiner_weights(L, kernels, scales, t->kernels, t->scales);
+    t->values = new_grid(base.nx, base.ny, base.nz, base.vs, base.origin);
+    try {
+        conv_combine(fields, t->kernels, t->scales, 0, base.nz, 0, base.nz, t->values->d, s);
+    } catch (...) {
+        free_grid(t->values);
+        throw;
+    }
     return t.release();
 }
 }  // namespace
@@ -577,7 +642,7 @@ int sf_conv3_replicate(const sf_grid* in, const float kernel[27], sf_grid** out,
     return guard([&] {
         sf_grid* g = new_grid(in->nx, in->ny, in->nz, in->vs, in->origin);
         try {
-            sfb::launch_conv3(*in, kernel, g->d, stream);
+            sfb::launch_conv3(*in, kernel, 0, in->nz, g->d, stream);
             sync(stream);
         } catch (...) {
             free_grid(g);
@@ -606,7 +671,7 @@ int sf_build_transmittance_volume(const sf_pyramid* p, const double light[3], co
         try {
             for (int i = 0; i < int(p->levels.size()); ++i) {
                 double step = step_scale * p->levels[size_t(i)]->vs;
-                fields.push_back(graded_level(p, i, light, lambda, step, stream));
+                fields.push_back(graded_level(p, i, light, lambda, step, stream, true));
             }
             std::vector<const sf_grid*> f(fields.begin(), fields.end());
             *out = combine(f, kernels, scales, light, stream);
@@ -615,6 +680,39 @@ int sf_build_transmittance_volume(const sf_pyramid* p, const double light[3], co
             throw;
         }
         for (sf_grid* g : fields) free_grid(g);
+    });
+}
+
+int sf_build_transmittance_slab(const sf_pyramid* p, const double light[3], const float* kernels,
+                                const float* scales, double lambda, double step_scale, int z0, int z1,
+                                float* out, sf_stream stream) {
+    return guard([&] {
+        const sf_grid& g0 = *p->levels[0];
+        if (z0 < 0 || z1 > g0.nz || z0 > z1) fail(SF_ERR_INVALID_ARGUMENT, "transmittance slab: z range outside the grid");
+        Out<float> o(out, size_t(g0.nx) * g0.ny * size_t(z1 - z0), stream);
+        if (z1 == z0) return;
+        std::vector<sf_grid*> fields;
+        try {
+            // level 0 marched only for the rows the slab's conv and combine read (a 2-row halo:
+            // the combine's trilinear at a level-0 centre may round into the next row), coarser
+            // levels whole (<= 1/8 of the work, computed by every shard)
+            const int c0 = std::max(z0 - 1, 0), c1 = std::min(z1 + 1, g0.nz);
+            const int m0 = std::max(z0 - 2, 0), m1 = std::min(z1 + 2, g0.nz);
+            for (int i = 0; i < int(p->levels.size()); ++i) {
+                const double step = step_scale * p->levels[size_t(i)]->vs;
+                fields.push_back(graded_level(p, i, light, lambda, step, stream, true, i == 0 ? m0 : 0, i == 0 ? m1 : -1));
+            }
+            std::vector<float> K, S;
+            combiner_weights(int(fields.size()), kernels, scales, K, S);
+            std::vector<const sf_grid*> f(fields.begin(), fields.end());
+            conv_combine(f, K, S, c0, c1, z0, z1, o.d, stream);
+        } catch (...) {
+            for (sf_grid* g : fields) free_grid(g);
+            throw;
+        }
+        for (sf_grid* g : fields) free_grid(g);
+        o.finish();
+        sync(stream);
     });
 }
 

@@ -44,6 +44,8 @@ struct sf_grid {
     double hi[3] = {0, 0, 0};  // origin + n*vs (DensityGrid::bounds)
     float* d = nullptr;
     bool owned = true;
+    cudaStream_t pool_stream = nullptr;  // set: stream-ordered scratch, freed with cudaFreeAsync
+    bool pooled = false;
     size_t count() const { return size_t(nx) * ny * nz; }
     sfb::GridDev dev() const {
         int e;
@@ -55,6 +57,7 @@ struct sf_grid {
 
 struct sf_pyramid {
     std::vector<sf_grid*> levels;  // level 0 is a copy of the finest grid
+    float* block = nullptr;        // one allocation holding every level (levels are views)
 };
 
 struct sf_tvol {
@@ -117,11 +120,13 @@ struct sf_scene {
 namespace sfb {
 
 void launch_pyramid_down(const sf_grid& src, sf_grid& dst, cudaStream_t s);
-void launch_graded(const sf_grid& level, const double to_source[3], double coeff, double step,
+// Per-light build kernels over voxel rows z in [zlo, zhi) (the whole grid, or a z-slab of a
+// build sharded over GPUs). launch_combine writes rows [zlo, zhi) to out[0...].
+void launch_graded(const sf_grid& level, const double to_source[3], double coeff, double step, int zlo, int zhi,
                    float* out, cudaStream_t s);
-void launch_conv3(const sf_grid& in, const float k27[27], float* out, cudaStream_t s);
+void launch_conv3(const sf_grid& in, const float k27[27], int zlo, int zhi, float* out, cudaStream_t s);
 void launch_combine(const std::vector<const sf_grid*>& conv, const std::vector<float>& scales,
-                    const sf_grid& base, float* out, cudaStream_t s);
+                    const sf_grid& base, int zlo, int zhi, float* out, cudaStream_t s);
 void launch_interleave(const float* density, const float* tvol, float2* out, size_t n,
                        cudaStream_t s);
 void launch_phase_table(int gr, int ar, int hr, const std::vector<double>& nodes,

@@ -1,4 +1,4 @@
-"""Multi-GPU sharding of shading-point queries.
+"""Multi-GPU sharding of shading-point queries and of the per-light build.
 
 Every query is independent given the replicated inputs (density volume,
 transmittance feature volume, phase table, templates, network weights), so the
@@ -6,6 +6,12 @@ image is split into square tiles dealt round-robin to the ranks (one process per
 GPU); each rank runs the fused query on its tiles and the per-tile radiance is
 gathered once per frame — the only exchange of the path. No collective touches
 the data path itself (weak scaling when every rank owns a fixed number of tiles).
+
+The per-light build (graded transmittance + combiner) is needed whole on every GPU but is
+embarrassingly parallel per voxel: each rank builds a z-slab of the level-0 transmittance
+feature volume (sf_build_transmittance_slab: level 0 marched for the slab plus a halo,
+coarser levels redundantly) and one all_gather assembles the volume on every rank
+(build_tvol_sharded) — bit-identical to the single-GPU build.
 
 Works with any torch.distributed backend: NCCL over NVLink on the B200 box, gloo
 for the CPU tests (tests/test_sharding_gloo.py).
@@ -73,3 +79,45 @@ def query_image(eval_fn, queries, width: int, height: int, tile: int, rank: int,
     if not isinstance(local, torch.Tensor):
         local = torch.as_tensor(np.ascontiguousarray(local))
     return gather_radiance(local, width, height, tile, rank, world, group)
+
+
+def z_slabs(nz: int, world: int):
+    """Contiguous z-row ranges [z0, z1) per rank, sizes differing by at most one row."""
+    base, extra = divmod(nz, world)
+    out, z = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append((z, z + n))
+        z += n
+    return out
+
+
+def gather_slabs(local, nz: int, rank: int, world: int, group=None):
+    """All-gather per-rank z-slabs [z1-z0, ny, nx] into the full [nz, ny, nx] volume on every rank
+    (slabs padded to the largest; NCCL over NVLink on GPUs, gloo in the CPU tests)."""
+    import torch
+    import torch.distributed as dist
+
+    slabs = z_slabs(nz, world)
+    pad = max(z1 - z0 for z0, z1 in slabs)
+    buf = torch.zeros((pad,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    buf[: local.shape[0]] = local
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([parts[r][: z1 - z0] for r, (z0, z1) in enumerate(slabs)], dim=0)
+
+
+def build_tvol_sharded(pyramid, light, rank: int, world: int, weights=None, cfg=None, group=None):
+    """build_transmittance_volume with the level-0 work split by z-slab over the ranks of `group`;
+    returns the TransmittanceFeatureVolume (identical on every rank)."""
+    import torch
+
+    from . import api
+
+    g0 = pyramid.level(0)
+    nx, ny, nz = g0.dims
+    z0, z1 = z_slabs(nz, world)[rank]
+    local = torch.empty((z1 - z0, ny, nx), dtype=torch.float32, device="cuda")
+    api.build_transmittance_slab(pyramid, light, z0, z1, weights, cfg, out=local)
+    full = gather_slabs(local, nz, rank, world, group)
+    return api.TransmittanceFeatureVolume.from_values(full.contiguous(), g0.voxel_size(), g0.origin(), light, weights)

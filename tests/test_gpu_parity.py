@@ -97,6 +97,31 @@ def test_transmittance_volume(small, small_dev):
     assert np.allclose(t3, 3 * t_r, rtol=1e-5)
 
 
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+def test_transmittance_slabs_bit_identical(small, small_dev, world):
+    """Per-light build sharded by z-slab: the slabs of sf_build_transmittance_slab,
+    concatenated, equal the single-GPU build bit for bit (identity and random combiner)."""
+    from paper_2401_14051_b200 import sharding
+    _, pyr = small_dev
+    for w in (None, sf.CombinerWeights(small["kern"], small["scales"])):
+        full = sf.build_transmittance_volume(pyr, LIGHT, w).values.values()
+        parts = [sf.build_transmittance_slab(pyr, LIGHT, z0, z1, w) for z0, z1 in sharding.z_slabs(16, world)]
+        assert np.array_equal(np.concatenate(parts, axis=0), full)
+
+
+def test_transmittance_slab_c1_device_out(c1, c1_scene):
+    import torch
+    from paper_2401_14051_b200.scenes import procedural_cloud
+    _, tv, _ = c1_scene
+    g = sf.DensityGrid.from_array(procedural_cloud(64, 0), 2.0 / 64, ORIGIN)
+    pyr = sf.DensityPyramid(g)
+    out = torch.empty((20, 64, 64), dtype=torch.float32, device="cuda")
+    sf.build_transmittance_slab(pyr, LIGHT, 30, 50, out=out)
+    assert np.array_equal(out.cpu().numpy(), tv.values.values()[30:50])
+    with pytest.raises(sf.ScatterfieldError):
+        sf.build_transmittance_slab(pyr, LIGHT, 50, 65)
+
+
 def test_phase_table_build(small, full_table):
     t = sf.PhaseTable(17, 33, 9, 8).values()
     assert ulp_diff(t, small["table"]).max() <= 1

@@ -82,3 +82,42 @@ def test_two_rank_gloo_matches_single_process(tmp_path):
     rows = scenes.draw_centers(vol, width * height, 5, scenes.LIGHT)
     ref = eval_fn(rows)
     assert np.array_equal(img, ref)
+
+
+# ---- per-light build sharded by z-slab -------------------------------
+def test_z_slabs_partition():
+    for nz, world in ((16, 2), (17, 3), (5, 8), (128, 8), (1, 4)):
+        slabs = sharding.z_slabs(nz, world)
+        assert len(slabs) == world and slabs[0][0] == 0 and slabs[-1][1] == nz
+        assert all(a[1] == b[0] for a, b in zip(slabs, slabs[1:]))
+        sizes = [z1 - z0 for z0, z1 in slabs]
+        assert max(sizes) - min(sizes) <= 1
+
+
+def _slab_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from conftest import ORIGIN
+    from oracle.oracle import Oracle
+    from paper_2401_14051_b200 import scenes
+    vol = scenes.procedural_cloud(16, 3)
+    # per-rank slab from the oracle (stand-in for sf_build_transmittance_slab on a GPU)
+    full = Oracle().build_tvol(vol, 2.0 / 16, ORIGIN, np.array(scenes.LIGHT)).reshape(16, 16, 16)
+    z0, z1 = sharding.z_slabs(16, world)[rank]
+    got = sharding.gather_slabs(torch.from_numpy(np.ascontiguousarray(full[z0:z1])), 16, rank, world)
+    if rank == 0:
+        np.save(out_path, np.stack([got.numpy(), full]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_three_rank_gloo_slab_gather(tmp_path):
+    out = str(tmp_path / "tvol.npy")
+    mp.spawn(_slab_worker, args=(3, _free_port(), out), nprocs=3, join=True)
+    got, full = np.load(out)
+    assert np.array_equal(got, full)
