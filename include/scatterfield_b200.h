@@ -215,6 +215,12 @@ void sf_scene_destroy(sf_scene* s);
 int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium,
              int64_t n, const double* queries, int precision, double* F_out, float* y_out,
              sf_stream stream);
+/* sf_query with a per-query medium (config C4: per-voxel albedo and g sampled at p by the
+ * caller): media h/d [n][4] = {g, albedo r, g, b}; each query uses PhaseModel::hg(g) for its
+ * phase features (sample_features(.., model, ..), feature_pipeline.h:105-110) and
+ * ConfigParams{g = {g}, albedo} for make_config / decode_prediction (predictor.h:20-31, 99). */
+int sf_query_media(const sf_scene* s, const sf_backbone* b, int64_t n, const double* queries,
+                   const double* media, int precision, double* F_out, float* y_out, sf_stream stream);
 
 /* ---- instrumentation (per-stage CUDA-event timing) -------------- */
 enum sf_stage {

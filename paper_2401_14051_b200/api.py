@@ -674,3 +674,18 @@ def query(scene: Scene, net: Backbone, medium: MediumParams, queries, precision=
     check(lib.sf_query(scene._h, net._h, C.byref(m), n, ptr(q), precision, ptr(F_out), ptr(y_out),
                        stream_ptr(stream)))
     return F_out
+
+
+def query_media(scene: Scene, net: Backbone, queries, media, precision=FP32, F_out=None, y_out=None, stream=None):
+    """query() with a per-query medium: media [n, 4] = (g, albedo r, g, b), each query using
+    PhaseModel.hg(g) for its phase features and ConfigParams(g=(g,), albedo) (config C4)."""
+    q = _arr(queries, np.float64)
+    md = _arr(media, np.float64)
+    n = q.shape[0]
+    if md.shape[0] != n or md.shape[-1] != 4:
+        raise ScatterfieldError(7, "query_media: media must be [n, 4]")
+    if F_out is None:
+        F_out = np.empty((n, 3), np.float64)
+    check(lib.sf_query_media(scene._h, net._h, n, ptr(q), ptr(md), precision, ptr(F_out), ptr(y_out),
+                             stream_ptr(stream)))
+    return F_out

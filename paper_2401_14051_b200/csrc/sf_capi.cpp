@@ -931,7 +931,7 @@ int sf_sample_features(const sf_grid* density, const sf_tvol* tvol, const sf_tem
         Scratch<int> err(1, stream);
         SFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
         sfb::SceneDev sc = sfb::scene_dev(*density, tv, nullptr, *model, *table, ts);
-        sfb::launch_sample_features(sc, sfb::template_dev(*tmpl), n, iq.d, of.d, 3 * tmpl->total, 0,
+        sfb::launch_sample_features(sc, sfb::template_dev(*tmpl), n, iq.d, nullptr, of.d, 3 * tmpl->total, 0,
                                     err.p, stream);
         int herr = 0;
         SFB_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -1120,11 +1120,26 @@ void sf_scene_destroy(sf_scene* s) {
     delete s;
 }
 
-int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium, int64_t n,
-             const double* queries, int precision, double* F_out, float* y_out, sf_stream stream) {
-    return guard([&] {
+namespace {
+// sf_query / sf_query_media: medium is the scene-wide medium, media (nullable) per-query
+// {g, albedo rgb} rows that override it (single-lobe HG per query).
+void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium, const double* media_in,
+                int64_t n, const double* queries, int precision, double* F_out, float* y_out, cudaStream_t stream) {
         if (n <= 0) return;
-        validate_albedo(medium->albedo);
+        sf_medium_params uniform{};
+        if (media_in) {
+            if (!is_device_ptr(media_in))
+                for (int64_t i = 0; i < n; ++i) {
+                    validate_albedo(media_in + 4 * i + 1);
+                    if (!(media_in[4 * i] > -1.0 && media_in[4 * i] < 1.0))
+                        fail(SF_ERR_INVALID_ARGUMENT, "PhaseModel::hg: g outside (-1, 1)");
+                }
+            medium = &uniform;
+        } else {
+            validate_albedo(medium->albedo);
+        }
+        In<double> imedia(media_in, media_in ? size_t(n) * 4 : 0, stream);
+        const double* media = media_in ? imedia.d : nullptr;
         const sf_backbone_config& c = b->cfg;
         int nd = 0, nh = 0;
         for (int i = 0; i < c.n_diffuse_layers; ++i) nd += c.diffuse_counts[i];
@@ -1169,7 +1184,8 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
                 const int64_t pm = std::min(span, n - p0);
                 {
                     StageScope st(SF_STAGE_CONFIG, stream);
-                    sfb::launch_query_prep(sc, ht, *medium, pm, iq.d + 9 * p0, cfg8.p, recs.p, stream);
+                    sfb::launch_query_prep(sc, ht, *medium, pm, iq.d + 9 * p0, media ? media + 4 * p0 : nullptr,
+                                           cfg8.p, recs.p, stream);
                 }
                 for (int64_t c0 = 0; c0 < pm; c0 += chunk, ++k) {
                     const int64_t m = std::min(chunk, pm - c0), q0 = p0 + c0;
@@ -1180,7 +1196,8 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
                     {
                         StageScope st(SF_STAGE_SAMPLE_SORT, stream);
                         sfb::launch_sample_sort(&sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, L, m,
-                                                recs.p + c0 * sfb::query_rec_bytes(), nullptr, ob, mb, err.p, stream);
+                                                recs.p + c0 * sfb::query_rec_bytes(), nullptr, ob, mb, err.p, stream,
+                                                media != nullptr);
                     }
                     if (aux != stream) {
                         SFB_CUDA(cudaEventRecord(ps.ready, stream));
@@ -1224,16 +1241,17 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
             const double* qd = iq.d + 9 * q0;
             {
                 StageScope st(SF_STAGE_CONFIG, stream);
-                sfb::launch_make_cfg8(*medium, m, qd, cfg8.p, stream);
+                sfb::launch_make_cfg8(*medium, m, qd, media ? media + 4 * q0 : nullptr, cfg8.p, stream);
             }
+            const double* mq = media ? media + 4 * q0 : nullptr;
             {
                 StageScope st(SF_STAGE_FEATURES_DIFFUSE, stream);
-                sfb::launch_sample_features(sc, sfb::template_dev(*s->dt), m, qd, feats.p, feat, 0,
+                sfb::launch_sample_features(sc, sfb::template_dev(*s->dt), m, qd, mq, feats.p, feat, 0,
                                             err.p, stream);
             }
             {
                 StageScope st(SF_STAGE_FEATURES_HIGHLIGHT, stream);
-                sfb::launch_sample_features(sc, sfb::template_dev(*s->ht), m, qd, feats.p, feat,
+                sfb::launch_sample_features(sc, sfb::template_dev(*s->ht), m, qd, mq, feats.p, feat,
                                             3 * nd, err.p, stream);
             }
             {
@@ -1258,6 +1276,19 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
         oy.finish();
         sync(stream);
         if (herr) fail(SF_ERR_INVALID_ARGUMENT, "place_template: entry coincides with p");
+}
+}  // namespace
+
+int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium, int64_t n,
+             const double* queries, int precision, double* F_out, float* y_out, sf_stream stream) {
+    return guard([&] { query_impl(s, b, medium, nullptr, n, queries, precision, F_out, y_out, stream); });
+}
+
+int sf_query_media(const sf_scene* s, const sf_backbone* b, int64_t n, const double* queries, const double* media,
+                   int precision, double* F_out, float* y_out, sf_stream stream) {
+    return guard([&] {
+        if (!media) fail(SF_ERR_INVALID_ARGUMENT, "query_media: media rows required");
+        query_impl(s, b, nullptr, media, n, queries, precision, F_out, y_out, stream);
     });
 }
 

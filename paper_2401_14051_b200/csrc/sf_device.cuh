@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../../include/scatterfield_b200.h"
+
 namespace sfb {
 
 constexpr double kPi = 3.14159265358979323846;
@@ -207,6 +209,30 @@ __device__ __forceinline__ double phase_lookup(const PhaseDev& pm, const double*
     for (int k = 0; k < pm.n_lobes; ++k)
         v += pm.w[k] * lookup_hg(pm.table, pm.gr, pm.ar, pm.hr, pm.g[k], angle, half);
     return v;
+}
+
+// make_config row {n_g, g0, g1, g2, albedo rgb, alpha = angle_between(omega, l)}
+// (src/predictor.cpp:261-274): scene-wide medium, or per-query {g, albedo rgb} (one HG lobe).
+__device__ __forceinline__ void write_cfg8(const sf_medium_params& m, const double* media, const double* c,
+                                           double* o) {
+    if (media) {
+        o[0] = 1.0;
+        o[1] = media[0];
+        o[2] = 0.0;
+        o[3] = 0.0;
+        o[4] = media[1];
+        o[5] = media[2];
+        o[6] = media[3];
+    } else {
+        o[0] = m.n_g;
+        o[1] = m.n_g > 0 ? m.g[0] : 0.0;
+        o[2] = m.n_g > 1 ? m.g[1] : 0.0;
+        o[3] = m.n_g > 2 ? m.g[2] : 0.0;
+        o[4] = m.albedo[0];
+        o[5] = m.albedo[1];
+        o[6] = m.albedo[2];
+    }
+    o[7] = angle_between(c + 3, c + 6);
 }
 
 #endif  // __CUDACC__

@@ -54,6 +54,9 @@ struct SortDesc {
     uint8_t chunk_j[kMaxChunks];
     uint8_t task_seg[2 * kMaxSegs];  // sort tasks by network size; bit 7 = upper half of a 64-wide pair
     int debug;                       // SF_DEBUG_SAMPLE_SORT: 1 skip sampling, 2 skip sort, 4 skip stores
+    int mixed;                       // per-query g (C4): phase from the full table at the query's g
+    int G;                           // table g resolution
+    const float* table;              // [G][A][H] (mixed only)
     int nbuf;                        // scratch buffers (2: one block barrier per group, if 3 blocks/SM still fit)
 };
 
@@ -83,6 +86,29 @@ __device__ __forceinline__ float cap_phase(const float2* planes, const SortDesc&
     return f;
 }
 
+// PhaseTable::lookup_hg (src/phase.cpp:191-219) at a per-query g cell (gi, gt) on the full
+// table [G][A][H] in global memory (L1/L2 resident): bilinear in (angle, aperture) on planes
+// gi and gi + 1, then the g lerp. FP32 (bf16 production path only).
+__device__ __forceinline__ float table_phase(const SortDesc& d, int gi, float gt, float cosine, float half) {
+    const float angle = acosf(fminf(fmaxf(cosine, -1.0f), 1.0f));
+    const int A = d.A, H = d.H;
+    const float u = fminf(fmaxf(angle, 0.0f), float(kPi)) * (float(A - 1) / float(kPi));
+    const int i0 = min(int(u), A - 2);
+    const float t = u - float(i0);
+    const float v = fminf(fmaxf(half, 0.0f), float(kPi)) * (float(H - 1) / float(kPi));
+    const int j0 = min(int(v), H - 2);
+    const float s = v - float(j0);
+    float pg[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const float* b = d.table + (size_t(gi + k) * A + i0) * H + j0;
+        const float r00 = __ldg(b), r01 = __ldg(b + 1), r10 = __ldg(b + H), r11 = __ldg(b + H + 1);
+        const float a = fmaf(s, r01 - r00, r00), c = fmaf(s, r11 - r10, r10);
+        pg[k] = fmaf(t, c - a, a);
+    }
+    return d.w[0] * fmaf(gt, pg[1] - pg[0], pg[0]);
+}
+
 // voxel-space coordinate (s - o)/vs - 0.5 split into an integer cell base and an FP32 fraction
 __device__ __forceinline__ void voxel_split(const GridDev& g, const double* s, int* base, float* frac) {
 #pragma unroll
@@ -109,9 +135,18 @@ struct __align__(16) QueryCtx {
     float lf[3], il;         // light and 1/|light|
     float pbox[6], ebox[6];  // in-box fraction bounds relative to pb / eb
     int ok;                  // highlight entry != p
-    int same_light;          // light equals query 0's (diffuse light side precomputed)
-    int pad_;
+    int same_light;          // light and medium equal query 0's (diffuse light side precomputed)
+    int gi;                  // per-query g (mixed media): table g cell and weight
+    float gt;
+    int pad_[2];
 };
+
+// Phase feature factor at the query's medium: the scene's pre-blended planes, or the full
+// table at the query's own g (mixed media).
+__device__ __forceinline__ float qphase(const float2* planes, const SortDesc& d, const QueryCtx& q, float cosine,
+                                       float half) {
+    return d.mixed ? table_phase(d, q.gi, q.gt, cosine, half) : cap_phase(planes, d, cosine, half);
+}
 
 __device__ __forceinline__ void box_bounds(const GridDev& g, const int* base, float* box) {
     const int n[3] = {g.nx, g.ny, g.nz};
@@ -223,10 +258,10 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
             ph = 1.0f;  // diffuse centre point (src/feature_pipeline.cpp:163-164)
             return;
         }
-        const float fw = cap_phase(planes, d, (q.wf[0] * p1.x + q.wf[1] * p1.y + q.wf[2] * p1.z) * q.iw, p0.w);
+        const float fw = qphase(planes, d, q, (q.wf[0] * p1.x + q.wf[1] * p1.y + q.wf[2] * p1.z) * q.iw, p0.w);
         const float fl = same_light
                              ? p1.w
-                             : cap_phase(planes, d, (q.lf[0] * p1.x + q.lf[1] * p1.y + q.lf[2] * p1.z) * q.il, p0.w);
+                             : qphase(planes, d, q, (q.lf[0] * p1.x + q.lf[1] * p1.y + q.lf[2] * p1.z) * q.il, p0.w);
         ph = fw * fl;
         return;
     }
@@ -246,8 +281,8 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
     const float r = tq.w * q.hs * inv;  // cap / dist, both in voxels
     const float half = r >= 1.0f ? float(kPi) : asinf(r);
     const float ax = dx * inv, ay = dy * inv, az = dz * inv;
-    ph = cap_phase(planes, d, (q.wf[0] * ax + q.wf[1] * ay + q.wf[2] * az) * q.iw, half) *
-         cap_phase(planes, d, (q.lf[0] * ax + q.lf[1] * ay + q.lf[2] * az) * q.il, half);
+    ph = qphase(planes, d, q, (q.wf[0] * ax + q.wf[1] * ay + q.wf[2] * az) * q.iw, half) *
+         qphase(planes, d, q, (q.lf[0] * ax + q.lf[1] * ay + q.lf[2] * az) * q.il, half);
 }
 
 // Per-scene diffuse constants: pre[2i] = {offset (voxels), half angle or -1 at the
@@ -279,24 +314,23 @@ __global__ void k_diffuse_prep(SceneDev sc, TemplateDev dt, SortDesc d, const fl
 // (src/predictor.cpp:261-274, alpha = angle_between(omega, l)) and the sampling
 // context (voxel-space bases, highlight frame, in-box bounds).
 __global__ void k_query_prep(SceneDev sc, TemplateDev ht, sf_medium_params m, int64_t n,
-                             const double* __restrict__ queries, double* __restrict__ cfg8,
-                             QueryCtx* __restrict__ recs) {
+                             const double* __restrict__ queries, const double* __restrict__ media,
+                             double* __restrict__ cfg8, QueryCtx* __restrict__ recs) {
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
         const double* c = queries + 9 * q;
         QueryCtx qc;
         query_ctx(sc, ht, c, qc);
-        qc.same_light = (c[6] == queries[6] && c[7] == queries[7] && c[8] == queries[8]) ? 1 : 0;
-        qc.pad_ = 0;
+        qc.same_light = (!media && c[6] == queries[6] && c[7] == queries[7] && c[8] == queries[8]) ? 1 : 0;
+        qc.gi = 0;
+        qc.gt = 0.0f;
+        if (media) {  // g axis of PhaseTable::lookup_hg (src/phase.cpp:196-205) at the query's g
+            double gt;
+            table_coord(media[4 * q], -0.99, 0.99, sc.phase.gr, qc.gi, gt);
+            qc.gt = float(gt);
+        }
+        qc.pad_[0] = qc.pad_[1] = 0;
         recs[q] = qc;
-        double* o = cfg8 + 8 * q;
-        o[0] = m.n_g;
-        o[1] = m.n_g > 0 ? m.g[0] : 0.0;
-        o[2] = m.n_g > 1 ? m.g[1] : 0.0;
-        o[3] = m.n_g > 2 ? m.g[2] : 0.0;
-        o[4] = m.albedo[0];
-        o[5] = m.albedo[1];
-        o[6] = m.albedo[2];
-        o[7] = angle_between(c + 3, c + 6);
+        write_cfg8(m, media ? media + 4 * q : nullptr, c, cfg8 + 8 * q);
     }
 }
 
@@ -677,20 +711,26 @@ void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float
 size_t query_rec_bytes() { return sizeof(QueryCtx); }
 
 void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_medium_params& m, int64_t n,
-                       const double* queries, double* cfg8, void* recs, cudaStream_t s) {
+                       const double* queries, const double* media, double* cfg8, void* recs, cudaStream_t s) {
     if (n <= 0) return;
     const int64_t blocks = std::min<int64_t>((n + 127) / 128, int64_t(sm_count()) * 16);
-    k_query_prep<<<unsigned(blocks), 128, 0, s>>>(sc, ht, m, n, queries, cfg8, static_cast<QueryCtx*>(recs));
+    k_query_prep<<<unsigned(blocks), 128, 0, s>>>(sc, ht, m, n, queries, media, cfg8, static_cast<QueryCtx*>(recs));
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
 
 void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht, const float* planes,
                         int n_planes, const float4* pre, const SortLayout& L, int64_t n, const void* recs,
-                        const float* feats, uint8_t* ops, float* mms, int* err, cudaStream_t s) {
+                        const float* feats, uint8_t* ops, float* mms, int* err, cudaStream_t s, bool mixed) {
     (void)dt;  // diffuse placement comes from `pre` (k_diffuse_prep)
     if (n <= 0) return;
     SortDesc d = make_desc(sc, n_planes, L, n);
+    if (mixed && sc) {
+        d.mixed = 1;
+        d.G = sc->phase.gr;
+        d.table = sc->phase.table;
+        d.w[0] = 1.0f;  // PhaseModel::hg(g): one lobe of weight 1
+    }
     auto smem_for = [&](int nbuf) {
         return size_t(2 * d.n_planes * d.A * (d.H + 1) + nbuf * kWarps * d.scr_floats) * sizeof(float) +
                2 * kWarps * sizeof(QueryCtx) + 16;

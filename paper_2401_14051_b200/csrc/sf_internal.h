@@ -160,15 +160,16 @@ SceneDev scene_dev(const sf_grid& density, const sf_grid& tvol, const float2* dt
                    const sf_phase_model& m, const sf_phase_table& t, double ts);
 TemplateDev template_dev(const sf_template& t);
 
+// media: NULL, or per-query {g, albedo rgb} [n][4] (single-lobe HG per query, config C4)
 void launch_sample_features(const SceneDev& sc, const TemplateDev& td, int64_t n,
-                            const double* queries, float* out, int64_t row_stride,
+                            const double* queries, const double* media, float* out, int64_t row_stride,
                             int64_t col_offset, int* err, cudaStream_t s);
 int64_t slices_per_query(const sf_backbone_config& c);
 void launch_slice(const sf_backbone_config& c, int64_t n, const float* feats, float* slices,
                   cudaStream_t s);
 void launch_backbone_fp32(const sf_backbone& b, int64_t n, const float* slices,
                           const double* cfg8, float* y, double* F, cudaStream_t s);
-void launch_make_cfg8(const sf_medium_params& m, int64_t n, const double* queries,
+void launch_make_cfg8(const sf_medium_params& m, int64_t n, const double* queries, const double* media,
                       double* cfg8, cudaStream_t s);
 
 // Layout of the sorted-feature operand blocks produced by k_sample_sort and
@@ -202,11 +203,11 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
 void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht,
                         const float* planes, int n_planes, const float4* pre, const SortLayout& L,
                         int64_t n, const void* recs, const float* feats, uint8_t* ops, float* mms,
-                        int* err, cudaStream_t s);
+                        int* err, cudaStream_t s, bool mixed = false);
 // Per-query context records (sampling bases, highlight frame) + make_config rows.
 size_t query_rec_bytes();
 void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_medium_params& m, int64_t n,
-                       const double* queries, double* cfg8, void* recs, cudaStream_t s);
+                       const double* queries, const double* media, double* cfg8, void* recs, cudaStream_t s);
 // Light-side phase of every diffuse point for the light of query 0 (diffuse
 // placement is a pure translation, so axis and aperture do not depend on p).
 void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float* planes, int n_planes,

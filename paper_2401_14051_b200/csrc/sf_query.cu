@@ -106,8 +106,8 @@ __device__ __forceinline__ bool place_point(const SceneDev& sc, const TemplateDe
 // Thread = (query, template point); output rows are SoA per block:
 // out[q*row_stride + col_offset + {0,1,2}*total + i] = {density, trans, phase}.
 __global__ void k_sample_features(SceneDev sc, TemplateDev td, int64_t n,
-                                  const double* __restrict__ queries, float* __restrict__ out,
-                                  int64_t row_stride, int64_t col_offset, int* err) {
+                                  const double* __restrict__ queries, const double* __restrict__ media,
+                                  float* __restrict__ out, int64_t row_stride, int64_t col_offset, int* err) {
     int64_t total = int64_t(n) * td.total;
     for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
          idx += int64_t(gridDim.x) * blockDim.x) {
@@ -133,7 +133,14 @@ __global__ void k_sample_features(SceneDev sc, TemplateDev td, int64_t n,
             double half = cap >= dist ? kPi : asin(cap / dist);
             double il = 1.0 / dist;
             double axis[3] = {d[0] * il, d[1] * il, d[2] * il};
-            f = phase_lookup(sc.phase, omega, axis, half) * phase_lookup(sc.phase, light, axis, half);
+            PhaseDev ph = sc.phase;
+            if (media) {  // per-query single-lobe HG (C4: per-voxel g sampled at p by the harness)
+                ph.kind = 1;
+                ph.n_lobes = 1;
+                ph.w[0] = 1.0;
+                ph.g[0] = media[4 * qi];
+            }
+            f = phase_lookup(ph, omega, axis, half) * phase_lookup(ph, light, axis, half);
         }
         o[i] = float(rho);
         o[td.total + i] = float(tr);
@@ -361,19 +368,12 @@ __global__ void __launch_bounds__(128) k_backbone_fp32(NetDesc nd, const float* 
 // make_config (src/predictor.cpp:261-274): g params + albedo of the medium,
 // alpha = angle_between(omega, light) per query.
 __global__ void k_make_cfg8(sf_medium_params m, int64_t n, const double* __restrict__ queries,
-                            double* __restrict__ cfg8) {
+                            const double* __restrict__ media, double* __restrict__ cfg8) {
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
          q += int64_t(gridDim.x) * blockDim.x) {
         const double* c = queries + 9 * q;
         double* o = cfg8 + 8 * q;
-        o[0] = m.n_g;
-        o[1] = m.n_g > 0 ? m.g[0] : 0.0;
-        o[2] = m.n_g > 1 ? m.g[1] : 0.0;
-        o[3] = m.n_g > 2 ? m.g[2] : 0.0;
-        o[4] = m.albedo[0];
-        o[5] = m.albedo[1];
-        o[6] = m.albedo[2];
-        o[7] = angle_between(c + 3, c + 6);
+        write_cfg8(m, media ? media + 4 * q : nullptr, c, o);
     }
 }
 
@@ -404,11 +404,11 @@ TemplateDev template_dev(const sf_template& t) {
 }
 
 void launch_sample_features(const SceneDev& sc, const TemplateDev& td, int64_t n,
-                            const double* queries, float* out, int64_t row_stride,
+                            const double* queries, const double* media, float* out, int64_t row_stride,
                             int64_t col_offset, int* err, cudaStream_t s) {
     if (n <= 0) return;
     k_sample_features<<<grid_for(size_t(n) * td.total, 128), 128, 0, s>>>(
-        sc, td, n, queries, out, row_stride, col_offset, err);
+        sc, td, n, queries, media, out, row_stride, col_offset, err);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
@@ -509,10 +509,10 @@ void launch_backbone_fp32(const sf_backbone& b, int64_t n, const float* slices,
     count_launch();
 }
 
-void launch_make_cfg8(const sf_medium_params& m, int64_t n, const double* queries, double* cfg8,
-                      cudaStream_t s) {
+void launch_make_cfg8(const sf_medium_params& m, int64_t n, const double* queries, const double* media,
+                      double* cfg8, cudaStream_t s) {
     if (n <= 0) return;
-    k_make_cfg8<<<grid_for(size_t(n)), kBlock, 0, s>>>(m, n, queries, cfg8);
+    k_make_cfg8<<<grid_for(size_t(n)), kBlock, 0, s>>>(m, n, queries, media, cfg8);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }

@@ -2,7 +2,8 @@
 
 * ``procedural_cloud`` restates the reference's ``generate_medium(ProceduralCloud)``
   (src/scene_gen.cpp:16-52, 74-109) bit-for-bit in vectorised numpy (C1 input).
-* ``fractal_ellipsoid`` (C2) and ``plume`` (C3) are this repo's generators for the
+* ``fractal_ellipsoid`` (C2), ``smoke_plume`` (C3), ``mixed_medium`` (C4) and
+  ``noise_volume`` + ``rotating_light`` (C5) are this repo's generators for the
   configurations the reference has no generator for.
 * ``draw_centers`` restates src/feature_pipeline.cpp:174-198 (uniform occupied
   voxel + jitter, omega uniform on S^2) with one PCG32 stream per center.
@@ -196,3 +197,132 @@ def config_rows(centers, g, albedo):
 
 
 LIGHT = (0.2, -1.0, 0.1)
+
+
+def _box_blur(v, r, axis):
+    """Separable box filter of radius r along one axis (edge-clamped), float64."""
+    n = v.shape[axis]
+    pad = [(0, 0)] * v.ndim
+    pad[axis] = (r + 1, r)
+    c = np.cumsum(np.pad(v, pad, mode="edge"), axis=axis)
+    hi = np.take(c, np.arange(2 * r + 1, 2 * r + 1 + n), axis=axis)
+    lo = np.take(c, np.arange(0, n), axis=axis)
+    return (hi - lo) / (2 * r + 1)
+
+
+def _curl_velocity(seed, n=24):
+    """Divergence-free velocity on an n^3 lattice over [0,1]^3: curl of a 3-component
+    value-noise potential (central differences), for the C3 plume advection."""
+    u = (np.arange(n) + 0.5) / n
+    uz, uy, ux = np.meshgrid(u, u, u, indexing="ij")
+    psi = [_fbm((seed + 101 * (k + 1)) & 0xFFFFFFFF, ux * 3.0, uy * 3.0, uz * 3.0, 3) for k in range(3)]
+    d = lambda f, ax: np.gradient(f, 1.0 / n, axis=ax)  # noqa: E731 (axis 0 = z, 1 = y, 2 = x)
+    vx = d(psi[2], 1) - d(psi[1], 0)
+    vy = d(psi[0], 0) - d(psi[2], 2)
+    vz = d(psi[1], 2) - d(psi[0], 1)
+    return np.stack([vx, vy, vz], axis=-1)
+
+
+def _lattice_lookup(field, p):
+    """Nearest-cell lookup of an [n,n,n,3] lattice field at points p in [0,1)^3."""
+    n = field.shape[0]
+    i = np.clip((p * n).astype(np.int64), 0, n - 1)
+    return field[i[:, 2], i[:, 1], i[:, 0]]
+
+
+def smoke_plume(dims, seed, particles=None, steps=24, empty=0.70):
+    """C3: seeded curl-noise-advected smoke blob, [z,y,x] f32 in [0,1], with ``empty``
+    (default 70%) of the voxels exactly zero. Particles are emitted from a Gaussian source
+    near the bottom, rise with buoyancy while a curl-noise field advects them, are splatted
+    into the grid, box-blurred, and the lowest 70% of voxels are cut to zero."""
+    rng = np.random.default_rng(seed)
+    npart = particles or max(20000, dims ** 3 // 8)
+    p = rng.normal([0.5, 0.2, 0.5], [0.06, 0.04, 0.06], size=(npart, 3))
+    birth = rng.uniform(0.0, 1.0, npart)
+    vel = _curl_velocity(seed)
+    dt = 0.7 / steps
+    for k in range(steps):
+        live = birth <= (k + 1) / steps
+        v = _lattice_lookup(vel, np.clip(p, 0.0, 0.999999)) * 0.6
+        v[:, 1] += 1.0  # buoyancy (+y)
+        p[live] += dt * v[live]
+    p = p[np.all((p >= 0.0) & (p < 1.0), axis=1)]
+    idx = (p * dims).astype(np.int64)
+    vol = np.zeros((dims, dims, dims), np.float64)
+    np.add.at(vol, (idx[:, 2], idx[:, 1], idx[:, 0]), 1.0)
+    r = max(1, dims // 16)
+    for ax in range(3):
+        vol = _box_blur(vol, r, ax)
+    cut = np.quantile(vol, empty)
+    vol = np.where(vol > cut, vol - cut, 0.0)
+    vol /= max(vol.max(), 1e-30)
+    return np.clip(vol, 0.0, 1.0).astype(np.float32)
+
+
+def mixed_medium(dims, seed, chunk=16):
+    """C4: seeded noise density in [0,1] with per-voxel albedo in [0.9, 0.999] and per-voxel HG
+    g in [0.3, 0.9]; returns (density, albedo, g), each [z,y,x] f32."""
+    dens = np.zeros((dims, dims, dims), np.float32)
+    alb = np.zeros_like(dens)
+    gg = np.zeros_like(dens)
+    for z0 in range(0, dims, chunk):
+        z1 = min(dims, z0 + chunk)
+        ux, uy, uz = _unit_coords(dims, z0, z1)
+        qx, qy, qz = 2.0 * ux - 1.0, 2.0 * uy - 1.0, 2.0 * uz - 1.0
+        falloff = np.clip(1.3 - 1.5 * np.sqrt(qx * qx + qy * qy + qz * qz), 0.0, 1.0)
+        dens[z0:z1] = np.clip(2.0 * (_fbm(seed, ux * 4.0, uy * 4.0, uz * 4.0, 4) - 0.4) * falloff, 0.0, 1.0)
+        alb[z0:z1] = 0.9 + 0.099 * _fbm((seed + 7) & 0xFFFFFFFF, ux * 2.0, uy * 2.0, uz * 2.0, 2)
+        gg[z0:z1] = 0.3 + 0.6 * _fbm((seed + 13) & 0xFFFFFFFF, ux * 2.0, uy * 2.0, uz * 2.0, 2)
+    return dens, alb, gg
+
+
+def sample_media(albedo, g, centers, voxel_size=None, origin=(-1.0, -1.0, -1.0)):
+    """Per-query medium rows [n, 4] = (g, albedo rgb) for C4: FP64 trilinear of the per-voxel
+    g / albedo grids at each query's p (DensityGrid::sample_trilinear semantics, clamp-to-edge
+    cell; queries lie inside the grid). Grey albedo (r = g = b)."""
+    nz, ny, nx = g.shape
+    vs = 2.0 / nx if voxel_size is None else voxel_size
+    f = (centers[:, :3] - np.asarray(origin)) / vs - 0.5
+    i0 = np.floor(f).astype(np.int64)
+    t = f - i0
+    dims = np.array([nx, ny, nz])
+    out = []
+    for grid in (g, albedo):
+        acc = np.zeros(len(centers))
+        for dz in (0, 1):
+            for dy in (0, 1):
+                for dx in (0, 1):
+                    d = np.array([dx, dy, dz])
+                    ii = np.clip(i0 + d, 0, dims - 1)
+                    w = np.prod(np.where(d == 1, t, 1.0 - t), axis=1)
+                    acc += w * grid[ii[:, 2], ii[:, 1], ii[:, 0]].astype(np.float64)
+        out.append(acc)
+    gq, aq = out
+    return np.stack([gq, aq, aq, aq], axis=1)
+
+
+def noise_volume(dims, seed, chunk=16):
+    """C5: seeded 5-octave value-noise volume in [0,1] (static across the sequence)."""
+    out = np.zeros((dims, dims, dims), np.float32)
+    for z0 in range(0, dims, chunk):
+        z1 = min(dims, z0 + chunk)
+        ux, uy, uz = _unit_coords(dims, z0, z1)
+        qx, qy, qz = 2.0 * ux - 1.0, 2.0 * uy - 1.0, 2.0 * uz - 1.0
+        falloff = np.clip(1.2 - 1.3 * np.sqrt(qx * qx + qy * qy + qz * qz), 0.0, 1.0)
+        out[z0:z1] = np.clip(2.0 * (_fbm(seed, ux * 4.0, uy * 4.0, uz * 4.0, 5) - 0.42) * falloff, 0.0, 1.0)
+    return out
+
+
+def rotating_light(frame, n_frames, base=LIGHT):
+    """C5: LIGHT rotated by 360 deg * frame / n_frames about +Y (normalised)."""
+    a = 2.0 * math.pi * frame / n_frames
+    x, y, z = base
+    c, s_ = math.cos(a), math.sin(a)
+    v = (c * x + s_ * z, y, -s_ * x + c * z)
+    n = math.sqrt(sum(t * t for t in v))
+    return tuple(t / n for t in v)
+
+
+def c3_lights():
+    """C3: four directional lights (LIGHT plus three rotated about Y) with intensities."""
+    return [rotating_light(k, 4) for k in range(4)], [1.0, 0.6, 0.4, 0.3]

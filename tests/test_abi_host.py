@@ -132,3 +132,26 @@ def test_backbone_config_json_key_order():
     import paper_2401_14051_b200 as sf
     j = sf.BackboneConfig().to_json()
     assert j.startswith('{"diffuse_counts":[6,8,12,16,24,32,48,48],"gamma":4.0')
+
+
+def test_config_generators_c3_c4_c5():
+    """Harness generators of the configurations the reference has no generator for
+    (SURVEY.md §8d): seeded, deterministic, and with the stated value ranges."""
+    from paper_2401_14051_b200 import configs, scenes
+    v = scenes.smoke_plume(32, 5)
+    assert v.dtype == np.float32 and 0.65 <= np.mean(v == 0) <= 0.75 and v.max() == 1.0
+    assert np.array_equal(v, scenes.smoke_plume(32, 5)) and not np.array_equal(v, scenes.smoke_plume(32, 6))
+    d, a, g = scenes.mixed_medium(16, 4)
+    assert a.min() >= 0.9 and a.max() <= 0.999 and g.min() >= 0.3 and g.max() <= 0.9
+    rows = scenes.draw_centers(d, 32, 1, scenes.LIGHT)
+    m = scenes.sample_media(a, g, rows)
+    assert m.shape == (32, 4) and np.all(m[:, 1] == m[:, 3])
+    assert 0.3 <= m[:, 0].min() and m[:, 0].max() <= 0.9
+    l0 = np.array(scenes.rotating_light(0, 32))
+    assert np.allclose(l0, np.array(scenes.LIGHT) / np.linalg.norm(scenes.LIGHT))
+    l16 = np.array(scenes.rotating_light(16, 32))  # half turn about +Y
+    assert np.allclose(l16, l0 * [-1, 1, -1]) and abs(np.linalg.norm(l16) - 1) < 1e-12
+    lights, inten = scenes.c3_lights()
+    assert len(lights) == 4 and len(inten) == 4
+    r2 = configs.with_light(rows, (0.0, -2.0, 0.0))
+    assert np.array_equal(r2[:, :6], rows[:, :6]) and np.allclose(r2[:, 6:], [0, -1, 0])
