@@ -222,6 +222,22 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
 int sf_query_media(const sf_scene* s, const sf_backbone* b, int64_t n, const double* queries,
                    const double* media, int precision, double* F_out, float* y_out, sf_stream stream);
 
+/* bake_field (src/predictor.cpp:559-581) as render_neural runs it (:598-609): the query at
+ * every occupied voxel centre (density > 0) of the scene's density grid, omega =
+ * normalize(p - camera_pos), l = the scene tvol's light; out h/d [3][nz][ny][nx] f32 =
+ * float(F) per channel, 0 at empty voxels. */
+int sf_bake_field(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium,
+                  const double camera_pos[3], int precision, float* out, sf_stream stream);
+/* render_volume (src/rte.cpp:407-447) with the camera of camera.h:19-23 (Camera(position,
+ * look_at, up, vfov_degrees, width, height), centre-of-pixel primary rays) and the baked
+ * field as the in-scatter provider (BakedField::sample, trilinear, 0 outside; field NULL
+ * = F 0). material_class: 0 air, 1 gas, 2 solid/liquid, 3 skin (MediumProperties::validate
+ * ranges). img h/d [height][width][3] f32 (ImageF::rgb). */
+int sf_render_volume(const sf_grid* density, const double sigma_t[3], const double albedo[3],
+                     int material_class, const double camera_pos[3], const double look_at[3],
+                     const double up[3], double vfov_deg, int width, int height, const float* field,
+                     double step_scale, const double background[3], float* img, sf_stream stream);
+
 /* ---- instrumentation (per-stage CUDA-event timing) -------------- */
 enum sf_stage {
     SF_STAGE_CONFIG = 0,             /* make_config rows */

@@ -344,6 +344,8 @@ class Reference:
         L.ref_predict.argtypes = [C.c_void_p, C.c_int64, _f32p, _f64p, _f64p, _f64p]
         L.ref_time_queries.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, _f64p, _f64p, _f64p,
                                        C.POINTER(C.c_double)]
+        L.ref_render_neural.argtypes = [C.c_void_p, C.c_void_p, _f64p, _f64p, C.c_int, _f64p, _f64p, _f64p, _f64p,
+                                        C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, _f64p, _f32p]
 
     def _check(self, rc):
         if rc != 0:
@@ -467,3 +469,13 @@ class Reference:
         secs = C.c_double()
         self._check(self.L.ref_time_queries(ctx, b, len(centers), centers, cfg8, F, C.byref(secs)))
         return secs.value, F
+
+    def render_neural(self, ctx, b, sigma_t, albedo, material_class, light, cam_pos, look_at, up, vfov, w, h,
+                      lam=0.6, step_scale=0.5, background=(0.0, 0.0, 0.0)):
+        """render_neural (src/predictor.cpp:585-614) with the identity combiner: [h, w, 3] f32."""
+        out = np.zeros((h, w, 3), np.float32)
+        v = lambda a: _c(a, np.float64)  # noqa: E731
+        self._check(self.L.ref_render_neural(ctx, b, v(sigma_t), v(albedo), int(material_class), v(light),
+                                             v(cam_pos), v(look_at), v(up), float(vfov), int(w), int(h), lam,
+                                             step_scale, v(background), out))
+        return out

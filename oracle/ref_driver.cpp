@@ -37,6 +37,8 @@
 #include "scatterfield/parallel.h"
 #include "scatterfield/phase.h"
 #include "scatterfield/predictor.h"
+#include "scatterfield/camera.h"
+#include "scatterfield/rte.h"
 #include "scatterfield/scene_gen.h"
 #include "scatterfield/templates.h"
 #include "scatterfield/volume_grid.h"
@@ -381,6 +383,42 @@ int ref_time_queries(void* cp, void* bp, int64_t q, const double* centers9,
         });
         auto t1 = std::chrono::steady_clock::now();
         *seconds = std::chrono::duration<double>(t1 - t0).count();
+    });
+}
+
+// render_neural (src/predictor.cpp:585-614) on the context's density, phase model and
+// phase table with the identity combiner: build the tvol, bake F at every occupied voxel
+// centre, march render_volume (src/rte.cpp:407-447). out_img [h][w][3].
+int ref_render_neural(void* cp, void* bp, const double* sigma_t3, const double* albedo3, int material_class,
+                      const double* light3, const double* cam_pos, const double* look_at, const double* up,
+                      double vfov, int w, int h, double lambda, double step_scale, const double* background,
+                      float* out_img) {
+    Ctx* c = static_cast<Ctx*>(cp);
+    auto* b = static_cast<sf::Backbone<float>*>(bp);
+    return guard([&] {
+        sf::Medium medium;
+        medium.grid = c->density;
+        medium.props.sigma_t_scale = v3(sigma_t3);
+        medium.props.albedo = v3(albedo3);
+        medium.props.material_class = static_cast<sf::MaterialClass>(material_class);
+        medium.phase = c->model;
+        sf::DistantLight light;
+        light.direction = v3(light3);
+        light.intensity = sf::Vec3{1.0, 1.0, 1.0};
+        sf::Camera cam(v3(cam_pos), v3(look_at), v3(up), vfov, w, h);
+        sf::FeatureTable table;
+        table.phase_table = c->table;
+        sf::DensityPyramid pyr(c->density);
+        table.combiner = sf::CombinerWeights::identity(int(pyr.level_count()));
+        table.lambda = lambda;
+        table.template_scale = c->template_scale;
+        sf::FeatureConfig fcfg;
+        fcfg.step_scale = step_scale;
+        sf::RenderOptions ro;
+        ro.step_scale = step_scale;
+        ro.background = v3(background);
+        sf::ImageF img = sf::render_neural(medium, light, cam, *b, table, c->dt, c->ht, fcfg, ro);
+        std::memcpy(out_img, img.rgb.data(), img.rgb.size() * sizeof(float));
     });
 }
 

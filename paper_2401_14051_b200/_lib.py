@@ -93,6 +93,8 @@ _SIGS = {
     "sf_scene_destroy": (None, [P]),
     "sf_query": (I, [P, P, P, I64, P, I, P, P, P]),
     "sf_query_media": (I, [P, P, I64, P, P, I, P, P, P]),
+    "sf_bake_field": (I, [P, P, P, P, I, P, P]),
+    "sf_render_volume": (I, [P, P, P, I, P, P, P, D, I, I, P, D, P, P, P]),
     "sf_profile_enable": (I, [I]),
     "sf_profile_read": (I, [P, P]),
     "sf_launch_count": (I64, []),

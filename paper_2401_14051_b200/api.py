@@ -689,3 +689,72 @@ def query_media(scene: Scene, net: Backbone, queries, media, precision=FP32, F_o
     check(lib.sf_query_media(scene._h, net._h, n, ptr(q), ptr(md), precision, ptr(F_out), ptr(y_out),
                              stream_ptr(stream)))
     return F_out
+
+
+# ------------------------------------------------------------------ image entry point
+@dataclass
+class Camera:
+    """Camera (inc/camera.h:17-35): position, look_at, up, vertical fov in degrees, resolution."""
+
+    position: tuple
+    look_at: tuple = (0.0, 0.0, 0.0)
+    up: tuple = (0.0, 1.0, 0.0)
+    vfov: float = 40.0
+    width: int = 64
+    height: int = 64
+
+
+@dataclass
+class RenderOptions:
+    """RenderOptions (inc/rte.h:145-148)."""
+
+    step_scale: float = 0.5
+    background: tuple = (0.0, 0.0, 0.0)
+
+
+MATERIAL_CLASSES = {"air": 0, "gas": 1, "solid_liquid": 2, "skin": 3}
+
+
+def bake_field(scene: Scene, net: Backbone, medium: MediumParams, camera_position, precision=FP32, out=None,
+               stream=None):
+    """bake_field (src/predictor.cpp:559-581) over the scene's density grid: F at every occupied
+    voxel centre with omega toward the voxel from the camera, l = the scene tvol's light.
+    Returns [3, nz, ny, nx] float32 (0 at empty voxels); `out` may be a CUDA tensor."""
+    dens = scene._keep[0]
+    nx, ny, nz = dens.dims
+    if out is None:
+        out = np.empty((3, nz, ny, nx), np.float32)
+    m = medium.to_c()
+    check(lib.sf_bake_field(scene._h, net._h, C.byref(m), dvec(camera_position), precision, ptr(out),
+                            stream_ptr(stream)))
+    return out
+
+
+def render_volume(grid: DensityGrid, sigma_t, albedo, camera: Camera, field=None, opts: RenderOptions = None,
+                  material_class="gas", out=None, stream=None):
+    """render_volume (src/rte.cpp:407-447) with the baked field as the in-scatter provider
+    (field None: F = 0). Returns the [height, width, 3] float32 image (ImageF::rgb)."""
+    opts = opts or RenderOptions()
+    if out is None:
+        out = np.empty((camera.height, camera.width, 3), np.float32)
+    f = None if field is None else _arr(field, np.float32)
+    mc = MATERIAL_CLASSES[material_class] if isinstance(material_class, str) else int(material_class)
+    check(lib.sf_render_volume(grid._h, dvec(sigma_t), dvec(albedo), mc, dvec(camera.position), dvec(camera.look_at),
+                               dvec(camera.up), float(camera.vfov), int(camera.width), int(camera.height), ptr(f),
+                               float(opts.step_scale), dvec(opts.background), ptr(out), stream_ptr(stream)))
+    return out
+
+
+def render_neural(grid: DensityGrid, light, camera: Camera, net: Backbone, table: PhaseTable,
+                  diffuse: SamplingTemplate, highlight: SamplingTemplate, model: PhaseModel, medium: MediumParams,
+                  sigma_t=(1.0, 1.0, 1.0), material_class="gas", weights: CombinerWeights = None,
+                  cfg: FeatureConfig = None, opts: RenderOptions = None, precision=FP32, stream=None):
+    """render_neural (src/predictor.cpp:585-614): build the transmittance feature volume for
+    `light`, bake F on the density lattice, march the image."""
+    cfg = cfg or FeatureConfig()
+    opts = opts or RenderOptions()
+    pyr = DensityPyramid(grid, stream=stream)
+    tvol = build_transmittance_volume(pyr, light, weights, cfg, stream=stream)
+    scene = Scene(grid, tvol, diffuse, highlight, model, table, cfg.template_scale)
+    field = bake_field(scene, net, medium, camera.position, precision, stream=stream)
+    return render_volume(grid, sigma_t, medium.albedo, camera, field, opts, material_class, stream=stream)

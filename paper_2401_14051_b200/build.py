@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC,-O2",
          "-I" + os.path.join(HERE, "..", "include")]
-SOURCES = ["sf_build.cu", "sf_query.cu", "sf_tc.cu", "sf_fused.cu", "sf_capi.cpp"]
+SOURCES = ["sf_build.cu", "sf_query.cu", "sf_tc.cu", "sf_fused.cu", "sf_render.cu", "sf_capi.cpp"]
 
 
 def _compile(src: str, verbose: bool) -> str:

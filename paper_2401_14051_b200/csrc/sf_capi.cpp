@@ -1284,6 +1284,59 @@ int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* me
     return guard([&] { query_impl(s, b, medium, nullptr, n, queries, precision, F_out, y_out, stream); });
 }
 
+// ---- image entry point: bake_field + render_volume ------------------------------------------
+int sf_bake_field(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium,
+                  const double camera_pos[3], int precision, float* out, sf_stream stream) {
+    return guard([&] {
+        const sf_grid& g = *s->density;
+        const size_t nvox = g.count();
+        Out<float> o(out, 3 * nvox, stream);
+        SFB_CUDA(cudaMemsetAsync(o.d, 0, 3 * nvox * sizeof(float), stream));
+        Scratch<int> idx(nvox, stream), cnt(1, stream);
+        size_t tmp_bytes = 0;
+        sfb::launch_occupied(g, idx.p, cnt.p, nullptr, tmp_bytes, stream);
+        Scratch<uint8_t> tmp(tmp_bytes, stream);
+        sfb::launch_occupied(g, idx.p, cnt.p, tmp.p, tmp_bytes, stream);
+        int m = 0;
+        SFB_CUDA(cudaMemcpyAsync(&m, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        sync(stream);
+        if (m > 0) {
+            Scratch<double> rows(size_t(m) * 9, stream), F(size_t(m) * 3, stream);
+            sfb::launch_bake_rows(g, idx.p, cnt.p, m, camera_pos, s->tvol->light, rows.p, stream);
+            query_impl(s, b, medium, nullptr, m, rows.p, precision, F.p, nullptr, stream);
+            sfb::launch_scatter_field(g, idx.p, cnt.p, m, F.p, o.d, stream);
+        }
+        o.finish();
+        sync(stream);
+    });
+}
+
+int sf_render_volume(const sf_grid* density, const double sigma_t[3], const double albedo[3], int material_class,
+                     const double camera_pos[3], const double look_at[3], const double up[3], double vfov_deg,
+                     int width, int height, const float* field, double step_scale, const double background[3],
+                     float* img, sf_stream stream) {
+    return guard([&] {
+        // Camera::Camera (src/camera.cpp:15-18), MediumProperties::validate (src/volume_grid.cpp:132-154)
+        if (width <= 0 || height <= 0) fail(SF_ERR_INVALID_ARGUMENT, "camera: resolution must be positive");
+        if (vfov_deg <= 0.0 || vfov_deg >= 180.0) fail(SF_ERR_INVALID_ARGUMENT, "camera: vfov out of range");
+        validate_albedo(albedo);
+        const double lo = (material_class <= 1) ? 0.0 : 0.5, hi = (material_class <= 1) ? 0.5 : 1.0;
+        for (int c = 0; c < 3; ++c)
+            if (albedo[c] < lo || albedo[c] > hi)
+                fail(SF_ERR_BAD_VALUE, "medium: albedo outside the material class range");
+        for (int c = 0; c < 3; ++c)
+            if (!(sigma_t[c] > 0.0) || !std::isfinite(sigma_t[c]))
+                fail(SF_ERR_BAD_VALUE, "medium: sigma_t scale must be positive");
+        if (!(step_scale > 0.0)) fail(SF_ERR_INVALID_ARGUMENT, "render: step_scale must be positive");
+        In<float> f(field, field ? 3 * density->count() : 0, stream);
+        Out<float> o(img, size_t(width) * height * 3, stream);
+        sfb::launch_render(*density, f.d, sigma_t, albedo, camera_pos, look_at, up, vfov_deg, width, height,
+                           step_scale, background, o.d, stream);
+        o.finish();
+        sync(stream);
+    });
+}
+
 int sf_query_media(const sf_scene* s, const sf_backbone* b, int64_t n, const double* queries, const double* media,
                    int precision, double* F_out, float* y_out, sf_stream stream) {
     return guard([&] {

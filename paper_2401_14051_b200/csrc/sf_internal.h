@@ -34,6 +34,16 @@ inline void cuda_check(cudaError_t e, const char* what) {
 int sm_count();
 void count_launch();  // every kernel launch of the library increments sf_launch_count()
 
+// Image entry point (sf_render.cu): occupied-voxel compaction, bake rows, field scatter, march.
+int64_t launch_occupied(const sf_grid& g, int* idx, int* count, void* tmp, size_t& tmp_bytes, cudaStream_t s);
+void launch_bake_rows(const sf_grid& g, const int* idx, const int* count, int64_t max_rows, const double cam[3],
+                      const double light[3], double* rows, cudaStream_t s);
+void launch_scatter_field(const sf_grid& g, const int* idx, const int* count, int64_t max_rows, const double* F,
+                          float* out, cudaStream_t s);
+void launch_render(const sf_grid& density, const float* field, const double mu[3], const double albedo[3],
+                   const double pos[3], const double look_at[3], const double up[3], double vfov_deg, int width,
+                   int height, double step_scale, const double bg[3], float* img, cudaStream_t s);
+
 }  // namespace sfb
 
 // ---- handle layouts ----------------------------------------------------------
@@ -217,5 +227,15 @@ void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStr
 // (PhaseTable::lookup_hg's g axis, src/phase.cpp:191-219), [n_lobes][angle][aperture].
 void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float* planes,
                          cudaStream_t s);
+
+// Image entry point (sf_render.cu): occupied-voxel compaction, bake rows, field scatter, march.
+int64_t launch_occupied(const sf_grid& g, int* idx, int* count, void* tmp, size_t& tmp_bytes, cudaStream_t s);
+void launch_bake_rows(const sf_grid& g, const int* idx, const int* count, int64_t max_rows, const double cam[3],
+                      const double light[3], double* rows, cudaStream_t s);
+void launch_scatter_field(const sf_grid& g, const int* idx, const int* count, int64_t max_rows, const double* F,
+                          float* out, cudaStream_t s);
+void launch_render(const sf_grid& density, const float* field, const double mu[3], const double albedo[3],
+                   const double pos[3], const double look_at[3], const double up[3], double vfov_deg, int width,
+                   int height, double step_scale, const double bg[3], float* img, cudaStream_t s);
 
 }  // namespace sfb

@@ -17,6 +17,10 @@ Fixtures
   c1.npz    : config 1 (64^3 cloud seed 0, HG g=0.7, albedo 0.99): tvol, 192
               centers, features with the full (64,128,32,16) table, y and F.
   phase_table_full.npz : PhaseTable(64,128,32,16) values.
+  render.npz: render_neural (src/predictor.cpp:585-614) of the small 16^3 cloud: gas
+              medium (sigma_t 14/12/10, albedo 0.45/0.40/0.35), HG 0.7, table (17,33,9,8),
+              backbone seed 0, camera (0.3,0.2,-3.5) -> origin, vfov 40, 24x16, background
+              (0.05,0.1,0.2). `python tests/golden/make_golden.py render` regenerates only it.
 """
 from __future__ import annotations
 
@@ -42,8 +46,30 @@ def cfg_rows(R, centers, g, albedo):
     return config_rows(centers, g, albedo)
 
 
+RENDER = dict(sigma_t=(14.0, 12.0, 10.0), albedo=(0.45, 0.40, 0.35), g=0.7, table=(17, 33, 9, 8),
+              cam=(0.3, 0.2, -3.5), look=(0.0, 0.0, 0.0), up=(0.0, 1.0, 0.0), vfov=40.0, w=24, h=16,
+              background=(0.05, 0.1, 0.2), step_scale=0.5, lam=0.6)
+
+
+def render_fixture(R):
+    n, vs = 16, 2.0 / 16
+    g = R.generate_medium(2, n, 3)
+    r = RENDER
+    tvol = R.build_tvol(g, vs, ORIGIN, LIGHT)
+    ctx = R.make_ctx(g, tvol, vs, ORIGIN, os.path.join(DATA, "diffuse_seed7.vtmpl"),
+                     os.path.join(DATA, "highlight_seed8.vtmpl"), PhaseModel.hg(r["g"]), R.phase_table(*r["table"]))
+    b = R.backbone(BackboneCfg(seed=0))
+    img = R.render_neural(ctx, b, r["sigma_t"], r["albedo"], 1, LIGHT, r["cam"], r["look"], r["up"], r["vfov"],
+                          r["w"], r["h"], r["lam"], r["step_scale"], r["background"])
+    np.savez_compressed(os.path.join(GOLD, "render.npz"), grid=g, img=img, light=LIGHT,
+                        **{k: np.asarray(v, np.float64) for k, v in r.items()})
+
+
 def main():
     R = Reference()
+    if sys.argv[1:] == ["render"]:
+        render_fixture(R)
+        return
     os.makedirs(DATA, exist_ok=True)
     dpath = os.path.join(DATA, "diffuse_seed7.vtmpl")
     hpath = os.path.join(DATA, "highlight_seed8.vtmpl")
@@ -123,6 +149,7 @@ def main():
     np.savez_compressed(os.path.join(GOLD, "c1.npz"), tvol=tvol, centers=centers, feats=f1, cfg8=cfg8, y=y1,
                         F=F1)
     np.savez_compressed(os.path.join(GOLD, "phase_table_full.npz"), table=table)
+    render_fixture(R)
     for f in sorted(os.listdir(GOLD)):
         print(f, os.path.getsize(os.path.join(GOLD, f)))
 

@@ -159,3 +159,41 @@ def test_phase_centre_and_lobe_linearity(oracle, small):
     assert abs((0.7 * v1 + 0.3 * v2) - (0.7 * v1 + 0.3 * v2)) < 1e-9
     # centre point phase == 1 (feature_pipeline.cpp:163-164): first diffuse point
     assert np.all(small["feats_hg"][:, 2 * 194] == 1.0)
+
+
+@pytest.fixture(scope="module")
+def render_gold():
+    from conftest import GOLD
+    return dict(np.load(os.path.join(GOLD, "render.npz")))
+
+
+def oracle_baked_field(oracle, templates, r):
+    """F at every occupied voxel centre of the render fixture from the C restatement."""
+    from oracle import render
+    from paper_2401_14051_b200.scenes import config_rows
+    g = r["grid"]
+    vs = 2.0 / g.shape[0]
+    tv = oracle.build_tvol(g, vs, ORIGIN, r["light"], float(r["lam"]), float(r["step_scale"]))
+    sc = oracle.make_scene(g, tv, vs, ORIGIN, templates[0], templates[1], PhaseModel.hg(float(r["g"])),
+                           oracle.phase_table(*[int(x) for x in r["table"]]))
+    idx, rows = render.bake_rows(g, vs, ORIGIN, r["cam"], r["light"])
+    cfg = BackboneCfg(seed=0)
+    _, F = oracle.predict(cfg, oracle.backbone_init(cfg), oracle.features(sc, rows),
+                          config_rows(rows, [float(r["g"])], r["albedo"]))
+    return render.field_from(g, idx, F)
+
+
+def test_render_restatement_matches_reference(oracle, templates, render_gold):
+    """oracle/render.py (Camera, bake_field, render_volume) composed with the C restatement's
+    F reproduces the reference's own render_neural image (tests/golden/render.npz)."""
+    from oracle import render
+    r = render_gold
+    field = oracle_baked_field(oracle, templates, r)
+    cam = render.Camera(r["cam"], r["look"], r["up"], float(r["vfov"]), int(r["w"]), int(r["h"]))
+    img = render.render_volume(r["grid"], 2.0 / r["grid"].shape[0], ORIGIN, r["sigma_t"], r["albedo"], cam, field,
+                               float(r["step_scale"]), r["background"])
+    assert np.abs(img - r["img"]).max() <= 1e-6 * np.abs(r["img"]).max()
+    # the in-scatter term is a real part of the image (not just background x transmittance)
+    bg_only = render.render_volume(r["grid"], 2.0 / r["grid"].shape[0], ORIGIN, r["sigma_t"], r["albedo"], cam, None,
+                                   float(r["step_scale"]), r["background"])
+    assert np.abs(img - bg_only).max() > 1e-3
