@@ -344,6 +344,9 @@ class Reference:
         L.ref_predict.argtypes = [C.c_void_p, C.c_int64, _f32p, _f64p, _f64p, _f64p]
         L.ref_time_queries.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, _f64p, _f64p, _f64p,
                                        C.POINTER(C.c_double)]
+        L.ref_save_density.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_double, _f64p, C.c_char_p]
+        L.ref_load_density.argtypes = [C.c_char_p, _f64p, C.c_void_p]
+        L.ref_save_feature_table.argtypes = [C.c_void_p, C.c_int64, _f64p, C.c_int, C.c_double, C.c_char_p]
         L.ref_render_neural.argtypes = [C.c_void_p, C.c_void_p, _f64p, _f64p, C.c_int, _f64p, _f64p, _f64p, _f64p,
                                         C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, _f64p, _f32p]
 
@@ -479,3 +482,24 @@ class Reference:
                                              v(cam_pos), v(look_at), v(up), float(vfov), int(w), int(h), lam,
                                              step_scale, v(background), out))
         return out
+
+    def save_density(self, grid, vs, origin, path):
+        nz, ny, nx = grid.shape
+        self._check(self.L.ref_save_density(_c(grid, np.float32), nx, ny, nz, vs, _c(origin, np.float64),
+                                            str(path).encode()))
+
+    def load_density(self, path):
+        info = np.zeros(7)
+        self._check(self.L.ref_load_density(str(path).encode(), info, None))
+        nx, ny, nz = (int(v) for v in info[:3])
+        out = np.zeros((nz, ny, nx), np.float32)
+        self._check(self.L.ref_load_density(str(path).encode(), info, out.ctypes.data))
+        return out, info[3], info[4:7]
+
+    def save_feature_table(self, ctx, centers, levels, lam, path):
+        centers = _c(centers, np.float64).reshape(-1, 9)
+        self._check(self.L.ref_save_feature_table(ctx, len(centers), centers, int(levels), float(lam),
+                                                  str(path).encode()))
+
+    def save_backbone(self, b, path):
+        self._check(self.L.ref_backbone_save(b, str(path).encode()))

@@ -422,4 +422,42 @@ int ref_render_neural(void* cp, void* bp, const double* sigma_t3, const double* 
     });
 }
 
+// save_density (src/volume_grid.cpp:224-238) of the given grid.
+int ref_save_density(const float* vals, int nx, int ny, int nz, double vs, const double* origin, const char* path) {
+    return guard([&] { sf::save_density(make_grid(vals, nx, ny, nz, vs, origin), path); });
+}
+
+// load_density (src/volume_grid.cpp:175-222): dims/vs/origin into info[7], values into out (may be null).
+int ref_load_density(const char* path, double* info, float* out) {
+    return guard([&] {
+        sf::DensityGrid g = sf::load_density(path);
+        info[0] = g.nx(); info[1] = g.ny(); info[2] = g.nz(); info[3] = g.voxel_size();
+        info[4] = g.origin().x; info[5] = g.origin().y; info[6] = g.origin().z;
+        if (out) std::memcpy(out, g.values().data(), g.values().size() * sizeof(float));
+    });
+}
+
+// precompute_tables' per-center blocks (sample_features x2 on the context) for the given
+// centers, then save_feature_table (src/feature_pipeline.cpp:268-294) with the context's
+// phase table, the identity combiner of `levels` levels, lambda and template_scale.
+int ref_save_feature_table(void* cp, int64_t q, const double* centers9, int levels, double lambda,
+                           const char* path) {
+    Ctx* c = static_cast<Ctx*>(cp);
+    return guard([&] {
+        sf::FeatureTable t;
+        for (int64_t i = 0; i < q; ++i) {
+            const double* s = centers9 + 9 * i;
+            t.diffuse.push_back(sf::sample_features(v3(s), v3(s + 3), v3(s + 6), c->dt, c->density, c->tvol,
+                                                    c->model, c->table, c->template_scale));
+            t.highlight.push_back(sf::sample_features(v3(s), v3(s + 3), v3(s + 6), c->ht, c->density, c->tvol,
+                                                      c->model, c->table, c->template_scale));
+        }
+        t.phase_table = c->table;
+        t.combiner = sf::CombinerWeights::identity(levels);
+        t.lambda = lambda;
+        t.template_scale = c->template_scale;
+        sf::save_feature_table(t, path);
+    });
+}
+
 }  // extern "C"

@@ -65,10 +65,35 @@ def render_fixture(R):
                         **{k: np.asarray(v, np.float64) for k, v in r.items()})
 
 
+def io_fixtures(R):
+    """Reference-written artifacts (tests/golden/io/): small.vgrid (16^3 cloud seed 3, origin
+    (-1,-1,-1), vs 1/8), small.vfeat (precompute_tables of 4 centers on it, HG 0.7, table
+    (9,17,5,8), identity combiner, lambda 0.6, template scale 1.5), tiny.vnet (backbone
+    counts (2,3)/(2,), widths 4/8/8, seed 5) and lit.vnet (same with literal attention)."""
+    out = os.path.join(GOLD, "io")
+    os.makedirs(out, exist_ok=True)
+    n, vs = 16, 2.0 / 16
+    g = R.generate_medium(2, n, 3)
+    R.save_density(g, vs, ORIGIN, os.path.join(out, "small.vgrid"))
+    tv = R.build_tvol(g, vs, ORIGIN, LIGHT)
+    ctx = R.make_ctx(g, tv, vs, ORIGIN, os.path.join(DATA, "diffuse_seed7.vtmpl"),
+                     os.path.join(DATA, "highlight_seed8.vtmpl"), PhaseModel.hg(0.7), R.phase_table(9, 17, 5, 8),
+                     template_scale=1.5)
+    centers = R.draw_centers(g, vs, ORIGIN, 4, 5, LIGHT)
+    R.save_feature_table(ctx, centers, 5, 0.6, os.path.join(out, "small.vfeat"))
+    for name, lit in (("tiny", False), ("lit", True)):
+        b = R.backbone(BackboneCfg(diffuse_counts=(2, 3), highlight_counts=(2,), width=4, merge_width=8,
+                                   head_width=8, seed=5, literal_attention=lit))
+        R.save_backbone(b, os.path.join(out, f"{name}.vnet"))
+
+
 def main():
     R = Reference()
     if sys.argv[1:] == ["render"]:
         render_fixture(R)
+        return
+    if sys.argv[1:] == ["io"]:
+        io_fixtures(R)
         return
     os.makedirs(DATA, exist_ok=True)
     dpath = os.path.join(DATA, "diffuse_seed7.vtmpl")
@@ -150,6 +175,7 @@ def main():
                         F=F1)
     np.savez_compressed(os.path.join(GOLD, "phase_table_full.npz"), table=table)
     render_fixture(R)
+    io_fixtures(R)
     for f in sorted(os.listdir(GOLD)):
         print(f, os.path.getsize(os.path.join(GOLD, f)))
 

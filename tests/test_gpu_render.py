@@ -94,3 +94,40 @@ def test_render_errors(setup):
     sf.render_volume(empty, (1, 1, 1), (0.9, 0.9, 0.9), sf.Camera((0, 0, -3), width=8, height=8),
                      opts=sf.RenderOptions(background=(0.1, 0.2, 0.3)), material_class="solid_liquid", out=out)
     assert np.allclose(out.cpu().numpy(), np.broadcast_to([0.1, 0.2, 0.3], (8, 8, 3)))
+
+
+# ---- artifact formats on the device ------------------------------
+def test_io_device_round_trips(tmp_path):
+    from paper_2401_14051_b200 import io
+    src = os.path.join(GOLD, "io")
+    net = io.load_backbone(os.path.join(src, "tiny.vnet"))
+    _, params = io.read_network(os.path.join(src, "tiny.vnet"))
+    assert np.array_equal(net.params(), params)
+    io.save_backbone(net, str(tmp_path / "t.vnet"))
+    assert (tmp_path / "t.vnet").read_bytes() == open(os.path.join(src, "tiny.vnet"), "rb").read()
+    g = io.load_density(os.path.join(src, "small.vgrid"))
+    io.save_density(g, str(tmp_path / "t.vgrid"))
+    assert (tmp_path / "t.vgrid").read_bytes() == open(os.path.join(src, "small.vgrid"), "rb").read()
+
+
+def test_precompute_tables_vs_reference_vfeat(tmp_path):
+    """precompute_tables on the GPU from the reference's .vgrid reproduces the reference's
+    .vfeat: features at the feature bar (1e-5 relative, floor 1e-6 max), the rest exact."""
+    from conftest import LIGHT
+    from paper_2401_14051_b200 import io
+    src = os.path.join(GOLD, "io")
+    want = io.load_feature_table(os.path.join(src, "small.vfeat"))
+    g = io.load_density(os.path.join(src, "small.vgrid"))
+    pyr = sf.DensityPyramid(g)
+    tv = sf.build_transmittance_volume(pyr, LIGHT)
+    tm = (sf.load_template(os.path.join(DATA, "diffuse_seed7.vtmpl")),
+          sf.load_template(os.path.join(DATA, "highlight_seed8.vtmpl")))
+    got = io.precompute_tables(want.centers, tm[0], tm[1], g, tv, sf.PhaseModel.hg(0.7), sf.PhaseTable(9, 17, 5, 8),
+                               sf.CombinerWeights.identity(pyr.level_count()), sf.FeatureConfig(template_scale=1.5))
+    assert np.array_equal(got.centers, want.centers) and np.array_equal(got.kernels, want.kernels)
+    assert np.array_equal(got.scales, want.scales) and (got.lambda_, got.template_scale) == (0.6, 1.5)
+    assert np.abs(got.phase_table.view(np.int32).astype(np.int64) - want.phase_table.view(np.int32)).max() <= 1
+    f, w = got.features(), want.features()
+    assert np.all(np.abs(f - w) <= 1e-5 * np.abs(w) + 1e-6 * np.abs(w).max())
+    io.save_feature_table(got, str(tmp_path / "t.vfeat"))
+    assert io.load_feature_table(str(tmp_path / "t.vfeat")).features().shape == w.shape
