@@ -990,30 +990,27 @@ void check_precision(const sf_backbone& b, int precision, cudaStream_t s) {
     sfb::tc_prepare(const_cast<sf_backbone&>(b), s);
 }
 
-// Second stream + events for the pipelined bf16 query (one set per process; calls serialise on it).
-struct PipeStreams {
+// Copy stream for the host-I/O overlap of the bf16 query (one per process; calls serialise on it).
+struct CopyStream {
     std::mutex mu;
-    cudaStream_t aux = nullptr;
-    cudaEvent_t ready = nullptr, done[2] = {nullptr, nullptr};
+    cudaStream_t cs = nullptr;
 };
-PipeStreams& pipe_streams() {
-    static PipeStreams* ps = [] {
-        auto* p = new PipeStreams;
-        SFB_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
-        SFB_CUDA(cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming));
-        for (auto& e : p->done) SFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+CopyStream& copy_stream() {
+    static CopyStream* c = [] {
+        auto* p = new CopyStream;
+        SFB_CUDA(cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking));
         return p;
     }();
-    return *ps;
+    return *c;
 }
-// tiles per pipelined chunk (SF_PIPE_TILES; default off: measured no gain at C2 once the
-// sample/sort kernel stopped round-tripping its scratch through a third phase)
-int64_t pipe_tiles() {
-    static const int64_t t = [] {
-        const char* e = std::getenv("SF_PIPE_TILES");
-        return e ? std::atoll(e) : int64_t(0);
-    }();
-    return t;
+
+// Event recorded on `from` and waited on by `to` (created per use: a few per call).
+void stream_wait(cudaStream_t to, cudaStream_t from) {
+    cudaEvent_t e;
+    SFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SFB_CUDA(cudaEventRecord(e, from));
+    SFB_CUDA(cudaStreamWaitEvent(to, e, 0));
+    SFB_CUDA(cudaEventDestroy(e));  // released once the wait completes
 }
 
 // bf16 path over one chunk: fused sample+sort (or sort of given features) -> tcgen05 backbone.
@@ -1147,86 +1144,106 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
         if (nd != s->dt->total || nh != s->ht->total)
             fail(SF_ERR_SHAPE_MISMATCH, "feature block does not match template counts");
         check_precision(*b, precision, stream);
-        In<double> iq(queries, size_t(n) * 9, stream);
-        Out<double> oF(F_out, size_t(n) * 3, stream);
-        Out<float> oy(y_out, size_t(n) * 3, stream);
         if (precision == SF_PRECISION_BF16) {
-            // production path: fused sample+sort -> tcgen05 backbone. The queries go in chunks
-            // of tiles through two streams: the backbone of chunk k (latency-bound: a few warps
-            // per SM waiting on tensor-core round trips) runs while chunk k+1 is sampled
-            // (throughput-bound), and chunk k's operand blocks are still L2-resident when read.
+            // production path: query_prep -> fused sample+sort -> tcgen05 backbone per chunk of
+            // tiles, all on the caller's stream. With host query rows / outputs the batch goes
+            // in two chunks and the host transfers ride a copy stream: chunk 1's rows land while
+            // chunk 0 computes, chunk 0's F returns while chunk 1 computes.
             const sfb::SortLayout L = sfb::sort_layout(c);
             const int64_t n_tiles = (n + sfb::kUmmaM - 1) / sfb::kUmmaM;
-            const int64_t span = std::min<int64_t>(n_tiles, 1 << 13) * sfb::kUmmaM;  // query_prep batch
-            int64_t chunk_tiles = pipe_tiles();
-            if (chunk_tiles <= 0 || chunk_tiles >= n_tiles) chunk_tiles = std::min<int64_t>(n_tiles, 1 << 12);
+            const bool h_in = !is_device_ptr(queries);
+            const bool h_out = (F_out && !is_device_ptr(F_out)) || (y_out && !is_device_ptr(y_out));
+            static const bool overlap_on = !std::getenv("SF_NO_HOST_OVERLAP");
+            const bool overlap = overlap_on && (h_in || h_out) && n_tiles >= 64;
+            int64_t chunk_tiles = overlap ? (n_tiles + 1) / 2 : n_tiles;
+            chunk_tiles = std::min<int64_t>(chunk_tiles, 1 << 12);  // operand blocks <= ~1.3 GB
             const int64_t chunk = chunk_tiles * sfb::kUmmaM;
-            const int nbuf = chunk < n ? 2 : 1;
-            Scratch<uint8_t> ops(size_t(nbuf) * chunk_tiles * L.tile_bytes, stream);
-            Scratch<float> mms(size_t(nbuf) * L.n_layers * chunk * 8, stream);
-            Scratch<double> cfg8(size_t(span) * 8, stream);
-            Scratch<uint8_t> recs(size_t(span) * sfb::query_rec_bytes(), stream);
+            Scratch<uint8_t> ops(size_t(chunk_tiles) * L.tile_bytes, stream);
+            Scratch<float> mms(size_t(L.n_layers) * chunk * 8, stream);
+            Scratch<double> cfg8(size_t(chunk) * 8, stream);
+            Scratch<uint8_t> recs(size_t(chunk) * sfb::query_rec_bytes(), stream);
             Scratch<int> err(1, stream);
             SFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
+            // device-side rows and outputs (the caller's when already on the device)
+            Scratch<double> rows_buf(h_in ? size_t(n) * 9 : 0, stream);
+            Scratch<double> F_buf(F_out && !is_device_ptr(F_out) ? size_t(n) * 3 : 0, stream);
+            Scratch<float> y_buf(y_out && !is_device_ptr(y_out) ? size_t(n) * 3 : 0, stream);
+            const double* rows = h_in ? rows_buf.p : queries;
+            double* Fd = F_out ? (F_buf.p ? F_buf.p : F_out) : nullptr;
+            float* yd = y_out ? (y_buf.p ? y_buf.p : y_out) : nullptr;
             sfb::SceneDev sc = sfb::scene_dev(*s->density, *s->tvol->values, s->d_dt, s->model, *s->table,
                                               s->template_scale);
             sc.dt4 = s->d_dt4;
             sfb::TemplateDev dt = sfb::template_dev(*s->dt), ht = sfb::template_dev(*s->ht);
-            {
-                StageScope st(SF_STAGE_CONFIG, stream);
-                sfb::launch_diffuse_light(sc, dt, s->d_planes, s->n_planes, iq.d, s->d_pre, stream);
+            CopyStream& cps = copy_stream();
+            std::unique_lock<std::mutex> clk(cps.mu, std::defer_lock);
+            cudaStream_t cs = stream;
+            if (h_in || h_out) {
+                clk.lock();
+                cs = cps.cs;
+                stream_wait(cs, stream);  // the scratch allocations above are ordered on `stream`
             }
-            PipeStreams& ps = pipe_streams();
-            cudaStream_t aux = nbuf > 1 ? ps.aux : stream;
-            std::lock_guard<std::mutex> plk(ps.mu);
-            int k = 0;
-            for (int64_t p0 = 0; p0 < n; p0 += span) {
-                const int64_t pm = std::min(span, n - p0);
+            // every chunk's rows are queued at once, each followed by its own event
+            std::vector<cudaEvent_t> rows_ready;
+            struct EvGuard {
+                std::vector<cudaEvent_t>& v;
+                ~EvGuard() {
+                    for (cudaEvent_t e : v) cudaEventDestroy(e);
+                }
+            } ev_guard{rows_ready};
+            if (h_in)
+                for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+                    const int64_t m = std::min(chunk, n - c0);
+                    SFB_CUDA(cudaMemcpyAsync(rows_buf.p + 9 * c0, queries + 9 * c0, size_t(m) * 9 * sizeof(double),
+                                             cudaMemcpyHostToDevice, cs));
+                    cudaEvent_t e;
+                    SFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    rows_ready.push_back(e);
+                    SFB_CUDA(cudaEventRecord(e, cs));
+                }
+            for (int64_t c0 = 0, k = 0; c0 < n; c0 += chunk, ++k) {
+                const int64_t m = std::min(chunk, n - c0);
+                if (h_in) SFB_CUDA(cudaStreamWaitEvent(stream, rows_ready[size_t(k)], 0));  // rows of chunk k
+                if (k == 0) {
+                    StageScope st(SF_STAGE_CONFIG, stream);
+                    sfb::launch_diffuse_light(sc, dt, s->d_planes, s->n_planes, rows, s->d_pre, stream);
+                }
                 {
                     StageScope st(SF_STAGE_CONFIG, stream);
-                    sfb::launch_query_prep(sc, ht, *medium, pm, iq.d + 9 * p0, media ? media + 4 * p0 : nullptr,
+                    sfb::launch_query_prep(sc, ht, *medium, m, rows + 9 * c0, media ? media + 4 * c0 : nullptr,
                                            cfg8.p, recs.p, stream);
                 }
-                for (int64_t c0 = 0; c0 < pm; c0 += chunk, ++k) {
-                    const int64_t m = std::min(chunk, pm - c0), q0 = p0 + c0;
-                    const int bi = k % nbuf;
-                    uint8_t* ob = ops.p + size_t(bi) * chunk_tiles * L.tile_bytes;
-                    float* mb = mms.p + size_t(bi) * L.n_layers * chunk * 8;
-                    if (k >= nbuf) SFB_CUDA(cudaStreamWaitEvent(stream, ps.done[bi], 0));  // buffer bi free
-                    {
-                        StageScope st(SF_STAGE_SAMPLE_SORT, stream);
-                        sfb::launch_sample_sort(&sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, L, m,
-                                                recs.p + c0 * sfb::query_rec_bytes(), nullptr, ob, mb, err.p, stream,
-                                                media != nullptr);
-                    }
-                    if (aux != stream) {
-                        SFB_CUDA(cudaEventRecord(ps.ready, stream));
-                        SFB_CUDA(cudaStreamWaitEvent(aux, ps.ready, 0));
-                    }
-                    {
-                        StageScope st(SF_STAGE_BACKBONE, aux);
-                        sfb::launch_backbone_tc(*b, m, ob, mb, cfg8.p + 8 * c0, oy.d ? oy.d + 3 * q0 : nullptr,
-                                                oF.d ? oF.d + 3 * q0 : nullptr, aux);
-                    }
-                    if (aux != stream) SFB_CUDA(cudaEventRecord(ps.done[bi], aux));
-                    // the next query_prep batch overwrites cfg8/recs that this chunk's backbone reads
-                    if (aux != stream && c0 + chunk >= pm && p0 + span < n)
-                        SFB_CUDA(cudaStreamWaitEvent(stream, ps.done[bi], 0));
+                {
+                    StageScope st(SF_STAGE_SAMPLE_SORT, stream);
+                    sfb::launch_sample_sort(&sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, L, m, recs.p, nullptr,
+                                            ops.p, mms.p, err.p, stream, media != nullptr);
+                }
+                {
+                    StageScope st(SF_STAGE_BACKBONE, stream);
+                    sfb::launch_backbone_tc(*b, m, ops.p, mms.p, cfg8.p, yd ? yd + 3 * c0 : nullptr,
+                                            Fd ? Fd + 3 * c0 : nullptr, stream);
+                }
+                if (h_out) {  // this chunk's results home while the next chunk computes
+                    stream_wait(cs, stream);
+                    if (F_buf.p)
+                        SFB_CUDA(cudaMemcpyAsync(F_out + 3 * c0, F_buf.p + 3 * c0, size_t(m) * 3 * sizeof(double),
+                                                 cudaMemcpyDeviceToHost, cs));
+                    if (y_buf.p)
+                        SFB_CUDA(cudaMemcpyAsync(y_out + 3 * c0, y_buf.p + 3 * c0, size_t(m) * 3 * sizeof(float),
+                                                 cudaMemcpyDeviceToHost, cs));
                 }
             }
-            if (aux != stream) {  // join: every chunk's backbone before the caller's stream continues
-                SFB_CUDA(cudaEventRecord(ps.ready, aux));
-                SFB_CUDA(cudaStreamWaitEvent(stream, ps.ready, 0));
-            }
-            if (!oF.host && !oy.host && !iq.buf.p) return;  // device in/out: asynchronous (see below)
+            if (cs != stream) stream_wait(stream, cs);  // scratch frees and the caller see the copies
+            if (!h_out && !h_in) return;  // device in/out: asynchronous (see below)
             int herr = 0;
             SFB_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
-            oF.finish();
-            oy.finish();
             sync(stream);
             if (herr) fail(SF_ERR_INVALID_ARGUMENT, "place_template: entry coincides with p");
             return;
         }
+        In<double> iq(queries, size_t(n) * 9, stream);
+        Out<double> oF(F_out, size_t(n) * 3, stream);
+        Out<float> oy(y_out, size_t(n) * 3, stream);
         const int64_t chunk = std::min<int64_t>(n, 1 << 17);
         const int64_t feat = 3 * int64_t(nd + nh);
         Scratch<float> feats(size_t(chunk) * feat, stream);

@@ -35,6 +35,10 @@ namespace sfb {
 namespace {
 
 constexpr int kWarps = 8;
+#ifndef SF_SORT_MINB
+#define SF_SORT_MINB 3
+#endif
+constexpr int kMinBlocks = SF_SORT_MINB;  // resident blocks per SM the register budget is sized for
 constexpr int kMaxSegs = 96;
 constexpr int kMaxChunks = 512;
 
@@ -496,7 +500,7 @@ __device__ __forceinline__ void sort_emit_pair(const float* seg, int cnt, bool u
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 3)
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     k_sample_sort(SceneDev sc, TemplateDev ht, SortDesc d, const float2* __restrict__ planes_g,
                   const float4* __restrict__ pre, int64_t n, const QueryCtx* __restrict__ recs,
                   const float* __restrict__ feats, uint8_t* __restrict__ ops, float* __restrict__ mms, int* err) {
@@ -741,17 +745,19 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
         return fa.sharedSizeBytes;
     }();
     // 3 blocks/SM (the register limit) within 228 KB, 1 KB reserved per block
-    d.nbuf = 3 * (smem_for(2) + static_smem + 1024) <= 228 * 1024 ? 2 : 1;
+    d.nbuf = kMinBlocks * (smem_for(2) + static_smem + 1024) <= 228 * 1024 ? 2 : 1;
     if (const char* e = std::getenv("SF_SORT_NBUF")) d.nbuf = std::atoi(e) == 1 ? 1 : d.nbuf;
     const size_t smem = smem_for(d.nbuf);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
+        // (no carveout preference: the gathers live on L1 hits; forcing the max-shared carveout
+        // shrank L1 and cost 25%)
         SFB_CUDA(cudaFuncSetAttribute(k_sample_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         attr = smem;
     }
     const int64_t q_pad = int64_t(d.n_tiles) * kUmmaM;
     int64_t blocks = q_pad / kWarps;
-    int64_t cap = int64_t(sm_count()) * 3;
+    int64_t cap = int64_t(sm_count()) * kMinBlocks;
     if (blocks > cap) blocks = cap;
     SceneDev scd = sc ? *sc : SceneDev{};
     TemplateDev htd = ht ? *ht : TemplateDev{1, 0, nullptr, nullptr, 1.0, nullptr};

@@ -696,6 +696,8 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
     static size_t attr_set = 0;
     if (attr_set != smem) {
         SFB_CUDA(cudaFuncSetAttribute(k_backbone_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        SFB_CUDA(cudaFuncSetAttribute(k_backbone_tc, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      int(cudaSharedmemCarveoutMaxShared)));
         attr_set = smem;
         int per_sm = 0;  // the design assumes two co-resident tiles per SM (registers, smem, 2 x 256 TMEM cols)
         SFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backbone_tc, kThreads, smem));
