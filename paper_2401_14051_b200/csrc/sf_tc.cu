@@ -384,13 +384,16 @@ __global__ void __launch_bounds__(kThreads, 2)
                 {
                     const float* b2 = reinterpret_cast<const float*>(s2 + kSlotB2);
                     tmem_ld32(tmem + lane + 32, o);
+                    PROF(9);
 #pragma unroll
                     for (int e = 0; e < 32; ++e) o[e] = relu(o[e] + b2[e]) + oa[e];
                 }
                 if (!last) {
 #pragma unroll
                     for (int e = 0; e < 32; ++e) oa[e] = o[e] * w_next;
+                    PROF(10);
                     store_row32(a_att, oa);
+                    PROF(11);
                 } else if (kind == 0) {  // od: K 0-31 of the merge input
                     store_row32(a_od, o);
                     stack_start(s2, tau, rc, oa);  // highlight stack (once per type: not overlapped)

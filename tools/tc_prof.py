@@ -23,5 +23,6 @@ sf.lib.sf_debug_tc_profile(buf)
 names = ["wait_full1", "mma_fc1", "epi_fc1", "wait_full2", "issue_fc2", "attention", "wait_fc2", "epi_fc2+loop", "total"]
 v = [buf[i] / 5 for i in range(16)]
 print({n: int(x) for n, x in zip(names, v)}, "per-layer-step avg (36 layers):", {n: int(x / 36) for n, x in zip(names[:7], v[:7])})
+print("fc2 epilogue split (per layer):", {k: int(v[i] / 36) for k, i in (("tmem_ld", 9), ("math", 10), ("store", 11))})
 n_mma = max(v[13], 1)
 print("run_mma per call (cycles):", {k: int(v[i] / n_mma) for k, i in (("sync", 9), ("prefetch", 10), ("issue", 11), ("wait", 12))}, "calls", n_mma)
