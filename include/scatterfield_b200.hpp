@@ -345,4 +345,108 @@ inline Vec3 decode_prediction(const Vec3& y, const Vec3& albedo, double gamma) {
             std::pow(albedo.z, gamma) * std::expm1(y.z)};
 }
 
+// ---- the fused per-shading-point query (render_neural's bake loop) ------------------------
+// Bound inputs of the query; the handles must outlive it (the reference's render_neural holds
+// the same objects while baking, src/predictor.cpp:585-614).
+class Scene {
+  public:
+    Scene(const DensityGrid& density, const TransmittanceFeatureVolume& tvol, const SamplingTemplate& diffuse,
+          const SamplingTemplate& highlight, const PhaseModel& model, const PhaseTable& table,
+          double template_scale = 1.0)
+        : dt_(diffuse.device()), ht_(highlight.device()), density_(density), tvol_(tvol), table_(table) {
+        sf_phase_model m = model.to_c();
+        sf_scene* s = nullptr;
+        check(sf_scene_create(density.handle(), tvol.handle(), dt_.get(), ht_.get(), &m, table.handle(),
+                              template_scale, &s));
+        h_.reset(s, sf_scene_destroy);
+    }
+    const sf_scene* handle() const { return h_.get(); }
+
+  private:
+    std::shared_ptr<sf_template> dt_, ht_;
+    DensityGrid density_;
+    TransmittanceFeatureVolume tvol_;
+    PhaseTable table_;
+    std::shared_ptr<sf_scene> h_;
+};
+
+// Per query (p, omega, l): sample_features x2 -> make_config -> predict_y -> decode_prediction.
+// rows: 9 doubles per query; returns F (3 doubles per query).
+inline std::vector<double> query(const Scene& scene, const Backbone& net, const ConfigParams& medium,
+                                 const std::vector<double>& rows, int precision = SF_PRECISION_FP32) {
+    sf_medium_params m{};
+    m.n_g = int(medium.g_params.size());
+    for (size_t i = 0; i < medium.g_params.size() && i < 3; ++i) m.g[i] = medium.g_params[i];
+    m.albedo[0] = medium.albedo.x;
+    m.albedo[1] = medium.albedo.y;
+    m.albedo[2] = medium.albedo.z;
+    std::vector<double> F(rows.size() / 9 * 3);
+    check(sf_query(scene.handle(), net.handle(), &m, int64_t(rows.size() / 9), rows.data(), precision, F.data(),
+                   nullptr, nullptr));
+    return F;
+}
+
+// Rows [z0, z1) of build_transmittance_volume's values (the per-light build sharded by z-slab).
+inline std::vector<float> build_transmittance_slab(const DensityPyramid& p, const Vec3& light,
+                                                   const CombinerWeights& w, const FeatureConfig& cfg, int z0,
+                                                   int z1, int nx, int ny) {
+    std::vector<float> k, s(w.scales), out(size_t(nx) * ny * size_t(z1 > z0 ? z1 - z0 : 0));
+    for (const auto& kk : w.kernels) k.insert(k.end(), kk.begin(), kk.end());
+    double l[3] = {light.x, light.y, light.z};
+    check(sf_build_transmittance_slab(p.handle(), l, k.data(), s.data(), cfg.lambda, cfg.step_scale, z0, z1,
+                                      out.data(), nullptr));
+    return out;
+}
+
+// ---- image entry point (inc/camera.h, inc/rte.h, inc/image.h) ----------------------------
+struct Camera {
+    Vec3 position, look_at{0, 0, 0}, up{0, 1, 0};
+    double vfov_degrees = 40.0;
+    int width = 64, height = 64;
+};
+
+struct RenderOptions {
+    double step_scale = 0.5;
+    Vec3 background{0.0, 0.0, 0.0};
+};
+
+struct ImageF {
+    int width = 0, height = 0;
+    std::vector<float> rgb;  // width * height * 3, row-major
+};
+
+enum class MaterialClass { Air, Gas, SolidLiquid, Skin };
+
+// render_neural (src/predictor.cpp:585-614): tvol for `light`, bake F on the density lattice
+// (sf_bake_field), march the image (sf_render_volume).
+inline ImageF render_neural(const DensityGrid& grid, const DensityPyramid& pyr, const Vec3& light,
+                            const Camera& cam, const Backbone& net, const PhaseTable& table,
+                            const SamplingTemplate& dt, const SamplingTemplate& ht, const PhaseModel& model,
+                            const Vec3& sigma_t, const ConfigParams& medium, MaterialClass mc,
+                            const FeatureConfig& fcfg = {}, const RenderOptions& ro = {},
+                            int precision = SF_PRECISION_FP32) {
+    TransmittanceFeatureVolume tvol =
+        build_transmittance_volume(pyr, light, CombinerWeights::identity(pyr.level_count()), fcfg);
+    Scene scene(grid, tvol, dt, ht, model, table, fcfg.template_scale);
+    sf_medium_params m{};
+    m.n_g = int(medium.g_params.size());
+    for (size_t i = 0; i < medium.g_params.size() && i < 3; ++i) m.g[i] = medium.g_params[i];
+    m.albedo[0] = medium.albedo.x;
+    m.albedo[1] = medium.albedo.y;
+    m.albedo[2] = medium.albedo.z;
+    int dims[3];
+    double vs, o[3];
+    check(sf_grid_info(grid.handle(), dims, &vs, o));
+    std::vector<float> field(size_t(3) * dims[0] * dims[1] * dims[2]);
+    double cp[3] = {cam.position.x, cam.position.y, cam.position.z};
+    check(sf_bake_field(scene.handle(), net.handle(), &m, cp, precision, field.data(), nullptr));
+    ImageF img{cam.width, cam.height, std::vector<float>(size_t(cam.width) * cam.height * 3)};
+    double st[3] = {sigma_t.x, sigma_t.y, sigma_t.z}, al[3] = {medium.albedo.x, medium.albedo.y, medium.albedo.z};
+    double la[3] = {cam.look_at.x, cam.look_at.y, cam.look_at.z}, up[3] = {cam.up.x, cam.up.y, cam.up.z};
+    double bg[3] = {ro.background.x, ro.background.y, ro.background.z};
+    check(sf_render_volume(grid.handle(), st, al, int(mc), cp, la, up, cam.vfov_degrees, cam.width, cam.height,
+                           field.data(), ro.step_scale, bg, img.rgb.data(), nullptr));
+    return img;
+}
+
 }  // namespace scatterfield_b200
