@@ -1154,7 +1154,14 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             const bool h_in = !is_device_ptr(queries);
             const bool h_out = (F_out && !is_device_ptr(F_out)) || (y_out && !is_device_ptr(y_out));
             static const bool overlap_on = !std::getenv("SF_NO_HOST_OVERLAP");
-            const bool overlap = overlap_on && (h_in || h_out) && n_tiles >= 64;
+            // Volumes beyond L2 (x-pair records of a 256^3 grid are 268 MB): process the queries in
+            // Morton order of p so concurrently sampled queries share the volume's cache lines;
+            // results are written back to the caller's rows.
+            static const int morton_env = std::getenv("SF_MORTON") ? std::atoi(std::getenv("SF_MORTON")) : -1;
+            const size_t vol_bytes = s->density->count() * sizeof(float4);
+            const bool reorder = morton_env >= 0 ? morton_env > 0 && n > 1
+                                                 : (vol_bytes > (size_t(96) << 20) && n >= 4096);
+            const bool overlap = overlap_on && !reorder && (h_in || h_out) && n_tiles >= 64;
             int64_t chunk_tiles = overlap ? (n_tiles + 1) / 2 : n_tiles;
             chunk_tiles = std::min<int64_t>(chunk_tiles, 1 << 12);  // operand blocks <= ~1.3 GB
             const int64_t chunk = chunk_tiles * sfb::kUmmaM;
@@ -1201,17 +1208,31 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                     rows_ready.push_back(e);
                     SFB_CUDA(cudaEventRecord(e, cs));
                 }
+            Scratch<int> perm(reorder ? size_t(n) : 0, stream);
+            if (reorder) {
+                for (cudaEvent_t e : rows_ready) SFB_CUDA(cudaStreamWaitEvent(stream, e, 0));  // every row
+                Scratch<uint32_t> keys(size_t(n) * 2, stream);
+                Scratch<int> idx(size_t(n), stream);
+                sfb::launch_morton(s->density->dev(), n, rows, keys.p, idx.p, stream);
+                size_t tmp_bytes = 0;
+                sfb::launch_sort_keys(keys.p, keys.p + n, idx.p, perm.p, int(n), 30, nullptr, tmp_bytes, stream);
+                Scratch<uint8_t> tmp(tmp_bytes, stream);
+                sfb::launch_sort_keys(keys.p, keys.p + n, idx.p, perm.p, int(n), 30, tmp.p, tmp_bytes, stream);
+            }
             for (int64_t c0 = 0, k = 0; c0 < n; c0 += chunk, ++k) {
                 const int64_t m = std::min(chunk, n - c0);
-                if (h_in) SFB_CUDA(cudaStreamWaitEvent(stream, rows_ready[size_t(k)], 0));  // rows of chunk k
+                if (h_in && !reorder) SFB_CUDA(cudaStreamWaitEvent(stream, rows_ready[size_t(k)], 0));  // chunk k
                 if (k == 0) {
                     StageScope st(SF_STAGE_CONFIG, stream);
                     sfb::launch_diffuse_light(sc, dt, s->d_planes, s->n_planes, rows, s->d_pre, stream);
                 }
                 {
                     StageScope st(SF_STAGE_CONFIG, stream);
-                    sfb::launch_query_prep(sc, ht, *medium, m, rows + 9 * c0, media ? media + 4 * c0 : nullptr,
-                                           cfg8.p, recs.p, stream);
+                    if (reorder)
+                        sfb::launch_query_prep(sc, ht, *medium, m, rows, media, cfg8.p, recs.p, stream, perm.p + c0);
+                    else
+                        sfb::launch_query_prep(sc, ht, *medium, m, rows + 9 * c0, media ? media + 4 * c0 : nullptr,
+                                               cfg8.p, recs.p, stream);
                 }
                 {
                     StageScope st(SF_STAGE_SAMPLE_SORT, stream);
@@ -1220,10 +1241,13 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                 }
                 {
                     StageScope st(SF_STAGE_BACKBONE, stream);
-                    sfb::launch_backbone_tc(*b, m, ops.p, mms.p, cfg8.p, yd ? yd + 3 * c0 : nullptr,
-                                            Fd ? Fd + 3 * c0 : nullptr, stream);
+                    if (reorder)
+                        sfb::launch_backbone_tc(*b, m, ops.p, mms.p, cfg8.p, yd, Fd, stream, perm.p + c0);
+                    else
+                        sfb::launch_backbone_tc(*b, m, ops.p, mms.p, cfg8.p, yd ? yd + 3 * c0 : nullptr,
+                                                Fd ? Fd + 3 * c0 : nullptr, stream);
                 }
-                if (h_out) {  // this chunk's results home while the next chunk computes
+                if (h_out && !reorder) {  // this chunk's results home while the next chunk computes
                     stream_wait(cs, stream);
                     if (F_buf.p)
                         SFB_CUDA(cudaMemcpyAsync(F_out + 3 * c0, F_buf.p + 3 * c0, size_t(m) * 3 * sizeof(double),
@@ -1232,6 +1256,13 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                         SFB_CUDA(cudaMemcpyAsync(y_out + 3 * c0, y_buf.p + 3 * c0, size_t(m) * 3 * sizeof(float),
                                                  cudaMemcpyDeviceToHost, cs));
                 }
+            }
+            if (h_out && reorder) {  // scattered rows: one copy home after the last chunk
+                stream_wait(cs, stream);
+                if (F_buf.p)
+                    SFB_CUDA(cudaMemcpyAsync(F_out, F_buf.p, size_t(n) * 3 * sizeof(double), cudaMemcpyDeviceToHost, cs));
+                if (y_buf.p)
+                    SFB_CUDA(cudaMemcpyAsync(y_out, y_buf.p, size_t(n) * 3 * sizeof(float), cudaMemcpyDeviceToHost, cs));
             }
             if (cs != stream) stream_wait(stream, cs);  // scratch frees and the caller see the copies
             if (!h_out && !h_in) return;  // device in/out: asynchronous (see below)

@@ -319,9 +319,10 @@ __global__ void k_diffuse_prep(SceneDev sc, TemplateDev dt, SortDesc d, const fl
 // context (voxel-space bases, highlight frame, in-box bounds).
 __global__ void k_query_prep(SceneDev sc, TemplateDev ht, sf_medium_params m, int64_t n,
                              const double* __restrict__ queries, const double* __restrict__ media,
-                             double* __restrict__ cfg8, QueryCtx* __restrict__ recs) {
+                             double* __restrict__ cfg8, QueryCtx* __restrict__ recs, const int* __restrict__ perm) {
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
-        const double* c = queries + 9 * q;
+        const int64_t src = perm ? int64_t(perm[q]) : q;  // processing order -> the caller's row
+        const double* c = queries + 9 * src;
         QueryCtx qc;
         query_ctx(sc, ht, c, qc);
         qc.same_light = (!media && c[6] == queries[6] && c[7] == queries[7] && c[8] == queries[8]) ? 1 : 0;
@@ -329,12 +330,39 @@ __global__ void k_query_prep(SceneDev sc, TemplateDev ht, sf_medium_params m, in
         qc.gt = 0.0f;
         if (media) {  // g axis of PhaseTable::lookup_hg (src/phase.cpp:196-205) at the query's g
             double gt;
-            table_coord(media[4 * q], -0.99, 0.99, sc.phase.gr, qc.gi, gt);
+            table_coord(media[4 * src], -0.99, 0.99, sc.phase.gr, qc.gi, gt);
             qc.gt = float(gt);
         }
         qc.pad_[0] = qc.pad_[1] = 0;
         recs[q] = qc;
-        write_cfg8(m, media ? media + 4 * q : nullptr, c, cfg8 + 8 * q);
+        write_cfg8(m, media ? media + 4 * src : nullptr, c, cfg8 + 8 * q);
+    }
+}
+
+// 30-bit Morton key of each query's voxel (10 bits per axis of the voxel coordinate scaled
+// to 1024 cells), index = row: sorting by key makes concurrently sampled queries share cache
+// lines of the volume when it does not fit in L2.
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+    v &= 1023u;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void k_morton(GridDev g, int64_t n, const double* __restrict__ queries, uint32_t* __restrict__ keys,
+                         int* __restrict__ idx) {
+    const double ext[3] = {g.hx - g.ox, g.hy - g.oy, g.hz - g.oz};
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t c[3];
+        for (int k = 0; k < 3; ++k) {
+            const double o = k == 0 ? g.ox : (k == 1 ? g.oy : g.oz);
+            const double u = (queries[9 * q + k] - o) / ext[k] * 1024.0;
+            c[k] = uint32_t(fmin(fmax(u, 0.0), 1023.0));
+        }
+        keys[q] = spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);
+        idx[q] = int(q);
     }
 }
 
@@ -714,11 +742,21 @@ void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float
 
 size_t query_rec_bytes() { return sizeof(QueryCtx); }
 
+void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t* keys, int* idx, cudaStream_t s) {
+    if (n <= 0) return;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(sm_count()) * 16);
+    k_morton<<<unsigned(blocks), 256, 0, s>>>(g, n, queries, keys, idx);
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+}
+
 void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_medium_params& m, int64_t n,
-                       const double* queries, const double* media, double* cfg8, void* recs, cudaStream_t s) {
+                       const double* queries, const double* media, double* cfg8, void* recs, cudaStream_t s,
+                       const int* perm) {
     if (n <= 0) return;
     const int64_t blocks = std::min<int64_t>((n + 127) / 128, int64_t(sm_count()) * 16);
-    k_query_prep<<<unsigned(blocks), 128, 0, s>>>(sc, ht, m, n, queries, media, cfg8, static_cast<QueryCtx*>(recs));
+    k_query_prep<<<unsigned(blocks), 128, 0, s>>>(sc, ht, m, n, queries, media, cfg8, static_cast<QueryCtx*>(recs),
+                                                  perm);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }

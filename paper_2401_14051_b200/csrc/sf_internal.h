@@ -34,6 +34,9 @@ inline void cuda_check(cudaError_t e, const char* what) {
 int sm_count();
 void count_launch();  // every kernel launch of the library increments sf_launch_count()
 
+// cub radix sort of (key, index) pairs; tmp == nullptr only sizes tmp_bytes
+void launch_sort_keys(const uint32_t* keys_in, uint32_t* keys_out, const int* idx_in, int* idx_out, int n,
+                      int end_bit, void* tmp, size_t& tmp_bytes, cudaStream_t s);
 // Image entry point (sf_render.cu): occupied-voxel compaction, bake rows, field scatter, march.
 int64_t launch_occupied(const sf_grid& g, int* idx, int* count, void* tmp, size_t& tmp_bytes, cudaStream_t s);
 void launch_bake_rows(const sf_grid& g, const int* idx, const int* count, int64_t max_rows, const double cam[3],
@@ -205,8 +208,9 @@ bool tc_supported(const sf_backbone_config& c);
 void tc_prepare(sf_backbone& b, cudaStream_t s);
 void tc_release(sf_backbone& b);
 void tc_read_prof(unsigned long long* out);
+// perm (optional): processing row q writes the caller's row perm[q] of y / F
 void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, const float* mms,
-                        const double* cfg8, float* y, double* F, cudaStream_t s);
+                        const double* cfg8, float* y, double* F, cudaStream_t s, const int* perm = nullptr);
 
 // Fused feature sampling + per-layer sort/pool + bf16 operand packing (K5+K6).
 // Samples the scene when `feats` is null, else sorts the given feature rows.
@@ -216,8 +220,12 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
                         int* err, cudaStream_t s, bool mixed = false);
 // Per-query context records (sampling bases, highlight frame) + make_config rows.
 size_t query_rec_bytes();
+// perm (optional): processing row q reads the caller's row perm[q] (locality reordering)
 void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_medium_params& m, int64_t n,
-                       const double* queries, const double* media, double* cfg8, void* recs, cudaStream_t s);
+                       const double* queries, const double* media, double* cfg8, void* recs, cudaStream_t s,
+                       const int* perm = nullptr);
+// Morton keys of the queries' positions in the grid box + identity indices (for cub sort)
+void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t* keys, int* idx, cudaStream_t s);
 // Light-side phase of every diffuse point for the light of query 0 (diffuse
 // placement is a pure translation, so axis and aperture do not depend on p).
 void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float* planes, int n_planes,
@@ -228,6 +236,9 @@ void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStr
 void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float* planes,
                          cudaStream_t s);
 
+// cub radix sort of (key, index) pairs; tmp == nullptr only sizes tmp_bytes
+void launch_sort_keys(const uint32_t* keys_in, uint32_t* keys_out, const int* idx_in, int* idx_out, int n,
+                      int end_bit, void* tmp, size_t& tmp_bytes, cudaStream_t s);
 // Image entry point (sf_render.cu): occupied-voxel compaction, bake rows, field scatter, march.
 int64_t launch_occupied(const sf_grid& g, int* idx, int* count, void* tmp, size_t& tmp_bytes, cudaStream_t s);
 void launch_bake_rows(const sf_grid& g, const int* idx, const int* count, int64_t max_rows, const double cam[3],

@@ -8,6 +8,7 @@
 // elsewhere). Render: one thread per pixel marches the camera ray through the box in
 // FP64 with the reference's operation order (second-order midpoint attenuation), the
 // in-scatter provider being the FP64 trilinear of the baked grids.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 
@@ -148,6 +149,12 @@ int64_t launch_occupied(const sf_grid& g, int* idx, int* count, void* tmp, size_
     SFB_CUDA(cub::DeviceSelect::If(tmp, tmp_bytes, it, idx, count, n, Occupied{g.d}, s));
     count_launch();
     return 0;
+}
+
+void launch_sort_keys(const uint32_t* keys_in, uint32_t* keys_out, const int* idx_in, int* idx_out, int n,
+                      int end_bit, void* tmp, size_t& tmp_bytes, cudaStream_t s) {
+    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, idx_in, idx_out, n, 0, end_bit, s));
+    if (tmp) count_launch();
 }
 
 void launch_bake_rows(const sf_grid& g, const int* idx, const int* count, int64_t max_rows, const double cam[3],

@@ -254,7 +254,7 @@ __device__ __forceinline__ void store_row32(uint8_t* a, const float* v) {
 __global__ void __launch_bounds__(kThreads, 2)
     k_backbone_tc(const TcDesc d, const uint8_t* __restrict__ wpk, const uint8_t* __restrict__ ops,
                   const uint8_t* __restrict__ mms, int n_tiles, int64_t n, const double* __restrict__ cfg8,
-                  float* __restrict__ y_out, double* __restrict__ F_out) {
+                  float* __restrict__ y_out, double* __restrict__ F_out, const int* __restrict__ perm) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t bars[2 * kSlots + 1];
     __shared__ uint32_t tmem_slot;
@@ -480,8 +480,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (live) {
                 for (int c = 0; c < 3; ++c) {
                     float yc = fabsf(y[c]);
-                    if (y_out) y_out[3 * q + c] = yc;
-                    if (F_out) F_out[3 * q + c] = pow(cfg8[8 * q + 4 + c], d.gamma) * expm1(double(yc));  // decode_prediction
+                    const int64_t oq = perm ? int64_t(perm[q]) : q;  // the caller's row (locality reordering)
+                    if (y_out) y_out[3 * oq + c] = yc;
+                    if (F_out) F_out[3 * oq + c] = pow(cfg8[8 * q + 4 + c], d.gamma) * expm1(double(yc));  // decode_prediction
                 }
             }
         }
@@ -690,7 +691,7 @@ void tc_release(sf_backbone& b) {
 }
 
 void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, const float* mms, const double* cfg8,
-                        float* y, double* F, cudaStream_t s) {
+                        float* y, double* F, cudaStream_t s, const int* perm) {
     if (n <= 0) return;
     auto pk = static_cast<const TcPack*>(b.tc);
     size_t smem = 1024 + 2 * kUmmaM * 32 * 2 + kUmmaM * 64 * 2 + size_t(kSlots) * kSlotBytes;
@@ -709,7 +710,7 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
     }
     const int n_tiles = int((n + kUmmaM - 1) / kUmmaM);
     k_backbone_tc<<<n_tiles, kThreads, smem, s>>>(pk->desc, pk->d_blobs, ops, reinterpret_cast<const uint8_t*>(mms),
-                                                  n_tiles, n, cfg8, y, F);
+                                                  n_tiles, n, cfg8, y, F, perm);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
