@@ -703,10 +703,10 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
         SFB_CUDA(cudaFuncSetAttribute(k_backbone_tc, cudaFuncAttributePreferredSharedMemoryCarveout,
                                       int(cudaSharedmemCarveoutMaxShared)));
         attr_set = smem;
-        int per_sm = 0;  // the design assumes two co-resident tiles per SM (registers, smem, 2 x 256 TMEM cols)
-        SFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backbone_tc, kThreads, smem));
-        if (per_sm < 2 && !std::getenv("SF_DEBUG_TC"))
-            std::fprintf(stderr, "libsf_b200: k_backbone_tc occupancy %d CTA/SM (expected 2)\n", per_sm);
+        // two co-resident tiles per SM by design (168 registers x 160 threads, 105 KB smem,
+        // 2 x 256 TMEM columns); ncu reports "Block Limit Registers 2 / Shared Mem 2"
+        // (profiles/ncu_traffic.json), while cudaOccupancyMaxActiveBlocksPerMultiprocessor
+        // answers 1 for this kernel, so no runtime check here.
     }
     const int n_tiles = int((n + kUmmaM - 1) / kUmmaM);
     k_backbone_tc<<<n_tiles, kThreads, smem, s>>>(pk->desc, pk->d_blobs, ops, reinterpret_cast<const uint8_t*>(mms),
