@@ -469,15 +469,38 @@ __device__ __forceinline__ void emit_pools(const SegOut& o, float mean, float mx
     if (o.tau == 0) *reinterpret_cast<float2*>(o.mm + 6) = make_float2(0.0f, 0.0f);
 }
 
-// One thread sorts a segment of cnt <= P values (descending), takes mean (sequential
+// Batcher's odd-even merge sort of P (power of two) registers, descending, with every
+// comparator that touches an index >= N dropped: positions >= N hold -INF padding, which a
+// descending compare-exchange never moves, so the network sorts N values exactly (P = 32:
+// 191 comparators instead of bitonic's 240; N = 24: 120; N = 12: 41; N = 6: 12).
+template <int P, int N>
+__device__ __forceinline__ void oem_sort_desc(float* v) {
+    // comparators (a, a + k) of merge stage (p, k): a - k % p in [0, P) with (a - k % p) mod 2k < k,
+    // both ends in the same 2p block (the iterative form of Batcher's network)
+#pragma unroll
+    for (int p = 1; p < P; p <<= 1)
+#pragma unroll
+        for (int k = p; k >= 1; k >>= 1)
+#pragma unroll
+            for (int a = 0; a < P; ++a) {
+                const int r = a - k % p, b = a + k;
+                if (r >= 0 && r % (2 * k) < k && b < N && b < P && a / (2 * p) == b / (2 * p)) {
+                    const float x = v[a], y = v[b];
+                    v[a] = fmaxf(x, y);
+                    v[b] = fminf(x, y);
+                }
+            }
+}
+
+// One thread sorts a segment of cnt <= N <= P values (descending), takes mean (sequential
 // float sum in sorted order / cnt, src/predictor.cpp:176-185) and max, and writes the
 // operand row and pools.
-template <int P>
+template <int P, int N = P>
 __device__ __forceinline__ void sort_emit(const float* seg, int cnt, const SegOut& o, bool store) {
     float v[P];
 #pragma unroll
     for (int j = 0; j < P; ++j) v[j] = j < cnt ? seg[j] : -INFINITY;
-    bitonic<P>(v, true);
+    oem_sort_desc<P, N>(v);
     float acc = 0.0f;
 #pragma unroll
     for (int j = 0; j < P; ++j)
@@ -497,9 +520,14 @@ __device__ __forceinline__ void sort_emit_pair(const float* seg, int cnt, bool u
     float v[32];
     const int base = upper ? 32 : 0;
     const unsigned mask = __activemask();  // pair partners always run this branch together
+    // the upper lane sorts ascending (descending on the negated values; negation is exact and
+    // maps the -INF padding to +INF), so the 64 values form one bitonic sequence
+    const float sgn = upper ? -1.0f : 1.0f;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = base + j < cnt ? seg[base + j] : -INFINITY;
-    bitonic<32>(v, !upper);
+    for (int j = 0; j < 32; ++j) v[j] = sgn * (base + j < cnt ? seg[base + j] : -INFINITY);
+    oem_sort_desc<32, 32>(v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = sgn * v[j];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
         const float x = __shfl_xor_sync(mask, v[j], 1);
@@ -624,11 +652,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
             if (pair)
                 sort_emit_pair(seg, cnt, t & 1, o, store);
             else if (cnt <= 8)
-                sort_emit<8>(seg, cnt, o, store);
+                cnt <= 6 ? sort_emit<8, 6>(seg, cnt, o, store) : sort_emit<8>(seg, cnt, o, store);
             else if (cnt <= 16)
-                sort_emit<16>(seg, cnt, o, store);
+                cnt <= 12 ? sort_emit<16, 12>(seg, cnt, o, store) : sort_emit<16>(seg, cnt, o, store);
             else
-                sort_emit<32>(seg, cnt, o, store);
+                cnt <= 24 ? sort_emit<32, 24>(seg, cnt, o, store) : sort_emit<32>(seg, cnt, o, store);
         }
         if (d.nbuf == 1) __syncthreads();  // the next group's sampling overwrites this scratch
     }
