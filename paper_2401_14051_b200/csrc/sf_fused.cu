@@ -516,18 +516,24 @@ __device__ __forceinline__ void sort_emit(const float* seg, int cnt, const SegOu
 // merge per lane; the lower lane's running sum continues on the upper lane, so the
 // sum is exactly sequential in sorted order. The lower lane emits chunks 0-3, the
 // upper the rest (mean and max land there) and the pools.
+template <int H>
 __device__ __forceinline__ void sort_emit_pair(const float* seg, int cnt, bool upper, const SegOut& o, bool store) {
+    // lane halves of H <= 32 values each (H = 24 for a 48-point layer: pruned 24-networks);
+    // -INF padding fills each lane's 32 slots
     float v[32];
-    const int base = upper ? 32 : 0;
+    const int base = upper ? H : 0, lim = upper ? cnt : (cnt < H ? cnt : H);
     const unsigned mask = __activemask();  // pair partners always run this branch together
-    // the upper lane sorts ascending (descending on the negated values; negation is exact and
-    // maps the -INF padding to +INF), so the 64 values form one bitonic sequence
-    const float sgn = upper ? -1.0f : 1.0f;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = sgn * (base + j < cnt ? seg[base + j] : -INFINITY);
-    oem_sort_desc<32, 32>(v);
+    for (int j = 0; j < 32; ++j) v[j] = (j < H && base + j < lim) ? seg[base + j] : -INFINITY;
+    oem_sort_desc<32, H>(v);
+    // the upper lane's half reversed to ascending: lower desc + upper asc is one bitonic
+    // sequence of 64 (the padding meets in the middle)
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = sgn * v[j];
+    for (int j = 0; j < 16; ++j) {
+        const float a = v[j], b = v[31 - j];
+        v[j] = upper ? b : a;
+        v[31 - j] = upper ? a : b;
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
         const float x = __shfl_xor_sync(mask, v[j], 1);
@@ -650,7 +656,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
             o.mm = mms + (int64_t(sg / 3) * q_pad + q0 + w) * 8;
             const float* seg = scr_all + w * d.scr_floats + s_scr[sg];
             if (pair)
-                sort_emit_pair(seg, cnt, t & 1, o, store);
+                cnt == 48 ? sort_emit_pair<24>(seg, cnt, t & 1, o, store)
+                          : sort_emit_pair<32>(seg, cnt, t & 1, o, store);
             else if (cnt <= 8)
                 cnt <= 6 ? sort_emit<8, 6>(seg, cnt, o, store) : sort_emit<8>(seg, cnt, o, store);
             else if (cnt <= 16)
