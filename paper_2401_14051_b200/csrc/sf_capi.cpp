@@ -11,6 +11,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -1004,13 +1005,44 @@ CopyStream& copy_stream() {
     return *c;
 }
 
-// Event recorded on `from` and waited on by `to` (created per use: a few per call).
-void stream_wait(cudaStream_t to, cudaStream_t from) {
-    cudaEvent_t e;
-    SFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+// Event recorded on `from` and waited on by `to`; `ev` a reusable event (a wait captures the
+// event's state when it is enqueued, so re-recording it later is safe).
+void stream_wait(cudaStream_t to, cudaStream_t from, cudaEvent_t ev = nullptr) {
+    cudaEvent_t e = ev;
+    if (!e) SFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     SFB_CUDA(cudaEventRecord(e, from));
     SFB_CUDA(cudaStreamWaitEvent(to, e, 0));
-    SFB_CUDA(cudaEventDestroy(e));  // released once the wait completes
+    if (!ev) SFB_CUDA(cudaEventDestroy(e));  // released once the wait completes
+}
+
+// Per-stream device workspace of the bf16 query path: one block carved into the call's
+// buffers and kept between calls (a query batch would otherwise pay ~10 stream-ordered
+// allocations, which dominate the fixed per-call cost). Reuse is safe because every use of a
+// stream's block is ordered on that stream (the copy stream's transfers are joined back into
+// it before the call returns); growing synchronises the stream first.
+struct Workspace {
+    uint8_t* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev[8] = {};
+    int next_ev = 0;
+};
+std::mutex g_ws_mu;
+std::unordered_map<cudaStream_t, Workspace>& workspaces() {
+    static auto* m = new std::unordered_map<cudaStream_t, Workspace>;
+    return *m;
+}
+
+extern "C++" {
+struct Carve {
+    uint8_t* base;
+    size_t off = 0;
+    template <typename T>
+    T* take(size_t count) {
+        T* r = count && base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += (count * sizeof(T) + 255) & ~size_t(255);
+        return r;
+    }
+};
 }
 
 // bf16 path over one chunk: fused sample+sort (or sort of given features) -> tcgen05 backbone.
@@ -1165,16 +1197,72 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             int64_t chunk_tiles = overlap ? (n_tiles + 1) / 2 : n_tiles;
             chunk_tiles = std::min<int64_t>(chunk_tiles, 1 << 12);  // operand blocks <= ~1.3 GB
             const int64_t chunk = chunk_tiles * sfb::kUmmaM;
-            Scratch<uint8_t> ops(size_t(chunk_tiles) * L.tile_bytes, stream);
-            Scratch<float> mms(size_t(L.n_layers) * chunk * 8, stream);
-            Scratch<double> cfg8(size_t(chunk) * 8, stream);
-            Scratch<uint8_t> recs(size_t(chunk) * sfb::query_rec_bytes(), stream);
-            Scratch<int> err(1, stream);
+            // the call's device buffers, carved from the stream's workspace
+            const bool hF = F_out && !is_device_ptr(F_out), hy = y_out && !is_device_ptr(y_out);
+            auto carve_all = [&](uint8_t* base, Carve& cv) {
+                cv = Carve{base};
+                struct {
+                    uint8_t *ops, *recs;
+                    float* mms;
+                    double *cfg8, *rows, *F;
+                    int *err, *perm;
+                    float* y;
+                    uint32_t* keys;
+                    int* idx;
+                } b{};
+                b.ops = cv.take<uint8_t>(size_t(chunk_tiles) * L.tile_bytes);
+                b.mms = cv.take<float>(size_t(L.n_layers) * chunk * 8);
+                b.cfg8 = cv.take<double>(size_t(chunk) * 8);
+                b.recs = cv.take<uint8_t>(size_t(chunk) * sfb::query_rec_bytes());
+                b.err = cv.take<int>(1);
+                b.rows = cv.take<double>(h_in ? size_t(n) * 9 : 0);
+                b.F = cv.take<double>(hF ? size_t(n) * 3 : 0);
+                b.y = cv.take<float>(hy ? size_t(n) * 3 : 0);
+                b.perm = cv.take<int>(reorder ? size_t(n) : 0);
+                b.keys = cv.take<uint32_t>(reorder ? size_t(n) * 2 : 0);
+                b.idx = cv.take<int>(reorder ? size_t(n) : 0);
+                return b;
+            };
+            Carve probe{nullptr};
+            carve_all(nullptr, probe);
+            size_t sort_tmp = 0;
+            if (reorder) sfb::launch_sort_keys(nullptr, nullptr, nullptr, nullptr, int(n), 30, nullptr, sort_tmp, stream);
+            const size_t need = probe.off + sort_tmp + 256;
+            std::unique_lock<std::mutex> wlk(g_ws_mu);
+            Workspace& ws = workspaces()[stream];
+            if (ws.cap < need) {
+                if (ws.p) {
+                    sync(stream);
+                    cudaFree(ws.p);
+                    ws.p = nullptr;
+                    ws.cap = 0;
+                }
+                SFB_CUDA(cudaMalloc(&ws.p, need));
+                ws.cap = need;
+                for (auto& e : ws.ev)
+                    if (!e) SFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+            Carve cv{nullptr};
+            auto bufs = carve_all(ws.p, cv);
+            uint8_t* sort_tmp_p = ws.p + cv.off;
+            auto next_event = [&]() {
+                cudaEvent_t e = ws.ev[ws.next_ev];
+                ws.next_ev = (ws.next_ev + 1) % 8;
+                return e;
+            };
+            struct {
+                uint8_t* p;
+            } ops{bufs.ops}, recs{bufs.recs};
+            struct {
+                float* p;
+            } mms{bufs.mms}, y_buf{bufs.y};
+            struct {
+                double* p;
+            } cfg8{bufs.cfg8}, rows_buf{bufs.rows}, F_buf{bufs.F};
+            struct {
+                int* p;
+            } err{bufs.err}, perm{bufs.perm};
             SFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
-            // device-side rows and outputs (the caller's when already on the device)
-            Scratch<double> rows_buf(h_in ? size_t(n) * 9 : 0, stream);
-            Scratch<double> F_buf(F_out && !is_device_ptr(F_out) ? size_t(n) * 3 : 0, stream);
-            Scratch<float> y_buf(y_out && !is_device_ptr(y_out) ? size_t(n) * 3 : 0, stream);
             const double* rows = h_in ? rows_buf.p : queries;
             double* Fd = F_out ? (F_buf.p ? F_buf.p : F_out) : nullptr;
             float* yd = y_out ? (y_buf.p ? y_buf.p : y_out) : nullptr;
@@ -1188,7 +1276,7 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             if (h_in || h_out) {
                 clk.lock();
                 cs = cps.cs;
-                stream_wait(cs, stream);  // the scratch allocations above are ordered on `stream`
+                stream_wait(cs, stream, next_event());  // earlier uses of the workspace are on `stream`
             }
             // every chunk's rows are queued at once, each followed by its own event
             std::vector<cudaEvent_t> rows_ready;
@@ -1208,16 +1296,12 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                     rows_ready.push_back(e);
                     SFB_CUDA(cudaEventRecord(e, cs));
                 }
-            Scratch<int> perm(reorder ? size_t(n) : 0, stream);
             if (reorder) {
                 for (cudaEvent_t e : rows_ready) SFB_CUDA(cudaStreamWaitEvent(stream, e, 0));  // every row
-                Scratch<uint32_t> keys(size_t(n) * 2, stream);
-                Scratch<int> idx(size_t(n), stream);
-                sfb::launch_morton(s->density->dev(), n, rows, keys.p, idx.p, stream);
-                size_t tmp_bytes = 0;
-                sfb::launch_sort_keys(keys.p, keys.p + n, idx.p, perm.p, int(n), 30, nullptr, tmp_bytes, stream);
-                Scratch<uint8_t> tmp(tmp_bytes, stream);
-                sfb::launch_sort_keys(keys.p, keys.p + n, idx.p, perm.p, int(n), 30, tmp.p, tmp_bytes, stream);
+                sfb::launch_morton(s->density->dev(), n, rows, bufs.keys, bufs.idx, stream);
+                size_t tmp_bytes = sort_tmp;
+                sfb::launch_sort_keys(bufs.keys, bufs.keys + n, bufs.idx, perm.p, int(n), 30, sort_tmp_p, tmp_bytes,
+                                      stream);
             }
             for (int64_t c0 = 0, k = 0; c0 < n; c0 += chunk, ++k) {
                 const int64_t m = std::min(chunk, n - c0);
@@ -1248,7 +1332,7 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                                                 Fd ? Fd + 3 * c0 : nullptr, stream);
                 }
                 if (h_out && !reorder) {  // this chunk's results home while the next chunk computes
-                    stream_wait(cs, stream);
+                    stream_wait(cs, stream, next_event());
                     if (F_buf.p)
                         SFB_CUDA(cudaMemcpyAsync(F_out + 3 * c0, F_buf.p + 3 * c0, size_t(m) * 3 * sizeof(double),
                                                  cudaMemcpyDeviceToHost, cs));
@@ -1258,13 +1342,13 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                 }
             }
             if (h_out && reorder) {  // scattered rows: one copy home after the last chunk
-                stream_wait(cs, stream);
+                stream_wait(cs, stream, next_event());
                 if (F_buf.p)
                     SFB_CUDA(cudaMemcpyAsync(F_out, F_buf.p, size_t(n) * 3 * sizeof(double), cudaMemcpyDeviceToHost, cs));
                 if (y_buf.p)
                     SFB_CUDA(cudaMemcpyAsync(y_out, y_buf.p, size_t(n) * 3 * sizeof(float), cudaMemcpyDeviceToHost, cs));
             }
-            if (cs != stream) stream_wait(stream, cs);  // scratch frees and the caller see the copies
+            if (cs != stream) stream_wait(stream, cs, next_event());  // the caller sees the copies
             if (!h_out && !h_in) return;  // device in/out: asynchronous (see below)
             int herr = 0;
             SFB_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
