@@ -1015,20 +1015,23 @@ void stream_wait(cudaStream_t to, cudaStream_t from, cudaEvent_t ev = nullptr) {
     if (!ev) SFB_CUDA(cudaEventDestroy(e));  // released once the wait completes
 }
 
-// Per-stream device workspace of the bf16 query path: one block carved into the call's
-// buffers and kept between calls (a query batch would otherwise pay ~10 stream-ordered
-// allocations, which dominate the fixed per-call cost). Reuse is safe because every use of a
-// stream's block is ordered on that stream (the copy stream's transfers are joined back into
-// it before the call returns); growing synchronises the stream first.
+// Per-device workspace of the bf16 query path: one block carved into the call's buffers and
+// kept between calls (instead of ~10 stream-ordered allocations per call). Calls on one device
+// are enqueued under a mutex; a call on a different stream than the previous user first waits
+// for the previous call's completion event, so the block is never used by two calls at once.
+// Growing synchronises the device.
 struct Workspace {
     uint8_t* p = nullptr;
     size_t cap = 0;
     cudaEvent_t ev[8] = {};
     int next_ev = 0;
+    cudaEvent_t done = nullptr;        // recorded at the end of the last call's work
+    cudaStream_t last = nullptr;
+    bool used = false;
 };
 std::mutex g_ws_mu;
-std::unordered_map<cudaStream_t, Workspace>& workspaces() {
-    static auto* m = new std::unordered_map<cudaStream_t, Workspace>;
+std::unordered_map<int, Workspace>& workspaces() {
+    static auto* m = new std::unordered_map<int, Workspace>;
     return *m;
 }
 
@@ -1229,19 +1232,32 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             if (reorder) sfb::launch_sort_keys(nullptr, nullptr, nullptr, nullptr, int(n), 30, nullptr, sort_tmp, stream);
             const size_t need = probe.off + sort_tmp + 256;
             std::unique_lock<std::mutex> wlk(g_ws_mu);
-            Workspace& ws = workspaces()[stream];
+            int dev = 0;
+            SFB_CUDA(cudaGetDevice(&dev));
+            Workspace& ws = workspaces()[dev];
+            if (!ws.done) {
+                SFB_CUDA(cudaEventCreateWithFlags(&ws.done, cudaEventDisableTiming));
+                for (auto& e : ws.ev) SFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
             if (ws.cap < need) {
                 if (ws.p) {
-                    sync(stream);
+                    SFB_CUDA(cudaDeviceSynchronize());
                     cudaFree(ws.p);
                     ws.p = nullptr;
                     ws.cap = 0;
                 }
                 SFB_CUDA(cudaMalloc(&ws.p, need));
                 ws.cap = need;
-                for (auto& e : ws.ev)
-                    if (!e) SFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            } else if (ws.used && ws.last != stream) {
+                SFB_CUDA(cudaStreamWaitEvent(stream, ws.done, 0));  // the previous call, other stream
             }
+            ws.used = true;
+            ws.last = stream;
+            struct DoneGuard {  // on every exit path: later calls order after this one
+                Workspace& w;
+                cudaStream_t s;
+                ~DoneGuard() { cudaEventRecord(w.done, s); }
+            } done_guard{ws, stream};
             Carve cv{nullptr};
             auto bufs = carve_all(ws.p, cv);
             uint8_t* sort_tmp_p = ws.p + cv.off;
