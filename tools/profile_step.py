@@ -25,6 +25,10 @@ scene = sf.Scene(g, tv, sf.load_template(os.path.join(data, "diffuse_seed7.vtmpl
 net = sf.make_backbone(sf.BackboneConfig(seed=0))
 med = sf.MediumParams((0.85,), (0.999,) * 3)
 prec = sf.BF16 if a.precision == "bf16" else sf.FP32
+import torch  # noqa: E402
+qd = torch.from_numpy(centers).cuda()  # device-resident rows, as bench.py's `value` leg
+Fd = torch.empty((len(centers), 3), dtype=torch.float64, device="cuda")
 for _ in range(a.steps):
-    F = sf.query(scene, net, med, centers, prec)
-print("ok", float(np.mean(F)))
+    sf.query(scene, net, med, qd, prec, F_out=Fd)
+torch.cuda.synchronize()
+print("ok", float(Fd.mean()))
