@@ -1539,6 +1539,7 @@ int sf_debug_tc_profile(uint64_t out[16]) {
 extern "C" void sf_backbone_destroy(sf_backbone* b) {
     if (!b) return;
     cudaFree(b->d_params);
+    if (b->d_paramsT) cudaFree(b->d_paramsT);
     sfb::tc_release(*b);
     delete b;
 }

@@ -111,6 +111,7 @@ struct sf_backbone {
     sf_backbone_config cfg{};
     BackboneLayout layout{};
     float* d_params = nullptr;  // canonical f32 params
+    float* d_paramsT = nullptr; // the same with every dense W [out][in] stored [in][out] (FP32 path, lazy)
     void* tc = nullptr;         // packed bf16 operands for the tensor-core path (lazy)
 };
 

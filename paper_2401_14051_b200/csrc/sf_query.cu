@@ -6,6 +6,9 @@
 // float2 level-0 volume ({rho, T} share the lattice, src/feature_pipeline.cpp:
 // 107-112 and :159-160), so each trilinear corner is a single 8-byte load; the
 // phase table (1 MiB at 64x128x32) stays L2-resident.
+#include <algorithm>
+#include <mutex>
+
 #include "sf_internal.h"
 
 namespace sfb {
@@ -365,6 +368,210 @@ __global__ void __launch_bounds__(128) k_backbone_fp32(NetDesc nd, const float* 
     }
 }
 
+// Exact FP32 backbone, warp-cooperative: a warp runs kQPW queries, lane j owns output
+// neurons j and j + 32 of every dense layer. Each neuron is still accumulated in the
+// reference's order (acc = b; acc += w * x over the inputs in order, src/neural.cpp:95-101,
+// no contraction), so the results are those of k_backbone_fp32; what changes is the
+// parallelism (32 lanes per query instead of one thread) and the weight traffic: weights
+// are read transposed ([in][out], one coalesced 128-byte row per input) once per warp for
+// kQPW queries. Widths <= 64.
+constexpr int kQPW = 4;
+constexpr int kXs = 200;  // per-query input buffer (fc1 <= 32 + 64 + 2, cross 3M <= 192)
+
+struct Acc2 {
+    float v[kQPW][2];
+};
+
+// acc[q][h] = b[j] + sum_k WT[k][j] * x[q][k] for j = lane + 32 h < m (exact order)
+__device__ __forceinline__ void dense_warp(const float* __restrict__ WT, const float* __restrict__ b, int m, int K,
+                                           const float (*x)[kXs], int lane, Acc2& acc) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        const float bj = j < m ? __ldg(b + j) : 0.0f;
+#pragma unroll
+        for (int q = 0; q < kQPW; ++q) acc.v[q][h] = bj;
+    }
+    for (int k = 0; k < K; ++k) {
+        const float w0 = lane < m ? __ldg(WT + int64_t(k) * m + lane) : 0.0f;
+        const float w1 = lane + 32 < m ? __ldg(WT + int64_t(k) * m + lane + 32) : 0.0f;
+#pragma unroll
+        for (int q = 0; q < kQPW; ++q) {
+            const float xk = x[q][k];
+            acc.v[q][0] += w0 * xk;
+            acc.v[q][1] += w1 * xk;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128) k_backbone_fp32w(NetDesc nd, const float* __restrict__ P,
+                                                        const float* __restrict__ PT, int64_t n,
+                                                        const float* __restrict__ slices,
+                                                        const double* __restrict__ cfg8, float* __restrict__ y_out,
+                                                        double* __restrict__ F_out) {
+    __shared__ float xs_all[4][2][kQPW][kXs];  // [warp][ping-pong][query][input]
+    __shared__ float keep_all[4][kQPW][3 * 64 + 2 * 64];  // merged (3M) then od | oh (2W)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float(*xa)[kXs] = xs_all[warp][0];
+    float(*xb)[kXs] = xs_all[warp][1];
+    float(*keep)[3 * 64 + 2 * 64] = keep_all[warp];
+    const int W = nd.W, M = nd.M, H = nd.H;
+    const int64_t n_warps = (n + kQPW - 1) / kQPW;
+    for (int64_t wi = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; wi < n_warps;
+         wi += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+        const int64_t q0 = wi * kQPW;
+        float cfgv[kQPW][7], g_mean[kQPW], alpha[kQPW];
+#pragma unroll
+        for (int q = 0; q < kQPW; ++q) {  // cfg_vector (src/predictor.cpp:193-202); padded rows repeat the last
+            const int64_t qq = q0 + q < n ? q0 + q : n - 1;
+            const double* c8 = cfg8 + 8 * qq;
+            const int ng = int(c8[0]);
+            g_mean[q] = 0.0f;
+            for (int i = 0; i < ng; ++i) g_mean[q] += float(c8[1 + i]);
+            if (ng > 0) g_mean[q] /= float(double(ng));
+            alpha[q] = float(c8[7]);
+            for (int i = 0; i < 3; ++i) cfgv[q][i] = i < ng ? float(c8[1 + i]) : 0.0f;
+            for (int i = 0; i < 4; ++i) cfgv[q][3 + i] = float(c8[4 + i]);
+        }
+        for (int t = 0; t < 3; ++t) {
+            for (int k = 0; k < 2; ++k) {
+                int64_t off = nd.stack_off[k][t];
+                // conditioning layer o = relu(W_init cfg + b) (run_stack, src/predictor.cpp:206-212)
+#pragma unroll
+                for (int q = 0; q < kQPW; ++q)
+                    if (lane < 7) xa[q][lane] = cfgv[q][lane];
+                __syncwarp();
+                Acc2 o;
+                dense_warp(PT + off, P + off + W * 7, W, 7, xa, lane, o);
+                off += W * 7 + W;
+#pragma unroll
+                for (int q = 0; q < kQPW; ++q) {
+                    o.v[q][0] = relu(o.v[q][0]);
+                    o.v[q][1] = relu(o.v[q][1]);
+                }
+                for (int i = 0; i < nd.nl[k]; ++i) {
+                    const int cnt = nd.counts[k][i];
+                    float wq[kQPW];
+#pragma unroll
+                    for (int q = 0; q < kQPW; ++q) {  // channel attention, redundantly per lane
+                        const int64_t qq = q0 + q < n ? q0 + q : n - 1;
+                        const float* sl = slices + int64_t(nd.slice_off[k][i]) * n + qq;
+                        float v[8];
+                        for (int c = 0; c < 3; ++c) {
+                            v[c] = sl[int64_t(c * (cnt + 2) + cnt) * n];
+                            v[3 + c] = sl[int64_t(c * (cnt + 2) + cnt + 1) * n];
+                        }
+                        v[6] = g_mean[q];
+                        v[7] = alpha[q];
+                        if (nd.literal) {
+                            float acc = 0.0f;
+                            for (int j = 0; j < 8; ++j) acc += (v[j] < 0.0f) ? 0.0f : v[j];
+                            wq[q] = sigmoid_ref(acc / 8.0f);
+                        } else {
+                            float hh[4], w3[3];
+                            dense_f32<4>(P + off, P + off + 32, 4, 8, v, hh);
+                            for (int j = 0; j < 4; ++j) hh[j] = relu(hh[j]);
+                            dense_f32<3>(P + off + 36, P + off + 48, 3, 4, hh, w3);
+                            wq[q] = sigmoid_ref(w3[t]);
+                        }
+                    }
+                    if (!nd.literal) off += 51;
+                    // fc1 input [o_att | sorted_tau, mean, max]
+                    Acc2 oa;
+                    __syncwarp();
+#pragma unroll
+                    for (int q = 0; q < kQPW; ++q) {
+                        const int64_t qq = q0 + q < n ? q0 + q : n - 1;
+                        oa.v[q][0] = o.v[q][0] * wq[q];
+                        oa.v[q][1] = o.v[q][1] * wq[q];
+                        if (lane < W) xa[q][lane] = oa.v[q][0];
+                        if (lane + 32 < W) xa[q][lane + 32] = oa.v[q][1];
+                        const float* st = slices + int64_t(nd.slice_off[k][i] + t * (cnt + 2)) * n + qq;
+                        for (int j = lane; j < cnt + 2; j += 32) xa[q][W + j] = st[int64_t(j) * n];
+                    }
+                    __syncwarp();
+                    const int K = W + cnt + 2;
+                    Acc2 u;
+                    dense_warp(PT + off, P + off + int64_t(W) * K, W, K, xa, lane, u);
+                    off += int64_t(W) * K + W;
+#pragma unroll
+                    for (int q = 0; q < kQPW; ++q) {
+                        if (lane < W) xb[q][lane] = relu(u.v[q][0]);
+                        if (lane + 32 < W) xb[q][lane + 32] = relu(u.v[q][1]);
+                    }
+                    __syncwarp();
+                    Acc2 t2;
+                    dense_warp(PT + off, P + off + W * W, W, W, xb, lane, t2);
+                    off += W * W + W;
+#pragma unroll
+                    for (int q = 0; q < kQPW; ++q) {
+                        o.v[q][0] = relu(t2.v[q][0]) + oa.v[q][0];
+                        o.v[q][1] = relu(t2.v[q][1]) + oa.v[q][1];
+                    }
+                }
+                // od (k = 0) / oh (k = 1) -> the merge input [od | oh]
+#pragma unroll
+                for (int q = 0; q < kQPW; ++q) {
+                    if (lane < W) keep[q][3 * 64 + k * W + lane] = o.v[q][0];
+                    if (lane + 32 < W) keep[q][3 * 64 + k * W + lane + 32] = o.v[q][1];
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < kQPW; ++q)
+                for (int j = lane; j < 2 * W; j += 32) xa[q][j] = keep[q][3 * 64 + j];
+            __syncwarp();
+            const int64_t mo = nd.merge_off + int64_t(t) * (int64_t(M) * 2 * W + M);
+            Acc2 mg;
+            dense_warp(PT + mo, P + mo + int64_t(M) * 2 * W, M, 2 * W, xa, lane, mg);
+#pragma unroll
+            for (int q = 0; q < kQPW; ++q) {
+                if (lane < M) keep[q][t * M + lane] = relu(mg.v[q][0]);
+                if (lane + 32 < M) keep[q][t * M + lane + 32] = relu(mg.v[q][1]);
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < kQPW; ++q)
+            for (int j = lane; j < 3 * M; j += 32) xa[q][j] = keep[q][j];
+        __syncwarp();
+        Acc2 h;
+        dense_warp(PT + nd.cross_off, P + nd.cross_off + int64_t(M) * 3 * M, M, 3 * M, xa, lane, h);
+#pragma unroll
+        for (int q = 0; q < kQPW; ++q) {
+            if (lane < M) xb[q][lane] = relu(h.v[q][0]);
+            if (lane + 32 < M) xb[q][lane + 32] = relu(h.v[q][1]);
+        }
+        __syncwarp();
+        dense_warp(PT + nd.head_off[0], P + nd.head_off[0] + int64_t(H) * M, H, M, xb, lane, h);
+#pragma unroll
+        for (int q = 0; q < kQPW; ++q) {
+            if (lane < H) xa[q][lane] = relu(h.v[q][0]);
+            if (lane + 32 < H) xa[q][lane + 32] = relu(h.v[q][1]);
+        }
+        __syncwarp();
+        dense_warp(PT + nd.head_off[1], P + nd.head_off[1] + int64_t(H) * H, H, H, xa, lane, h);
+#pragma unroll
+        for (int q = 0; q < kQPW; ++q) {
+            if (lane < H) xb[q][lane] = relu(h.v[q][0]);
+            if (lane + 32 < H) xb[q][lane + 32] = relu(h.v[q][1]);
+        }
+        __syncwarp();
+        dense_warp(PT + nd.head_off[2], P + nd.head_off[2] + 3 * H, 3, H, xb, lane, h);
+#pragma unroll
+        for (int q = 0; q < kQPW; ++q) {
+            const int64_t qq = q0 + q;
+            if (lane < 3 && qq < n) {
+                const float yc = fabsf(h.v[q][0]);
+                if (y_out) y_out[3 * qq + lane] = yc;
+                // decode_prediction (src/predictor.cpp:406-409)
+                if (F_out) F_out[3 * qq + lane] = pow(cfg8[8 * qq + 4 + lane], nd.gamma) * expm1(double(yc));
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // make_config (src/predictor.cpp:261-274): g params + albedo of the medium,
 // alpha = angle_between(omega, light) per query.
 __global__ void k_make_cfg8(sf_medium_params m, int64_t n, const double* __restrict__ queries,
@@ -479,6 +686,47 @@ void launch_slice(const sf_backbone_config& c, int64_t n, const float* feats, fl
     count_launch();
 }
 
+// d_paramsT: the canonical parameters with every dense W [out][in] of the backbone stored
+// transposed [in][out] at the same offset (biases and attention records unchanged), built
+// once per backbone on first FP32 use.
+static void prepare_transposed(sf_backbone& b, const NetDesc& nd, cudaStream_t s) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (b.d_paramsT) return;
+    std::vector<float> P(size_t(b.layout.total)), T;
+    SFB_CUDA(cudaMemcpyAsync(P.data(), b.d_params, P.size() * sizeof(float), cudaMemcpyDeviceToHost, s));
+    SFB_CUDA(cudaStreamSynchronize(s));
+    T = P;
+    auto tr = [&](int64_t off, int rows, int cols) {  // W [rows][cols] -> [cols][rows]
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < cols; ++c) T[size_t(off + int64_t(c) * rows + r)] = P[size_t(off + int64_t(r) * cols + c)];
+    };
+    const int W = nd.W, M = nd.M, H = nd.H;
+    for (int k = 0; k < 2; ++k)
+        for (int t = 0; t < 3; ++t) {  // walk_params order (src/predictor.cpp:62-109)
+            int64_t off = nd.stack_off[k][t];
+            tr(off, W, 7);
+            off += W * 7 + W;
+            for (int i = 0; i < nd.nl[k]; ++i) {
+                if (!nd.literal) off += 51;
+                const int K = W + nd.counts[k][i] + 2;
+                tr(off, W, K);
+                off += int64_t(W) * K + W;
+                tr(off, W, W);
+                off += W * W + W;
+            }
+        }
+    for (int t = 0; t < 3; ++t) tr(nd.merge_off + int64_t(t) * (int64_t(M) * 2 * W + M), M, 2 * W);
+    tr(nd.cross_off, M, 3 * M);
+    tr(nd.head_off[0], H, M);
+    tr(nd.head_off[1], H, H);
+    tr(nd.head_off[2], 3, H);
+    float* d = nullptr;
+    SFB_CUDA(cudaMalloc(&d, T.size() * sizeof(float)));
+    SFB_CUDA(cudaMemcpy(d, T.data(), T.size() * sizeof(float), cudaMemcpyHostToDevice));
+    b.d_paramsT = d;
+}
+
 void launch_backbone_fp32(const sf_backbone& b, int64_t n, const float* slices,
                           const double* cfg8, float* y, double* F, cudaStream_t s) {
     if (n <= 0) return;
@@ -504,7 +752,14 @@ void launch_backbone_fp32(const sf_backbone& b, int64_t n, const float* slices,
     nd.merge_off = b.layout.merge_off;
     nd.cross_off = b.layout.cross_off;
     for (int l = 0; l < 3; ++l) nd.head_off[l] = b.layout.head_off[l];
-    k_backbone_fp32<<<grid_for(size_t(n), 128), 128, 0, s>>>(nd, b.d_params, n, slices, cfg8, y, F);
+    if (c.width <= 64 && c.merge_width <= 64 && c.head_width <= 64) {  // warp-cooperative kernel
+        prepare_transposed(const_cast<sf_backbone&>(b), nd, s);
+        const int64_t warps = (n + kQPW - 1) / kQPW;
+        const int64_t blocks = std::min<int64_t>((warps + 3) / 4, int64_t(sm_count()) * 16);
+        k_backbone_fp32w<<<unsigned(blocks), 128, 0, s>>>(nd, b.d_params, b.d_paramsT, n, slices, cfg8, y, F);
+    } else {
+        k_backbone_fp32<<<grid_for(size_t(n), 128), 128, 0, s>>>(nd, b.d_params, n, slices, cfg8, y, F);
+    }
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
