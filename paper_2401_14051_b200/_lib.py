@@ -117,7 +117,7 @@ EXPORTS = tuple(_SIGS)
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} not found: build it with `python -m paper_2401_14051_b200.build` "
+            f"{LIB_PATH} not found: build it with `python paper_2401_14051_b200/build.py` "
             "(there is no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in _SIGS.items():
