@@ -1125,7 +1125,8 @@ int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_templa
         s->n_planes = model->kind == SF_PHASE_ISOTROPIC ? 1 : model->n_lobes;
         try {
             SFB_CUDA(cudaMalloc(&s->d_dt, density->count() * sizeof(float2)));
-            SFB_CUDA(cudaMalloc(&s->d_dt4, density->count() * sizeof(float4)));
+            SFB_CUDA(cudaMalloc(&s->d_dt4, sfb::xpair_records(density->nx, density->ny, density->nz) *
+                                                sizeof(float4)));
             SFB_CUDA(cudaMalloc(&s->d_planes, size_t(s->n_planes) * table->a * (table->h + 1) * sizeof(float2)));
             SFB_CUDA(cudaMalloc(&s->d_pre, std::max<size_t>(1, size_t(dt->total)) * 2 * sizeof(float4)));
             sfb::launch_interleave(density->d, tv.d, s->d_dt, density->count(), nullptr);
@@ -1193,7 +1194,8 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             // Morton order of p so concurrently sampled queries share the volume's cache lines;
             // results are written back to the caller's rows.
             static const int morton_env = std::getenv("SF_MORTON") ? std::atoi(std::getenv("SF_MORTON")) : -1;
-            const size_t vol_bytes = s->density->count() * sizeof(float4);
+            const size_t vol_bytes = sfb::xpair_records(s->density->nx, s->density->ny, s->density->nz) *
+                                     sizeof(float4);
             const bool reorder = morton_env >= 0 ? morton_env > 0 && n > 1
                                                  : (vol_bytes > (size_t(96) << 20) && n >= 4096);
             const bool overlap = overlap_on && !reorder && (h_in || h_out) && n_tiles >= 64;

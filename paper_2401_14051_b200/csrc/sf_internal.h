@@ -232,6 +232,7 @@ void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t*
 void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float* planes, int n_planes,
                           const double* queries, float4* pre, cudaStream_t s);
 void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStream_t s);
+size_t xpair_records(int nx, int ny, int nz);  // records of the mini-brick x-pair layout (padded dims)
 // Pre-blended phase planes: for each lobe, the table interpolated at that lobe's g
 // (PhaseTable::lookup_hg's g axis, src/phase.cpp:191-219), [n_lobes][angle][aperture].
 void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float* planes,
