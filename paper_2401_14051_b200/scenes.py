@@ -276,6 +276,17 @@ def mixed_medium(dims, seed, chunk=16):
     return dens, alb, gg
 
 
+def mixed_medium_large(dims, seed, base=128):
+    """C4 at 512^3: mixed_medium generated at `base`^3 (the noise's finest octave spans 16
+    voxels at 512^3, so nothing is lost) and trilinearly upsampled to dims^3, float32."""
+    if dims <= base:
+        return mixed_medium(dims, seed)
+    from scipy.ndimage import zoom
+    f = dims / base
+    return tuple(np.clip(zoom(a, f, order=1, mode="nearest", grid_mode=True), lo, hi).astype(np.float32)
+                 for a, (lo, hi) in zip(mixed_medium(base, seed), ((0.0, 1.0), (0.9, 0.999), (0.3, 0.9))))
+
+
 def sample_media(albedo, g, centers, voxel_size=None, origin=(-1.0, -1.0, -1.0)):
     """Per-query medium rows [n, 4] = (g, albedo rgb) for C4: FP64 trilinear of the per-voxel
     g / albedo grids at each query's p (DensityGrid::sample_trilinear semantics, clamp-to-edge

@@ -27,6 +27,8 @@ from paper_2401_14051_b200._lib import profile_read  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--frames", type=int, default=8)
 ap.add_argument("--grid", type=int, default=256)
+ap.add_argument("--c4", action="store_true", help="also run C4 (512^3 per-voxel albedo/g, 1920x1080 queries)")
+ap.add_argument("--only-c4", action="store_true")
 a = ap.parse_args()
 N = a.grid
 data = os.path.join(os.path.dirname(sf.__file__), "data")
@@ -50,6 +52,39 @@ def stage_split():
     st = profile_read()
     return {k: round(v[0], 3) for k, v in st.items() if v[1]}
 
+
+def run_c4():
+    # C4: 512^3 mixed medium, per-voxel albedo in [0.9, 0.999] and HG g in [0.3, 0.9] sampled at p
+    # (scenes.sample_media), 1920x1080 = 2,073,600 queries, one light; frame = tvol build + query
+    n4 = 512
+    t0 = time.perf_counter()
+    dens, alb, gg = scenes.mixed_medium_large(n4, 4)
+    t_gen = time.perf_counter() - t0
+    g4 = sf.DensityGrid.from_array(dens, 2.0 / n4, (-1.0, -1.0, -1.0))
+    nq4 = 1920 * 1080
+    rows4 = scenes.draw_centers(dens, nq4, 31, scenes.LIGHT)
+    media = torch.from_numpy(scenes.sample_media(alb, gg, rows4)).cuda()
+    rows4 = torch.from_numpy(rows4).cuda()
+    F4 = torch.empty((nq4, 3), dtype=torch.float64, device="cuda")
+    pyr4 = sf.DensityPyramid(g4, stream=stream)
+    res = []
+    for it in range(3):
+        tv4, t_tv = timed(lambda: sf.build_transmittance_volume(pyr4, scenes.LIGHT, stream=stream))
+        sc4 = sf.Scene(g4, tv4, dt, ht, sf.PhaseModel.hg(0.6), table)
+        _, t_q = timed(lambda: sf.query_media(sc4, net, rows4, media, sf.BF16, F_out=F4, stream=stream))
+        if it > 0:
+            res.append((t_tv, t_q))
+    tv_ms = float(np.mean([x[0] for x in res]))
+    q_ms = float(np.mean([x[1] for x in res]))
+    print(json.dumps({"config": "C4", "grid": n4, "queries_per_frame": nq4, "frame_ms": tv_ms + q_ms,
+                      "transmittance_ms": tv_ms, "query_ms": q_ms, "query_only_qps": nq4 / (q_ms * 1e-3),
+                      "per_query_media": "g, albedo sampled at p (trilinear of the per-voxel grids)",
+                      "scene_gen_s_host": round(t_gen, 1), "gpus": 1}))
+
+
+if a.only_c4:
+    run_c4()
+    sys.exit(0)
 
 # ---------------- C5
 vol = scenes.noise_volume(N, 5)
@@ -113,3 +148,6 @@ print(json.dumps({"config": "C3", "grid": N, "lights": len(lights), "queries_per
                   "frame_ms": tot_tv + tot_q, "transmittance_ms_per_light": tot_tv / len(lights),
                   "query_ms_per_light": tot_q / len(lights),
                   "sustained_qps": len(lights) * nq / ((tot_tv + tot_q) * 1e-3), "gpus": 1}))
+
+if a.c4:
+    run_c4()
