@@ -132,13 +132,20 @@ int sf_combine_transmittance(const sf_grid* const* fields, int n, const float* k
 int sf_build_transmittance_volume(const sf_pyramid* p, const double light[3],
                                   const float* kernels, const float* scales, double lambda,
                                   double step_scale, sf_tvol** out, sf_stream stream);
+/* Build flags. SF_BUILD_FP32_MARCH: the graded-transmittance march in FP32 (ray setup still
+ * FP64, compensated sum) — the production build feeding the bf16 query path: ~1e-6 relative
+ * optical depth against the FP64 reference march, 2-3x faster. 0 = the reference's FP64. */
+enum { SF_BUILD_FP32_MARCH = 1 };
+int sf_build_transmittance_volume_ex(const sf_pyramid* p, const double light[3],
+                                     const float* kernels, const float* scales, double lambda,
+                                     double step_scale, int flags, sf_tvol** out, sf_stream stream);
 /* Rows z in [z0, z1) of build_transmittance_volume's level-0 values, bit-identical to the
  * same rows of the full build: the per-light build sharded by z-slab over GPUs (SURVEY.md
  * §8e). Level 0 is marched only for the slab plus a 2-row halo, coarser levels whole.
  * out h/d [(z1-z0)][ny][nx]; gather the slabs and wrap them with sf_tvol_from_values. */
 int sf_build_transmittance_slab(const sf_pyramid* p, const double light[3], const float* kernels,
-                                const float* scales, double lambda, double step_scale, int z0, int z1,
-                                float* out, sf_stream stream);
+                                const float* scales, double lambda, double step_scale, int flags, int z0,
+                                int z1, float* out, sf_stream stream);
 /* TransmittanceFeatureVolume{light_dir, values} from explicit values (the struct's
  * public members, feature_pipeline.h:38-41); values h/d [nz][ny][nx]. */
 int sf_tvol_from_values(int nx, int ny, int nz, double voxel_size, const double origin[3],

@@ -393,7 +393,7 @@ inline std::vector<float> build_transmittance_slab(const DensityPyramid& p, cons
     std::vector<float> k, s(w.scales), out(size_t(nx) * ny * size_t(z1 > z0 ? z1 - z0 : 0));
     for (const auto& kk : w.kernels) k.insert(k.end(), kk.begin(), kk.end());
     double l[3] = {light.x, light.y, light.z};
-    check(sf_build_transmittance_slab(p.handle(), l, k.data(), s.data(), cfg.lambda, cfg.step_scale, z0, z1,
+    check(sf_build_transmittance_slab(p.handle(), l, k.data(), s.data(), cfg.lambda, cfg.step_scale, 0, z0, z1,
                                       out.data(), nullptr));
     return out;
 }

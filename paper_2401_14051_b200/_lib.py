@@ -68,7 +68,8 @@ _SIGS = {
     "sf_conv3_replicate": (I, [P, P, PP, P]),
     "sf_combine_transmittance": (I, [P, I, P, P, P, PP, P]),
     "sf_build_transmittance_volume": (I, [P, P, P, P, D, D, PP, P]),
-    "sf_build_transmittance_slab": (I, [P, P, P, P, D, D, I, I, P, P]),
+    "sf_build_transmittance_slab": (I, [P, P, P, P, D, D, I, I, I, P, P]),
+    "sf_build_transmittance_volume_ex": (I, [P, P, P, P, D, D, I, PP, P]),
     "sf_tvol_from_values": (I, [I, I, I, D, P, P, P, PP]),
     "sf_tvol_values": (P, [P]),
     "sf_tvol_destroy": (None, [P]),

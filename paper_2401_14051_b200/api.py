@@ -245,9 +245,13 @@ def combine_transmittance(fields, weights: CombinerWeights, stream=None):
     return TransmittanceFeatureVolume(h, l0, weights)
 
 
+BUILD_FP32_MARCH = 1
+
+
 def build_transmittance_volume(pyramid: DensityPyramid, light, weights: CombinerWeights = None,
-                               cfg: FeatureConfig = None, stream=None):
-    """build_transmittance_volume (src/feature_pipeline.cpp:200-211)."""
+                               cfg: FeatureConfig = None, stream=None, fast: bool = False):
+    """build_transmittance_volume (src/feature_pipeline.cpp:200-211). fast=True marches in FP32
+    (the production build for the bf16 query path, ~1e-6 relative optical depth)."""
     cfg = cfg or FeatureConfig()
     weights = weights or CombinerWeights.identity(pyramid.level_count())
     if weights.level_count() != pyramid.level_count():
@@ -255,13 +259,14 @@ def build_transmittance_volume(pyramid: DensityPyramid, light, weights: Combiner
     k = np.ascontiguousarray(weights.kernels, np.float32)
     s = np.ascontiguousarray(weights.scales, np.float32)
     h = C.c_void_p()
-    check(lib.sf_build_transmittance_volume(pyramid._h, dvec(light), ptr(k), ptr(s), float(cfg.lambda_),
-                                            float(cfg.step_scale), C.byref(h), stream_ptr(stream)))
+    check(lib.sf_build_transmittance_volume_ex(pyramid._h, dvec(light), ptr(k), ptr(s), float(cfg.lambda_),
+                                               float(cfg.step_scale), BUILD_FP32_MARCH if fast else 0, C.byref(h),
+                                               stream_ptr(stream)))
     return TransmittanceFeatureVolume(h, _normalize(light), weights)
 
 
 def build_transmittance_slab(pyramid: DensityPyramid, light, z0: int, z1: int, weights: CombinerWeights = None,
-                             cfg: FeatureConfig = None, out=None, stream=None):
+                             cfg: FeatureConfig = None, out=None, stream=None, fast: bool = False):
     """Level-0 rows [z0, z1) of build_transmittance_volume, bit-identical to the full build's
     rows (the per-light build sharded by z-slab). `out`: a CUDA tensor
     [(z1-z0), ny, nx] float32 to fill in place (stays on the device), else returns numpy."""
@@ -275,7 +280,8 @@ def build_transmittance_slab(pyramid: DensityPyramid, light, z0: int, z1: int, w
     nx, ny, _ = g0.dims
     dst = out if out is not None else np.empty((max(z1 - z0, 0), ny, nx), np.float32)
     check(lib.sf_build_transmittance_slab(pyramid._h, dvec(light), ptr(k), ptr(s), float(cfg.lambda_),
-                                          float(cfg.step_scale), int(z0), int(z1), ptr(dst), stream_ptr(stream)))
+                                          float(cfg.step_scale), BUILD_FP32_MARCH if fast else 0, int(z0), int(z1),
+                                          ptr(dst), stream_ptr(stream)))
     return dst
 
 

@@ -546,7 +546,8 @@ void normalize3(const double l[3], double o[3]) {
 }
 
 sf_grid* graded_level(const sf_pyramid* p, int level, const double light[3], double lambda,
-                      double step, cudaStream_t s, bool scratch = false, int zlo = 0, int zhi = -1) {
+                      double step, cudaStream_t s, bool scratch = false, int zlo = 0, int zhi = -1,
+                      bool fast = false) {
     if (level < 0 || level >= int(p->levels.size()))
         fail(SF_ERR_INVALID_ARGUMENT, "graded_transmittance: invalid level");
     if (!(lambda > 0.0 && lambda < 1.0))
@@ -560,7 +561,7 @@ sf_grid* graded_level(const sf_pyramid* p, int level, const double light[3], dou
     sf_grid* out = scratch ? new_scratch_grid(rho->nx, rho->ny, rho->nz, rho->vs, rho->origin, s)
                            : new_grid(rho->nx, rho->ny, rho->nz, rho->vs, rho->origin);
     try {
-        sfb::launch_graded(*rho, ts, coeff, step, zlo, zhi < 0 ? rho->nz : zhi, out->d, s);
+        sfb::launch_graded(*rho, ts, coeff, step, zlo, zhi < 0 ? rho->nz : zhi, out->d, s, fast);
     } catch (...) {
         free_grid(out);
         throw;
@@ -664,15 +665,16 @@ int sf_combine_transmittance(const sf_grid* const* fields, int n, const float* k
     });
 }
 
-int sf_build_transmittance_volume(const sf_pyramid* p, const double light[3], const float* kernels,
-                                  const float* scales, double lambda, double step_scale,
-                                  sf_tvol** out, sf_stream stream) {
+int sf_build_transmittance_volume_ex(const sf_pyramid* p, const double light[3], const float* kernels,
+                                     const float* scales, double lambda, double step_scale, int flags,
+                                     sf_tvol** out, sf_stream stream) {
     return guard([&] {
+        const bool fast = (flags & SF_BUILD_FP32_MARCH) != 0;
         std::vector<sf_grid*> fields;
         try {
             for (int i = 0; i < int(p->levels.size()); ++i) {
                 double step = step_scale * p->levels[size_t(i)]->vs;
-                fields.push_back(graded_level(p, i, light, lambda, step, stream, true));
+                fields.push_back(graded_level(p, i, light, lambda, step, stream, true, 0, -1, fast));
             }
             std::vector<const sf_grid*> f(fields.begin(), fields.end());
             *out = combine(f, kernels, scales, light, stream);
@@ -684,10 +686,17 @@ int sf_build_transmittance_volume(const sf_pyramid* p, const double light[3], co
     });
 }
 
+int sf_build_transmittance_volume(const sf_pyramid* p, const double light[3], const float* kernels,
+                                  const float* scales, double lambda, double step_scale,
+                                  sf_tvol** out, sf_stream stream) {
+    return sf_build_transmittance_volume_ex(p, light, kernels, scales, lambda, step_scale, 0, out, stream);
+}
+
 int sf_build_transmittance_slab(const sf_pyramid* p, const double light[3], const float* kernels,
-                                const float* scales, double lambda, double step_scale, int z0, int z1,
+                                const float* scales, double lambda, double step_scale, int flags, int z0, int z1,
                                 float* out, sf_stream stream) {
     return guard([&] {
+        const bool fast = (flags & SF_BUILD_FP32_MARCH) != 0;
         const sf_grid& g0 = *p->levels[0];
         if (z0 < 0 || z1 > g0.nz || z0 > z1) fail(SF_ERR_INVALID_ARGUMENT, "transmittance slab: z range outside the grid");
         Out<float> o(out, size_t(g0.nx) * g0.ny * size_t(z1 - z0), stream);
@@ -701,7 +710,8 @@ int sf_build_transmittance_slab(const sf_pyramid* p, const double light[3], cons
             const int m0 = std::max(z0 - 2, 0), m1 = std::min(z1 + 2, g0.nz);
             for (int i = 0; i < int(p->levels.size()); ++i) {
                 const double step = step_scale * p->levels[size_t(i)]->vs;
-                fields.push_back(graded_level(p, i, light, lambda, step, stream, true, i == 0 ? m0 : 0, i == 0 ? m1 : -1));
+                fields.push_back(
+                    graded_level(p, i, light, lambda, step, stream, true, i == 0 ? m0 : 0, i == 0 ? m1 : -1, fast));
             }
             std::vector<float> K, S;
             combiner_weights(int(fields.size()), kernels, scales, K, S);

@@ -136,8 +136,9 @@ namespace sfb {
 void launch_pyramid_down(const sf_grid& src, sf_grid& dst, cudaStream_t s);
 // Per-light build kernels over voxel rows z in [zlo, zhi) (the whole grid, or a z-slab of a
 // build sharded over GPUs). launch_combine writes rows [zlo, zhi) to out[0...].
+// fast: FP32 march (production bf16 path; ~1e-6 relative optical depth) instead of the FP64 reference march
 void launch_graded(const sf_grid& level, const double to_source[3], double coeff, double step, int zlo, int zhi,
-                   float* out, cudaStream_t s);
+                   float* out, cudaStream_t s, bool fast = false);
 void launch_conv3(const sf_grid& in, const float k27[27], int zlo, int zhi, float* out, cudaStream_t s);
 void launch_combine(const std::vector<const sf_grid*>& conv, const std::vector<float>& scales,
                     const sf_grid& base, int zlo, int zhi, float* out, cudaStream_t s);

@@ -107,7 +107,7 @@ def gather_slabs(local, nz: int, rank: int, world: int, group=None):
     return torch.cat([parts[r][: z1 - z0] for r, (z0, z1) in enumerate(slabs)], dim=0)
 
 
-def build_tvol_sharded(pyramid, light, rank: int, world: int, weights=None, cfg=None, group=None):
+def build_tvol_sharded(pyramid, light, rank: int, world: int, weights=None, cfg=None, group=None, fast=False):
     """build_transmittance_volume with the level-0 work split by z-slab over the ranks of `group`;
     returns the TransmittanceFeatureVolume (identical on every rank)."""
     import torch
@@ -118,6 +118,6 @@ def build_tvol_sharded(pyramid, light, rank: int, world: int, weights=None, cfg=
     nx, ny, nz = g0.dims
     z0, z1 = z_slabs(nz, world)[rank]
     local = torch.empty((z1 - z0, ny, nx), dtype=torch.float32, device="cuda")
-    api.build_transmittance_slab(pyramid, light, z0, z1, weights, cfg, out=local)
+    api.build_transmittance_slab(pyramid, light, z0, z1, weights, cfg, out=local, fast=fast)
     full = gather_slabs(local, nz, rank, world, group)
     return api.TransmittanceFeatureVolume.from_values(full.contiguous(), g0.voxel_size(), g0.origin(), light, weights)

@@ -437,3 +437,44 @@ def test_bf16_query_c2_vs_fp32(tmpl):
     _stats("bf16_vs_fp32_c2", max_dy=dy.max(), median_dy=np.median(dy), max_F_rel=fr.max(),
            p99_F_rel=np.quantile(fr, 0.99))
     assert dy.max() <= BF16_Y_ABS and np.all(_f_ok(F16, F32, np.full((1, 3), 0.999)))
+
+
+# ---- production (FP32-march) transmittance build ---------------------------------------
+@pytest.mark.parametrize("n,seed", [(64, 0), (128, 1)])
+def test_fast_build_close_to_reference_march(n, seed):
+    """SF_BUILD_FP32_MARCH (the build feeding the bf16 query path) against the FP64 reference
+    march: |dT| <= 2e-5 on every voxel (identity and random combiner), and its z-slabs are
+    bit-identical to its own full build."""
+    from paper_2401_14051_b200 import scenes, sharding
+    vol = scenes.procedural_cloud(n, seed) if n == 64 else scenes.fractal_ellipsoid(n, seed)
+    pyr = sf.DensityPyramid(sf.DensityGrid.from_array(vol, 2.0 / n, ORIGIN))
+    rng = np.random.default_rng(3)
+    L = pyr.level_count()
+    k = rng.uniform(-0.2, 0.2, (L, 27)).astype(np.float32)
+    k[:, 13] += 1
+    for w in (None, sf.CombinerWeights(k, np.full(L, 1.0 / L, np.float32))):
+        exact = sf.build_transmittance_volume(pyr, LIGHT, w).values.values()
+        fast = sf.build_transmittance_volume(pyr, LIGHT, w, fast=True).values.values()
+        assert np.abs(fast - exact).max() <= 2e-5, np.abs(fast - exact).max()
+    parts = [sf.build_transmittance_slab(pyr, LIGHT, z0, z1, w, fast=True) for z0, z1 in sharding.z_slabs(n, 3)]
+    assert np.array_equal(np.concatenate(parts), fast)  # w, fast: the random-combiner pass
+
+
+def test_bf16_query_on_fast_build(tmpl):
+    """The production pair (FP32-march build + bf16 query) against the exact pair at C2."""
+    from paper_2401_14051_b200 import scenes
+    vol = scenes.fractal_ellipsoid(128, 1)
+    g = sf.DensityGrid.from_array(vol, 2.0 / 128, ORIGIN)
+    pyr = sf.DensityPyramid(g)
+    d, h = tmpl
+    table = sf.PhaseTable(64, 128, 32, 16)
+    exact = sf.Scene(g, sf.build_transmittance_volume(pyr, LIGHT), d, h, sf.PhaseModel.hg(0.85), table)
+    prod = sf.Scene(g, sf.build_transmittance_volume(pyr, LIGHT, fast=True), d, h, sf.PhaseModel.hg(0.85), table)
+    rows = scenes.draw_centers(vol, 4096, 11, scenes.LIGHT)
+    net = _net(0)
+    med = sf.MediumParams((0.85,), (0.999,) * 3)
+    y32 = np.empty((len(rows), 3), np.float32)
+    y16 = np.empty((len(rows), 3), np.float32)
+    F32 = sf.query(exact, net, med, rows, sf.FP32, y_out=y32)
+    F16 = sf.query(prod, net, med, rows, sf.BF16, y_out=y16)
+    assert np.abs(y16 - y32).max() <= BF16_Y_ABS and np.all(_f_ok(F16, F32, np.full((1, 3), 0.999)))

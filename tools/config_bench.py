@@ -29,7 +29,9 @@ ap.add_argument("--frames", type=int, default=8)
 ap.add_argument("--grid", type=int, default=256)
 ap.add_argument("--c4", action="store_true", help="also run C4 (512^3 per-voxel albedo/g, 1920x1080 queries)")
 ap.add_argument("--only-c4", action="store_true")
+ap.add_argument("--exact-build", action="store_true", help="FP64 reference march for the tvol (default: FP32 march)")
 a = ap.parse_args()
+FAST = not a.exact_build
 N = a.grid
 data = os.path.join(os.path.dirname(sf.__file__), "data")
 dt = sf.load_template(os.path.join(data, "diffuse_seed7.vtmpl"))
@@ -69,7 +71,7 @@ def run_c4():
     pyr4 = sf.DensityPyramid(g4, stream=stream)
     res = []
     for it in range(3):
-        tv4, t_tv = timed(lambda: sf.build_transmittance_volume(pyr4, scenes.LIGHT, stream=stream))
+        tv4, t_tv = timed(lambda: sf.build_transmittance_volume(pyr4, scenes.LIGHT, stream=stream, fast=FAST))
         sc4 = sf.Scene(g4, tv4, dt, ht, sf.PhaseModel.hg(0.6), table)
         _, t_q = timed(lambda: sf.query_media(sc4, net, rows4, media, sf.BF16, F_out=F4, stream=stream))
         if it > 0:
@@ -79,7 +81,8 @@ def run_c4():
     print(json.dumps({"config": "C4", "grid": n4, "queries_per_frame": nq4, "frame_ms": tv_ms + q_ms,
                       "transmittance_ms": tv_ms, "query_ms": q_ms, "query_only_qps": nq4 / (q_ms * 1e-3),
                       "per_query_media": "g, albedo sampled at p (trilinear of the per-voxel grids)",
-                      "scene_gen_s_host": round(t_gen, 1), "gpus": 1}))
+                      "scene_gen_s_host": round(t_gen, 1), "build": "fp64 march" if not FAST else "fp32 march",
+                      "gpus": 1}))
 
 
 if a.only_c4:
@@ -101,7 +104,7 @@ sf.lib.sf_profile_enable(1)
 profile_read()
 for f in range(a.frames + 1):
     light = scenes.rotating_light(f, 32)
-    tv, t_tv = timed(lambda: sf.build_transmittance_volume(pyr, light, stream=stream))
+    tv, t_tv = timed(lambda: sf.build_transmittance_volume(pyr, light, stream=stream, fast=FAST))
     sc = sf.Scene(g, tv, dt, ht, model, table)
     r = rows.clone()
     r[:, 6:] = torch.tensor(np.asarray(light) / np.linalg.norm(light), device="cuda")
@@ -119,7 +122,7 @@ print(json.dumps({"config": "C5", "grid": N, "queries_per_frame": nq, "frames": 
                   "sustained_qps": nq / (frame_ms * 1e-3), "frame_ms": frame_ms, "transmittance_ms": tv_ms,
                   "query_ms": q_ms, "query_only_qps": nq / (q_ms * 1e-3), "pyramid_ms_once": t_pyr,
                   "query_stage_ms_per_frame": {k: v / a.frames for k, v in stages.items()},
-                  "dtype": "bf16 network, fp32/fp64 build", "gpus": 1}))
+                  "dtype": "bf16 network", "build": "fp64 march" if not FAST else "fp32 march", "gpus": 1}))
 
 # ---------------- C3
 vol = scenes.smoke_plume(N, 3)
@@ -135,7 +138,7 @@ for it in range(2):  # warm, then timed
     tot_tv = tot_q = 0.0
     total = torch.zeros((nq, 3), dtype=torch.float64, device="cuda")
     for light, I in zip(lights, inten):
-        tv, t_tv = timed(lambda: sf.build_transmittance_volume(pyr, light, stream=stream))
+        tv, t_tv = timed(lambda: sf.build_transmittance_volume(pyr, light, stream=stream, fast=FAST))
         sc = sf.Scene(g, tv, dt, ht, model, table)
         r = torch.from_numpy(configs.with_light(rows, light)).cuda()
         Fl = torch.empty((nq, 3), dtype=torch.float64, device="cuda")
