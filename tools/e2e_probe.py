@@ -1,4 +1,5 @@
-"""Time sf.query with pinned host rows in / host F out (the bench e2e leg), plain and chunked."""
+"""Time sf.query with pinned host rows in / host F out (the bench e2e leg) against device
+buffers, one side at a time (where does the end-to-end gap come from?)."""
 import os, sys, json
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
@@ -16,7 +17,7 @@ q = torch.from_numpy(c).pin_memory().numpy()
 F = torch.empty((65536, 3), dtype=torch.float64).pin_memory().numpy()
 qd = torch.from_numpy(c).cuda(); Fd = torch.empty((65536, 3), dtype=torch.float64, device="cuda")
 out = {}
-for name, (qi, fo) in {"host": (q, F), "device": (qd, Fd)}.items():
+for name, (qi, fo) in {"host": (q, F), "host_in": (q, Fd), "host_out": (qd, F), "device": (qd, Fd)}.items():
     for _ in range(3): sf.query(sc, net, med, qi, sf.BF16, F_out=fo, stream=stream)
     torch.cuda.synchronize()
     reps = []
@@ -26,5 +27,5 @@ for name, (qi, fo) in {"host": (q, F), "device": (qd, Fd)}.items():
         for _ in range(40): sf.query(sc, net, med, qi, sf.BF16, F_out=fo, stream=stream)
         b.record(stream); torch.cuda.synchronize()
         reps.append(a.elapsed_time(b) / 40)
-    out[name] = {"min": min(reps), "median": sorted(reps)[3], "max": max(reps)}
+    out[name] = round(sorted(reps)[3], 4)
 print(json.dumps(out))
