@@ -288,8 +288,14 @@ def run_b200(args):
     # ---- e2e through the public API with pinned host buffers
     q_host = torch.from_numpy(centers).pin_memory().numpy()
     F_host = torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy()
-    for _ in range(2):
+    # the host<->device path needs a longer warm-up than the kernels: the first ~100 calls
+    # after a stretch of device-only work run ~15% slower (PCIe link / host wake-up), so warm
+    # it for >= 50 calls and >= 0.3 s (tools/e2e_dist.py)
+    t_w = time.perf_counter()
+    for i in range(10 ** 6):
         sf.query(scene, net, medium, q_host, precision, F_out=F_host, stream=stream)
+        if i + 1 >= max(args.warmup, 50) and time.perf_counter() - t_w >= 0.3:
+            break
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()

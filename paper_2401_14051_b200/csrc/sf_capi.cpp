@@ -11,6 +11,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <numeric>
 #include <unordered_map>
 #include <string>
 #include <vector>
@@ -1192,9 +1193,11 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
         check_precision(*b, precision, stream);
         if (precision == SF_PRECISION_BF16) {
             // production path: query_prep -> fused sample+sort -> tcgen05 backbone per chunk of
-            // tiles, all on the caller's stream. With host query rows / outputs the batch goes
-            // in two chunks and the host transfers ride a copy stream: chunk 1's rows land while
-            // chunk 0 computes, chunk 0's F returns while chunk 1 computes.
+            // up to 4096 tiles, all on the caller's stream. With host query rows the chunk's rows
+            // arrive on a copy stream in two windows: the first (~1/5 of the rows, a whole number
+            // of the sampling grid's rounds) is prepared and sampled while the rest lands; both
+            // windows fill one operand layout, so the backbone still runs once per chunk (no
+            // extra wave tail).
             const sfb::SortLayout L = sfb::sort_layout(c);
             const int64_t n_tiles = (n + sfb::kUmmaM - 1) / sfb::kUmmaM;
             const bool h_in = !is_device_ptr(queries);
@@ -1208,10 +1211,32 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                                      sizeof(float4);
             const bool reorder = morton_env >= 0 ? morton_env > 0 && n > 1
                                                  : (vol_bytes > (size_t(96) << 20) && n >= 4096);
-            const bool overlap = overlap_on && !reorder && (h_in || h_out) && n_tiles >= 64;
-            int64_t chunk_tiles = overlap ? (n_tiles + 1) / 2 : n_tiles;
-            chunk_tiles = std::min<int64_t>(chunk_tiles, 1 << 12);  // operand blocks <= ~1.3 GB
+            const bool overlap = overlap_on && !reorder && h_in && n_tiles >= 64;
+            const int64_t chunk_tiles = std::min<int64_t>(n_tiles, 1 << 12);  // operand blocks <= ~1.3 GB
             const int64_t chunk = chunk_tiles * sfb::kUmmaM;
+            // sampling windows {first row, rows, chunk's first row}
+            struct Win {
+                int64_t r0, m, c0;
+            };
+            std::vector<Win> wins;
+            {
+                const int64_t grid = sfb::sample_sort_grid(), gpt = sfb::kUmmaM / 8;  // 8-query groups per tile
+                const int64_t unit = grid / std::gcd(grid, gpt);  // tiles per whole number of grid rounds
+                static const double first = std::getenv("SF_FIRST_WINDOW") ? std::atof(std::getenv("SF_FIRST_WINDOW"))
+                                                                           : 0.2;
+                for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+                    const int64_t m = std::min(chunk, n - c0), tiles = (m + sfb::kUmmaM - 1) / sfb::kUmmaM;
+                    int64_t w0 = overlap ? std::max<int64_t>(1, std::llround(first * double(tiles) / double(unit))) * unit
+                                         : 0;
+                    if (w0 >= tiles || first <= 0.0) w0 = 0;
+                    if (w0) {
+                        wins.push_back({c0, w0 * sfb::kUmmaM, c0});
+                        wins.push_back({c0 + w0 * sfb::kUmmaM, m - w0 * sfb::kUmmaM, c0});
+                    } else {
+                        wins.push_back({c0, m, c0});
+                    }
+                }
+            }
             // the call's device buffers, carved from the stream's workspace
             const bool hF = F_out && !is_device_ptr(F_out), hy = y_out && !is_device_ptr(y_out);
             auto carve_all = [&](uint8_t* base, Carve& cv) {
@@ -1315,9 +1340,8 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                 }
             } ev_guard{rows_ready};
             if (h_in)
-                for (int64_t c0 = 0; c0 < n; c0 += chunk) {
-                    const int64_t m = std::min(chunk, n - c0);
-                    SFB_CUDA(cudaMemcpyAsync(rows_buf.p + 9 * c0, queries + 9 * c0, size_t(m) * 9 * sizeof(double),
+                for (const Win& w : wins) {
+                    SFB_CUDA(cudaMemcpyAsync(rows_buf.p + 9 * w.r0, queries + 9 * w.r0, size_t(w.m) * 9 * sizeof(double),
                                              cudaMemcpyHostToDevice, cs));
                     cudaEvent_t e;
                     SFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1331,25 +1355,31 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                 sfb::launch_sort_keys(bufs.keys, bufs.keys + n, bufs.idx, perm.p, int(n), 30, sort_tmp_p, tmp_bytes,
                                       stream);
             }
-            for (int64_t c0 = 0, k = 0; c0 < n; c0 += chunk, ++k) {
-                const int64_t m = std::min(chunk, n - c0);
-                if (h_in && !reorder) SFB_CUDA(cudaStreamWaitEvent(stream, rows_ready[size_t(k)], 0));  // chunk k
-                if (k == 0) {
-                    StageScope st(SF_STAGE_CONFIG, stream);
-                    sfb::launch_diffuse_light(sc, dt, s->d_planes, s->n_planes, rows, s->d_pre, stream);
-                }
-                {
-                    StageScope st(SF_STAGE_CONFIG, stream);
-                    if (reorder)
-                        sfb::launch_query_prep(sc, ht, *medium, m, rows, media, cfg8.p, recs.p, stream, perm.p + c0);
-                    else
-                        sfb::launch_query_prep(sc, ht, *medium, m, rows + 9 * c0, media ? media + 4 * c0 : nullptr,
-                                               cfg8.p, recs.p, stream);
-                }
-                {
-                    StageScope st(SF_STAGE_SAMPLE_SORT, stream);
-                    sfb::launch_sample_sort(&sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, L, m, recs.p, nullptr,
-                                            ops.p, mms.p, err.p, stream, media != nullptr);
+            size_t wi = 0;
+            for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+                const int64_t m = std::min(chunk, n - c0), layout_tiles = (m + sfb::kUmmaM - 1) / sfb::kUmmaM;
+                for (; wi < wins.size() && wins[wi].c0 == c0; ++wi) {
+                    const Win& w = wins[wi];
+                    if (h_in && !reorder) SFB_CUDA(cudaStreamWaitEvent(stream, rows_ready[wi], 0));  // window's rows
+                    if (wi == 0) {
+                        StageScope st(SF_STAGE_CONFIG, stream);
+                        sfb::launch_diffuse_light(sc, dt, s->d_planes, s->n_planes, rows, s->d_pre, stream);
+                    }
+                    {
+                        StageScope st(SF_STAGE_CONFIG, stream);
+                        if (reorder)
+                            sfb::launch_query_prep(sc, ht, *medium, w.m, rows, media, cfg8.p + 8 * (w.r0 - c0), recs.p,
+                                                   stream, perm.p + w.r0);
+                        else
+                            sfb::launch_query_prep(sc, ht, *medium, w.m, rows + 9 * w.r0, media ? media + 4 * w.r0 : nullptr,
+                                                   cfg8.p + 8 * (w.r0 - c0), recs.p, stream);
+                    }
+                    {
+                        StageScope st(SF_STAGE_SAMPLE_SORT, stream);
+                        sfb::launch_sample_sort(&sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, L, w.m, recs.p,
+                                                nullptr, ops.p, mms.p, err.p, stream, media != nullptr,
+                                                (w.r0 - c0) / sfb::kUmmaM, layout_tiles);
+                    }
                 }
                 {
                     StageScope st(SF_STAGE_BACKBONE, stream);
@@ -1359,22 +1389,25 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                         sfb::launch_backbone_tc(*b, m, ops.p, mms.p, cfg8.p, yd ? yd + 3 * c0 : nullptr,
                                                 Fd ? Fd + 3 * c0 : nullptr, stream);
                 }
-                if (h_out && !reorder) {  // this chunk's results home while the next chunk computes
-                    stream_wait(cs, stream, next_event());
+                if (h_out && !reorder) {  // results home: on the copy stream while a next chunk computes
+                    const bool last = c0 + chunk >= n;
+                    cudaStream_t ds = last ? stream : cs;
+                    if (!last) stream_wait(cs, stream, next_event());
                     if (F_buf.p)
                         SFB_CUDA(cudaMemcpyAsync(F_out + 3 * c0, F_buf.p + 3 * c0, size_t(m) * 3 * sizeof(double),
-                                                 cudaMemcpyDeviceToHost, cs));
+                                                 cudaMemcpyDeviceToHost, ds));
                     if (y_buf.p)
                         SFB_CUDA(cudaMemcpyAsync(y_out + 3 * c0, y_buf.p + 3 * c0, size_t(m) * 3 * sizeof(float),
-                                                 cudaMemcpyDeviceToHost, cs));
+                                                 cudaMemcpyDeviceToHost, ds));
                 }
             }
             if (h_out && reorder) {  // scattered rows: one copy home after the last chunk
-                stream_wait(cs, stream, next_event());
                 if (F_buf.p)
-                    SFB_CUDA(cudaMemcpyAsync(F_out, F_buf.p, size_t(n) * 3 * sizeof(double), cudaMemcpyDeviceToHost, cs));
+                    SFB_CUDA(cudaMemcpyAsync(F_out, F_buf.p, size_t(n) * 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                                             stream));
                 if (y_buf.p)
-                    SFB_CUDA(cudaMemcpyAsync(y_out, y_buf.p, size_t(n) * 3 * sizeof(float), cudaMemcpyDeviceToHost, cs));
+                    SFB_CUDA(cudaMemcpyAsync(y_out, y_buf.p, size_t(n) * 3 * sizeof(float), cudaMemcpyDeviceToHost,
+                                             stream));
             }
             if (cs != stream) stream_wait(stream, cs, next_event());  // the caller sees the copies
             if (!h_out && !h_in) return;  // device in/out: asynchronous (see below)

@@ -45,7 +45,9 @@ constexpr int kMaxChunks = 512;
 struct SortDesc {
     int npts0, ntot;
     int n_segs, n_layers, n_chunks, n_tasks;
-    int n_tiles;
+    int n_tiles;  // tiles of the operand layout (the backbone launch's batch)
+    int tile0;    // first tile this launch fills; its rows / recs / feats start at row 0
+    int64_t n_groups;  // 8-query groups this launch processes
     int64_t feat_stride;
     int A, H, n_planes;
     float w[3];
@@ -596,8 +598,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     float* scr_buf = sm + plane_floats;
     QueryCtx* s_qc =
         reinterpret_cast<QueryCtx*>(sm + ((plane_floats + d.nbuf * kWarps * d.scr_floats + 3) & ~3));  // [2][8]
-    const int64_t q_pad = int64_t(d.n_tiles) * kUmmaM;
-    const int64_t n_groups = q_pad / kWarps;
+    const int64_t q_pad = int64_t(d.n_tiles) * kUmmaM;  // operand / pool layout
+    const int64_t n_groups = d.n_groups;
+    const int64_t qg0 = int64_t(d.tile0) * kUmmaM;      // global row of local row 0
     // per-warp prefetch of a group's query context (cp.async, 12 x 16 bytes)
     auto prefetch_ctx = [&](int64_t grp, int buf) {
         const int64_t q = grp * kWarps + warp;
@@ -648,7 +651,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         // ---- phase 2: register sorts, tasks ordered by network size; each thread writes its
         // segment's operand chunks (8 consecutive threads = 8 query rows = one 128-byte line)
         // and pools straight from registers
-        const int64_t tile = q0 / kUmmaM;
+        const int64_t tile = d.tile0 + q0 / kUmmaM;
         const int row0 = int(q0 % kUmmaM);
         const bool store = !(d.debug & 4);
         for (int t = threadIdx.x; t < ((d.debug & 2) ? 0 : d.n_tasks * kWarps); t += blockDim.x) {
@@ -663,7 +666,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
             o.blk = ops + s_prefix[sg] * d.n_tiles + tile * (int64_t(kUmmaM) * o.kf * 2);
             o.row = row0 + w;
             o.tau = sg % 3;
-            o.mm = mms + (int64_t(sg / 3) * q_pad + q0 + w) * 8;
+            o.mm = mms + (int64_t(sg / 3) * q_pad + qg0 + q0 + w) * 8;
             const float* seg = scr_all + w * d.scr_floats + s_scr[sg];
             if (pair)
                 cnt == 48 ? sort_emit_pair<24>(seg, cnt, t & 1, o, store)
@@ -704,6 +707,8 @@ SortDesc make_desc(const SceneDev* sc, int n_planes, const SortLayout& L, int64_
     d.ntot = L.npts[0] + L.npts[1];
     d.n_layers = L.n_layers;
     d.n_tiles = int((n + kUmmaM - 1) / kUmmaM);
+    d.tile0 = 0;
+    d.n_groups = int64_t(d.n_tiles) * (kUmmaM / kWarps);
     d.feat_stride = 3 * int64_t(d.ntot);
     if (sc) {
         d.A = sc->phase.ar;
@@ -787,6 +792,8 @@ void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float
 
 size_t query_rec_bytes() { return sizeof(QueryCtx); }
 
+int64_t sample_sort_grid() { return int64_t(sm_count()) * kMinBlocks; }
+
 size_t xpair_records(int nx, int ny, int nz) { return size_t((nx + 1) / 2) * ((ny + 1) / 2) * ((nz + 1) / 2) * 8; }
 
 void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t* keys, int* idx, cudaStream_t s) {
@@ -810,10 +817,16 @@ void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_mediu
 
 void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht, const float* planes,
                         int n_planes, const float4* pre, const SortLayout& L, int64_t n, const void* recs,
-                        const float* feats, uint8_t* ops, float* mms, int* err, cudaStream_t s, bool mixed) {
+                        const float* feats, uint8_t* ops, float* mms, int* err, cudaStream_t s, bool mixed,
+                        int64_t tile0, int64_t layout_tiles) {
     (void)dt;  // diffuse placement comes from `pre` (k_diffuse_prep)
     if (n <= 0) return;
     SortDesc d = make_desc(sc, n_planes, L, n);
+    if (layout_tiles > 0) {  // a window of a larger operand layout
+        if (tile0 < 0 || tile0 + d.n_tiles > layout_tiles) fail(SF_ERR_INVALID_ARGUMENT, "sample_sort: tile window");
+        d.tile0 = int(tile0);
+        d.n_tiles = int(layout_tiles);
+    }
     if (mixed && sc) {
         d.mixed = 1;
         d.G = sc->phase.gr;
@@ -840,9 +853,8 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
         SFB_CUDA(cudaFuncSetAttribute(k_sample_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         attr = smem;
     }
-    const int64_t q_pad = int64_t(d.n_tiles) * kUmmaM;
-    int64_t blocks = q_pad / kWarps;
-    int64_t cap = int64_t(sm_count()) * kMinBlocks;
+    int64_t blocks = d.n_groups;
+    int64_t cap = sample_sort_grid();
     if (blocks > cap) blocks = cap;
     SceneDev scd = sc ? *sc : SceneDev{};
     TemplateDev htd = ht ? *ht : TemplateDev{1, 0, nullptr, nullptr, 1.0, nullptr};

@@ -219,7 +219,13 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
 void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht,
                         const float* planes, int n_planes, const float4* pre, const SortLayout& L,
                         int64_t n, const void* recs, const float* feats, uint8_t* ops, float* mms,
-                        int* err, cudaStream_t s, bool mixed = false);
+                        int* err, cudaStream_t s, bool mixed = false, int64_t tile0 = 0,
+                        int64_t layout_tiles = 0);
+// layout_tiles > 0: this launch fills tiles [tile0, tile0 + ceil(n / 128)) of an operand /
+// pool layout of layout_tiles tiles (one backbone launch over several sampling launches).
+// Persistent grid of the sampling kernel (blocks): a window of a multiple of
+// grid * 8 queries has no partial last round.
+int64_t sample_sort_grid();
 // Per-query context records (sampling bases, highlight frame) + make_config rows.
 size_t query_rec_bytes();
 // perm (optional): processing row q reads the caller's row perm[q] (locality reordering)

@@ -10,7 +10,7 @@
 plus the C ABI's determinism contract ("results must not depend on thread
 count"): every query row is computed independently, so F is bit-identical whatever batch it
 travels in, whether its buffers are on the device, in pinned or in pageable host memory (the
-host path splits large batches into overlapped chunks), on both precisions."""
+host path streams large batches in two windows), on both precisions."""
 import os
 
 import numpy as np
@@ -123,7 +123,7 @@ def det():
     scene = sf.Scene(g, tv, sf.load_template(os.path.join(DATA, "diffuse_seed7.vtmpl")),
                      sf.load_template(os.path.join(DATA, "highlight_seed8.vtmpl")), sf.PhaseModel.hg(0.7),
                      sf.PhaseTable(64, 128, 32, 16))
-    rows = scenes.draw_centers(vol, 9000, 21, scenes.LIGHT)  # 71 tiles: the host path overlaps 2 chunks
+    rows = scenes.draw_centers(vol, 30000, 21, scenes.LIGHT)  # 235 tiles: host rows arrive in 2 windows
     return scene, sf.make_backbone(sf.BackboneConfig(seed=0)), sf.MediumParams((0.7,), (0.99,) * 3), rows
 
 
@@ -140,7 +140,7 @@ def test_rows_independent_of_batch_and_buffers(det, precision):
     pin_out = torch.empty((len(rows), 3), dtype=torch.float64).pin_memory()
     sf.query(scene, net, med, pin_in.numpy(), prec, F_out=pin_out.numpy())
     assert np.array_equal(pin_out.numpy(), ref)
-    for a, b in ((0, 1), (1234, 5678), (8191, 9000), (100, 229)):  # sub-batches, ragged tiles
+    for a, b in ((0, 1), (1234, 5678), (14207, 30000), (100, 229)):  # sub-batches, ragged tiles
         assert np.array_equal(sf.query(scene, net, med, rows[a:b], prec), ref[a:b]), (a, b)
     perm = np.random.default_rng(5).permutation(len(rows))
     assert np.array_equal(sf.query(scene, net, med, rows[perm], prec), ref[perm])
