@@ -17,9 +17,11 @@ separately and reported under "stages".
 
   value : queries/s with queries and outputs resident in HBM, L2 flushed
           (256 MiB write) between timed steps, CUDA events per step, max over ranks.
-  e2e   : the same through the public API (paper_2401_14051_b200.query) with
-          pinned HOST query rows in and HOST radiance out, copies inside the timed
-          region.
+  e2e   : the same through the public API (paper_2401_14051_b200.query) with HOST
+          query rows in and HOST radiance out, in the library's page-locked buffers
+          (sf.pinned_empty); every step moves the rows host->device (two copy-engine
+          windows overlapped with sampling) and F device->host (written in place into
+          the pinned buffer by the backbone's epilogue) inside the timed region.
 
 Multi-GPU (torchrun): each rank owns its own 65,536-query tile set (weak
 scaling, no data-path collective); the radiance tiles are gathered to rank 0
@@ -277,6 +279,7 @@ def run_b200(args):
     if ws > 1:
         dist.barrier()
     clocks.active = False
+    clocks.stop()  # nvidia-smi polls the driver every 20 ms; keep it off the synchronous e2e leg
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if ws > 1:
@@ -286,8 +289,9 @@ def run_b200(args):
     value = ws * n / (ms_per_step * 1e-3)
 
     # ---- e2e through the public API with pinned host buffers
-    q_host = torch.from_numpy(centers).pin_memory().numpy()
-    F_host = torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy()
+    q_host = sf.pinned_empty(centers.shape)  # the library's page-locked host buffers
+    q_host[:] = centers
+    F_host = sf.pinned_empty((n, 3))
     # the host<->device path needs a longer warm-up than the kernels: the first ~100 calls
     # after a stretch of device-only work run ~15% slower (PCIe link / host wake-up), so warm
     # it for >= 50 calls and >= 0.3 s (tools/e2e_dist.py)
@@ -310,7 +314,6 @@ def run_b200(args):
     if ws > 1:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
     e2e_value = ws * n / (float(e_ms.item()) * 1e-3)
-    clocks.stop()
 
     # ---- per-stage device times (CUDA events on the launching stream), L2 flushed
     sf.lib.sf_profile_enable(1)

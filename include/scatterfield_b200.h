@@ -261,6 +261,13 @@ enum sf_stage {
  * resets the accumulators. */
 int sf_profile_enable(int on);
 int sf_profile_read(double stage_ms[SF_STAGE_COUNT], int64_t stage_launches[SF_STAGE_COUNT]);
+/* Page-locked host buffers for the host-memory query path (no reference counterpart: the
+ * reference computes on host vectors). Allocated 2 MiB-aligned with transparent huge pages
+ * requested (madvise), touched, then registered with CUDA: the DMA engine's address
+ * translations stay few and warm, where 4 KiB-page pinned memory starts ~4x slower on its
+ * first transfers (tools/e2e_state.py). sf_host_free unregisters and frees. */
+int sf_host_alloc(size_t bytes, void** out);
+int sf_host_free(void* p);
 /* Number of kernels this library has launched since load (all entry points). */
 int64_t sf_launch_count(void);
 /* Diagnostics: with SF_DEBUG_TC set in the environment, CTA 0 of the tensor-core

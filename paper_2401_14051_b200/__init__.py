@@ -14,7 +14,7 @@ from .api import (BF16, DIFFUSE, FP32, HIGHLIGHT, Backbone, BackboneConfig, Comb
                   build_transmittance_slab, build_transmittance_volume, combine_transmittance, config_rows, conv3_replicate,
                   decode_prediction, encode_label, graded_transmittance, light_entry_point, load_template,
                   make_backbone, make_config, place_template, predict, predict_y, query, query_media, sample_features,
-                  Camera, RenderOptions, bake_field, render_volume, render_neural,
+                  Camera, RenderOptions, bake_field, render_volume, render_neural, pinned_empty,
                   save_template)
 
 __version__ = "0.1.0"

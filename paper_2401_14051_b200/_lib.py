@@ -99,6 +99,8 @@ _SIGS = {
     "sf_profile_enable": (I, [I]),
     "sf_profile_read": (I, [P, P]),
     "sf_launch_count": (I64, []),
+    "sf_host_alloc": (I, [C.c_size_t, PP]),
+    "sf_host_free": (I, [P]),
     "sf_debug_tc_profile": (I, [P]),
 }
 

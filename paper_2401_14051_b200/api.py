@@ -666,6 +666,35 @@ class MediumParams:
         return m
 
 
+class _HostBlock:
+    def __init__(self, p):
+        self.p = p
+
+    def __del__(self):
+        if self.p:
+            lib.sf_host_free(C.c_void_p(self.p))
+            self.p = None
+
+
+class PinnedArray(np.ndarray):
+    """numpy array over an sf_host_alloc block; views keep the block alive through .base."""
+    _block = None
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """Page-locked host array for the host-memory query path (sf_host_alloc: huge-page backed,
+    registered with CUDA), so rows in / F out move at PCIe speed from the first call."""
+    dt = np.dtype(dtype)
+    nbytes = max(int(np.prod(shape)), 1) * dt.itemsize
+    h = C.c_void_p()
+    check(lib.sf_host_alloc(nbytes, C.byref(h)))
+    block = _HostBlock(h.value)
+    buf = (C.c_char * nbytes).from_address(h.value)
+    arr = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape).view(PinnedArray)
+    arr._block = block
+    return arr
+
+
 def query(scene: Scene, net: Backbone, medium: MediumParams, queries, precision=FP32, F_out=None, y_out=None,
           stream=None):
     """The fused per-shading-point hot path: features for both templates, make_config,

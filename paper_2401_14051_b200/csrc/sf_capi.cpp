@@ -5,6 +5,8 @@
 // thread-local message (reference Errc semantics, inc/error.h:11-32).
 #include <cuda_runtime.h>
 
+#include <sys/mman.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -51,6 +53,20 @@ bool is_device_ptr(const void* p) {
         return false;
     }
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Device alias of pinned (page-locked, mapped) host memory, else nullptr. The backbone writes
+// F into such a buffer in place (16-byte chunks over PCIe, overlapped with the tiles still
+// computing) instead of a copy after the last tile (SF_NO_ZERO_COPY=1: copy).
+void* mapped_alias(const void* p) {
+    static const bool off = std::getenv("SF_NO_ZERO_COPY") != nullptr;
+    if (!p || off) return nullptr;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
 }
 
 // Stream-ordered scratch buffer.
@@ -1201,7 +1217,10 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             const sfb::SortLayout L = sfb::sort_layout(c);
             const int64_t n_tiles = (n + sfb::kUmmaM - 1) / sfb::kUmmaM;
             const bool h_in = !is_device_ptr(queries);
-            const bool h_out = (F_out && !is_device_ptr(F_out)) || (y_out && !is_device_ptr(y_out));
+            // pinned host F (not on the Morton path, whose rows are scattered): written in place
+            double* z_F = nullptr;
+            const bool hF0 = F_out && !is_device_ptr(F_out);
+            bool zero_copy = false;
             static const bool overlap_on = !std::getenv("SF_NO_HOST_OVERLAP");
             // Volumes beyond L2 (x-pair records of a 256^3 grid are 268 MB): process the queries in
             // Morton order of p so concurrently sampled queries share the volume's cache lines;
@@ -1211,6 +1230,11 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                                      sizeof(float4);
             const bool reorder = morton_env >= 0 ? morton_env > 0 && n > 1
                                                  : (vol_bytes > (size_t(96) << 20) && n >= 4096);
+            if (hF0 && !reorder && (reinterpret_cast<uintptr_t>(F_out) & 15) == 0) {
+                z_F = static_cast<double*>(mapped_alias(F_out));
+                zero_copy = z_F != nullptr;
+            }
+            const bool h_out = (hF0 && !zero_copy) || (y_out && !is_device_ptr(y_out));
             const bool overlap = overlap_on && !reorder && h_in && n_tiles >= 64;
             const int64_t chunk_tiles = std::min<int64_t>(n_tiles, 1 << 12);  // operand blocks <= ~1.3 GB
             const int64_t chunk = chunk_tiles * sfb::kUmmaM;
@@ -1238,7 +1262,7 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                 }
             }
             // the call's device buffers, carved from the stream's workspace
-            const bool hF = F_out && !is_device_ptr(F_out), hy = y_out && !is_device_ptr(y_out);
+            const bool hF = hF0 && !zero_copy, hy = y_out && !is_device_ptr(y_out);
             auto carve_all = [&](uint8_t* base, Carve& cv) {
                 cv = Carve{base};
                 struct {
@@ -1317,7 +1341,7 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             } err{bufs.err}, perm{bufs.perm};
             SFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), stream));
             const double* rows = h_in ? rows_buf.p : queries;
-            double* Fd = F_out ? (F_buf.p ? F_buf.p : F_out) : nullptr;
+            double* Fd = F_out ? (zero_copy ? z_F : (F_buf.p ? F_buf.p : F_out)) : nullptr;
             float* yd = y_out ? (y_buf.p ? y_buf.p : y_out) : nullptr;
             sfb::SceneDev sc = sfb::scene_dev(*s->density, *s->tvol->values, s->d_dt, s->model, *s->table,
                                               s->template_scale);
@@ -1410,7 +1434,7 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                                              stream));
             }
             if (cs != stream) stream_wait(stream, cs, next_event());  // the caller sees the copies
-            if (!h_out && !h_in) return;  // device in/out: asynchronous (see below)
+            if (!h_out && !h_in && !zero_copy) return;  // device in/out: asynchronous (see below)
             int herr = 0;
             SFB_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
             sync(stream);
@@ -1566,6 +1590,34 @@ int sf_profile_read(double stage_ms[SF_STAGE_COUNT], int64_t stage_launches[SF_S
             cudaEventDestroy(r.b);
         }
         sfb::cuda_check(first, "profile events");
+    });
+}
+
+int sf_host_alloc(size_t bytes, void** out) {
+    return guard([&] {
+        if (!out) fail(SF_ERR_INVALID_ARGUMENT, "sf_host_alloc: null output");
+        *out = nullptr;
+        if (bytes == 0) return;
+        constexpr size_t kHuge = size_t(2) << 20;
+        const size_t size = (bytes + kHuge - 1) / kHuge * kHuge;
+        void* p = nullptr;
+        if (posix_memalign(&p, kHuge, size) != 0 || !p) fail(SF_ERR_CUDA, "sf_host_alloc: out of host memory");
+        madvise(p, size, MADV_HUGEPAGE);  // best effort (THP may be off)
+        std::memset(p, 0, size);          // fault the pages in before pinning
+        const cudaError_t e = cudaHostRegister(p, size, cudaHostRegisterPortable);
+        if (e != cudaSuccess) {
+            free(p);
+            sfb::cuda_check(e, "cudaHostRegister");
+        }
+        *out = p;
+    });
+}
+
+int sf_host_free(void* p) {
+    return guard([&] {
+        if (!p) return;
+        sfb::cuda_check(cudaHostUnregister(p), "cudaHostUnregister");
+        free(p);
     });
 }
 

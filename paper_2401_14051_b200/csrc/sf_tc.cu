@@ -254,7 +254,8 @@ __device__ __forceinline__ void store_row32(uint8_t* a, const float* v) {
 __global__ void __launch_bounds__(kThreads, 2)
     k_backbone_tc(const TcDesc d, const uint8_t* __restrict__ wpk, const uint8_t* __restrict__ ops,
                   const uint8_t* __restrict__ mms, int n_tiles, int64_t n, const double* __restrict__ cfg8,
-                  float* __restrict__ y_out, double* __restrict__ F_out, const int* __restrict__ perm) {
+                  float* __restrict__ y_out, double* __restrict__ F_out, const int* __restrict__ perm,
+                  int f_stage) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t bars[2 * kSlots + 1];
     __shared__ uint32_t tmem_slot;
@@ -477,13 +478,32 @@ __global__ void __launch_bounds__(kThreads, 2)
             const float* h2 = reinterpret_cast<const float*>(sh + kSlotHead2);
             float y[3];
             dense_s<3, 64>(h2, h2 + 192, h, y);
+            // f_stage: the tile's F rows (128 x 24 contiguous bytes) are staged in the free a2
+            // operand buffer and stored as 16-byte chunks — full sectors whether F is device
+            // memory or mapped pinned host memory written over PCIe (zero copy)
+            double* fs = reinterpret_cast<double*>(a2);
             if (live) {
                 for (int c = 0; c < 3; ++c) {
                     float yc = fabsf(y[c]);
                     const int64_t oq = perm ? int64_t(perm[q]) : q;  // the caller's row (locality reordering)
                     if (y_out) y_out[3 * oq + c] = yc;
-                    if (F_out) F_out[3 * oq + c] = pow(cfg8[8 * q + 4 + c], d.gamma) * expm1(double(yc));  // decode_prediction
+                    if (F_out) {
+                        const double f = pow(cfg8[8 * q + 4 + c], d.gamma) * expm1(double(yc));  // decode_prediction
+                        if (f_stage)
+                            fs[3 * tid + c] = f;
+                        else
+                            F_out[3 * oq + c] = f;
+                    }
                 }
+            }
+            if (f_stage && F_out) {
+                consumer_bar_sync();
+                const int64_t rem = n - int64_t(tile) * kUmmaM, rows = rem < kUmmaM ? rem : kUmmaM;
+                const int chunks = int(rows * 3 / 2);  // 16-byte chunks; an odd row count leaves 8 bytes
+                double* dst = F_out + int64_t(tile) * kUmmaM * 3;
+                for (int k = tid; k < chunks; k += kConsumers)
+                    reinterpret_cast<double2*>(dst)[k] = reinterpret_cast<const double2*>(fs)[k];
+                if ((rows & 1) && tid == 0) dst[rows * 3 - 1] = fs[rows * 3 - 1];
             }
         }
         ++j;
@@ -709,8 +729,9 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
         // answers 1 for this kernel, so no runtime check here.
     }
     const int n_tiles = int((n + kUmmaM - 1) / kUmmaM);
+    const int f_stage = F && !perm && (reinterpret_cast<uintptr_t>(F) & 15) == 0 ? 1 : 0;
     k_backbone_tc<<<n_tiles, kThreads, smem, s>>>(pk->desc, pk->d_blobs, ops, reinterpret_cast<const uint8_t*>(mms),
-                                                  n_tiles, n, cfg8, y, F, perm);
+                                                  n_tiles, n, cfg8, y, F, perm, f_stage);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }

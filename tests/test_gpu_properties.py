@@ -9,8 +9,9 @@
 
 plus the C ABI's determinism contract ("results must not depend on thread
 count"): every query row is computed independently, so F is bit-identical whatever batch it
-travels in, whether its buffers are on the device, in pinned or in pageable host memory (the
-host path streams large batches in two windows), on both precisions."""
+travels in, whether its buffers are on the device, in pinned (torch or sf.pinned_empty) or in
+pageable host memory (the host path streams large batches in two windows; pinned F is written
+in place by the backbone), on both precisions."""
 import os
 
 import numpy as np
@@ -140,6 +141,13 @@ def test_rows_independent_of_batch_and_buffers(det, precision):
     pin_out = torch.empty((len(rows), 3), dtype=torch.float64).pin_memory()
     sf.query(scene, net, med, pin_in.numpy(), prec, F_out=pin_out.numpy())
     assert np.array_equal(pin_out.numpy(), ref)
+    hp_in, hp_out = sf.pinned_empty(rows.shape), sf.pinned_empty((len(rows), 3))  # sf_host_alloc buffers
+    hp_in[:] = rows
+    sf.query(scene, net, med, hp_in, prec, F_out=hp_out)
+    assert np.array_equal(hp_out, ref)
+    odd = sf.pinned_empty((len(rows) * 3 + 1,))[1:].reshape(-1, 3)  # 8-byte aligned F: no in-place path
+    sf.query(scene, net, med, hp_in, prec, F_out=odd)
+    assert np.array_equal(odd, ref)
     for a, b in ((0, 1), (1234, 5678), (14207, 30000), (100, 229)):  # sub-batches, ragged tiles
         assert np.array_equal(sf.query(scene, net, med, rows[a:b], prec), ref[a:b]), (a, b)
     perm = np.random.default_rng(5).permutation(len(rows))
