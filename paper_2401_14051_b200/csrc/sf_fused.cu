@@ -50,6 +50,7 @@ struct SortDesc {
     int64_t n_groups;  // 8-query groups this launch processes
     int64_t feat_stride;
     int A, H, n_planes;
+    float su, sv;  // float(A - 1) / float(pi), float(H - 1) / float(pi): IEEE quotients, made once on the host
     float w[3];
     int scr_floats;
     int seg_scr[kMaxSegs];  // offset of the segment in the query scratch row
@@ -68,11 +69,12 @@ struct SortDesc {
 
 // Bilinear lookup in a pre-blended phase plane stored as aperture pairs
 // pl[a][h] = {P(a,h), P(a,h+1)}, rows padded to H+1 pairs (no bank aliasing).
-__device__ __forceinline__ float plane_lookup(const float2* pl, int A, int H, float angle, float half) {
-    float u = fminf(fmaxf(angle, 0.0f), float(kPi)) * (float(A - 1) / float(kPi));
+__device__ __forceinline__ float plane_lookup(const float2* pl, int A, int H, float su, float sv, float angle,
+                                              float half) {
+    float u = fminf(fmaxf(angle, 0.0f), float(kPi)) * su;
     int i0 = min(int(u), A - 2);
     float t = u - float(i0);
-    float v = fminf(fmaxf(half, 0.0f), float(kPi)) * (float(H - 1) / float(kPi));
+    float v = fminf(fmaxf(half, 0.0f), float(kPi)) * sv;
     int j0 = min(int(v), H - 2);
     float s = v - float(j0);
     const float2 r0 = pl[i0 * (H + 1) + j0];
@@ -85,10 +87,10 @@ __device__ __forceinline__ float plane_lookup(const float2* pl, int A, int H, fl
 // PhaseTable::lookup (src/phase.cpp:221-230) on the pre-blended planes.
 __device__ __forceinline__ float cap_phase(const float2* planes, const SortDesc& d, float cosine, float half) {
     const float angle = acosf(fminf(fmaxf(cosine, -1.0f), 1.0f));
-    if (d.n_planes == 1) return d.w[0] * plane_lookup(planes, d.A, d.H, angle, half);  // single lobe / isotropic
+    if (d.n_planes == 1) return d.w[0] * plane_lookup(planes, d.A, d.H, d.su, d.sv, angle, half);  // one lobe / iso
     float f = 0.0f;
     for (int k = 0; k < d.n_planes; ++k)
-        f = fmaf(d.w[k], plane_lookup(planes + k * d.A * (d.H + 1), d.A, d.H, angle, half), f);
+        f = fmaf(d.w[k], plane_lookup(planes + k * d.A * (d.H + 1), d.A, d.H, d.su, d.sv, angle, half), f);
     return f;
 }
 
@@ -98,10 +100,10 @@ __device__ __forceinline__ float cap_phase(const float2* planes, const SortDesc&
 __device__ __forceinline__ float table_phase(const SortDesc& d, int gi, float gt, float cosine, float half) {
     const float angle = acosf(fminf(fmaxf(cosine, -1.0f), 1.0f));
     const int A = d.A, H = d.H;
-    const float u = fminf(fmaxf(angle, 0.0f), float(kPi)) * (float(A - 1) / float(kPi));
+    const float u = fminf(fmaxf(angle, 0.0f), float(kPi)) * d.su;
     const int i0 = min(int(u), A - 2);
     const float t = u - float(i0);
-    const float v = fminf(fmaxf(half, 0.0f), float(kPi)) * (float(H - 1) / float(kPi));
+    const float v = fminf(fmaxf(half, 0.0f), float(kPi)) * d.sv;
     const int j0 = min(int(v), H - 2);
     const float s = v - float(j0);
     float pg[2];
@@ -713,6 +715,8 @@ SortDesc make_desc(const SceneDev* sc, int n_planes, const SortLayout& L, int64_
     if (sc) {
         d.A = sc->phase.ar;
         d.H = sc->phase.hr;
+        d.su = float(d.A - 1) / float(kPi);
+        d.sv = float(d.H - 1) / float(kPi);
         d.n_planes = n_planes;
         if (sc->phase.kind == SF_PHASE_ISOTROPIC) {
             d.w[0] = 1.0f;
