@@ -1385,18 +1385,16 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                 for (; wi < wins.size() && wins[wi].c0 == c0; ++wi) {
                     const Win& w = wins[wi];
                     if (h_in && !reorder) SFB_CUDA(cudaStreamWaitEvent(stream, rows_ready[wi], 0));  // window's rows
-                    if (wi == 0) {
+                    {  // the first window's launch also makes the diffuse constants (light of row 0)
                         StageScope st(SF_STAGE_CONFIG, stream);
-                        sfb::launch_diffuse_light(sc, dt, s->d_planes, s->n_planes, rows, s->d_pre, stream);
-                    }
-                    {
-                        StageScope st(SF_STAGE_CONFIG, stream);
+                        const sfb::TemplateDev* dtp = wi == 0 ? &dt : nullptr;
                         if (reorder)
                             sfb::launch_query_prep(sc, ht, *medium, w.m, rows, media, cfg8.p + 8 * (w.r0 - c0), recs.p,
-                                                   stream, perm.p + w.r0);
+                                                   stream, perm.p + w.r0, rows, dtp, s->d_planes, s->n_planes, s->d_pre);
                         else
                             sfb::launch_query_prep(sc, ht, *medium, w.m, rows + 9 * w.r0, media ? media + 4 * w.r0 : nullptr,
-                                                   cfg8.p + 8 * (w.r0 - c0), recs.p, stream);
+                                                   cfg8.p + 8 * (w.r0 - c0), recs.p, stream, nullptr, rows, dtp,
+                                                   s->d_planes, s->n_planes, s->d_pre);
                     }
                     {
                         StageScope st(SF_STAGE_SAMPLE_SORT, stream);

@@ -23,7 +23,7 @@
 // FP32 (relative errors ~1e-6, far inside the 3.9e-3 bf16 rounding the operands
 // then undergo). Diffuse placement is a pure translation, so each diffuse point's
 // voxel offset, unit axis, aperture and light-side cap integral are per-scene
-// constants (k_diffuse_prep).
+// constants (made by the first blocks of k_query_prep).
 #include <algorithm>
 #include <cstdlib>
 
@@ -298,10 +298,9 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
 
 // Per-scene diffuse constants: pre[2i] = {offset (voxels), half angle or -1 at the
 // centre}, pre[2i+1] = {unit axis, light-side cap integral for the light of query 0}.
-__global__ void k_diffuse_prep(SceneDev sc, TemplateDev dt, SortDesc d, const float2* __restrict__ planes,
-                               const double* __restrict__ queries, float4* __restrict__ pre) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= dt.total) return;
+__device__ __forceinline__ void diffuse_point(const SceneDev& sc, const TemplateDev& dt, const SortDesc& d,
+                                              const float2* __restrict__ planes, const double* __restrict__ queries,
+                                              int i, float4* __restrict__ pre) {
     const double* qq = dt.pts + 3 * i;
     const double ts = sc.template_scale;
     const double ivs = sc.grid.ivs != 0.0 ? sc.grid.ivs : 1.0 / sc.grid.vs;
@@ -323,26 +322,54 @@ __global__ void k_diffuse_prep(SceneDev sc, TemplateDev dt, SortDesc d, const fl
 
 // Per-query preparation for the production path: make_config rows
 // (src/predictor.cpp:261-274, alpha = angle_between(omega, l)) and the sampling
-// context (voxel-space bases, highlight frame, in-box bounds).
-__global__ void k_query_prep(SceneDev sc, TemplateDev ht, sf_medium_params m, int64_t n,
-                             const double* __restrict__ queries, const double* __restrict__ media,
-                             double* __restrict__ cfg8, QueryCtx* __restrict__ recs, const int* __restrict__ perm) {
-    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t src = perm ? int64_t(perm[q]) : q;  // processing order -> the caller's row
-        const double* c = queries + 9 * src;
-        QueryCtx qc;
-        query_ctx(sc, ht, c, qc);
-        qc.same_light = (!media && c[6] == queries[6] && c[7] == queries[7] && c[8] == queries[8]) ? 1 : 0;
-        qc.gi = 0;
-        qc.gt = 0.0f;
-        if (media) {  // g axis of PhaseTable::lookup_hg (src/phase.cpp:196-205) at the query's g
-            double gt;
-            table_coord(media[4 * src], -0.99, 0.99, sc.phase.gr, qc.gi, gt);
-            qc.gt = float(gt);
+// context (voxel-space bases, highlight frame, in-box bounds). One thread per query; the
+// block's records and config rows are staged in shared memory and stored as contiguous
+// 16-byte chunks. With `dt` set, the first blocks also make the per-scene diffuse constants
+// (diffuse placement is a pure translation, so axis and aperture do not depend on p).
+constexpr int kPrepThreads = 128;
+
+__global__ void __launch_bounds__(kPrepThreads)
+    k_query_prep(SceneDev sc, TemplateDev ht, sf_medium_params m, int64_t n, const double* __restrict__ queries,
+                 const double* __restrict__ media, double* __restrict__ cfg8, QueryCtx* __restrict__ recs,
+                 const int* __restrict__ perm, const double* __restrict__ row0, TemplateDev dt, SortDesc d,
+                 const float2* __restrict__ planes, float4* __restrict__ pre, int diffuse_blocks) {
+    if (int(blockIdx.x) < diffuse_blocks) {
+        const int i = blockIdx.x * kPrepThreads + threadIdx.x;
+        if (i < dt.total) diffuse_point(sc, dt, d, planes, row0, i, pre);
+        return;
+    }
+    __shared__ __align__(16) QueryCtx s_rec[kPrepThreads];
+    __shared__ __align__(16) double s_cfg[kPrepThreads * 8];
+    const int64_t nblk = int64_t(gridDim.x) - diffuse_blocks;
+    for (int64_t q0 = (int64_t(blockIdx.x) - diffuse_blocks) * kPrepThreads; q0 < n; q0 += nblk * kPrepThreads) {
+        const int64_t q = q0 + threadIdx.x;
+        if (q < n) {
+            const int64_t src = perm ? int64_t(perm[q]) : q;  // processing order -> the caller's row
+            const double* c = queries + 9 * src;
+            QueryCtx qc;
+            query_ctx(sc, ht, c, qc);
+            // the diffuse light side was precomputed for the light of the batch's row 0
+            qc.same_light = (!media && c[6] == row0[6] && c[7] == row0[7] && c[8] == row0[8]) ? 1 : 0;
+            qc.gi = 0;
+            qc.gt = 0.0f;
+            if (media) {  // g axis of PhaseTable::lookup_hg (src/phase.cpp:196-205) at the query's g
+                double gt;
+                table_coord(media[4 * src], -0.99, 0.99, sc.phase.gr, qc.gi, gt);
+                qc.gt = float(gt);
+            }
+            qc.pad_[0] = qc.pad_[1] = 0;
+            s_rec[threadIdx.x] = qc;
+            write_cfg8(m, media ? media + 4 * src : nullptr, c, s_cfg + 8 * threadIdx.x);
         }
-        qc.pad_[0] = qc.pad_[1] = 0;
-        recs[q] = qc;
-        write_cfg8(m, media ? media + 4 * src : nullptr, c, cfg8 + 8 * q);
+        __syncthreads();
+        const int rows = n - q0 < kPrepThreads ? int(n - q0) : kPrepThreads;
+        const int4* rs = reinterpret_cast<const int4*>(s_rec);
+        int4* rd = reinterpret_cast<int4*>(recs + q0);
+        for (int k = threadIdx.x; k < rows * int(sizeof(QueryCtx) / 16); k += kPrepThreads) rd[k] = rs[k];
+        const int4* cs = reinterpret_cast<const int4*>(s_cfg);
+        int4* cd = reinterpret_cast<int4*>(cfg8 + 8 * q0);
+        for (int k = threadIdx.x; k < rows * 4; k += kPrepThreads) cd[k] = cs[k];
+        __syncthreads();
     }
 }
 
@@ -784,16 +811,6 @@ void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStr
     count_launch();
 }
 
-void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float* planes, int n_planes,
-                          const double* queries, float4* pre, cudaStream_t s) {
-    SortLayout L{};
-    SortDesc d = make_desc(&sc, n_planes, L, 1);
-    k_diffuse_prep<<<(dt.total + 127) / 128, 128, 0, s>>>(sc, dt, d, reinterpret_cast<const float2*>(planes),
-                                                          queries, pre);
-    SFB_CUDA(cudaGetLastError());
-    count_launch();
-}
-
 size_t query_rec_bytes() { return sizeof(QueryCtx); }
 
 int64_t sample_sort_grid() { return int64_t(sm_count()) * kMinBlocks; }
@@ -810,11 +827,20 @@ void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t*
 
 void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_medium_params& m, int64_t n,
                        const double* queries, const double* media, double* cfg8, void* recs, cudaStream_t s,
-                       const int* perm) {
+                       const int* perm, const double* row0, const TemplateDev* dt, const float* planes, int n_planes,
+                       float4* pre) {
     if (n <= 0) return;
-    const int64_t blocks = std::min<int64_t>((n + 127) / 128, int64_t(sm_count()) * 16);
-    k_query_prep<<<unsigned(blocks), 128, 0, s>>>(sc, ht, m, n, queries, media, cfg8, static_cast<QueryCtx*>(recs),
-                                                  perm);
+    const int diffuse_blocks = dt ? (dt->total + kPrepThreads - 1) / kPrepThreads : 0;
+    SortDesc d{};
+    if (dt) {
+        SortLayout L{};
+        d = make_desc(&sc, n_planes, L, 1);
+    }
+    const int64_t blocks = std::min<int64_t>((n + kPrepThreads - 1) / kPrepThreads, int64_t(sm_count()) * 16);
+    k_query_prep<<<unsigned(blocks + diffuse_blocks), kPrepThreads, 0, s>>>(
+        sc, ht, m, n, queries, media, cfg8, static_cast<QueryCtx*>(recs), perm, row0 ? row0 : queries,
+        dt ? *dt : TemplateDev{}, d,
+        reinterpret_cast<const float2*>(planes), pre, diffuse_blocks);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
@@ -823,7 +849,7 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
                         int n_planes, const float4* pre, const SortLayout& L, int64_t n, const void* recs,
                         const float* feats, uint8_t* ops, float* mms, int* err, cudaStream_t s, bool mixed,
                         int64_t tile0, int64_t layout_tiles) {
-    (void)dt;  // diffuse placement comes from `pre` (k_diffuse_prep)
+    (void)dt;  // diffuse placement comes from `pre` (k_query_prep's diffuse blocks)
     if (n <= 0) return;
     SortDesc d = make_desc(sc, n_planes, L, n);
     if (layout_tiles > 0) {  // a window of a larger operand layout

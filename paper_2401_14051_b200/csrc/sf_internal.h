@@ -229,15 +229,15 @@ int64_t sample_sort_grid();
 // Per-query context records (sampling bases, highlight frame) + make_config rows.
 size_t query_rec_bytes();
 // perm (optional): processing row q reads the caller's row perm[q] (locality reordering)
+// row0: the batch's first row (its light is the one the diffuse constants hold; default:
+// queries). dt (optional): also make those diffuse constants (launch_diffuse_light's work)
+// in the same launch.
 void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_medium_params& m, int64_t n,
                        const double* queries, const double* media, double* cfg8, void* recs, cudaStream_t s,
-                       const int* perm = nullptr);
+                       const int* perm = nullptr, const double* row0 = nullptr, const TemplateDev* dt = nullptr,
+                       const float* planes = nullptr, int n_planes = 0, float4* pre = nullptr);
 // Morton keys of the queries' positions in the grid box + identity indices (for cub sort)
 void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t* keys, int* idx, cudaStream_t s);
-// Light-side phase of every diffuse point for the light of query 0 (diffuse
-// placement is a pure translation, so axis and aperture do not depend on p).
-void launch_diffuse_light(const SceneDev& sc, const TemplateDev& dt, const float* planes, int n_planes,
-                          const double* queries, float4* pre, cudaStream_t s);
 void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStream_t s);
 size_t xpair_records(int nx, int ny, int nz);  // records of the mini-brick x-pair layout (padded dims)
 // Pre-blended phase planes: for each lobe, the table interpolated at that lobe's g

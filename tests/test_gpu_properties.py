@@ -152,3 +152,24 @@ def test_rows_independent_of_batch_and_buffers(det, precision):
         assert np.array_equal(sf.query(scene, net, med, rows[a:b], prec), ref[a:b]), (a, b)
     perm = np.random.default_rng(5).permutation(len(rows))
     assert np.array_equal(sf.query(scene, net, med, rows[perm], prec), ref[perm])
+
+
+def test_two_lights_across_windows(det):
+    """Rows lit by two lights, the second starting inside the host path's second window:
+    every window compares its rows' lights with the batch's row 0 (whose light the diffuse
+    constants hold), so the host-window path equals the single-window device path bit for bit
+    and the FP32 path within the bf16 bound."""
+    import torch
+    scene, net, med, rows = det
+    rows = rows.copy()
+    other = np.array([0.6, -0.7, 0.3]) / np.linalg.norm([0.6, -0.7, 0.3])
+    rows[20000:, 6:9] = other
+    F_host = sf.query(scene, net, med, rows, sf.BF16)
+    F_dev = torch.empty((len(rows), 3), dtype=torch.float64, device="cuda")
+    sf.query(scene, net, med, torch.from_numpy(rows).cuda(), sf.BF16, F_out=F_dev)
+    assert np.array_equal(F_dev.cpu().numpy(), F_host)
+    y16 = np.empty((len(rows), 3), np.float32)
+    y32 = np.empty((len(rows), 3), np.float32)
+    sf.query(scene, net, med, rows[19000:21000], sf.BF16, y_out=y16[:2000])
+    sf.query(scene, net, med, rows[19000:21000], sf.FP32, y_out=y32[:2000])
+    assert np.all(np.abs(y16[:2000] - y32[:2000]) <= 0.03 * np.maximum(1.0, np.abs(y32[:2000])))
