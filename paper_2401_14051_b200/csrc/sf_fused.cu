@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kWarps = 8;
 #ifndef SF_SORT_MINB
-#define SF_SORT_MINB 3
+#define SF_SORT_MINB 4
 #endif
 constexpr int kMinBlocks = SF_SORT_MINB;  // resident blocks per SM the register budget is sized for
 constexpr int kMaxSegs = 96;
@@ -67,9 +67,9 @@ struct SortDesc {
     int nbuf;                        // scratch buffers (2: one block barrier per group, if 3 blocks/SM still fit)
 };
 
-// Bilinear lookup in a pre-blended phase plane stored as aperture pairs
-// pl[a][h] = {P(a,h), P(a,h+1)}, rows padded to H+1 pairs (no bank aliasing).
-__device__ __forceinline__ float plane_lookup(const float2* pl, int A, int H, float su, float sv, float angle,
+// Bilinear lookup in a pre-blended phase plane pl[a][h] = P(a,h), rows padded to H+1 floats
+// (rows a and a+1 in different banks).
+__device__ __forceinline__ float plane_lookup(const float* pl, int A, int H, float su, float sv, float angle,
                                               float half) {
     float u = fminf(fmaxf(angle, 0.0f), float(kPi)) * su;
     int i0 = min(int(u), A - 2);
@@ -77,15 +77,16 @@ __device__ __forceinline__ float plane_lookup(const float2* pl, int A, int H, fl
     float v = fminf(fmaxf(half, 0.0f), float(kPi)) * sv;
     int j0 = min(int(v), H - 2);
     float s = v - float(j0);
-    const float2 r0 = pl[i0 * (H + 1) + j0];
-    const float2 r1 = pl[(i0 + 1) * (H + 1) + j0];
-    float a = fmaf(s, r0.y - r0.x, r0.x);
-    float b = fmaf(s, r1.y - r1.x, r1.x);
+    const float* p0 = pl + i0 * (H + 1) + j0;
+    const float* p1 = p0 + (H + 1);
+    const float r00 = p0[0], r01 = p0[1], r10 = p1[0], r11 = p1[1];
+    float a = fmaf(s, r01 - r00, r00);
+    float b = fmaf(s, r11 - r10, r10);
     return fmaf(t, b - a, a);
 }
 
 // PhaseTable::lookup (src/phase.cpp:221-230) on the pre-blended planes.
-__device__ __forceinline__ float cap_phase(const float2* planes, const SortDesc& d, float cosine, float half) {
+__device__ __forceinline__ float cap_phase(const float* planes, const SortDesc& d, float cosine, float half) {
     const float angle = acosf(fminf(fmaxf(cosine, -1.0f), 1.0f));
     if (d.n_planes == 1) return d.w[0] * plane_lookup(planes, d.A, d.H, d.su, d.sv, angle, half);  // one lobe / iso
     float f = 0.0f;
@@ -151,7 +152,7 @@ struct __align__(16) QueryCtx {
 
 // Phase feature factor at the query's medium: the scene's pre-blended planes, or the full
 // table at the query's own g (mixed media).
-__device__ __forceinline__ float qphase(const float2* planes, const SortDesc& d, const QueryCtx& q, float cosine,
+__device__ __forceinline__ float qphase(const float* planes, const SortDesc& d, const QueryCtx& q, float cosine,
                                        float half) {
     return d.mixed ? table_phase(d, q.gi, q.gt, cosine, half) : cap_phase(planes, d, cosine, half);
 }
@@ -259,7 +260,7 @@ __device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, c
 
 // Features of template point i (diffuse 0..npts0-1, then highlight).
 __device__ __forceinline__ void point_features(const SceneDev& sc, const TemplateDev& ht, const QueryCtx& q, int i,
-                                               const SortDesc& d, const float2* planes, const float4* __restrict__ pre,
+                                               const SortDesc& d, const float* planes, const float4* __restrict__ pre,
                                                bool same_light, float& rho, float& tr, float& ph) {
     if (i < d.npts0) {
         const float4 p0 = __ldg(pre + 2 * i), p1 = __ldg(pre + 2 * i + 1);  // {offset, half}, {axis, light side}
@@ -299,7 +300,7 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
 // Per-scene diffuse constants: pre[2i] = {offset (voxels), half angle or -1 at the
 // centre}, pre[2i+1] = {unit axis, light-side cap integral for the light of query 0}.
 __device__ __forceinline__ void diffuse_point(const SceneDev& sc, const TemplateDev& dt, const SortDesc& d,
-                                              const float2* __restrict__ planes, const double* __restrict__ queries,
+                                              const float* __restrict__ planes, const double* __restrict__ queries,
                                               int i, float4* __restrict__ pre) {
     const double* qq = dt.pts + 3 * i;
     const double ts = sc.template_scale;
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(kPrepThreads)
     k_query_prep(SceneDev sc, TemplateDev ht, sf_medium_params m, int64_t n, const double* __restrict__ queries,
                  const double* __restrict__ media, double* __restrict__ cfg8, QueryCtx* __restrict__ recs,
                  const int* __restrict__ perm, const double* __restrict__ row0, TemplateDev dt, SortDesc d,
-                 const float2* __restrict__ planes, float4* __restrict__ pre, int diffuse_blocks) {
+                 const float* __restrict__ planes, float4* __restrict__ pre, int diffuse_blocks) {
     if (int(blockIdx.x) < diffuse_blocks) {
         const int i = blockIdx.x * kPrepThreads + threadIdx.x;
         if (i < dt.total) diffuse_point(sc, dt, d, planes, row0, i, pre);
@@ -604,13 +605,13 @@ __device__ __forceinline__ void sort_emit_pair(const float* seg, int cnt, bool u
 }
 
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
-    k_sample_sort(SceneDev sc, TemplateDev ht, SortDesc d, const float2* __restrict__ planes_g,
+    k_sample_sort(SceneDev sc, TemplateDev ht, SortDesc d, const float* __restrict__ planes_g,
                   const float4* __restrict__ pre, int64_t n, const QueryCtx* __restrict__ recs,
                   const float* __restrict__ feats, uint8_t* __restrict__ ops, float* __restrict__ mms, int* err) {
     extern __shared__ __align__(16) float sm[];
-    const int plane_floats = 2 * d.n_planes * d.A * (d.H + 1);
-    float2* planes = reinterpret_cast<float2*>(sm);
-    for (int i = threadIdx.x; i < plane_floats / 2; i += blockDim.x) planes[i] = planes_g[i];
+    const int plane_floats = d.n_planes * d.A * (d.H + 1);
+    float* planes = sm;
+    for (int i = threadIdx.x; i < plane_floats; i += blockDim.x) planes[i] = planes_g[i];
     __shared__ int s_scr[kMaxSegs], s_n[kMaxSegs], s_kf[kMaxSegs];
     __shared__ int64_t s_prefix[kMaxSegs];
     __shared__ uint8_t s_task[2 * kMaxSegs];
@@ -713,20 +714,17 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 }
 
 __global__ void k_blend_planes(const float* __restrict__ T, int G, int A, int H, int n_planes, double g0, double g1,
-                               double g2, float2* __restrict__ out) {
-    const int total = n_planes * A * H;
+                               double g2, float* __restrict__ out) {
+    const int total = n_planes * A * (H + 1);
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-        const int k = idx / (A * H), ah = idx % (A * H), h = ah % H, a = ah / H;
+        const int k = idx / (A * (H + 1)), ah = idx % (A * (H + 1)), h = min(ah % (H + 1), H - 1), a = ah / (H + 1);
         const double g = k == 0 ? g0 : (k == 1 ? g1 : g2);
         int gi;
         double gt;
         table_coord(g, -0.99, 0.99, G, gi, gt);  // PhaseTable::lookup_hg's g axis (src/phase.cpp:196-205)
-        const float* t0 = T + size_t(gi) * A * H + ah;
+        const float* t0 = T + (size_t(gi) * A + a) * H + h;
         const float* t1 = t0 + size_t(A) * H;
-        const int dh = h + 1 < H ? 1 : 0;
-        const float v0 = float((1.0 - gt) * double(t0[0]) + gt * double(t1[0]));
-        const float v1 = float((1.0 - gt) * double(t0[dh]) + gt * double(t1[dh]));
-        out[(k * A + a) * (H + 1) + h] = make_float2(v0, v1);
+        out[idx] = float((1.0 - gt) * double(t0[0]) + gt * double(t1[0]));  // the pad column repeats h = H - 1
     }
 }
 
@@ -796,9 +794,8 @@ void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float
     double g[3] = {0, 0, 0};
     if (m.kind != SF_PHASE_ISOTROPIC)
         for (int k = 0; k < n_planes; ++k) g[k] = m.g[k];
-    int total = n_planes * t.a * t.h;
-    k_blend_planes<<<(total + 255) / 256, 256, 0, s>>>(t.d, t.g, t.a, t.h, n_planes, g[0], g[1], g[2],
-                                                        reinterpret_cast<float2*>(planes));
+    int total = n_planes * t.a * (t.h + 1);
+    k_blend_planes<<<(total + 255) / 256, 256, 0, s>>>(t.d, t.g, t.a, t.h, n_planes, g[0], g[1], g[2], planes);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
@@ -840,7 +837,7 @@ void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_mediu
     k_query_prep<<<unsigned(blocks + diffuse_blocks), kPrepThreads, 0, s>>>(
         sc, ht, m, n, queries, media, cfg8, static_cast<QueryCtx*>(recs), perm, row0 ? row0 : queries,
         dt ? *dt : TemplateDev{}, d,
-        reinterpret_cast<const float2*>(planes), pre, diffuse_blocks);
+        planes, pre, diffuse_blocks);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
@@ -864,7 +861,7 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
         d.w[0] = 1.0f;  // PhaseModel::hg(g): one lobe of weight 1
     }
     auto smem_for = [&](int nbuf) {
-        return size_t(2 * d.n_planes * d.A * (d.H + 1) + nbuf * kWarps * d.scr_floats) * sizeof(float) +
+        return size_t(d.n_planes * d.A * (d.H + 1) + nbuf * kWarps * d.scr_floats) * sizeof(float) +
                2 * kWarps * sizeof(QueryCtx) + 16;
     };
     static const size_t static_smem = [] {
@@ -872,9 +869,12 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
         SFB_CUDA(cudaFuncGetAttributes(&fa, k_sample_sort));
         return fa.sharedSizeBytes;
     }();
-    // 3 blocks/SM (the register limit) within 228 KB, 1 KB reserved per block
-    d.nbuf = kMinBlocks * (smem_for(2) + static_smem + 1024) <= 228 * 1024 ? 2 : 1;
-    if (const char* e = std::getenv("SF_SORT_NBUF")) d.nbuf = std::atoi(e) == 1 ? 1 : d.nbuf;
+    // One scratch buffer (two block barriers per group): a second buffer, where it fits,
+    // measured slower in every configuration tried. SF_SORT_NBUF=2 forces it
+    // when kMinBlocks blocks still fit in 228 KB (1 KB reserved per block).
+    d.nbuf = 1;
+    if (const char* e = std::getenv("SF_SORT_NBUF"))
+        if (std::atoi(e) == 2 && kMinBlocks * (smem_for(2) + static_smem + 1024) <= 228 * 1024) d.nbuf = 2;
     const size_t smem = smem_for(d.nbuf);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
@@ -888,7 +888,7 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
     if (blocks > cap) blocks = cap;
     SceneDev scd = sc ? *sc : SceneDev{};
     TemplateDev htd = ht ? *ht : TemplateDev{1, 0, nullptr, nullptr, 1.0, nullptr};
-    k_sample_sort<<<unsigned(blocks), kWarps * 32, smem, s>>>(scd, htd, d, reinterpret_cast<const float2*>(planes),
+    k_sample_sort<<<unsigned(blocks), kWarps * 32, smem, s>>>(scd, htd, d, planes,
                                                               pre, n, static_cast<const QueryCtx*>(recs), feats,
                                                               ops, mms, err);
     SFB_CUDA(cudaGetLastError());

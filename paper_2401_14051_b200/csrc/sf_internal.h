@@ -124,7 +124,7 @@ struct sf_scene {
     const sf_phase_table* table = nullptr;
     double template_scale = 1.0;
     float2* d_dt = nullptr;  // interleaved {density, transmittance} level-0 volume
-    float* d_planes = nullptr;  // phase table pre-blended at each lobe's g, [n_planes][A][H] float2 pairs
+    float* d_planes = nullptr;  // phase table pre-blended at each lobe's g, [n_planes][A][H + 1] floats
     int n_planes = 0;
     float4* d_dt4 = nullptr;    // x-pair records of the {density, transmittance} volume
     float4* d_pre = nullptr;    // per diffuse point {offset (voxels), half angle}, {unit axis, light side}
