@@ -152,9 +152,10 @@ struct __align__(16) QueryCtx {
 
 // Phase feature factor at the query's medium: the scene's pre-blended planes, or the full
 // table at the query's own g (mixed media).
+template <bool kMixed>
 __device__ __forceinline__ float qphase(const float* planes, const SortDesc& d, const QueryCtx& q, float cosine,
                                        float half) {
-    return d.mixed ? table_phase(d, q.gi, q.gt, cosine, half) : cap_phase(planes, d, cosine, half);
+    return kMixed ? table_phase(d, q.gi, q.gt, cosine, half) : cap_phase(planes, d, cosine, half);
 }
 
 __device__ __forceinline__ void box_bounds(const GridDev& g, const int* base, float* box) {
@@ -259,6 +260,7 @@ __device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, c
 }
 
 // Features of template point i (diffuse 0..npts0-1, then highlight).
+template <bool kMixed>
 __device__ __forceinline__ void point_features(const SceneDev& sc, const TemplateDev& ht, const QueryCtx& q, int i,
                                                const SortDesc& d, const float* planes, const float4* __restrict__ pre,
                                                bool same_light, float& rho, float& tr, float& ph) {
@@ -270,10 +272,10 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
             ph = 1.0f;  // diffuse centre point (src/feature_pipeline.cpp:163-164)
             return;
         }
-        const float fw = qphase(planes, d, q, (q.wf[0] * p1.x + q.wf[1] * p1.y + q.wf[2] * p1.z) * q.iw, p0.w);
+        const float fw = qphase<kMixed>(planes, d, q, (q.wf[0] * p1.x + q.wf[1] * p1.y + q.wf[2] * p1.z) * q.iw, p0.w);
         const float fl = same_light
                              ? p1.w
-                             : qphase(planes, d, q, (q.lf[0] * p1.x + q.lf[1] * p1.y + q.lf[2] * p1.z) * q.il, p0.w);
+                             : qphase<kMixed>(planes, d, q, (q.lf[0] * p1.x + q.lf[1] * p1.y + q.lf[2] * p1.z) * q.il, p0.w);
         ph = fw * fl;
         return;
     }
@@ -293,8 +295,8 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
     const float r = tq.w * q.hs * inv;  // cap / dist, both in voxels
     const float half = r >= 1.0f ? float(kPi) : asinf(r);
     const float ax = dx * inv, ay = dy * inv, az = dz * inv;
-    ph = qphase(planes, d, q, (q.wf[0] * ax + q.wf[1] * ay + q.wf[2] * az) * q.iw, half) *
-         qphase(planes, d, q, (q.lf[0] * ax + q.lf[1] * ay + q.lf[2] * az) * q.il, half);
+    ph = qphase<kMixed>(planes, d, q, (q.wf[0] * ax + q.wf[1] * ay + q.wf[2] * az) * q.iw, half) *
+         qphase<kMixed>(planes, d, q, (q.lf[0] * ax + q.lf[1] * ay + q.lf[2] * az) * q.il, half);
 }
 
 // Per-scene diffuse constants: pre[2i] = {offset (voxels), half angle or -1 at the
@@ -604,6 +606,7 @@ __device__ __forceinline__ void sort_emit_pair(const float* seg, int cnt, bool u
     }
 }
 
+template <bool kMixed>  // per-query g (C4): phase from the full table at the query's g
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     k_sample_sort(SceneDev sc, TemplateDev ht, SortDesc d, const float* __restrict__ planes_g,
                   const float4* __restrict__ pre, int64_t n, const QueryCtx* __restrict__ recs,
@@ -664,7 +667,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
                 const bool same_light = qc.same_light != 0;
                 for (int i = lane; i < d.ntot; i += 32) {
                     float rho, tr, ph;
-                    point_features(sc, ht, qc, i, d, planes, pre, same_light, rho, tr, ph);
+                    point_features<kMixed>(sc, ht, qc, i, d, planes, pre, same_light, rho, tr, ph);
                     scr[i] = rho;
                     scr[d.ntot + i] = tr;
                     scr[2 * d.ntot + i] = ph;
@@ -866,7 +869,7 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
     };
     static const size_t static_smem = [] {
         cudaFuncAttributes fa{};
-        SFB_CUDA(cudaFuncGetAttributes(&fa, k_sample_sort));
+        SFB_CUDA(cudaFuncGetAttributes(&fa, k_sample_sort<true>));
         return fa.sharedSizeBytes;
     }();
     // One scratch buffer (two block barriers per group): a second buffer, where it fits,
@@ -880,7 +883,8 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
     if (smem > 48 * 1024 && smem > attr) {
         // (no carveout preference: the gathers live on L1 hits; forcing the max-shared carveout
         // shrank L1 and cost 25%)
-        SFB_CUDA(cudaFuncSetAttribute(k_sample_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        SFB_CUDA(cudaFuncSetAttribute(k_sample_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        SFB_CUDA(cudaFuncSetAttribute(k_sample_sort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         attr = smem;
     }
     int64_t blocks = d.n_groups;
@@ -888,7 +892,7 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
     if (blocks > cap) blocks = cap;
     SceneDev scd = sc ? *sc : SceneDev{};
     TemplateDev htd = ht ? *ht : TemplateDev{1, 0, nullptr, nullptr, 1.0, nullptr};
-    k_sample_sort<<<unsigned(blocks), kWarps * 32, smem, s>>>(scd, htd, d, planes,
+    (d.mixed ? k_sample_sort<true> : k_sample_sort<false>)<<<unsigned(blocks), kWarps * 32, smem, s>>>(scd, htd, d, planes,
                                                               pre, n, static_cast<const QueryCtx*>(recs), feats,
                                                               ops, mms, err);
     SFB_CUDA(cudaGetLastError());
