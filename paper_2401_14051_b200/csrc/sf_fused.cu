@@ -85,9 +85,28 @@ __device__ __forceinline__ float plane_lookup(const float* pl, int A, int H, flo
     return fmaf(t, b - a, a);
 }
 
+// acos on [-1, 1] for the phase-plane coordinate: sqrt(1 - |x|) P7(|x|) (Abramowitz & Stegun
+// 4.4.46, |error| <= 2e-8 rad) and acos(-x) = pi - acos(x) — 16 instructions where acosf
+// compiles to ~32. The lookup is continuous across cells, so the ~1e-7 rad difference
+// moves the phase feature by ~1e-7 relative, far inside the bf16 rounding it then gets.
+__device__ __forceinline__ float acos_fast(float x) {
+    const float ax = fabsf(x);
+    float p = -0.0012624911f;
+    p = fmaf(p, ax, 0.0066700901f);
+    p = fmaf(p, ax, -0.0170881256f);
+    p = fmaf(p, ax, 0.0308918810f);
+    p = fmaf(p, ax, -0.0501743046f);
+    p = fmaf(p, ax, 0.0889789874f);
+    p = fmaf(p, ax, -0.2145988016f);
+    p = fmaf(p, ax, 1.5707963050f);
+    const float s = fmaxf(1.0f - ax, 1e-30f);
+    const float r = s * rsqrtf(s) * p;
+    return x < 0.0f ? float(kPi) - r : r;
+}
+
 // PhaseTable::lookup (src/phase.cpp:221-230) on the pre-blended planes.
 __device__ __forceinline__ float cap_phase(const float* planes, const SortDesc& d, float cosine, float half) {
-    const float angle = acosf(fminf(fmaxf(cosine, -1.0f), 1.0f));
+    const float angle = acos_fast(fminf(fmaxf(cosine, -1.0f), 1.0f));
     if (d.n_planes == 1) return d.w[0] * plane_lookup(planes, d.A, d.H, d.su, d.sv, angle, half);  // one lobe / iso
     float f = 0.0f;
     for (int k = 0; k < d.n_planes; ++k)
@@ -99,7 +118,7 @@ __device__ __forceinline__ float cap_phase(const float* planes, const SortDesc& 
 // table [G][A][H] in global memory (L1/L2 resident): bilinear in (angle, aperture) on planes
 // gi and gi + 1, then the g lerp. FP32 (bf16 production path only).
 __device__ __forceinline__ float table_phase(const SortDesc& d, int gi, float gt, float cosine, float half) {
-    const float angle = acosf(fminf(fmaxf(cosine, -1.0f), 1.0f));
+    const float angle = acos_fast(fminf(fmaxf(cosine, -1.0f), 1.0f));
     const int A = d.A, H = d.H;
     const float u = fminf(fmaxf(angle, 0.0f), float(kPi)) * d.su;
     const int i0 = min(int(u), A - 2);
