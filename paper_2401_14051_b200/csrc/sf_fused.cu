@@ -522,7 +522,7 @@ __device__ __forceinline__ void emit_chunks(const float* v, int off, int j0, int
 #pragma unroll
             for (int e = 0; e < 8; ++e) v8[e] = row_value<P>(v, off, 8 * jj + e, cnt, mean, mx);
         }
-        store_chunk(o.blk, o.row, jj, o.kf, v8);
+        store_chunk_stream(o.blk, o.row, jj, o.kf, v8);
     }
 }
 

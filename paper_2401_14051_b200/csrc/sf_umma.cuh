@@ -135,6 +135,17 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Streaming variant for operand blocks written to global memory and read back by a later
+// kernel: evict-first in L2, so the stream does not push out what the writer gathers from.
+__device__ __forceinline__ void store_chunk_stream(uint8_t* base, int row, int kchunk, int K, const float* v8) {
+    uint4 u;
+    u.x = pack_bf16(v8[0], v8[1]);
+    u.y = pack_bf16(v8[2], v8[3]);
+    u.z = pack_bf16(v8[4], v8[5]);
+    u.w = pack_bf16(v8[6], v8[7]);
+    __stcs(reinterpret_cast<uint4*>(base + canon_off(row, kchunk * 8, K)), u);
+}
+
 // Chunk `kchunk` (8 consecutive K elements, 16 B) of row `row` of a K-wide operand.
 __device__ __forceinline__ void store_chunk(uint8_t* base, int row, int kchunk, int K, const float* v8) {
     uint4 u;
