@@ -274,8 +274,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         t_last = t_now;                                                     \
     }
 
-    uintptr_t base = (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023);
-    uint8_t* a_att = reinterpret_cast<uint8_t*>(base);  // [128 x 32] o_att operand of FC-1
+    // 1024-byte aligned in the shared window; derived from smem_raw by pointer arithmetic so the
+    // compiler keeps the shared address space (LDS/STS, not generic LD/ST, for every ring read)
+    uint8_t* a_att = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // [128 x 32] o_att of FC-1
     uint8_t* a_od = a_att + kUmmaM * 32 * 2;            // [128 x 32] diffuse stack output (merge, K 0-31)
     uint8_t* a2 = a_od + kUmmaM * 32 * 2;               // [128 x 64] FC-2 / merge (K 32-63) / cross / head
     Ring r;
