@@ -155,7 +155,6 @@ __global__ void k_graded_f32(GridDev g, const float2* __restrict__ xp, double ts
     const double lo[3] = {g.ox, g.oy, g.oz};
     const double hi[3] = {g.hx, g.hy, g.hz};
     const double ts[3] = {tsx, tsy, tsz};
-    const float fnx = float(g.nx) - 0.5f, fny = float(g.ny) - 0.5f, fnz = float(g.nz) - 0.5f;
     for (int idx = i0 + blockIdx.x * blockDim.x + threadIdx.x; idx < i1; idx += gridDim.x * blockDim.x) {
         const int x = idx % g.nx;
         const int y = (idx / g.nx) % g.ny;
@@ -180,8 +179,9 @@ __global__ void k_graded_f32(GridDev g, const float2* __restrict__ xp, double ts
                 for (int i = 0; i < ns; ++i) {
                     const float sf = (float(i) + 0.5f) * hf;
                     const float fx = fmaf(df[0], sf, f0[0]), fy = fmaf(df[1], sf, f0[1]), fz = fmaf(df[2], sf, f0[2]);
-                    // closed box: world in [lo, hi] <=> voxel coordinate in [-0.5, n - 0.5]
-                    if (!(fx >= -0.5f && fx <= fnx && fy >= -0.5f && fy <= fny && fz >= -0.5f && fz <= fnz)) continue;
+                    // No box test: every sample lies strictly inside the closed box (the ray runs from
+                    // a voxel centre to the box exit and the last sample is h/2 before the exit), so
+                    // sample_trilinear's outside branch (0) never applies; the clamps below still do.
                     const float flx = floorf(fx), fly = floorf(fy), flz = floorf(fz);
                     const int x0 = int(flx), y0 = int(fly), z0 = int(flz);
                     float tx = fx - flx;
@@ -189,10 +189,10 @@ __global__ void k_graded_f32(GridDev g, const float2* __restrict__ xp, double ts
                     if (x0 < 0) tx = 0.0f;
                     const int xc = x0 < 0 ? 0 : x0;
                     const int ya = max(y0, 0), yb = min(y0 + 1, g.ny - 1), za = max(z0, 0), zb = min(z0 + 1, g.nz - 1);
-                    const float2 r00 = __ldg(xp + (za * g.ny + ya) * g.nx + xc);
-                    const float2 r10 = __ldg(xp + (za * g.ny + yb) * g.nx + xc);
-                    const float2 r01 = __ldg(xp + (zb * g.ny + ya) * g.nx + xc);
-                    const float2 r11 = __ldg(xp + (zb * g.ny + yb) * g.nx + xc);
+                    const float2* row = xp + ((za * g.ny + ya) * g.nx + xc);
+                    const int dy = (yb - ya) * g.nx, dz = (zb - za) * plane;
+                    const float2 r00 = __ldg(row), r10 = __ldg(row + dy);
+                    const float2 r01 = __ldg(row + dz), r11 = __ldg(row + dz + dy);
                     const float c00 = fmaf(tx, r00.y - r00.x, r00.x), c10 = fmaf(tx, r10.y - r10.x, r10.x);
                     const float c01 = fmaf(tx, r01.y - r01.x, r01.x), c11 = fmaf(tx, r11.y - r11.x, r11.x);
                     const float e0 = fmaf(ty, c10 - c00, c00), e1 = fmaf(ty, c11 - c01, c01);
