@@ -67,9 +67,11 @@ __global__ void k_xpair_f64(const float* __restrict__ v, int nx, int ny, int nz,
 // operations in the same order as sf_device.cuh trilinear(). At x0 = -1 the reference lerps
 // v(0) with itself; the pair at 0 is {v(0), v(1)}, so tx = 0 gives v(0) + 0 * (v(1) - v(0)) =
 // v(0) exactly. At x0 = nx-1 the pair is {v(nx-1), v(nx-1)} as in the reference.
+// The march calls it only at points strictly inside the closed box (a ray from a voxel centre to
+// the box exit, the last sample h/2 before the exit), where the reference's outside test is
+// always false, so the test is left out.
 __device__ __forceinline__ double trilinear_xp(const GridDev& g, const double2* __restrict__ xp, double px,
                                                double py, double pz) {
-    if (!in_box(g, px, py, pz)) return 0.0;
     double fx, fy, fz;
     if (g.ivs != 0.0) {
         fx = (px - g.ox) * g.ivs - 0.5;
@@ -88,8 +90,10 @@ __device__ __forceinline__ double trilinear_xp(const GridDev& g, const double2* 
     const int xc = x0 < 0 ? 0 : x0;
     const int ya = clampi(y0, 0, g.ny - 1), yb = clampi(y0 + 1, 0, g.ny - 1);
     const int za = clampi(z0, 0, g.nz - 1), zb = clampi(z0 + 1, 0, g.nz - 1);
-    const double2 r00 = __ldg(xp + (za * g.ny + ya) * g.nx + xc), r10 = __ldg(xp + (za * g.ny + yb) * g.nx + xc);
-    const double2 r01 = __ldg(xp + (zb * g.ny + ya) * g.nx + xc), r11 = __ldg(xp + (zb * g.ny + yb) * g.nx + xc);
+    const double2* row = xp + ((za * g.ny + ya) * g.nx + xc);
+    const int dy = (yb - ya) * g.nx, dz = (zb - za) * g.nx * g.ny;
+    const double2 r00 = __ldg(row), r10 = __ldg(row + dy);
+    const double2 r01 = __ldg(row + dz), r11 = __ldg(row + dz + dy);
     const double c00 = lerp1(r00.x, r00.y, tx), c10 = lerp1(r10.x, r10.y, tx);
     const double c01 = lerp1(r01.x, r01.y, tx), c11 = lerp1(r11.x, r11.y, tx);
     return lerp1(lerp1(c00, c10, ty), lerp1(c01, c11, ty), tz);
