@@ -260,6 +260,8 @@ struct Kernel27 {
 
 // K3a: conv3_replicate (src/feature_pipeline.cpp:70-92); FP64 accumulation in
 // tap order dz, dy, dx.
+// kFast (production build): the same taps in the same order accumulated in FP32 (fmaf).
+template <bool kFast>
 __global__ void k_conv3(const float* __restrict__ in, int nx, int ny, int nz, Kernel27 k, int zlo, int zhi,
                         float* __restrict__ out) {
     const size_t n = size_t(nx) * ny * zhi;
@@ -269,6 +271,7 @@ __global__ void k_conv3(const float* __restrict__ in, int nx, int ny, int nz, Ke
         int y = int((idx / nx) % ny);
         int z = int(idx / (size_t(nx) * ny));
         double acc = 0.0;
+        float accf = 0.0f;
         int t = 0;
 #pragma unroll
         for (int dz = -1; dz <= 1; ++dz)
@@ -279,9 +282,12 @@ __global__ void k_conv3(const float* __restrict__ in, int nx, int ny, int nz, Ke
                     int sx = clampi(x + dx, 0, nx - 1);
                     int sy = clampi(y + dy, 0, ny - 1);
                     int sz = clampi(z + dz, 0, nz - 1);
-                    acc += double(k.k[t]) * in[(size_t(sz) * ny + sy) * nx + sx];
+                    if (kFast)
+                        accf = fmaf(k.k[t], __ldg(in + (size_t(sz) * ny + sy) * nx + sx), accf);
+                    else
+                        acc += double(k.k[t]) * in[(size_t(sz) * ny + sy) * nx + sx];
                 }
-        out[idx] = float(acc);
+        out[idx] = kFast ? accf : float(acc);
     }
 }
 
@@ -296,6 +302,30 @@ struct Levels {
 // level-0 voxel centre, FP64 trilinear of each convolved level, scaled, then
 // accumulated in float in level order. One pass over all levels per voxel keeps
 // the float accumulation order of the reference while writing the output once.
+// kFast (production build): the level-0 term is the convolved value at the voxel itself (the
+// trilinear at a voxel's own centre has zero weights), coarser levels are interpolated in FP32,
+// and the box test is left out (level-0 centres lie inside every level's box).
+__device__ __forceinline__ float trilinear_f32(const GridDev& g, float fx, float fy, float fz) {
+    const float flx = floorf(fx), fly = floorf(fy), flz = floorf(fz);
+    const int x0 = int(flx), y0 = int(fly), z0 = int(flz);
+    float tx = fx - flx, ty = fy - fly, tz = fz - flz;
+    const int xa = max(x0, 0), xb = min(x0 + 1, g.nx - 1), ya = max(y0, 0), yb = min(y0 + 1, g.ny - 1);
+    const int za = max(z0, 0), zb = min(z0 + 1, g.nz - 1);
+    const float* v = g.v;
+    const int sy = g.nx, sz = g.nx * g.ny;
+    const float c00 = fmaf(tx, __ldg(v + za * sz + ya * sy + xb) - __ldg(v + za * sz + ya * sy + xa),
+                           __ldg(v + za * sz + ya * sy + xa));
+    const float c10 = fmaf(tx, __ldg(v + za * sz + yb * sy + xb) - __ldg(v + za * sz + yb * sy + xa),
+                           __ldg(v + za * sz + yb * sy + xa));
+    const float c01 = fmaf(tx, __ldg(v + zb * sz + ya * sy + xb) - __ldg(v + zb * sz + ya * sy + xa),
+                           __ldg(v + zb * sz + ya * sy + xa));
+    const float c11 = fmaf(tx, __ldg(v + zb * sz + yb * sy + xb) - __ldg(v + zb * sz + yb * sy + xa),
+                           __ldg(v + zb * sz + yb * sy + xa));
+    const float e0 = fmaf(ty, c10 - c00, c00), e1 = fmaf(ty, c11 - c01, c01);
+    return fmaf(tz, e1 - e0, e0);
+}
+
+template <bool kFast>
 __global__ void k_combine(Levels lv, GridDev base, int zlo, int zhi, float* __restrict__ out) {
     const size_t off = size_t(base.nx) * base.ny * zlo;
     const size_t n = size_t(base.nx) * base.ny * zhi;
@@ -304,14 +334,27 @@ __global__ void k_combine(Levels lv, GridDev base, int zlo, int zhi, float* __re
         int x = int(idx % base.nx);
         int y = int((idx / base.nx) % base.ny);
         int z = int(idx / (size_t(base.nx) * base.ny));
-        double c[3] = {base.ox + (x + 0.5) * base.vs, base.oy + (y + 0.5) * base.vs,
-                       base.oz + (z + 0.5) * base.vs};
-        float acc = 0.0f;
-        for (int li = 0; li < lv.n; ++li) {
-            double v = trilinear(lv.g[li], c[0], c[1], c[2]);
-            acc += float(lv.scale[li] * v);
+        if (kFast) {
+            // level li's voxel coordinate of this centre: (x + 0.5) / 2^li - 0.5 (exact in float)
+            float acc = float(lv.scale[0] * double(__ldg(lv.g[0].v + idx)));
+            float inv = 1.0f;
+            for (int li = 1; li < lv.n; ++li) {
+                inv *= 0.5f;
+                const float v = trilinear_f32(lv.g[li], (float(x) + 0.5f) * inv - 0.5f, (float(y) + 0.5f) * inv - 0.5f,
+                                              (float(z) + 0.5f) * inv - 0.5f);
+                acc += float(lv.scale[li]) * v;
+            }
+            out[idx - off] = acc;
+        } else {
+            double c[3] = {base.ox + (x + 0.5) * base.vs, base.oy + (y + 0.5) * base.vs,
+                           base.oz + (z + 0.5) * base.vs};
+            float acc = 0.0f;
+            for (int li = 0; li < lv.n; ++li) {
+                double v = trilinear(lv.g[li], c[0], c[1], c[2]);
+                acc += float(lv.scale[li] * v);
+            }
+            out[idx - off] = acc;
         }
-        out[idx - off] = acc;
     }
 }
 
@@ -426,18 +469,18 @@ void launch_graded(const sf_grid& level, const double ts[3], double coeff, doubl
     SFB_CUDA(cudaFreeAsync(xp, s));
 }
 
-void launch_conv3(const sf_grid& in, const float k27[27], int zlo, int zhi, float* out, cudaStream_t s) {
+void launch_conv3(const sf_grid& in, const float k27[27], int zlo, int zhi, float* out, cudaStream_t s, bool fast) {
     if (zhi <= zlo) return;
     Kernel27 k;
     for (int i = 0; i < 27; ++i) k.k[i] = k27[i];
-    k_conv3<<<grid_for(size_t(in.nx) * in.ny * size_t(zhi - zlo)), kBlock, 0, s>>>(in.d, in.nx, in.ny, in.nz, k, zlo,
-                                                                                   zhi, out);
+    (fast ? k_conv3<true> : k_conv3<false>)<<<grid_for(size_t(in.nx) * in.ny * size_t(zhi - zlo)), kBlock, 0, s>>>(
+        in.d, in.nx, in.ny, in.nz, k, zlo, zhi, out);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
 
 void launch_combine(const std::vector<const sf_grid*>& conv, const std::vector<float>& scales,
-                    const sf_grid& base, int zlo, int zhi, float* out, cudaStream_t s) {
+                    const sf_grid& base, int zlo, int zhi, float* out, cudaStream_t s, bool fast) {
     if (zhi <= zlo) return;
     if (conv.size() > size_t(kMaxLevels)) fail(SF_ERR_INVALID_ARGUMENT, "combine: too many levels");
     Levels lv{};
@@ -446,8 +489,18 @@ void launch_combine(const std::vector<const sf_grid*>& conv, const std::vector<f
         lv.g[i] = conv[size_t(i)]->dev();
         lv.scale[i] = double(scales[size_t(i)]);
     }
-    k_combine<<<grid_for(size_t(base.nx) * base.ny * size_t(zhi - zlo)), kBlock, 0, s>>>(lv, base.dev(), zlo, zhi,
-                                                                                         out);
+    // the fast form needs every level to halve the previous one exactly (pyramid levels do,
+    // down to 1 voxel; an odd size falls back to the FP64 form)
+    bool halving = fast;
+    for (int i = 1; i < lv.n && halving; ++i) {
+        const sf_grid& a = *conv[size_t(i - 1)];
+        const sf_grid& b = *conv[size_t(i)];
+        halving = (a.nx == 2 * b.nx || (a.nx == 1 && b.nx == 1)) && (a.ny == 2 * b.ny || (a.ny == 1 && b.ny == 1)) &&
+                  (a.nz == 2 * b.nz || (a.nz == 1 && b.nz == 1)) && b.vs == 2.0 * a.vs &&
+                  b.origin[0] == a.origin[0] && b.origin[1] == a.origin[1] && b.origin[2] == a.origin[2];
+    }
+    (halving ? k_combine<true> : k_combine<false>)<<<grid_for(size_t(base.nx) * base.ny * size_t(zhi - zlo)), kBlock, 0,
+                                                      s>>>(lv, base.dev(), zlo, zhi, out);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }

@@ -603,7 +603,8 @@ void combiner_weights(int L, const float* kernels, const float* scales, std::vec
 // conv3 of every level (level 0 over rows [c0, c1) only) then the combine of level-0 rows
 // [z0, z1) into out.
 void conv_combine(const std::vector<const sf_grid*>& fields, const std::vector<float>& K,
-                  const std::vector<float>& S, int c0, int c1, int z0, int z1, float* out, cudaStream_t s) {
+                  const std::vector<float>& S, int c0, int c1, int z0, int z1, float* out, cudaStream_t s,
+                  bool fast = false) {
     const sf_grid& base = *fields[0];
     std::vector<sf_grid*> conv;
     try {
@@ -611,10 +612,10 @@ void conv_combine(const std::vector<const sf_grid*>& fields, const std::vector<f
             const sf_grid& f = *fields[l];
             sf_grid* c = new_scratch_grid(f.nx, f.ny, f.nz, f.vs, f.origin, s);
             conv.push_back(c);
-            sfb::launch_conv3(f, &K[l * 27], l == 0 ? c0 : 0, l == 0 ? c1 : f.nz, c->d, s);
+            sfb::launch_conv3(f, &K[l * 27], l == 0 ? c0 : 0, l == 0 ? c1 : f.nz, c->d, s, fast);
         }
         std::vector<const sf_grid*> cv(conv.begin(), conv.end());
-        sfb::launch_combine(cv, S, base, z0, z1, out, s);
+        sfb::launch_combine(cv, S, base, z0, z1, out, s, fast);
         sync(s);
     } catch (...) {
         for (sf_grid* c : conv) free_grid(c);
@@ -624,7 +625,7 @@ void conv_combine(const std::vector<const sf_grid*>& fields, const std::vector<f
 }
 
 sf_tvol* combine(const std::vector<const sf_grid*>& fields, const float* kernels,
-                 const float* scales, const double light[3], cudaStream_t s) {
+                 const float* scales, const double light[3], cudaStream_t s, bool fast = false) {
     if (fields.empty()) fail(SF_ERR_INVALID_ARGUMENT, "combine_transmittance: no fields");
     const sf_grid& base = *fields[0];
     const int L = int(fields.size());
@@ -633,7 +634,7 @@ sf_tvol* combine(const std::vector<const sf_grid*>& fields, const float* kernels
     combiner_weights(L, kernels, scales, t->kernels, t->scales);
     t->values = new_grid(base.nx, base.ny, base.nz, base.vs, base.origin);
     try {
-        conv_combine(fields, t->kernels, t->scales, 0, base.nz, 0, base.nz, t->values->d, s);
+        conv_combine(fields, t->kernels, t->scales, 0, base.nz, 0, base.nz, t->values->d, s, fast);
     } catch (...) {
         free_grid(t->values);
         throw;
@@ -694,7 +695,7 @@ int sf_build_transmittance_volume_ex(const sf_pyramid* p, const double light[3],
                 fields.push_back(graded_level(p, i, light, lambda, step, stream, true, 0, -1, fast));
             }
             std::vector<const sf_grid*> f(fields.begin(), fields.end());
-            *out = combine(f, kernels, scales, light, stream);
+            *out = combine(f, kernels, scales, light, stream, fast);
         } catch (...) {
             for (sf_grid* g : fields) free_grid(g);
             throw;
@@ -733,7 +734,7 @@ int sf_build_transmittance_slab(const sf_pyramid* p, const double light[3], cons
             std::vector<float> K, S;
             combiner_weights(int(fields.size()), kernels, scales, K, S);
             std::vector<const sf_grid*> f(fields.begin(), fields.end());
-            conv_combine(f, K, S, c0, c1, z0, z1, o.d, stream);
+            conv_combine(f, K, S, c0, c1, z0, z1, o.d, stream, fast);
         } catch (...) {
             for (sf_grid* g : fields) free_grid(g);
             throw;

@@ -139,9 +139,11 @@ void launch_pyramid_down(const sf_grid& src, sf_grid& dst, cudaStream_t s);
 // fast: FP32 march (production bf16 path; ~1e-6 relative optical depth) instead of the FP64 reference march
 void launch_graded(const sf_grid& level, const double to_source[3], double coeff, double step, int zlo, int zhi,
                    float* out, cudaStream_t s, bool fast = false);
-void launch_conv3(const sf_grid& in, const float k27[27], int zlo, int zhi, float* out, cudaStream_t s);
+// fast: FP32 accumulation / interpolation (production build), else the reference's FP64.
+void launch_conv3(const sf_grid& in, const float k27[27], int zlo, int zhi, float* out, cudaStream_t s,
+                  bool fast = false);
 void launch_combine(const std::vector<const sf_grid*>& conv, const std::vector<float>& scales,
-                    const sf_grid& base, int zlo, int zhi, float* out, cudaStream_t s);
+                    const sf_grid& base, int zlo, int zhi, float* out, cudaStream_t s, bool fast = false);
 void launch_interleave(const float* density, const float* tvol, float2* out, size_t n,
                        cudaStream_t s);
 void launch_phase_table(int gr, int ar, int hr, const std::vector<double>& nodes,
