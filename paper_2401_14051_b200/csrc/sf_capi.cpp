@@ -1245,8 +1245,8 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             };
             std::vector<Win> wins;
             {
-                const int64_t grid = sfb::sample_sort_grid(), gpt = sfb::kUmmaM / 8;  // 8-query groups per tile
-                const int64_t unit = grid / std::gcd(grid, gpt);  // tiles per whole number of grid rounds
+                const int64_t rq = sfb::sample_sort_round_queries();
+                const int64_t unit = rq / std::gcd(rq, int64_t(sfb::kUmmaM));  // tiles per whole number of rounds
                 static const double first = std::getenv("SF_FIRST_WINDOW") ? std::atof(std::getenv("SF_FIRST_WINDOW"))
                                                                            : 0.2;
                 for (int64_t c0 = 0; c0 < n; c0 += chunk) {

@@ -34,11 +34,14 @@ namespace sfb {
 
 namespace {
 
-constexpr int kWarps = 8;
-#ifndef SF_SORT_MINB
-#define SF_SORT_MINB 4
-#endif
-constexpr int kMinBlocks = SF_SORT_MINB;  // resident blocks per SM the register budget is sized for
+// Block shapes of k_sample_sort: kW queries per group = warps per block, kMinB blocks per SM
+// (64 registers either way, 32 warps per SM). The 32-warp block is preferred (one copy of the
+// phase planes per SM and the largest L1); the 8-warp block is the fallback when its shared
+// memory does not fit (very large templates).
+constexpr int kWBig = 32, kMinBBig = 1, kWSmall = 8, kMinBSmall = 4;
+constexpr int kSortThreadsPerSM = kWBig * 32 * kMinBBig;
+static_assert(kWSmall * 32 * kMinBSmall == kSortThreadsPerSM, "both shapes: one query per warp, 32 warps per SM");
+
 constexpr int kMaxSegs = 96;
 constexpr int kMaxChunks = 512;
 
@@ -625,8 +628,8 @@ __device__ __forceinline__ void sort_emit_pair(const float* seg, int cnt, bool u
     }
 }
 
-template <bool kMixed>  // per-query g (C4): phase from the full table at the query's g
-__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
+template <bool kMixed, int kWarps, int kMinB>  // kMixed: per-query g (C4), phase from the full table
+__global__ void __launch_bounds__(kWarps * 32, kMinB)
     k_sample_sort(SceneDev sc, TemplateDev ht, SortDesc d, const float* __restrict__ planes_g,
                   const float4* __restrict__ pre, int64_t n, const QueryCtx* __restrict__ recs,
                   const float* __restrict__ feats, uint8_t* __restrict__ ops, float* __restrict__ mms, int* err) {
@@ -757,7 +760,7 @@ SortDesc make_desc(const SceneDev* sc, int n_planes, const SortLayout& L, int64_
     d.n_layers = L.n_layers;
     d.n_tiles = int((n + kUmmaM - 1) / kUmmaM);
     d.tile0 = 0;
-    d.n_groups = int64_t(d.n_tiles) * (kUmmaM / kWarps);
+    d.n_groups = 0;  // set by the launcher for the chosen block shape
     d.feat_stride = 3 * int64_t(d.ntot);
     if (sc) {
         d.A = sc->phase.ar;
@@ -832,7 +835,7 @@ void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStr
 
 size_t query_rec_bytes() { return sizeof(QueryCtx); }
 
-int64_t sample_sort_grid() { return int64_t(sm_count()) * kMinBlocks; }
+int64_t sample_sort_round_queries() { return int64_t(sm_count()) * (kSortThreadsPerSM / 32); }
 
 size_t xpair_records(int nx, int ny, int nz) { return size_t((nx + 1) / 2) * ((ny + 1) / 2) * ((nz + 1) / 2) * 8; }
 
@@ -882,38 +885,42 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
         d.table = sc->phase.table;
         d.w[0] = 1.0f;  // PhaseModel::hg(g): one lobe of weight 1
     }
-    auto smem_for = [&](int nbuf) {
-        return size_t(d.n_planes * d.A * (d.H + 1) + nbuf * kWarps * d.scr_floats) * sizeof(float) +
-               2 * kWarps * sizeof(QueryCtx) + 16;
+    auto smem_for = [&](int w, int nbuf) {
+        return size_t(d.n_planes * d.A * (d.H + 1) + size_t(nbuf) * w * d.scr_floats) * sizeof(float) +
+               2 * size_t(w) * sizeof(QueryCtx) + 16;
     };
     static const size_t static_smem = [] {
         cudaFuncAttributes fa{};
-        SFB_CUDA(cudaFuncGetAttributes(&fa, k_sample_sort<true>));
+        SFB_CUDA(cudaFuncGetAttributes(&fa, k_sample_sort<true, kWBig, kMinBBig>));
         return fa.sharedSizeBytes;
     }();
+    // Block shape: 32 warps (one block per SM) when its shared memory fits, else 8 warps x 4.
     // One scratch buffer (two block barriers per group): a second buffer, where it fits,
-    // measured slower in every configuration tried. SF_SORT_NBUF=2 forces it
-    // when kMinBlocks blocks still fit in 228 KB (1 KB reserved per block).
+    // measured slower in every configuration tried; SF_SORT_NBUF=2 forces it
+    // when it fits. SF_SORT_WARPS=8 forces the small shape.
+    static const int force_w = std::getenv("SF_SORT_WARPS") ? std::atoi(std::getenv("SF_SORT_WARPS")) : 0;
+    const size_t budget = 227 * 1024;
+    const bool big = force_w != kWSmall && smem_for(kWBig, 1) + static_smem <= budget;
+    const int w = big ? kWBig : kWSmall, minb = big ? kMinBBig : kMinBSmall;
     d.nbuf = 1;
     if (const char* e = std::getenv("SF_SORT_NBUF"))
-        if (std::atoi(e) == 2 && kMinBlocks * (smem_for(2) + static_smem + 1024) <= 228 * 1024) d.nbuf = 2;
-    const size_t smem = smem_for(d.nbuf);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        // (no carveout preference: the gathers live on L1 hits; forcing the max-shared carveout
-        // shrank L1 and cost 25%)
-        SFB_CUDA(cudaFuncSetAttribute(k_sample_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        SFB_CUDA(cudaFuncSetAttribute(k_sample_sort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        attr = smem;
-    }
+        if (std::atoi(e) == 2 && minb * (smem_for(w, 2) + static_smem + 1024) <= 228 * 1024) d.nbuf = 2;
+    const size_t smem = smem_for(w, d.nbuf);
+    if (smem + static_smem > budget) fail(SF_ERR_INVALID_ARGUMENT, "sample_sort: templates too large for shared memory");
+    auto kern = big ? (d.mixed ? k_sample_sort<true, kWBig, kMinBBig> : k_sample_sort<false, kWBig, kMinBBig>)
+                    : (d.mixed ? k_sample_sort<true, kWSmall, kMinBSmall> : k_sample_sort<false, kWSmall, kMinBSmall>);
+    if (smem > 48 * 1024)
+        // (no carveout preference: the driver's choice from the occupancy need is the fastest)
+        SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const int64_t window_tiles = (n + kUmmaM - 1) / kUmmaM;
+    d.n_groups = window_tiles * (kUmmaM / w);
     int64_t blocks = d.n_groups;
-    int64_t cap = sample_sort_grid();
+    const int64_t cap = int64_t(sm_count()) * minb;
     if (blocks > cap) blocks = cap;
     SceneDev scd = sc ? *sc : SceneDev{};
     TemplateDev htd = ht ? *ht : TemplateDev{1, 0, nullptr, nullptr, 1.0, nullptr};
-    (d.mixed ? k_sample_sort<true> : k_sample_sort<false>)<<<unsigned(blocks), kWarps * 32, smem, s>>>(scd, htd, d, planes,
-                                                              pre, n, static_cast<const QueryCtx*>(recs), feats,
-                                                              ops, mms, err);
+    kern<<<unsigned(blocks), w * 32, smem, s>>>(scd, htd, d, planes, pre, n, static_cast<const QueryCtx*>(recs), feats,
+                                                ops, mms, err);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }

@@ -225,9 +225,9 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
                         int64_t layout_tiles = 0);
 // layout_tiles > 0: this launch fills tiles [tile0, tile0 + ceil(n / 128)) of an operand /
 // pool layout of layout_tiles tiles (one backbone launch over several sampling launches).
-// Persistent grid of the sampling kernel (blocks): a window of a multiple of
-// grid * 8 queries has no partial last round.
-int64_t sample_sort_grid();
+// Queries the persistent sampling grid processes per round (one per warp, every SM full):
+// a window of a multiple of this many queries has no partial last round.
+int64_t sample_sort_round_queries();
 // Per-query context records (sampling bases, highlight frame) + make_config rows.
 size_t query_rec_bytes();
 // perm (optional): processing row q reads the caller's row perm[q] (locality reordering)
