@@ -42,7 +42,7 @@ constexpr int kWBig = 32, kMinBBig = 1, kWSmall = 8, kMinBSmall = 4;
 constexpr int kSortThreadsPerSM = kWBig * 32 * kMinBBig;
 static_assert(kWSmall * 32 * kMinBSmall == kSortThreadsPerSM, "both shapes: one query per warp, 32 warps per SM");
 
-constexpr int kMaxSegs = 96;
+constexpr int kMaxSegs = 72;  // (kind, layer, tau) segments: 24 template layers
 constexpr int kMaxChunks = 512;
 
 struct SortDesc {
@@ -638,13 +638,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
     float* planes = sm;
     for (int i = threadIdx.x; i < plane_floats; i += blockDim.x) planes[i] = planes_g[i];
     __shared__ int s_scr[kMaxSegs], s_n[kMaxSegs], s_kf[kMaxSegs];
-    __shared__ int64_t s_prefix[kMaxSegs];
+    __shared__ int s_prefix[kMaxSegs];  // bytes per tile before the segment's block (< 2^31)
     __shared__ uint8_t s_task[2 * kMaxSegs];
     for (int i = threadIdx.x; i < d.n_segs; i += blockDim.x) {
         s_scr[i] = d.seg_scr[i];
         s_n[i] = d.seg_n[i];
         s_kf[i] = d.seg_kf[i];
-        s_prefix[i] = d.seg_prefix[i];
+        s_prefix[i] = int(d.seg_prefix[i]);
     }
     for (int i = threadIdx.x; i < d.n_tasks; i += blockDim.x) s_task[i] = d.task_seg[i];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
             const int w = pair ? (t % (2 * kWarps)) >> 1 : t % kWarps;
             SegOut o;
             o.kf = s_kf[sg];
-            o.blk = ops + s_prefix[sg] * d.n_tiles + tile * (int64_t(kUmmaM) * o.kf * 2);
+            o.blk = ops + int64_t(s_prefix[sg]) * d.n_tiles + tile * (int64_t(kUmmaM) * o.kf * 2);
             o.row = row0 + w;
             o.tau = sg % 3;
             o.mm = mms + (int64_t(sg / 3) * q_pad + qg0 + q0 + w) * 8;
