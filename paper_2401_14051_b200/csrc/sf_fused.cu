@@ -242,8 +242,10 @@ __device__ __forceinline__ void query_ctx(const SceneDev& sc, const TemplateDev&
 __device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, const float* box, const float* f,
                                           float& rho, float& tr) {
     const GridDev& g = sc.grid;
-    if (!(f[0] >= box[0] && f[0] <= box[1] && f[1] >= box[2] && f[1] <= box[3] && f[2] >= box[4] &&
-          f[2] <= box[5])) {
+    // non-short-circuit: one predicate chain instead of six compare-and-branch pairs
+    const bool inside = (f[0] >= box[0]) & (f[0] <= box[1]) & (f[1] >= box[2]) & (f[1] <= box[3]) &
+                        (f[2] >= box[4]) & (f[2] <= box[5]);
+    if (!inside) {
         rho = 0.0f;
         tr = 1.0f;
         return;
@@ -261,13 +263,17 @@ __device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, c
     // share one 128-byte line when y0 and z0 are even, two or four otherwise (x-fastest: four)
     const int y1 = max(min(i0[1] + 1, g.ny - 1), 0), z1 = max(min(i0[2] + 1, g.nz - 1), 0);
     const int x0 = max(i0[0], 0), y0 = max(i0[1], 0), z0 = max(i0[2], 0);
-    const int sxh = ((g.nx + 1) >> 1) << 3, szh = ((g.ny + 1) >> 1) * sxh;  // 32-bit (< 2^31 voxels)
-    const int bx = ((x0 >> 1) << 3) + (x0 & 1);
-    const int ry0 = (y0 >> 1) * sxh + ((y0 & 1) << 1), ry1 = (y1 >> 1) * sxh + ((y1 & 1) << 1);
-    const int rz0 = (z0 >> 1) * szh + ((z0 & 1) << 2) + bx, rz1 = (z1 >> 1) * szh + ((z1 & 1) << 2) + bx;
+    // record indices as unsigned 32-bit sums (< 2^31 records): one IMAD.WIDE.U32 per address
+    // instead of a sign-extended 64-bit add chain per load
+    const uint32_t sxh = uint32_t((g.nx + 1) >> 1) << 3, szh = uint32_t((g.ny + 1) >> 1) * sxh;
+    const uint32_t bx = (uint32_t(x0 >> 1) << 3) + uint32_t(x0 & 1);
+    const uint32_t ry0 = uint32_t(y0 >> 1) * sxh + (uint32_t(y0 & 1) << 1);
+    const uint32_t ry1 = uint32_t(y1 >> 1) * sxh + (uint32_t(y1 & 1) << 1);
+    const uint32_t rz0 = uint32_t(z0 >> 1) * szh + (uint32_t(z0 & 1) << 2) + bx;
+    const uint32_t rz1 = uint32_t(z1 >> 1) * szh + (uint32_t(z1 & 1) << 2) + bx;
     const float4* v = sc.dt4;
-    const float4 r00 = __ldg(v + rz0 + ry0), r10 = __ldg(v + rz0 + ry1);
-    const float4 r01 = __ldg(v + rz1 + ry0), r11 = __ldg(v + rz1 + ry1);
+    const float4 r00 = __ldg(v + (rz0 + ry0)), r10 = __ldg(v + (rz0 + ry1));
+    const float4 r01 = __ldg(v + (rz1 + ry0)), r11 = __ldg(v + (rz1 + ry1));
     float c00 = fmaf(t[0], r00.z - r00.x, r00.x), c10 = fmaf(t[0], r10.z - r10.x, r10.x);
     float c01 = fmaf(t[0], r01.z - r01.x, r01.x), c11 = fmaf(t[0], r11.z - r11.x, r11.x);
     float e0 = fmaf(t[1], c10 - c00, c00), e1 = fmaf(t[1], c11 - c01, c01);
