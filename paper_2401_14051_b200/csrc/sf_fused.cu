@@ -232,6 +232,10 @@ __device__ __forceinline__ void query_ctx(const SceneDev& sc, const TemplateDev&
     q.hs = float(len / ht.gen_distance * ivs);
     box_bounds(g, q.pb, q.pbox);
     box_bounds(g, q.eb, q.ebox);
+    for (int i = 0; i < 3; ++i) {  // bases in the padded record coordinates (voxel + 1), see k_xpair
+        ++q.pb[i];
+        ++q.eb[i];
+    }
 }
 
 // {density, transmittance} at voxel coordinate base + frac: 0 / 1 outside the box
@@ -250,27 +254,24 @@ __device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, c
         tr = 1.0f;
         return;
     }
-    int i0[3];
+    // padded record coordinates (voxel + 1, edges replicated: see k_xpair) need no clamps: a
+    // clamped corner reads a record equal to its neighbour, so a + t (b - a) = a exactly
+    uint32_t i0[3];
     float t[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const float fl = floorf(f[c]);
-        i0[c] = base[c] + int(fl);
+        i0[c] = uint32_t(base[c] + int(fl));
         t[c] = f[c] - fl;
     }
-    if (i0[0] < 0) t[0] = 0.0f;
-    // corner records in the 2x2x2 mini-brick layout (xpair_rec): the four (y, z) rows of a cell
-    // share one 128-byte line when y0 and z0 are even, two or four otherwise (x-fastest: four)
-    const int y1 = max(min(i0[1] + 1, g.ny - 1), 0), z1 = max(min(i0[2] + 1, g.nz - 1), 0);
-    const int x0 = max(i0[0], 0), y0 = max(i0[1], 0), z0 = max(i0[2], 0);
-    // record indices as unsigned 32-bit sums (< 2^31 records): one IMAD.WIDE.U32 per address
-    // instead of a sign-extended 64-bit add chain per load
-    const uint32_t sxh = uint32_t((g.nx + 1) >> 1) << 3, szh = uint32_t((g.ny + 1) >> 1) * sxh;
-    const uint32_t bx = (uint32_t(x0 >> 1) << 3) + uint32_t(x0 & 1);
-    const uint32_t ry0 = uint32_t(y0 >> 1) * sxh + (uint32_t(y0 & 1) << 1);
-    const uint32_t ry1 = uint32_t(y1 >> 1) * sxh + (uint32_t(y1 & 1) << 1);
-    const uint32_t rz0 = uint32_t(z0 >> 1) * szh + (uint32_t(z0 & 1) << 2) + bx;
-    const uint32_t rz1 = uint32_t(z1 >> 1) * szh + (uint32_t(z1 & 1) << 2) + bx;
+    // corner records in the 2x2x2 mini-brick layout: the four (y, z) rows of a cell share one
+    // 128-byte line when y0 and z0 are even, two or four otherwise; record indices as unsigned
+    // 32-bit sums (< 2^31 records): one IMAD.WIDE.U32 per address
+    const uint32_t sxh = g.rec_sx, szh = g.rec_sz;
+    const uint32_t x0 = i0[0], y0 = i0[1], z0 = i0[2], y1 = y0 + 1, z1 = z0 + 1;
+    const uint32_t bx = ((x0 >> 1) << 3) + (x0 & 1);
+    const uint32_t ry0 = (y0 >> 1) * sxh + ((y0 & 1) << 1), ry1 = (y1 >> 1) * sxh + ((y1 & 1) << 1);
+    const uint32_t rz0 = (z0 >> 1) * szh + ((z0 & 1) << 2) + bx, rz1 = (z1 >> 1) * szh + ((z1 & 1) << 2) + bx;
     const float4* v = sc.dt4;
     const float4 r00 = __ldg(v + (rz0 + ry0)), r10 = __ldg(v + (rz0 + ry1));
     const float4 r01 = __ldg(v + (rz1 + ry0)), r11 = __ldg(v + (rz1 + ry1));
@@ -431,18 +432,25 @@ __global__ void k_morton(GridDev g, int64_t n, const double* __restrict__ querie
     }
 }
 
-// x-pair record {rho, T}(x), {rho, T}(min(x + 1, nx - 1)) of voxel (x, y, z), stored in 2x2x2
-// mini-bricks of 8 records (one 128-byte line): brick (x/2, y/2, z/2) x-fastest, record
-// (z&1, y&1, x&1) inside. A trilinear cell's four corner rows then touch 1-4 lines (2.25 on
-// average) instead of 4.
+// x-pair record {rho, T}(x), {rho, T}(x + 1) of padded voxel (x, y, z) = voxel (x-1, y-1, z-1)
+// with every coordinate clamped to the grid (edge replication: record x' in [0, nx], y' in
+// [0, ny + 1], z' in [0, nz + 1]). The clamp-to-edge corners of sample_trilinear
+// (src/volume_grid.cpp:45-56) then read the replicated records, so the sampler has no clamps.
+// Stored in 2x2x2 mini-bricks of 8 records (one 128-byte line): brick (x/2, y/2, z/2)
+// x-fastest, record (z&1, y&1, x&1) inside. A trilinear cell's four corner rows then touch 1-4
+// lines (2.25 on average) instead of 4.
 __global__ void k_xpair(const float2* __restrict__ v, int nx, int ny, int nz, float4* __restrict__ out) {
-    const size_t n = size_t(nx) * ny * nz;
-    const int sxh = ((nx + 1) >> 1) << 3, szh = ((ny + 1) >> 1) * sxh;
+    const int px = nx + 1, py = ny + 2, pz = nz + 2;
+    const size_t n = size_t(px) * py * pz;
+    const size_t sxh = size_t((px + 1) >> 1) << 3, szh = size_t((py + 1) >> 1) * sxh;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
-        const int x = int(i % nx), y = int((i / nx) % ny), z = int(i / (size_t(nx) * ny));
-        const float2 a = v[i], b = v[x + 1 < nx ? i + 1 : i];
+        const int x = int(i % px), y = int((i / px) % py), z = int(i / (size_t(px) * py));
+        const int cx0 = min(max(x - 1, 0), nx - 1), cx1 = min(x, nx - 1);
+        const int cy = min(max(y - 1, 0), ny - 1), cz = min(max(z - 1, 0), nz - 1);
+        const size_t row = (size_t(cz) * ny + cy) * nx;
+        const float2 a = v[row + cx0], b = v[row + cx1];
         const size_t rec = size_t(z >> 1) * szh + ((z & 1) << 2) + size_t(y >> 1) * sxh + ((y & 1) << 1) +
-                           ((x >> 1) << 3) + (x & 1);
+                           (size_t(x >> 1) << 3) + (x & 1);
         out[rec] = make_float4(a.x, a.y, b.x, b.y);
     }
 }
@@ -832,7 +840,7 @@ void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float
 }
 
 void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStream_t s) {
-    const size_t n = size_t(nx) * ny * nz;
+    const size_t n = size_t(nx + 1) * (ny + 2) * (nz + 2);
     k_xpair<<<unsigned(std::min<size_t>((n + 255) / 256, size_t(sm_count()) * 32)), 256, 0, s>>>(dt, nx, ny, nz,
                                                                                                  out);
     SFB_CUDA(cudaGetLastError());
@@ -843,7 +851,8 @@ size_t query_rec_bytes() { return sizeof(QueryCtx); }
 
 int64_t sample_sort_round_queries() { return int64_t(sm_count()) * (kSortThreadsPerSM / 32); }
 
-size_t xpair_records(int nx, int ny, int nz) { return size_t((nx + 1) / 2) * ((ny + 1) / 2) * ((nz + 1) / 2) * 8; }
+// padded dims (nx + 1, ny + 2, nz + 2) rounded up to whole bricks
+size_t xpair_records(int nx, int ny, int nz) { return size_t((nx + 2) / 2) * ((ny + 3) / 2) * ((nz + 3) / 2) * 8; }
 
 void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t* keys, int* idx, cudaStream_t s) {
     if (n <= 0) return;

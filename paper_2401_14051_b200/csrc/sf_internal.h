@@ -64,7 +64,8 @@ struct sf_grid {
         int e;
         double ivs = std::frexp(vs, &e) == 0.5 ? 1.0 / vs : 0.0;
         return sfb::GridDev{d,         nx,        ny,    nz,    vs,    origin[0],
-                            origin[1], origin[2], hi[0], hi[1], hi[2], ivs};
+                            origin[1], origin[2], hi[0], hi[1], hi[2], ivs,
+                            uint32_t((nx + 2) >> 1) << 3, uint32_t((ny + 3) >> 1) * (uint32_t((nx + 2) >> 1) << 3)};
     }
 };
 
