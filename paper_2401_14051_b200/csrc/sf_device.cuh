@@ -25,7 +25,8 @@ struct GridDev {
     double ox, oy, oz;
     double hx, hy, hz;
     double ivs;  // 1/vs when vs is a power of two (x/vs == x*ivs exactly), else 0
-    // strides of the padded x-pair record layout (k_xpair): records per brick row / brick slab
+    // strides of the padded xy-quad record layout (k_xpair), in 32-byte records: per y row / per
+    // z brick slab
     uint32_t rec_sx, rec_sz;
 };
 

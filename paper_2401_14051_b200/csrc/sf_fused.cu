@@ -238,6 +238,14 @@ __device__ __forceinline__ void query_ctx(const SceneDev& sc, const TemplateDev&
     }
 }
 
+// 256-bit read-only load (sm_100: LDG.E.ENL2.256): one L1 wavefront per distinct line for
+// the whole 32-byte record instead of one per 16-byte half
+__device__ __forceinline__ void ld_nc_256(const float4* p, float4& a, float4& b) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
+}
+
 // {density, transmittance} at voxel coordinate base + frac: 0 / 1 outside the box
 // (sample_trilinear + TransmittanceFeatureVolume::sample), else trilinear over
 // x-pair records with the clamp-to-edge cell of src/volume_grid.cpp:45-56.
@@ -264,17 +272,15 @@ __device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, c
         i0[c] = uint32_t(base[c] + int(fl));
         t[c] = f[c] - fl;
     }
-    // corner records in the 2x2x2 mini-brick layout: the four (y, z) rows of a cell share one
-    // 128-byte line when y0 and z0 are even, two or four otherwise; record indices as unsigned
-    // 32-bit sums (< 2^31 records): one IMAD.WIDE.U32 per address
-    const uint32_t sxh = g.rec_sx, szh = g.rec_sz;
-    const uint32_t x0 = i0[0], y0 = i0[1], z0 = i0[2], y1 = y0 + 1, z1 = z0 + 1;
-    const uint32_t bx = ((x0 >> 1) << 3) + (x0 & 1);
-    const uint32_t ry0 = (y0 >> 1) * sxh + ((y0 & 1) << 1), ry1 = (y1 >> 1) * sxh + ((y1 & 1) << 1);
-    const uint32_t rz0 = (z0 >> 1) * szh + ((z0 & 1) << 2) + bx, rz1 = (z1 >> 1) * szh + ((z1 & 1) << 2) + bx;
+    // the cell's two xy-quad records (z0 and z0 + 1), one 256-bit load each; record indices as
+    // unsigned 32-bit sums (< 2^31 records): one IMAD.WIDE.U32 per address
+    const uint32_t x0 = i0[0], z0 = i0[2], z1 = z0 + 1;
+    const uint32_t b = ((x0 >> 1) << 2) + (x0 & 1) + i0[1] * g.rec_sx;
+    const uint32_t ra = (z0 >> 1) * g.rec_sz + ((z0 & 1) << 1) + b, rb = (z1 >> 1) * g.rec_sz + ((z1 & 1) << 1) + b;
     const float4* v = sc.dt4;
-    const float4 r00 = __ldg(v + (rz0 + ry0)), r10 = __ldg(v + (rz0 + ry1));
-    const float4 r01 = __ldg(v + (rz1 + ry0)), r11 = __ldg(v + (rz1 + ry1));
+    float4 r00, r10, r01, r11;  // r<y><z>: {rho, T}(x0), {rho, T}(x0 + 1) of row (y, z)
+    ld_nc_256(v + 2 * size_t(ra), r00, r10);
+    ld_nc_256(v + 2 * size_t(rb), r01, r11);
     float c00 = fmaf(t[0], r00.z - r00.x, r00.x), c10 = fmaf(t[0], r10.z - r10.x, r10.x);
     float c01 = fmaf(t[0], r01.z - r01.x, r01.x), c11 = fmaf(t[0], r11.z - r11.x, r11.x);
     float e0 = fmaf(t[1], c10 - c00, c00), e1 = fmaf(t[1], c11 - c01, c01);
@@ -432,26 +438,27 @@ __global__ void k_morton(GridDev g, int64_t n, const double* __restrict__ querie
     }
 }
 
-// x-pair record {rho, T}(x), {rho, T}(x + 1) of padded voxel (x, y, z) = voxel (x-1, y-1, z-1)
-// with every coordinate clamped to the grid (edge replication: record x' in [0, nx], y' in
-// [0, ny + 1], z' in [0, nz + 1]). The clamp-to-edge corners of sample_trilinear
-// (src/volume_grid.cpp:45-56) then read the replicated records, so the sampler has no clamps.
-// Stored in 2x2x2 mini-bricks of 8 records (one 128-byte line): brick (x/2, y/2, z/2)
-// x-fastest, record (z&1, y&1, x&1) inside. A trilinear cell's four corner rows then touch 1-4
-// lines (2.25 on average) instead of 4.
+// xy-quad record of padded voxel (x, y, z) = voxel (x-1, y-1, z-1) with every coordinate
+// clamped to the grid (edge replication; x in [0, nx], y in [0, ny], z in [0, nz + 1]):
+// 32 bytes {rho, T}(x, y), {rho, T}(x+1, y), {rho, T}(x, y+1), {rho, T}(x+1, y+1) at z. The
+// clamp-to-edge corners of sample_trilinear (src/volume_grid.cpp:45-56) then read replicated
+// values, so the sampler has no clamps, and a trilinear cell is two 256-bit loads (z0, z0+1).
+// Four records share a 128-byte line as a 2x1x2 (x, y, z) brick: a cell's two records are in
+// one line when z0 is even. Index ((z/2 * PY + y) * XH + x/2) * 4 + (z&1) * 2 + (x&1).
 __global__ void k_xpair(const float2* __restrict__ v, int nx, int ny, int nz, float4* __restrict__ out) {
-    const int px = nx + 1, py = ny + 2, pz = nz + 2;
+    const int px = nx + 1, py = ny + 1, pz = nz + 2;
     const size_t n = size_t(px) * py * pz;
-    const size_t sxh = size_t((px + 1) >> 1) << 3, szh = size_t((py + 1) >> 1) * sxh;
+    const size_t sx = size_t((px + 1) >> 1) << 2, sz = size_t(py) * sx;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
         const int x = int(i % px), y = int((i / px) % py), z = int(i / (size_t(px) * py));
         const int cx0 = min(max(x - 1, 0), nx - 1), cx1 = min(x, nx - 1);
-        const int cy = min(max(y - 1, 0), ny - 1), cz = min(max(z - 1, 0), nz - 1);
-        const size_t row = (size_t(cz) * ny + cy) * nx;
-        const float2 a = v[row + cx0], b = v[row + cx1];
-        const size_t rec = size_t(z >> 1) * szh + ((z & 1) << 2) + size_t(y >> 1) * sxh + ((y & 1) << 1) +
-                           (size_t(x >> 1) << 3) + (x & 1);
-        out[rec] = make_float4(a.x, a.y, b.x, b.y);
+        const int cy0 = min(max(y - 1, 0), ny - 1), cy1 = min(y, ny - 1);
+        const int cz = min(max(z - 1, 0), nz - 1);
+        const size_t r0 = (size_t(cz) * ny + cy0) * nx, r1 = (size_t(cz) * ny + cy1) * nx;
+        const float2 a = v[r0 + cx0], b = v[r0 + cx1], c = v[r1 + cx0], d = v[r1 + cx1];
+        const size_t rec = size_t(z >> 1) * sz + size_t(y) * sx + (size_t(x >> 1) << 2) + ((z & 1) << 1) + (x & 1);
+        out[2 * rec] = make_float4(a.x, a.y, b.x, b.y);
+        out[2 * rec + 1] = make_float4(c.x, c.y, d.x, d.y);
     }
 }
 
@@ -840,7 +847,7 @@ void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float
 }
 
 void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStream_t s) {
-    const size_t n = size_t(nx + 1) * (ny + 2) * (nz + 2);
+    const size_t n = size_t(nx + 1) * (ny + 1) * (nz + 2);
     k_xpair<<<unsigned(std::min<size_t>((n + 255) / 256, size_t(sm_count()) * 32)), 256, 0, s>>>(dt, nx, ny, nz,
                                                                                                  out);
     SFB_CUDA(cudaGetLastError());
@@ -851,8 +858,11 @@ size_t query_rec_bytes() { return sizeof(QueryCtx); }
 
 int64_t sample_sort_round_queries() { return int64_t(sm_count()) * (kSortThreadsPerSM / 32); }
 
-// padded dims (nx + 1, ny + 2, nz + 2) rounded up to whole bricks
-size_t xpair_records(int nx, int ny, int nz) { return size_t((nx + 2) / 2) * ((ny + 3) / 2) * ((nz + 3) / 2) * 8; }
+// float4 units of the xy-quad layout: padded dims (nx + 1, ny + 1, nz + 2) in whole 2x1x2
+// bricks, two float4 per record
+size_t xpair_records(int nx, int ny, int nz) {
+    return size_t((nx + 2) / 2) * size_t(ny + 1) * ((nz + 3) / 2) * 4 * 2;
+}
 
 void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t* keys, int* idx, cudaStream_t s) {
     if (n <= 0) return;

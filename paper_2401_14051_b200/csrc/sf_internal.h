@@ -65,7 +65,7 @@ struct sf_grid {
         double ivs = std::frexp(vs, &e) == 0.5 ? 1.0 / vs : 0.0;
         return sfb::GridDev{d,         nx,        ny,    nz,    vs,    origin[0],
                             origin[1], origin[2], hi[0], hi[1], hi[2], ivs,
-                            uint32_t((nx + 2) >> 1) << 3, uint32_t((ny + 3) >> 1) * (uint32_t((nx + 2) >> 1) << 3)};
+                            uint32_t((nx + 2) >> 1) << 2, uint32_t(ny + 1) * (uint32_t((nx + 2) >> 1) << 2)};
     }
 };
 
@@ -127,7 +127,7 @@ struct sf_scene {
     float2* d_dt = nullptr;  // interleaved {density, transmittance} level-0 volume
     float* d_planes = nullptr;  // phase table pre-blended at each lobe's g, [n_planes][A][H + 1] floats
     int n_planes = 0;
-    float4* d_dt4 = nullptr;    // x-pair records of the {density, transmittance} volume
+    float4* d_dt4 = nullptr;    // xy-quad records of the {density, transmittance} volume (k_xpair)
     float4* d_pre = nullptr;    // per diffuse point {offset (voxels), half angle}, {unit axis, light side}
 };
 
@@ -161,7 +161,7 @@ void launch_place_template(const sf_template& t, int64_t n, const double* p,
 struct SceneDev {
     GridDev grid;          // density geometry (v = density)
     const float2* dt;      // interleaved {density, tvol}
-    const float4* dt4;     // x-pair records {rho(x), T(x), rho(x+1), T(x+1)} (fused path)
+    const float4* dt4;     // xy-quad records, two float4 each (k_xpair; fused path)
     const float* tvol;     // plain tvol (when dt == nullptr)
     PhaseDev phase;
     double template_scale;
@@ -242,7 +242,7 @@ void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_mediu
 // Morton keys of the queries' positions in the grid box + identity indices (for cub sort)
 void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t* keys, int* idx, cudaStream_t s);
 void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStream_t s);
-size_t xpair_records(int nx, int ny, int nz);  // records of the mini-brick x-pair layout (padded dims)
+size_t xpair_records(int nx, int ny, int nz);  // float4 units of the padded xy-quad record layout
 // Pre-blended phase planes: for each lobe, the table interpolated at that lobe's g
 // (PhaseTable::lookup_hg's g axis, src/phase.cpp:191-219), [n_lobes][angle][aperture].
 void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float* planes,
