@@ -275,6 +275,10 @@ int64_t sf_launch_count(void);
  * 2 FC-1 MMA, 3 FC-1 epilogue, 4 bundle wait FC-2, 5 FC-2 MMA, 6 FC-2 epilogue,
  * 7 other, 8 total); reading resets them. */
 int sf_debug_tc_profile(uint64_t out[16]);
+/* Diagnostics (no reference counterpart): L2 read bandwidth in GB/s of 32-byte loads (the
+ * sampler's gather width) streaming `reps` times over an L2-resident buffer of `bytes`;
+ * bench.py reports the sampling kernel's roofline against it next to the HBM figure. */
+int sf_probe_l2_read(size_t bytes, int reps, double* gbs);
 
 #ifdef __cplusplus
 }

@@ -102,6 +102,7 @@ _SIGS = {
     "sf_host_alloc": (I, [C.c_size_t, PP]),
     "sf_host_free": (I, [P]),
     "sf_debug_tc_profile": (I, [P]),
+    "sf_probe_l2_read": (I, [C.c_size_t, I, P]),
 }
 
 STAGES = ("config", "features_diffuse", "features_highlight", "slice", "backbone", "sample_sort")

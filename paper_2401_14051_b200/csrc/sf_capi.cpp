@@ -1622,6 +1622,13 @@ int sf_host_free(void* p) {
 
 int64_t sf_launch_count(void) { return g_launches.load(); }
 
+int sf_probe_l2_read(size_t bytes, int reps, double* gbs) {
+    return guard([&] {
+        if (!gbs || bytes < 4096 || reps < 1) fail(SF_ERR_INVALID_ARGUMENT, "sf_probe_l2_read: bad arguments");
+        *gbs = sfb::probe_l2_read_gbs(bytes, reps);
+    });
+}
+
 int sf_debug_tc_profile(uint64_t out[16]) {
     return guard([&] {
         unsigned long long v[16];

@@ -858,6 +858,47 @@ size_t query_rec_bytes() { return sizeof(QueryCtx); }
 
 int64_t sample_sort_round_queries() { return int64_t(sm_count()) * (kSortThreadsPerSM / 32); }
 
+// L2 read-bandwidth probe for the sampler's roofline (bench.py): every thread streams 32-byte
+// records (the sampler's load width) over an L2-resident buffer, `reps` passes.
+__global__ void k_l2_probe(const float4* __restrict__ buf, size_t n32, int reps, float* __restrict__ sink) {
+    float acc = 0.0f;
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (int r = 0; r < reps; ++r)
+        for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n32; i += stride) {
+            float4 a, b;
+            ld_nc_256(buf + 2 * i, a, b);
+            acc += a.x + b.w;
+        }
+    if (acc == 1.2345f) sink[0] = acc;  // never true for the zeroed buffer; keeps the loads live
+}
+
+double probe_l2_read_gbs(size_t bytes, int reps) {
+    const size_t n32 = bytes / 32;
+    float4* buf = nullptr;
+    float* sink = nullptr;
+    SFB_CUDA(cudaMalloc(&buf, n32 * 32));
+    SFB_CUDA(cudaMalloc(&sink, sizeof(float)));
+    SFB_CUDA(cudaMemset(buf, 0, n32 * 32));
+    cudaEvent_t e0, e1;
+    SFB_CUDA(cudaEventCreate(&e0));
+    SFB_CUDA(cudaEventCreate(&e1));
+    const unsigned grid = unsigned(sm_count()) * 8;
+    k_l2_probe<<<grid, 256>>>(buf, n32, 2, sink);  // warm: buffer into L2
+    SFB_CUDA(cudaEventRecord(e0));
+    k_l2_probe<<<grid, 256>>>(buf, n32, reps, sink);
+    SFB_CUDA(cudaEventRecord(e1));
+    SFB_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.0f;
+    SFB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(buf);
+    cudaFree(sink);
+    count_launch();
+    count_launch();
+    return double(n32 * 32) * reps / (double(ms) * 1e-3) / 1e9;
+}
+
 // float4 units of the xy-quad layout: padded dims (nx + 1, ny + 1, nz + 2) in whole 2x1x2
 // bricks, two float4 per record
 size_t xpair_records(int nx, int ny, int nz) {

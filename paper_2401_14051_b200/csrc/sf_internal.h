@@ -242,6 +242,7 @@ void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_mediu
 // Morton keys of the queries' positions in the grid box + identity indices (for cub sort)
 void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t* keys, int* idx, cudaStream_t s);
 void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStream_t s);
+double probe_l2_read_gbs(size_t bytes, int reps);  // k_l2_probe: 32-byte reads of an L2-resident buffer
 size_t xpair_records(int nx, int ny, int nz);  // float4 units of the padded xy-quad record layout
 // Pre-blended phase planes: for each lobe, the table interpolated at that lobe's g
 // (PhaseTable::lookup_hg's g axis, src/phase.cpp:191-219), [n_lobes][angle][aperture].

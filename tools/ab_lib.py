@@ -1,5 +1,7 @@
 """A/B two library builds on the C2 bf16 query: F bit-identity and device time per step.
-usage: python tools/ab_lib.py OTHER.so  (the in-tree build is the other arm)."""
+usage: python tools/ab_lib.py OTHER.so  (the in-tree build is the other arm).
+AB_ENV_OTHER="K=V,K2=V2" sets environment variables for the other arm only (OTHER.so may then be
+the in-tree library itself, for an A/B of a runtime switch)."""
 import os, subprocess, sys, json
 code = r'''
 import os, sys, json
@@ -31,6 +33,9 @@ for name, lib in (("tree", ""), ("other", sys.argv[1])):
     env = dict(os.environ)
     if lib:
         env["SF_B200_LIB"] = os.path.abspath(lib)
+        for kv in filter(None, os.environ.get("AB_ENV_OTHER", "").split(",")):
+            k, v = kv.split("=", 1)
+            env[k] = v
     r = subprocess.run([sys.executable, "-c", code, f"/tmp/ab_{name}.npy"], env=env, capture_output=True, text=True)
     out[name] = r.stdout.strip() or r.stderr[-400:]
 import numpy as np

@@ -18,6 +18,9 @@ METRICS = {
     "sm_throughput_pct": ("sm__throughput.avg.pct_of_peak_sustained_elapsed", 1),
     "tensor_pipe_active_pct": ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", 1),
     "inst_executed": ("smsp__inst_executed.sum", 1),
+    "l1_data_pipe_pct": ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", 1),
+    "lts_throughput_pct": ("lts__throughput.avg.pct_of_peak_sustained_elapsed", 1),
+    "issue_active_pct": ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", 1),
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3,
               "msecond": 1e6, "ms": 1e6}
