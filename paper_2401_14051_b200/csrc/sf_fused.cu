@@ -815,16 +815,24 @@ SortDesc make_desc(const SceneDev* sc, int n_planes, const SortLayout& L, int64_
             }
     d.n_segs = segs;
     d.n_chunks = chunks;
-    // Sort tasks: 64-wide segments first as lane pairs (2 task slots = 16 threads),
-    // then 32/16/8-wide, so each warp runs (mostly) one network size.
+    // Sort tasks, one slot = one network size for the group's queries (a warp of the 32-warp
+    // block runs one slot; 64-wide segments take two slots as lane pairs, aligned to an even
+    // slot). Slots beyond the block's threads run as a second round on the threads of the
+    // first slots, so the light 16-wide tasks go first (their threads also take the
+    // second-round 32/8-wide tasks), then the lane pairs (the longest), then 32 and 8.
     auto net = [](int c) { return c <= 8 ? 8 : c <= 16 ? 16 : c <= 32 ? 32 : 64; };
+    std::vector<int> small, rest;
+    for (int s2 = 0; s2 < segs; ++s2)
+        if (net(d.seg_n[s2]) == 16) small.push_back(s2);
     int t = 0;
+    for (size_t k = 0; k + (small.size() & 1) < small.size(); ++k) d.task_seg[t++] = uint8_t(small[k]);
     for (int s2 = 0; s2 < segs; ++s2)
         if (net(d.seg_n[s2]) == 64) {
             d.task_seg[t++] = uint8_t(s2);
             d.task_seg[t++] = uint8_t(s2 | 0x80);
         }
-    for (int p : {32, 16, 8})
+    if (small.size() & 1) d.task_seg[t++] = uint8_t(small.back());  // keeps the pairs on even slots
+    for (int p : {32, 8})
         for (int s2 = 0; s2 < segs; ++s2)
             if (net(d.seg_n[s2]) == p) d.task_seg[t++] = uint8_t(s2);
     d.n_tasks = t;
