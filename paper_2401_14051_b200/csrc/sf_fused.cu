@@ -300,7 +300,8 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
                                                const SortDesc& d, const float* planes, const float4* __restrict__ pre,
                                                bool same_light, float& rho, float& tr, float& ph) {
     if (i < d.npts0) {
-        const float4 p0 = __ldg(pre + 2 * i), p1 = __ldg(pre + 2 * i + 1);  // {offset, half}, {axis, light side}
+        float4 p0, p1;  // {offset, half}, {axis, light side}: one 256-bit load
+        ld_nc_256(pre + 2 * i, p0, p1);
         const float f[3] = {q.pf[0] + p0.x, q.pf[1] + p0.y, q.pf[2] + p0.z};
         sample_rt(sc, q.pb, q.pbox, f, rho, tr);
         if (p0.w < 0.0f) {
