@@ -8,6 +8,7 @@
 // All kernels are SIMT: none of these operations has a channel or reduction
 // dimension that a tensor-core GEMM could use (the combiner is one 1-in/1-out
 // 27-tap stencil per level).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -99,43 +100,52 @@ __device__ __forceinline__ double trilinear_xp(const GridDev& g, const double2* 
     return lerp1(lerp1(c00, c10, ty), lerp1(c01, c11, ty), tz);
 }
 
+// Optical depth of the ray from voxel (x, y, z)'s centre toward the light (graded_transmittance,
+// src/feature_pipeline.cpp:57-66, with DensityGrid::optical_depth, src/volume_grid.cpp:64-78):
+// intersect_box, q = p + ts * t1, len, n = max(1, ceil(len / step)), h = len / n, dir = d * (1 / len),
+// midpoint samples. FP64 throughout, the reference's operations in its order.
+__device__ __forceinline__ double graded_tau_f64(const GridDev& g, const double2* __restrict__ xp, int x, int y,
+                                                 int z, const double ts[3], double step) {
+    const double lo[3] = {g.ox, g.oy, g.oz};
+    const double hi[3] = {g.hx, g.hy, g.hz};
+    double p[3] = {g.ox + (x + 0.5) * g.vs, g.oy + (y + 0.5) * g.vs, g.oz + (z + 0.5) * g.vs};
+    double t0, t1, tau = 0.0;
+    if (intersect_box(lo, hi, p, ts, t0, t1) && t1 > 0.0) {
+        double q[3] = {p[0] + ts[0] * t1, p[1] + ts[1] * t1, p[2] + ts[2] * t1};
+        double d[3] = {q[0] - p[0], q[1] - p[1], q[2] - p[2]};
+        double len = sqrt(dot3(d, d));
+        if (len != 0.0) {
+            int ns = int(ceil(len / step));
+            ns = ns < 1 ? 1 : ns;
+            double h = len / ns;
+            double il = 1.0 / len;
+            double dir[3] = {d[0] * il, d[1] * il, d[2] * il};
+            double sum = 0.0;
+            for (int i = 0; i < ns; ++i) {
+                double s = (i + 0.5) * h;
+                sum += trilinear_xp(g, xp, p[0] + dir[0] * s, p[1] + dir[1] * s, p[2] + dir[2] * s);
+            }
+            tau = sum * h;
+        }
+    }
+    return tau;
+}
+
 // K2: graded transmittance of one level (src/feature_pipeline.cpp:37-68) with the
 // midpoint-rule optical depth (src/volume_grid.cpp:64-78), for voxel rows z in [zlo, zhi)
 // (a z-slab when the build is sharded over GPUs). One thread per voxel; neighbouring
 // threads march neighbouring parallel rays, so a warp's gathers stay within a few lines.
-// FP64 throughout, as the reference: the kernel is FP64-pipe bound.
+// FP64 throughout, as the reference. (k_graded_taps below is the fast form of the same march.)
 __global__ void k_graded(GridDev g, const double2* __restrict__ xp, double tsx, double tsy, double tsz,
                          double coeff, double step, int zlo, int zhi, float* __restrict__ out) {
     const int plane = g.nx * g.ny;
     const int i0 = zlo * plane, i1 = zhi * plane;
-    const double lo[3] = {g.ox, g.oy, g.oz};
-    const double hi[3] = {g.hx, g.hy, g.hz};
     const double ts[3] = {tsx, tsy, tsz};
     for (int idx = i0 + blockIdx.x * blockDim.x + threadIdx.x; idx < i1; idx += gridDim.x * blockDim.x) {
         const int x = idx % g.nx;
         const int y = (idx / g.nx) % g.ny;
         const int z = idx / plane;
-        double p[3] = {g.ox + (x + 0.5) * g.vs, g.oy + (y + 0.5) * g.vs, g.oz + (z + 0.5) * g.vs};
-        double t0, t1, tau = 0.0;
-        if (intersect_box(lo, hi, p, ts, t0, t1) && t1 > 0.0) {
-            double q[3] = {p[0] + ts[0] * t1, p[1] + ts[1] * t1, p[2] + ts[2] * t1};
-            double d[3] = {q[0] - p[0], q[1] - p[1], q[2] - p[2]};
-            double len = sqrt(dot3(d, d));
-            if (len != 0.0) {
-                int ns = int(ceil(len / step));
-                ns = ns < 1 ? 1 : ns;
-                double h = len / ns;
-                double il = 1.0 / len;
-                double dir[3] = {d[0] * il, d[1] * il, d[2] * il};
-                double sum = 0.0;
-                for (int i = 0; i < ns; ++i) {
-                    double s = (i + 0.5) * h;
-                    sum += trilinear_xp(g, xp, p[0] + dir[0] * s, p[1] + dir[1] * s, p[2] + dir[2] * s);
-                }
-                tau = sum * h;
-            }
-        }
-        out[idx] = float(exp(-coeff * tau));
+        out[idx] = float(exp(-coeff * graded_tau_f64(g, xp, x, y, z, ts, step)));
     }
 }
 
@@ -152,105 +162,622 @@ __global__ void k_xpair_f32(const float* __restrict__ v, int nx, int ny, int nz,
     }
 }
 
+__device__ __forceinline__ double graded_tau_f32(const GridDev& g, const float2* __restrict__ xp, int x, int y,
+                                                 int z, const double ts[3], double step) {
+    const int plane = g.nx * g.ny;
+    const double lo[3] = {g.ox, g.oy, g.oz};
+    const double hi[3] = {g.hx, g.hy, g.hz};
+    double p[3] = {g.ox + (x + 0.5) * g.vs, g.oy + (y + 0.5) * g.vs, g.oz + (z + 0.5) * g.vs};
+    double t0, t1, tau = 0.0;
+    if (intersect_box(lo, hi, p, ts, t0, t1) && t1 > 0.0) {
+        double q[3] = {p[0] + ts[0] * t1, p[1] + ts[1] * t1, p[2] + ts[2] * t1};
+        double d[3] = {q[0] - p[0], q[1] - p[1], q[2] - p[2]};
+        double len = sqrt(dot3(d, d));
+        if (len != 0.0) {
+            int ns = int(ceil(len / step));
+            ns = ns < 1 ? 1 : ns;
+            const double h = len / ns;
+            const double il = 1.0 / len;
+            // voxel-space ray: f(s) = f0 + df * s, f0 = the voxel centre's own coordinates
+            const float f0[3] = {float(x), float(y), float(z)};
+            const float df[3] = {float(d[0] * il * (1.0 / g.vs)), float(d[1] * il * (1.0 / g.vs)),
+                                 float(d[2] * il * (1.0 / g.vs))};
+            const float hf = float(h);
+            float sum = 0.0f, comp = 0.0f;
+            // Samples whose cell and its +1 neighbour are in range on every axis need no clamps:
+            // [ia, ib) from the ray's interior interval, with a 1e-3 voxel margin, so the fast
+            // loop does exactly what the clamped one would (the sum order is unchanged).
+            float slo = 0.0f, shi = float(len) * float(1.0 / g.vs) * 2.0f + 4.0f;
+            const int nn[3] = {g.nx, g.ny, g.nz};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const float lo_f = 1e-3f, hi_f = float(nn[a] - 1) - 1e-3f;  // floor(f) in [0, n - 2]
+                if (df[a] > 0.0f) {
+                    slo = fmaxf(slo, (lo_f - f0[a]) / df[a]);
+                    shi = fminf(shi, (hi_f - f0[a]) / df[a]);
+                } else if (df[a] < 0.0f) {
+                    slo = fmaxf(slo, (hi_f - f0[a]) / df[a]);
+                    shi = fminf(shi, (lo_f - f0[a]) / df[a]);
+                } else if (!(f0[a] >= lo_f && f0[a] <= hi_f)) {
+                    shi = -1.0f;  // this axis never interior
+                }
+            }
+            int ia = ns, ib = ns;
+            if (shi > slo) {
+                ia = max(0, int(ceilf(slo / hf - 0.5f)) + 1);
+                ib = min(ns, int(floorf(shi / hf - 0.5f)));  // exclusive bound: one sample of margin
+                if (ib < ia) ia = ib = ns;
+            }
+            auto add = [&](float v) {
+                const float yk = v - comp;  // Kahan
+                const float tk = sum + yk;
+                comp = (tk - sum) - yk;
+                sum = tk;
+            };
+            auto clamped = [&](int i) {
+                const float sf = (float(i) + 0.5f) * hf;
+                const float fx = fmaf(df[0], sf, f0[0]), fy = fmaf(df[1], sf, f0[1]), fz = fmaf(df[2], sf, f0[2]);
+                // No box test: every sample lies strictly inside the closed box (the ray runs from
+                // a voxel centre to the box exit and the last sample is h/2 before the exit), so
+                // sample_trilinear's outside branch (0) never applies; the clamps below still do.
+                const float flx = floorf(fx), fly = floorf(fy), flz = floorf(fz);
+                const int x0 = int(flx), y0 = int(fly), z0 = int(flz);
+                float tx = fx - flx;
+                const float ty = fy - fly, tz = fz - flz;
+                if (x0 < 0) tx = 0.0f;
+                const int xc = x0 < 0 ? 0 : x0;
+                const int ya = max(y0, 0), yb = min(y0 + 1, g.ny - 1), za = max(z0, 0), zb = min(z0 + 1, g.nz - 1);
+                const float2* row = xp + ((za * g.ny + ya) * g.nx + xc);
+                const int dy = (yb - ya) * g.nx, dz = (zb - za) * plane;
+                const float2 r00 = __ldg(row), r10 = __ldg(row + dy);
+                const float2 r01 = __ldg(row + dz), r11 = __ldg(row + dz + dy);
+                const float c00 = fmaf(tx, r00.y - r00.x, r00.x), c10 = fmaf(tx, r10.y - r10.x, r10.x);
+                const float c01 = fmaf(tx, r01.y - r01.x, r01.x), c11 = fmaf(tx, r11.y - r11.x, r11.x);
+                const float e0 = fmaf(ty, c10 - c00, c00), e1 = fmaf(ty, c11 - c01, c01);
+                add(fmaf(tz, e1 - e0, e0));
+            };
+            for (int i = 0; i < ia; ++i) clamped(i);
+            for (int i = ia; i < ib; ++i) {  // interior: 0 <= cell, cell + 1 <= n - 1 on every axis
+                const float sf = (float(i) + 0.5f) * hf;
+                const float fx = fmaf(df[0], sf, f0[0]), fy = fmaf(df[1], sf, f0[1]), fz = fmaf(df[2], sf, f0[2]);
+                const float flx = floorf(fx), fly = floorf(fy), flz = floorf(fz);
+                const float tx = fx - flx, ty = fy - fly, tz = fz - flz;
+                const float2* row = xp + ((int(flz) * g.ny + int(fly)) * g.nx + int(flx));
+                const float2 r00 = __ldg(row), r10 = __ldg(row + g.nx);
+                const float2 r01 = __ldg(row + plane), r11 = __ldg(row + plane + g.nx);
+                const float c00 = fmaf(tx, r00.y - r00.x, r00.x), c10 = fmaf(tx, r10.y - r10.x, r10.x);
+                const float c01 = fmaf(tx, r01.y - r01.x, r01.x), c11 = fmaf(tx, r11.y - r11.x, r11.x);
+                const float e0 = fmaf(ty, c10 - c00, c00), e1 = fmaf(ty, c11 - c01, c01);
+                add(fmaf(tz, e1 - e0, e0));
+            }
+            for (int i = max(ib, ia); i < ns; ++i) clamped(i);
+            tau = double(sum) * h;
+        }
+    }
+    return tau;
+}
+
 __global__ void k_graded_f32(GridDev g, const float2* __restrict__ xp, double tsx, double tsy, double tsz,
                              double coeff, double step, int zlo, int zhi, float* __restrict__ out) {
     const int plane = g.nx * g.ny;
     const int i0 = zlo * plane, i1 = zhi * plane;
-    const double lo[3] = {g.ox, g.oy, g.oz};
-    const double hi[3] = {g.hx, g.hy, g.hz};
     const double ts[3] = {tsx, tsy, tsz};
     for (int idx = i0 + blockIdx.x * blockDim.x + threadIdx.x; idx < i1; idx += gridDim.x * blockDim.x) {
         const int x = idx % g.nx;
         const int y = (idx / g.nx) % g.ny;
         const int z = idx / plane;
-        double p[3] = {g.ox + (x + 0.5) * g.vs, g.oy + (y + 0.5) * g.vs, g.oz + (z + 0.5) * g.vs};
-        double t0, t1, tau = 0.0;
-        if (intersect_box(lo, hi, p, ts, t0, t1) && t1 > 0.0) {
-            double q[3] = {p[0] + ts[0] * t1, p[1] + ts[1] * t1, p[2] + ts[2] * t1};
-            double d[3] = {q[0] - p[0], q[1] - p[1], q[2] - p[2]};
-            double len = sqrt(dot3(d, d));
-            if (len != 0.0) {
-                int ns = int(ceil(len / step));
-                ns = ns < 1 ? 1 : ns;
-                const double h = len / ns;
-                const double il = 1.0 / len;
-                // voxel-space ray: f(s) = f0 + df * s, f0 = the voxel centre's own coordinates
-                const float f0[3] = {float(x), float(y), float(z)};
-                const float df[3] = {float(d[0] * il * (1.0 / g.vs)), float(d[1] * il * (1.0 / g.vs)),
-                                     float(d[2] * il * (1.0 / g.vs))};
-                const float hf = float(h);
-                float sum = 0.0f, comp = 0.0f;
-                // Samples whose cell and its +1 neighbour are in range on every axis need no clamps:
-                // [ia, ib) from the ray's interior interval, with a 1e-3 voxel margin, so the fast
-                // loop does exactly what the clamped one would (the sum order is unchanged).
-                float slo = 0.0f, shi = float(len) * float(1.0 / g.vs) * 2.0f + 4.0f;
-                const int nn[3] = {g.nx, g.ny, g.nz};
+        out[idx] = float(exp(-coeff * graded_tau_f32(g, xp, x, y, z, ts, step)));
+    }
+}
+
+// ---- K2 as shared tap lists ("graded taps") -------------------------------------------------
+// Every voxel whose ray toward the light leaves the box through a face perpendicular to axis E
+// has an exit distance t1 = (face - p_E) / ts_E that depends on its E coordinate alone, hence
+// the same n, h and the same sample offsets relative to its own centre: the midpoint sum
+//     sum_i trilinear(p + dir (i + 1/2) h)
+// is one linear functional of the density, translated, for every voxel of that plane. Grouping
+// the sum by grid corner gives, with L the lane axis and O the third axis,
+//     sum = sum_k  w0 rho[v+o] + w1 rho[v+o+e_L] + w2 rho[v+o+e_O] + w3 rho[v+o+e_L+e_O]
+// over "column" taps o_k (the 2 x 2 (L, O) corners of a cell row; ~0.8 taps per sample instead
+// of 8 corners), the same value in exact arithmetic. k_tap_build makes the tap list of every
+// (E, c) plane once per level and light (FP64 weights); k_graded_cols walks it for 32
+// L-consecutive voxels x K O-consecutive voxels per warp: warp-uniform tap loads, coalesced
+// 2-corner (L-pair) gathers, and row j + 1 of one voxel's column is row j of the next voxel's,
+// so K voxels need K + 1 gathers per tap.
+//   E = y (rows x, blocks along z) and E = z (rows x, blocks along y) read x-fastest pairs;
+//   E = x (voxels leaving through an x face) reads z-fastest pairs (lanes along z).
+// A voxel belongs to the face it leaves through (ties: y, then z, then x). Pair records carry a
+// one-voxel halo with the edge values replicated (the pair at L = -1 is {v(0), v(0)}), so the
+// clamps of sample_trilinear (src/volume_grid.cpp:45-56) cost nothing: a ray that stays in the
+// box only touches corners in [-1, n] on every axis. A voxel whose sample count differs from its
+// plane's (len / step within rounding of an integer) marches alone. FP64 taps and sums for the
+// exact build (bit-identical to the march in practice), FP32 for the production build.
+template <typename W>
+struct alignas(16) ColTap {
+    W w[4];  // weights of (o), (o + e_L), (o + e_O), (o + e_L + e_O)
+    int lin; // o_L s_L + o_E s_E + o_O s_O in the padded record strides (E offset clamped to the grid)
+};
+
+struct TapGroup {
+    int tap0, n, ns, pad;  // n <= 0: no list (the plane's voxels march)
+    double h, texit;
+};
+
+constexpr int kTapWarps = 4;
+constexpr int kColK = 4;  // voxels per lane along O
+
+// Padded pair layout of one lane axis. L = 0: x-fastest, index (x+1) + (y+1) sy + (z+1) sz over
+// x in [-1, nx-1], y in [-1, ny], z in [-1, nz]; L = 2: z-fastest, (z+1) + (y+1) sy + (x+1) sx.
+struct PadLayout {
+    int L;
+    int64_t s[3];  // strides of x, y, z
+    int64_t count;
+};
+
+inline PadLayout pad_layout(int nx, int ny, int nz, int L) {
+    PadLayout p;
+    p.L = L;
+    if (L == 0) {
+        p.s[0] = 1;
+        p.s[1] = nx + 1;
+        p.s[2] = int64_t(nx + 1) * (ny + 2);
+        p.count = p.s[2] * (nz + 2);
+    } else {
+        p.s[2] = 1;
+        p.s[1] = nz + 1;
+        p.s[0] = int64_t(nz + 1) * (ny + 2);
+        p.count = p.s[0] * (nx + 2);
+    }
+    return p;
+}
+
+template <typename T2>
+__global__ void k_pad_pairs(const float* __restrict__ v, int nx, int ny, int nz, PadLayout pl, T2* __restrict__ out) {
+    const int n[3] = {nx, ny, nz};
+    const int a0 = pl.L, a2 = pl.L == 0 ? 2 : 0;
+    const int64_t n0 = n[a0] + 1, n1 = ny + 2;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < pl.count; i += int64_t(gridDim.x) * blockDim.x) {
+        int c[3];
+        c[a0] = int(i % n0) - 1;
+        c[1] = int((i / n0) % n1) - 1;
+        c[a2] = int(i / (n0 * n1)) - 1;
+        int lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = c[a] < 0 ? 0 : (c[a] > n[a] - 1 ? n[a] - 1 : c[a]);
+            hi[a] = lo[a];
+        }
+        hi[a0] = c[a0] + 1 > n[a0] - 1 ? n[a0] - 1 : c[a0] + 1;
+        T2 r;
+        r.x = v[(size_t(lo[2]) * ny + lo[1]) * nx + lo[0]];
+        r.y = v[(size_t(hi[2]) * ny + hi[1]) * nx + hi[0]];
+        out[i] = r;
+    }
+}
+
+__device__ __forceinline__ double axis_lo(const GridDev& g, int a) { return a == 0 ? g.ox : (a == 1 ? g.oy : g.oz); }
+__device__ __forceinline__ double axis_hi(const GridDev& g, int a) { return a == 0 ? g.hx : (a == 1 ? g.hy : g.hz); }
+__device__ __forceinline__ int axis_n(const GridDev& g, int a) { return a == 0 ? g.nx : (a == 1 ? g.ny : g.nz); }
+
+// intersect_box's far-plane distance for axis a (inc/math.h:85-107: inv = 1 / d, ta, tb, swap)
+__device__ __forceinline__ double face_exit(const GridDev& g, const double ts[3], int a, double pa) {
+    if (ts[a] == 0.0) return 1e300;
+    const double inv = 1.0 / ts[a];
+    const double ta = (axis_lo(g, a) - pa) * inv, tb = (axis_hi(g, a) - pa) * inv;
+    return ta > tb ? ta : tb;
+}
+
+// Exit face of a voxel centre (intersect_box's t1 = min over the axes of the far-plane
+// distances; the centre is inside, so the box is always hit): 1 = y, 2 = z, 0 = x; ties go to
+// y, then z.
+__device__ __forceinline__ int exit_face(double tx, double ty, double tz) {
+    if (ty <= tz && ty <= tx) return 1;
+    if (tz <= tx) return 2;
+    return 0;
+}
+
+// n = max(1, ceil(len / step)) of the ray from p to p + ts t1 (src/volume_grid.cpp:64-72)
+__device__ __forceinline__ int sample_count(const double p[3], const double ts[3], double t1, double step) {
+    const double q[3] = {p[0] + ts[0] * t1, p[1] + ts[1] * t1, p[2] + ts[2] * t1};
+    const double d[3] = {q[0] - p[0], q[1] - p[1], q[2] - p[2]};
+    const double len = sqrt(dot3(d, d));
+    if (len == 0.0) return 0;
+    const int ns = int(ceil(len / step));
+    return ns < 1 ? 1 : ns;
+}
+
+// Group index layout: [E = y: ny planes][E = z: nz][E = x: nx].
+__device__ __forceinline__ int group_index(const GridDev& g, int E, int c) {
+    return E == 1 ? c : (E == 2 ? g.ny + c : g.ny + g.nz + c);
+}
+
+// One warp per (E, c) plane; lane j streams samples [j*chunk, (j+1)*chunk) keeping the eight
+// corner weights of the current cell in registers and emitting a column (the cell's 2 x 2
+// (L, O) corners of one E row) when that row leaves the cell; a move along L, or a jump of more
+// than one cell, flushes both rows. Cells advance monotonically along every axis. A lane whose
+// chunk ends in the cell the next lane starts in hands its pending weights over instead of
+// emitting them (no duplicate columns at chunk seams). Pass 0 counts, pass 1 writes after a
+// warp prefix sum.
+template <typename W>
+__global__ void __launch_bounds__(kTapWarps * 32) k_tap_build(GridDev g, double tsx, double tsy, double tsz,
+                                                               double step, int cap, PadLayout plx, PadLayout plz,
+                                                               TapGroup* __restrict__ groups,
+                                                               ColTap<W>* __restrict__ taps) {
+    const int gi = blockIdx.x * kTapWarps + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (gi >= g.nx + g.ny + g.nz) return;
+    TapGroup& G = groups[gi];
+    const int E = gi < g.ny ? 1 : (gi < g.ny + g.nz ? 2 : 0);
+    const int c = gi - (E == 1 ? 0 : (E == 2 ? g.ny : g.ny + g.nz));
+    const double ts[3] = {tsx, tsy, tsz};
+    if (ts[E] == 0.0) {
+        if (lane == 0) G.n = 0;
+        return;
+    }
+    // plane geometry: exit through E's far face, len, n, h, dir (as optical_depth computes them)
+    const double pE = axis_lo(g, E) + (c + 0.5) * g.vs;
+    const double texit = face_exit(g, ts, E, pE);
+    double d[3] = {ts[0] * texit, ts[1] * texit, ts[2] * texit};
+    const double len = sqrt(dot3(d, d));
+    int ns = int(ceil(len / step));
+    ns = ns < 1 ? 1 : ns;
+    const double h = len / ns, il = 1.0 / len;
+    const int L = E == 0 ? 2 : 0, O = 3 - E - L;
+    const double dirL = d[L] * il, dirE = d[E] * il, dirO = d[O] * il;
+    // cap bounds the lists of the planes a voxel can leave through (exit distance at most the
+    // box's shortest span over |ts|); longer planes are never selected and get no list
+    if (4 * ns + 4 * 32 + 8 > cap) {
+        if (lane == 0) G.n = 0;
+        return;
+    }
+    const PadLayout& pl = L == 0 ? plx : plz;
+    const int64_t sL = pl.s[L], sE = pl.s[E], sO = pl.s[O];
+    const int nE = axis_n(g, E);
+    const double oE = axis_lo(g, E);
+    const int tap0 = gi * cap;
+    const int chunk = max(8, (ns + 31) / 32);
+    const int i0 = min(ns, lane * chunk), i1 = min(ns, i0 + chunk);
+    // cell of sample i: (L, E relative to c, O) and the fractions
+    auto cell_of = [&](int i, int cc[3], double t[3]) {
+        const double s = (i + 0.5) * h;
+        double ul, uo, fe;
+        const double pe = pE + dirE * s;
+        if (g.ivs != 0.0) {
+            ul = dirL * s * g.ivs;
+            uo = dirO * s * g.ivs;
+            fe = (pe - oE) * g.ivs - 0.5;
+        } else {
+            ul = dirL * s / g.vs;
+            uo = dirO * s / g.vs;
+            fe = (pe - oE) / g.vs - 0.5;
+        }
+        const double fl = floor(ul), fo = floor(uo), fE = floor(fe);
+        cc[0] = int(fl);
+        cc[1] = int(fE) - c;
+        cc[2] = int(fo);
+        t[0] = ul - fl;
+        t[1] = fe - fE;
+        t[2] = uo - fo;
+    };
+    // seams: does my last cell equal the next lane's first cell (and differ from my first)?
+    int first[3] = {0, 0, 0}, last[3] = {0, 0, 0};
+    double tt[3];
+    if (i1 > i0) {
+        cell_of(i0, first, tt);
+        cell_of(i1 - 1, last, tt);
+    }
+    const int nf0 = __shfl_down_sync(0xffffffffu, first[0], 1), nf1 = __shfl_down_sync(0xffffffffu, first[1], 1),
+              nf2 = __shfl_down_sync(0xffffffffu, first[2], 1);
+    const int next_i0 = __shfl_down_sync(0xffffffffu, i0, 1), next_i1 = __shfl_down_sync(0xffffffffu, i1, 1);
+    const bool hand_over = lane < 31 && i1 > i0 && next_i1 > next_i0 && last[0] == nf0 && last[1] == nf1 &&
+                           last[2] == nf2 && !(first[0] == last[0] && first[1] == last[1] && first[2] == last[2]);
+    const bool receive = __shfl_up_sync(0xffffffffu, hand_over ? 1 : 0, 1) && lane > 0;
+    double acc[2][2][2];  // [bO][bE][bL]
+    double fin[2][2][2] = {};  // pass 0's final cell weights (handed to the next lane in pass 1)
+    int base = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        int cnt = 0;
+        int C[3] = {first[0], first[1], first[2]};
 #pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    const float lo_f = 1e-3f, hi_f = float(nn[a] - 1) - 1e-3f;  // floor(f) in [0, n - 2]
-                    if (df[a] > 0.0f) {
-                        slo = fmaxf(slo, (lo_f - f0[a]) / df[a]);
-                        shi = fminf(shi, (hi_f - f0[a]) / df[a]);
-                    } else if (df[a] < 0.0f) {
-                        slo = fmaxf(slo, (hi_f - f0[a]) / df[a]);
-                        shi = fminf(shi, (lo_f - f0[a]) / df[a]);
-                    } else if (!(f0[a] >= lo_f && f0[a] <= hi_f)) {
-                        shi = -1.0f;  // this axis never interior
+        for (int bo = 0; bo < 2; ++bo)
+#pragma unroll
+            for (int be = 0; be < 2; ++be)
+#pragma unroll
+                for (int bl = 0; bl < 2; ++bl) {
+                    const double v = __shfl_up_sync(0xffffffffu, fin[bo][be][bl], 1);
+                    acc[bo][be][bl] = (pass == 1 && receive) ? v : 0.0;
+                }
+        auto emit = [&](int cl, int ce, int co, double w0, double w1, double w2, double w3) {
+            int ae = c + ce;  // absolute E corner, clamped as sample_trilinear clamps it
+            ae = ae < 0 ? 0 : (ae > nE - 1 ? nE - 1 : ae);
+            if (pass == 1) {
+                ColTap<W> t;
+                t.w[0] = W(w0);
+                t.w[1] = W(w1);
+                t.w[2] = W(w2);
+                t.w[3] = W(w3);
+                t.lin = int(cl * sL + (ae - c) * sE + co * sO);
+                taps[tap0 + base + cnt] = t;
+            }
+            ++cnt;
+        };
+        auto emit_row = [&](int be) {  // E row be of the current cell, both O rows
+            emit(C[0], C[1] + be, C[2], acc[0][be][0], acc[0][be][1], acc[1][be][0], acc[1][be][1]);
+            acc[0][be][0] = acc[0][be][1] = acc[1][be][0] = acc[1][be][1] = 0.0;
+        };
+        for (int i = i0; i < i1; ++i) {
+            int cc[3];
+            double t[3];
+            cell_of(i, cc, t);
+            if (cc[0] != C[0] || cc[1] != C[1] || cc[2] != C[2]) {
+                const int dl = cc[0] - C[0], de = cc[1] - C[1], dO = cc[2] - C[2];
+                if (dl != 0 || de > 1 || de < -1 || dO > 1 || dO < -1) {
+                    emit_row(0);
+                    emit_row(1);
+                } else {
+                    if (de == 1) {  // row bE = 0 leaves; bE = 1 becomes bE = 0
+                        emit_row(0);
+#pragma unroll
+                        for (int bo = 0; bo < 2; ++bo) {
+                            acc[bo][0][0] = acc[bo][1][0];
+                            acc[bo][0][1] = acc[bo][1][1];
+                            acc[bo][1][0] = acc[bo][1][1] = 0.0;
+                        }
+                    } else if (de == -1) {
+                        emit_row(1);
+#pragma unroll
+                        for (int bo = 0; bo < 2; ++bo) {
+                            acc[bo][1][0] = acc[bo][0][0];
+                            acc[bo][1][1] = acc[bo][0][1];
+                            acc[bo][0][0] = acc[bo][0][1] = 0.0;
+                        }
+                    }
+                    C[1] = cc[1];
+                    if (dO == 1) {  // O row bO = 0 leaves (as columns with only their low row)
+#pragma unroll
+                        for (int be = 0; be < 2; ++be) {
+                            emit(C[0], C[1] + be, C[2], acc[0][be][0], acc[0][be][1], 0.0, 0.0);
+                            acc[0][be][0] = acc[1][be][0];
+                            acc[0][be][1] = acc[1][be][1];
+                            acc[1][be][0] = acc[1][be][1] = 0.0;
+                        }
+                    } else if (dO == -1) {
+#pragma unroll
+                        for (int be = 0; be < 2; ++be) {
+                            emit(C[0], C[1] + be, C[2] + 1, acc[1][be][0], acc[1][be][1], 0.0, 0.0);
+                            acc[1][be][0] = acc[0][be][0];
+                            acc[1][be][1] = acc[0][be][1];
+                            acc[0][be][0] = acc[0][be][1] = 0.0;
+                        }
                     }
                 }
-                int ia = ns, ib = ns;
-                if (shi > slo) {
-                    ia = max(0, int(ceilf(slo / hf - 0.5f)) + 1);
-                    ib = min(ns, int(floorf(shi / hf - 0.5f)));  // exclusive bound: one sample of margin
-                    if (ib < ia) ia = ib = ns;
-                }
-                auto add = [&](float v) {
-                    const float yk = v - comp;  // Kahan
-                    const float tk = sum + yk;
-                    comp = (tk - sum) - yk;
-                    sum = tk;
-                };
-                auto clamped = [&](int i) {
-                    const float sf = (float(i) + 0.5f) * hf;
-                    const float fx = fmaf(df[0], sf, f0[0]), fy = fmaf(df[1], sf, f0[1]), fz = fmaf(df[2], sf, f0[2]);
-                    // No box test: every sample lies strictly inside the closed box (the ray runs from
-                    // a voxel centre to the box exit and the last sample is h/2 before the exit), so
-                    // sample_trilinear's outside branch (0) never applies; the clamps below still do.
-                    const float flx = floorf(fx), fly = floorf(fy), flz = floorf(fz);
-                    const int x0 = int(flx), y0 = int(fly), z0 = int(flz);
-                    float tx = fx - flx;
-                    const float ty = fy - fly, tz = fz - flz;
-                    if (x0 < 0) tx = 0.0f;
-                    const int xc = x0 < 0 ? 0 : x0;
-                    const int ya = max(y0, 0), yb = min(y0 + 1, g.ny - 1), za = max(z0, 0), zb = min(z0 + 1, g.nz - 1);
-                    const float2* row = xp + ((za * g.ny + ya) * g.nx + xc);
-                    const int dy = (yb - ya) * g.nx, dz = (zb - za) * plane;
-                    const float2 r00 = __ldg(row), r10 = __ldg(row + dy);
-                    const float2 r01 = __ldg(row + dz), r11 = __ldg(row + dz + dy);
-                    const float c00 = fmaf(tx, r00.y - r00.x, r00.x), c10 = fmaf(tx, r10.y - r10.x, r10.x);
-                    const float c01 = fmaf(tx, r01.y - r01.x, r01.x), c11 = fmaf(tx, r11.y - r11.x, r11.x);
-                    const float e0 = fmaf(ty, c10 - c00, c00), e1 = fmaf(ty, c11 - c01, c01);
-                    add(fmaf(tz, e1 - e0, e0));
-                };
-                for (int i = 0; i < ia; ++i) clamped(i);
-                for (int i = ia; i < ib; ++i) {  // interior: 0 <= cell, cell + 1 <= n - 1 on every axis
-                    const float sf = (float(i) + 0.5f) * hf;
-                    const float fx = fmaf(df[0], sf, f0[0]), fy = fmaf(df[1], sf, f0[1]), fz = fmaf(df[2], sf, f0[2]);
-                    const float flx = floorf(fx), fly = floorf(fy), flz = floorf(fz);
-                    const float tx = fx - flx, ty = fy - fly, tz = fz - flz;
-                    const float2* row = xp + ((int(flz) * g.ny + int(fly)) * g.nx + int(flx));
-                    const float2 r00 = __ldg(row), r10 = __ldg(row + g.nx);
-                    const float2 r01 = __ldg(row + plane), r11 = __ldg(row + plane + g.nx);
-                    const float c00 = fmaf(tx, r00.y - r00.x, r00.x), c10 = fmaf(tx, r10.y - r10.x, r10.x);
-                    const float c01 = fmaf(tx, r01.y - r01.x, r01.x), c11 = fmaf(tx, r11.y - r11.x, r11.x);
-                    const float e0 = fmaf(ty, c10 - c00, c00), e1 = fmaf(ty, c11 - c01, c01);
-                    add(fmaf(tz, e1 - e0, e0));
-                }
-                for (int i = max(ib, ia); i < ns; ++i) clamped(i);
-                tau = double(sum) * h;
+                C[0] = cc[0];
+                C[1] = cc[1];
+                C[2] = cc[2];
             }
+            const double wl[2] = {1.0 - t[0], t[0]}, we[2] = {1.0 - t[1], t[1]}, wo[2] = {1.0 - t[2], t[2]};
+#pragma unroll
+            for (int bo = 0; bo < 2; ++bo)
+#pragma unroll
+                for (int be = 0; be < 2; ++be) {
+                    acc[bo][be][0] += wo[bo] * we[be] * wl[0];
+                    acc[bo][be][1] += wo[bo] * we[be] * wl[1];
+                }
         }
-        out[idx] = float(exp(-coeff * tau));
+        if (pass == 0) {
+#pragma unroll
+            for (int bo = 0; bo < 2; ++bo)
+#pragma unroll
+                for (int be = 0; be < 2; ++be)
+#pragma unroll
+                    for (int bl = 0; bl < 2; ++bl) fin[bo][be][bl] = acc[bo][be][bl];
+        }
+        if (i1 > i0 && !hand_over) {
+            emit_row(0);
+            emit_row(1);
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, dd);
+            if (lane >= dd) incl += v;
+        }
+        base = incl - cnt;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        if (pass == 1 && lane == 0) G.n = total;
+    }
+    if (lane == 0) {
+        G.tap0 = tap0;
+        G.ns = ns;
+        G.h = h;
+        G.texit = texit;
+    }
+}
+
+// The midpoint march of one voxel on the x-fastest padded pairs: the reference's FP64 operations
+// (bit-identical values: the halo holds exactly the clamped corners). For the rare voxel whose
+// sample count differs from its plane's.
+template <typename Rec>
+__device__ double march_padded(const GridDev& g, const Rec* __restrict__ px, const PadLayout& pl, const double p[3],
+                               const double ts[3], double t1, double step) {
+    const double q[3] = {p[0] + ts[0] * t1, p[1] + ts[1] * t1, p[2] + ts[2] * t1};
+    const double d[3] = {q[0] - p[0], q[1] - p[1], q[2] - p[2]};
+    const double len = sqrt(dot3(d, d));
+    if (len == 0.0) return 0.0;
+    int ns = int(ceil(len / step));
+    ns = ns < 1 ? 1 : ns;
+    const double h = len / ns, il = 1.0 / len;
+    const double dir[3] = {d[0] * il, d[1] * il, d[2] * il};
+    double sum = 0.0;
+    for (int i = 0; i < ns; ++i) {
+        const double s = (i + 0.5) * h;
+        double f[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double pa = p[a] + dir[a] * s;
+            f[a] = g.ivs != 0.0 ? (pa - axis_lo(g, a)) * g.ivs - 0.5 : (pa - axis_lo(g, a)) / g.vs - 0.5;
+        }
+        const double fl[3] = {floor(f[0]), floor(f[1]), floor(f[2])};
+        const double tx = f[0] - fl[0], ty = f[1] - fl[1], tz = f[2] - fl[2];
+        const Rec* row =
+            px + (int64_t(fl[0]) + 1) * pl.s[0] + (int64_t(fl[1]) + 1) * pl.s[1] + (int64_t(fl[2]) + 1) * pl.s[2];
+        const Rec r00 = __ldg(row), r10 = __ldg(row + pl.s[1]);
+        const Rec r01 = __ldg(row + pl.s[2]), r11 = __ldg(row + pl.s[2] + pl.s[1]);
+        const double c00 = lerp1(r00.x, r00.y, tx), c10 = lerp1(r10.x, r10.y, tx);
+        const double c01 = lerp1(r01.x, r01.y, tx), c11 = lerp1(r11.x, r11.y, tx);
+        sum += lerp1(lerp1(c00, c10, ty), lerp1(c01, c11, ty), tz);
+    }
+    return sum * h;
+}
+
+// The voxels leaving through face E. A block takes 32 L-consecutive x K O-consecutive voxels on
+// 8 consecutive E planes, one plane per warp: the rays of neighbouring planes are the same ray
+// shifted by one voxel along E, so the warps (kept in step by the tile barriers) read the same
+// record rows a tap or two apart and the block's L1 serves most of them. Each warp's tap list
+// is staged through shared memory in tiles. Voxel rows z are restricted to [zlo, zhi) (a
+// z-slab when the build is sharded over GPUs). Rows no owned voxel needs are redirected to a
+// row that one does (no predicates in the tap loop; their sums are discarded).
+constexpr int kColTile = 64;   // taps per warp per tile
+constexpr int kColPlanes = 8;  // E planes (warps) per block
+
+template <typename W, typename Rec, int E>
+__global__ void __launch_bounds__(256, 3) k_graded_cols(GridDev g, const Rec* __restrict__ rec, PadLayout pl,
+                                                        const Rec* __restrict__ recx, PadLayout plx, double tsx,
+                                                        double tsy, double tsz, double coeff, double step, int zlo,
+                                                        int zhi, const TapGroup* __restrict__ groups,
+                                                        const ColTap<W>* __restrict__ taps, float* __restrict__ out) {
+    constexpr int L = E == 0 ? 2 : 0, O = 3 - E - L, K = kColK;
+    __shared__ ColTap<W> tile[kColPlanes][kColTile];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lo[3] = {0, 0, zlo}, hi[3] = {g.nx, g.ny, zhi};
+    const int nch = (hi[L] - lo[L] + 31) / 32, nOb = (hi[O] - lo[O] + K - 1) / K;
+    const int bt = int(blockIdx.x % (unsigned(nch) * nOb));
+    const int e = lo[E] + int(blockIdx.x / (unsigned(nch) * nOb)) * kColPlanes + warp;
+    int v[3] = {0, 0, 0};
+    v[L] = lo[L] + (bt % nch) * 32 + lane;
+    v[E] = e;
+    const int o0 = lo[O] + (bt / nch) * K;
+    const double ts[3] = {tsx, tsy, tsz};
+    const bool lane_in = e < hi[E] && v[L] < hi[L];
+    double p[3];
+    p[L] = axis_lo(g, L) + (v[L] + 0.5) * g.vs;
+    p[E] = axis_lo(g, E) + (v[E] + 0.5) * g.vs;
+    const double tE = face_exit(g, ts, E, p[E]), tL = face_exit(g, ts, L, p[L]);
+    TapGroup G;
+    G.n = 0;
+    G.tap0 = 0;
+    G.ns = 0;
+    G.h = 0.0;
+    G.texit = 0.0;
+    if (e < hi[E]) G = groups[group_index(g, E, e)];
+    bool own[K], ok[K];
+    bool any_own = false, any_ok = false;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const int o = o0 + j;
+        p[O] = axis_lo(g, O) + (o + 0.5) * g.vs;
+        const double tO = face_exit(g, ts, O, p[O]);
+        double t3[3];
+        t3[L] = tL;
+        t3[E] = tE;
+        t3[O] = tO;
+        own[j] = lane_in && o < hi[O] && exit_face(t3[0], t3[1], t3[2]) == E;
+        ok[j] = own[j] && G.n > 0 && tE == G.texit && sample_count(p, ts, tE, step) == G.ns;
+        any_own |= own[j];
+        any_ok |= ok[j];
+    }
+    W acc[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] = W(0);
+    const int block_taps = __syncthreads_or(any_ok) ? 1 : 0;
+    if (block_taps) {
+        // row j's gather serves voxel j (low O row) and voxel j - 1 (high O row); rows no ok voxel
+        // uses point at a row some ok voxel of the warp uses, so every gather stays in bounds
+        const unsigned okmask = __ballot_sync(0xffffffffu, any_ok);
+        const bool warp_taps = okmask != 0u;
+        int vb[3] = {v[0], v[1], v[2]};
+        vb[O] = o0;
+        const int64_t base = (vb[0] + 1) * pl.s[0] + (vb[1] + 1) * pl.s[1] + (vb[2] + 1) * pl.s[2];
+        int jfirst = K;
+#pragma unroll
+        for (int j = K; j >= 0; --j)
+            if ((j < K && ok[j]) || (j > 0 && ok[j - 1])) jfirst = j;
+        const int src = warp_taps ? __ffs(okmask) - 1 : 0;
+        int64_t fallback = __shfl_sync(0xffffffffu, base + int64_t(jfirst) * pl.s[O], src);
+        const Rec* rowp[K + 1];
+#pragma unroll
+        for (int j = 0; j <= K; ++j) {
+            const bool need = (j < K && ok[j]) || (j > 0 && ok[j - 1]);
+            rowp[j] = rec + (need ? base + int64_t(j) * pl.s[O] : fallback);
+        }
+        const ColTap<W>* tp = taps + G.tap0;
+        const int n = G.n > 0 ? G.n : 0;
+        int max_n = n;
+        // block-wide tile rounds: the longest list of the block's planes
+        {
+            __shared__ int smax;
+            if (threadIdx.x == 0) smax = 0;
+            __syncthreads();
+            if (lane == 0) atomicMax(&smax, n);
+            __syncthreads();
+            max_n = smax;
+        }
+        for (int t0 = 0; t0 < max_n; t0 += kColTile) {
+            const int nt = max(0, min(kColTile, n - t0));
+            __syncwarp();
+            for (int i = lane; i < nt; i += 32) tile[warp][i] = tp[t0 + i];
+            __syncthreads();
+            if (warp_taps) {
+                constexpr int U = sizeof(W) == 4 ? 2 : 1;  // taps in flight (FP64: registers)
+                int k = 0;
+                for (; k + U <= nt; k += U) {
+                    ColTap<W> t[U];
+                    Rec r[U][K + 1];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) t[u] = tile[warp][k + u];
+#pragma unroll
+                    for (int j = 0; j <= K; ++j)
+#pragma unroll
+                        for (int u = 0; u < U; ++u) r[u][j] = __ldg(rowp[j] + t[u].lin);
+#pragma unroll
+                    for (int j = 0; j < K; ++j) {
+                        W a = acc[j];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            a = fma(t[u].w[0], W(r[u][j].x), a);
+                            a = fma(t[u].w[1], W(r[u][j].y), a);
+                            a = fma(t[u].w[2], W(r[u][j + 1].x), a);
+                            a = fma(t[u].w[3], W(r[u][j + 1].y), a);
+                        }
+                        acc[j] = a;
+                    }
+                }
+                for (; k < nt; ++k) {
+                    const ColTap<W> ta = tile[warp][k];
+                    Rec ra[K + 1];
+#pragma unroll
+                    for (int j = 0; j <= K; ++j) ra[j] = __ldg(rowp[j] + ta.lin);
+#pragma unroll
+                    for (int j = 0; j < K; ++j) {
+                        W a = acc[j];
+                        a = fma(ta.w[0], W(ra[j].x), a);
+                        a = fma(ta.w[1], W(ra[j].y), a);
+                        a = fma(ta.w[2], W(ra[j + 1].x), a);
+                        a = fma(ta.w[3], W(ra[j + 1].y), a);
+                        acc[j] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (!any_own) return;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        if (!own[j]) continue;
+        v[O] = o0 + j;
+        p[O] = axis_lo(g, O) + (v[O] + 0.5) * g.vs;
+        const double tau = ok[j] ? double(acc[j]) * G.h : march_padded<Rec>(g, recx, plx, p, ts, tE, step);
+        out[(size_t(v[2]) * g.ny + v[1]) * g.nx + v[0]] = float(exp(-coeff * tau));
     }
 }
 
@@ -440,18 +967,102 @@ void launch_pyramid_down(const sf_grid& src, sf_grid& dst, cudaStream_t s) {
     count_launch();
 }
 
+namespace {
+// K2 through the shared tap lists: padded pair records of the level (x-fastest, and z-fastest
+// when some rays leave through an x face), k_tap_build for every plane, then one
+// k_graded_cols pass per exit face over voxel rows [zlo, zhi).
+template <typename W, typename Rec>
+void graded_taps(const sf_grid& level, const double ts[3], double coeff, double step, int zlo, int zhi, float* out,
+                 cudaStream_t s) {
+    const GridDev g = level.dev();
+    // a voxel's exit distance is at most the box's shortest span over |ts_a|: it bounds the
+    // sample count of every plane some voxel selects
+    double T = 1e300;
+    for (int a = 0; a < 3; ++a)
+        if (ts[a] != 0.0) {
+            const double lo = a == 0 ? g.ox : (a == 1 ? g.oy : g.oz), hi = a == 0 ? g.hx : (a == 1 ? g.hy : g.hz);
+            T = std::min(T, (hi - lo) / std::fabs(ts[a]));
+        }
+    const int ns_max = int(std::ceil(T / step)) + 3;
+    const int cap = 4 * ns_max + 4 * 32 + 16;
+    const int n_groups = g.nx + g.ny + g.nz;
+    const PadLayout plx = pad_layout(g.nx, g.ny, g.nz, 0), plz = pad_layout(g.nx, g.ny, g.nz, 2);
+    const bool face_x = ts[0] != 0.0;
+    TapGroup* groups = nullptr;
+    ColTap<W>* taps = nullptr;
+    Rec *px = nullptr, *pz = nullptr;
+    SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&groups), size_t(n_groups) * sizeof(TapGroup), s));
+    SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&taps), size_t(n_groups) * cap * sizeof(ColTap<W>), s));
+    SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&px), size_t(plx.count) * sizeof(Rec), s));
+    if (face_x) SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pz), size_t(plz.count) * sizeof(Rec), s));
+    k_pad_pairs<Rec><<<grid_for(size_t(plx.count)), kBlock, 0, s>>>(level.d, g.nx, g.ny, g.nz, plx, px);
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+    if (face_x) {
+        k_pad_pairs<Rec><<<grid_for(size_t(plz.count)), kBlock, 0, s>>>(level.d, g.nx, g.ny, g.nz, plz, pz);
+        SFB_CUDA(cudaGetLastError());
+        count_launch();
+    }
+    k_tap_build<W><<<(n_groups + kTapWarps - 1) / kTapWarps, kTapWarps * 32, 0, s>>>(g, ts[0], ts[1], ts[2], step,
+                                                                                     cap, plx, plz, groups, taps);
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+    const int lo[3] = {0, 0, zlo}, hi[3] = {g.nx, g.ny, zhi};
+    auto blocks = [&](int E) {  // (L chunk, O block) x (groups of kColPlanes E planes)
+        const int L = E == 0 ? 2 : 0, O = 3 - E - L;
+        const int64_t tiles = int64_t((hi[L] - lo[L] + 31) / 32) * ((hi[O] - lo[O] + kColK - 1) / kColK);
+        return unsigned(tiles * ((hi[E] - lo[E] + kColPlanes - 1) / kColPlanes));
+    };
+    if (ts[1] != 0.0) {
+        k_graded_cols<W, Rec, 1><<<blocks(1), 256, 0, s>>>(
+            g, px, plx, px, plx, ts[0], ts[1], ts[2], coeff, step, zlo, zhi, groups, taps, out);
+        SFB_CUDA(cudaGetLastError());
+        count_launch();
+    }
+    if (ts[2] != 0.0) {
+        k_graded_cols<W, Rec, 2><<<blocks(2), 256, 0, s>>>(
+            g, px, plx, px, plx, ts[0], ts[1], ts[2], coeff, step, zlo, zhi, groups, taps, out);
+        SFB_CUDA(cudaGetLastError());
+        count_launch();
+    }
+    if (face_x) {
+        k_graded_cols<W, Rec, 0><<<blocks(0), 256, 0, s>>>(
+            g, pz, plz, px, plx, ts[0], ts[1], ts[2], coeff, step, zlo, zhi, groups, taps, out);
+        SFB_CUDA(cudaGetLastError());
+        count_launch();
+    }
+    if (pz) SFB_CUDA(cudaFreeAsync(pz, s));
+    SFB_CUDA(cudaFreeAsync(px, s));
+    SFB_CUDA(cudaFreeAsync(taps, s));
+    SFB_CUDA(cudaFreeAsync(groups, s));
+}
+
+bool use_taps(const double ts[3]) {
+    static const int mode = std::getenv("SF_GRADED") ? std::atoi(std::getenv("SF_GRADED")) : 1;  // 0: march
+    (void)ts;
+    return mode != 0;
+}
+}  // namespace
+
 void launch_graded(const sf_grid& level, const double ts[3], double coeff, double step, int zlo, int zhi,
                    float* out, cudaStream_t s, bool fast) {
     if (zhi <= zlo) return;
+    if (use_taps(ts)) {
+        if (fast)
+            graded_taps<float, float2>(level, ts, coeff, step, zlo, zhi, out, s);
+        else
+            graded_taps<double, double2>(level, ts, coeff, step, zlo, zhi, out, s);
+        return;
+    }
+    const size_t rows = size_t(level.nx) * level.ny * size_t(zhi - zlo);
     if (fast) {
         float2* xp = nullptr;
         SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xp), level.count() * sizeof(float2), s));
         k_xpair_f32<<<grid_for(level.count()), kBlock, 0, s>>>(level.d, level.nx, level.ny, level.nz, xp);
         SFB_CUDA(cudaGetLastError());
         count_launch();
-        const size_t rows = size_t(level.nx) * level.ny * size_t(zhi - zlo);
-        k_graded_f32<<<grid_for(rows, 128), 128, 0, s>>>(level.dev(), xp, ts[0], ts[1], ts[2], coeff, step, zlo,
-                                                         zhi, out);
+        k_graded_f32<<<grid_for(rows, 128), 128, 0, s>>>(level.dev(), xp, ts[0], ts[1], ts[2], coeff, step, zlo, zhi,
+                                                         out);
         SFB_CUDA(cudaGetLastError());
         count_launch();
         SFB_CUDA(cudaFreeAsync(xp, s));
@@ -462,7 +1073,6 @@ void launch_graded(const sf_grid& level, const double ts[3], double coeff, doubl
     k_xpair_f64<<<grid_for(level.count()), kBlock, 0, s>>>(level.d, level.nx, level.ny, level.nz, xp);
     SFB_CUDA(cudaGetLastError());
     count_launch();
-    const size_t rows = size_t(level.nx) * level.ny * size_t(zhi - zlo);
     k_graded<<<grid_for(rows, 128), 128, 0, s>>>(level.dev(), xp, ts[0], ts[1], ts[2], coeff, step, zlo, zhi, out);
     SFB_CUDA(cudaGetLastError());
     count_launch();
