@@ -649,13 +649,17 @@ __global__ void __launch_bounds__(256, 3) k_graded_cols(GridDev g, const Rec* __
     __shared__ ColTap<W> tile[kColPlanes][kColTile];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int lo[3] = {0, 0, zlo}, hi[3] = {g.nx, g.ny, zhi};
-    const int nch = (hi[L] - lo[L] + 31) / 32, nOb = (hi[O] - lo[O] + K - 1) / K;
-    const int bt = int(blockIdx.x % (unsigned(nch) * nOb));
-    const int e = lo[E] + int(blockIdx.x / (unsigned(nch) * nOb)) * kColPlanes + warp;
+    // block order: L chunk, then E plane group, then O block, so the blocks in flight cover a thin
+    // O slab of the volume (their rays overlap; a small L2 working set)
+    const int nch = (hi[L] - lo[L] + 31) / 32, neb = (hi[E] - lo[E] + kColPlanes - 1) / kColPlanes;
+    const int ch = int(blockIdx.x % unsigned(nch));
+    const int eb = int((blockIdx.x / unsigned(nch)) % unsigned(neb));
+    const int ob = int(blockIdx.x / (unsigned(nch) * neb));
+    const int e = lo[E] + eb * kColPlanes + warp;
     int v[3] = {0, 0, 0};
-    v[L] = lo[L] + (bt % nch) * 32 + lane;
+    v[L] = lo[L] + ch * 32 + lane;
     v[E] = e;
-    const int o0 = lo[O] + (bt / nch) * K;
+    const int o0 = lo[O] + ob * K;
     const double ts[3] = {tsx, tsy, tsz};
     const bool lane_in = e < hi[E] && v[L] < hi[L];
     double p[3];
@@ -702,12 +706,14 @@ __global__ void __launch_bounds__(256, 3) k_graded_cols(GridDev g, const Rec* __
         for (int j = K; j >= 0; --j)
             if ((j < K && ok[j]) || (j > 0 && ok[j - 1])) jfirst = j;
         const int src = warp_taps ? __ffs(okmask) - 1 : 0;
-        int64_t fallback = __shfl_sync(0xffffffffu, base + int64_t(jfirst) * pl.s[O], src);
-        const Rec* rowp[K + 1];
+        // 32-bit element offsets (a padded level has < 2^31 records): one add + one wide multiply-add
+        // per gather
+        const unsigned fallback = unsigned(__shfl_sync(0xffffffffu, base + int64_t(jfirst) * pl.s[O], src));
+        unsigned rowo[K + 1];
 #pragma unroll
         for (int j = 0; j <= K; ++j) {
             const bool need = (j < K && ok[j]) || (j > 0 && ok[j - 1]);
-            rowp[j] = rec + (need ? base + int64_t(j) * pl.s[O] : fallback);
+            rowo[j] = need ? unsigned(base + int64_t(j) * pl.s[O]) : fallback;
         }
         const ColTap<W>* tp = taps + G.tap0;
         const int n = G.n > 0 ? G.n : 0;
@@ -737,7 +743,7 @@ __global__ void __launch_bounds__(256, 3) k_graded_cols(GridDev g, const Rec* __
 #pragma unroll
                     for (int j = 0; j <= K; ++j)
 #pragma unroll
-                        for (int u = 0; u < U; ++u) r[u][j] = __ldg(rowp[j] + t[u].lin);
+                        for (int u = 0; u < U; ++u) r[u][j] = __ldg(rec + (rowo[j] + unsigned(t[u].lin)));
 #pragma unroll
                     for (int j = 0; j < K; ++j) {
                         W a = acc[j];
@@ -755,7 +761,7 @@ __global__ void __launch_bounds__(256, 3) k_graded_cols(GridDev g, const Rec* __
                     const ColTap<W> ta = tile[warp][k];
                     Rec ra[K + 1];
 #pragma unroll
-                    for (int j = 0; j <= K; ++j) ra[j] = __ldg(rowp[j] + ta.lin);
+                    for (int j = 0; j <= K; ++j) ra[j] = __ldg(rec + (rowo[j] + unsigned(ta.lin)));
 #pragma unroll
                     for (int j = 0; j < K; ++j) {
                         W a = acc[j];
@@ -885,6 +891,137 @@ __global__ void k_combine(Levels lv, GridDev base, int zlo, int zhi, float* __re
     }
 }
 
+// K3a production form: the same 27 taps in the same order with FP32 fmaf (bit-identical to
+// k_conv3<true>), one thread per (x, y) column walking kConvZ rows of z with the 3 x 3 neighbourhoods
+// of planes z - 1, z, z + 1 held in registers: 9 loads per output instead of 27.
+constexpr int kConvZ = 16;
+
+__global__ void __launch_bounds__(256) k_conv3_zwin(const float* __restrict__ in, int nx, int ny, int nz, Kernel27 k,
+                                                    int zlo, int zhi, float* __restrict__ out) {
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
+    const int z0 = zlo + blockIdx.z * kConvZ, z1 = min(z0 + kConvZ, zhi);
+    if (x >= nx || y >= ny) return;
+    const int xs[3] = {max(x - 1, 0), x, min(x + 1, nx - 1)};
+    const int ys[3] = {max(y - 1, 0), y, min(y + 1, ny - 1)};
+    float w[3][3][3];  // [plane z-1, z, z+1][dy][dx]
+    auto load = [&](int zz, float (&pl)[3][3]) {
+        const int zc = zz < 0 ? 0 : (zz > nz - 1 ? nz - 1 : zz);
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) pl[dy][dx] = __ldg(in + (size_t(zc) * ny + ys[dy]) * nx + xs[dx]);
+    };
+    load(z0 - 1, w[0]);
+    load(z0, w[1]);
+    for (int z = z0; z < z1; ++z) {
+        load(z + 1, w[2]);
+        float acc = 0.0f;
+        int t = 0;
+#pragma unroll
+        for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx, ++t) acc = fmaf(k.k[t], w[dz][dy][dx], acc);
+        out[(size_t(z) * ny + y) * nx + x] = acc;
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+                w[0][dy][dx] = w[1][dy][dx];
+                w[1][dy][dx] = w[2][dy][dx];
+            }
+    }
+}
+
+// K3b production form: one thread per 2 x 2 x 2 block of level-0 voxels. For every coarser level
+// the block's eight trilinear cells lie in one 3 x 3 x 3 neighbourhood of that level (the two
+// fine centres of an axis fall in the same or in adjacent coarse cells), loaded once: 27 loads
+// per level for eight voxels instead of 64. Each voxel's lerps are the FP32 operations of
+// k_combine<true> in the same order (bit-identical).
+__global__ void __launch_bounds__(256) k_combine_blk(Levels lv, GridDev base, int zlo, int zhi,
+                                                     float* __restrict__ out) {
+    const int bx = blockIdx.x * 32 + threadIdx.x, by = blockIdx.y * 8 + threadIdx.y;
+    const int x0 = 2 * bx, y0 = 2 * by, z0 = zlo + 2 * int(blockIdx.z);
+    if (x0 >= base.nx || y0 >= base.ny || z0 >= zhi) return;
+    const int c0[3] = {x0, y0, z0};
+    const int lim[3] = {base.nx, base.ny, zhi};
+    float acc[2][2][2];  // [z][y][x]
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int x = min(x0 + k, base.nx - 1), y = min(y0 + j, base.ny - 1), z = min(z0 + i, zhi - 1);
+                acc[i][j][k] = float(lv.scale[0] * double(__ldg(lv.g[0].v + (size_t(z) * base.ny + y) * base.nx + x)));
+            }
+    float inv = 1.0f;
+    for (int li = 1; li < lv.n; ++li) {
+        inv *= 0.5f;
+        const GridDev& g = lv.g[li];
+        const int n[3] = {g.nx, g.ny, g.nz};
+        int idx[3][3];       // clamped coarse indices b, b + 1, b + 2 per axis
+        float t[3][2];       // fractions of the two fine centres
+        int sel[3];          // 1: the high fine centre's cell starts at b + 1
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float flo = (float(c0[a]) + 0.5f) * inv - 0.5f, fhi = (float(c0[a] + 1) + 0.5f) * inv - 0.5f;
+            const float llo = floorf(flo), lhi = floorf(fhi);
+            const int b = int(llo);
+            t[a][0] = flo - llo;
+            t[a][1] = fhi - lhi;
+            sel[a] = int(lhi) - b;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) idx[a][q] = max(0, min(b + q, n[a] - 1));
+        }
+        float V[3][3][3];  // [z][y][x]
+#pragma unroll
+        for (int qz = 0; qz < 3; ++qz)
+#pragma unroll
+            for (int qy = 0; qy < 3; ++qy)
+#pragma unroll
+                for (int qx = 0; qx < 3; ++qx)
+                    V[qz][qy][qx] = __ldg(g.v + (size_t(idx[2][qz]) * g.ny + idx[1][qy]) * g.nx + idx[0][qx]);
+        // x lerps of every (y', z') row for the low / high fine x
+        float cx[2][3][3];  // [fine x][z'][y']
+#pragma unroll
+        for (int qz = 0; qz < 3; ++qz)
+#pragma unroll
+            for (int qy = 0; qy < 3; ++qy) {
+                const float* r = V[qz][qy];
+                cx[0][qz][qy] = fmaf(t[0][0], r[1] - r[0], r[0]);
+                cx[1][qz][qy] = sel[0] ? fmaf(t[0][1], r[2] - r[1], r[1]) : fmaf(t[0][1], r[1] - r[0], r[0]);
+            }
+        const float sc = float(lv.scale[li]);
+#pragma unroll
+        for (int fz = 0; fz < 2; ++fz)
+#pragma unroll
+            for (int fy = 0; fy < 2; ++fy)
+#pragma unroll
+                for (int fx = 0; fx < 2; ++fx) {
+                    const int oy = fy ? sel[1] : 0, oz = fz ? sel[2] : 0;
+                    const float ty = t[1][fy], tz = t[2][fz];
+                    // rows (y0, z0), (y1, z0), (y0, z1), (y1, z1) of this voxel's cell
+                    const float c00 = oy ? (oz ? cx[fx][1][1] : cx[fx][0][1]) : (oz ? cx[fx][1][0] : cx[fx][0][0]);
+                    const float c10 = oy ? (oz ? cx[fx][1][2] : cx[fx][0][2]) : (oz ? cx[fx][1][1] : cx[fx][0][1]);
+                    const float c01 = oy ? (oz ? cx[fx][2][1] : cx[fx][1][1]) : (oz ? cx[fx][2][0] : cx[fx][1][0]);
+                    const float c11 = oy ? (oz ? cx[fx][2][2] : cx[fx][1][2]) : (oz ? cx[fx][2][1] : cx[fx][1][1]);
+                    const float e0 = fmaf(ty, c10 - c00, c00), e1 = fmaf(ty, c11 - c01, c01);
+                    acc[fz][fy][fx] += sc * fmaf(tz, e1 - e0, e0);
+                }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int x = x0 + k, y = y0 + j, z = z0 + i;
+                if (x < lim[0] && y < lim[1] && z < lim[2]) out[(size_t(z - zlo) * base.ny + y) * base.nx + x] = acc[i][j][k];
+            }
+}
+
 __global__ void k_interleave(const float* __restrict__ a, const float* __restrict__ b,
                              float2* __restrict__ out, size_t n) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
@@ -971,9 +1108,47 @@ namespace {
 // K2 through the shared tap lists: padded pair records of the level (x-fastest, and z-fastest
 // when some rays leave through an x face), k_tap_build for every plane, then one
 // k_graded_cols pass per exit face over voxel rows [zlo, zhi).
+// The level's padded records of one layout: from the pyramid's cache (made on first use), else
+// stream-ordered scratch that the caller frees.
+template <typename Rec>
+Rec* padded_records(const sf_grid& level, const PadLayout& pl, PadCache* cache, cudaStream_t s, bool& scratch) {
+    const int prec = sizeof(Rec) == sizeof(double2) ? 1 : 0, lay = pl.L == 0 ? 0 : 1;
+    auto fill = [&](Rec* r) {
+        k_pad_pairs<Rec><<<grid_for(size_t(pl.count)), kBlock, 0, s>>>(level.d, level.nx, level.ny, level.nz, pl, r);
+        SFB_CUDA(cudaGetLastError());
+        count_launch();
+    };
+    if (!cache) {
+        Rec* r = nullptr;
+        SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&r), size_t(pl.count) * sizeof(Rec), s));
+        fill(r);
+        scratch = true;
+        return r;
+    }
+    std::lock_guard<std::mutex> lk(cache->mu);
+    scratch = false;
+    if (!cache->rec[prec][lay]) {
+        void* r = nullptr;
+        SFB_CUDA(cudaMalloc(&r, size_t(pl.count) * sizeof(Rec)));
+        cudaEvent_t ev = nullptr;
+        const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            cudaFree(r);
+            cuda_check(e, "cudaEventCreate");
+        }
+        cache->rec[prec][lay] = r;
+        cache->ready[prec][lay] = ev;
+        fill(static_cast<Rec*>(r));
+        SFB_CUDA(cudaEventRecord(ev, s));
+    } else {
+        SFB_CUDA(cudaStreamWaitEvent(s, cache->ready[prec][lay], 0));
+    }
+    return static_cast<Rec*>(cache->rec[prec][lay]);
+}
+
 template <typename W, typename Rec>
 void graded_taps(const sf_grid& level, const double ts[3], double coeff, double step, int zlo, int zhi, float* out,
-                 cudaStream_t s) {
+                 cudaStream_t s, PadCache* cache) {
     const GridDev g = level.dev();
     // a voxel's exit distance is at most the box's shortest span over |ts_a|: it bounds the
     // sample count of every plane some voxel selects
@@ -991,24 +1166,17 @@ void graded_taps(const sf_grid& level, const double ts[3], double coeff, double 
     TapGroup* groups = nullptr;
     ColTap<W>* taps = nullptr;
     Rec *px = nullptr, *pz = nullptr;
+    bool px_scratch = false, pz_scratch = false;
     SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&groups), size_t(n_groups) * sizeof(TapGroup), s));
     SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&taps), size_t(n_groups) * cap * sizeof(ColTap<W>), s));
-    SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&px), size_t(plx.count) * sizeof(Rec), s));
-    if (face_x) SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pz), size_t(plz.count) * sizeof(Rec), s));
-    k_pad_pairs<Rec><<<grid_for(size_t(plx.count)), kBlock, 0, s>>>(level.d, g.nx, g.ny, g.nz, plx, px);
-    SFB_CUDA(cudaGetLastError());
-    count_launch();
-    if (face_x) {
-        k_pad_pairs<Rec><<<grid_for(size_t(plz.count)), kBlock, 0, s>>>(level.d, g.nx, g.ny, g.nz, plz, pz);
-        SFB_CUDA(cudaGetLastError());
-        count_launch();
-    }
+    px = padded_records<Rec>(level, plx, cache, s, px_scratch);
+    if (face_x) pz = padded_records<Rec>(level, plz, cache, s, pz_scratch);
     k_tap_build<W><<<(n_groups + kTapWarps - 1) / kTapWarps, kTapWarps * 32, 0, s>>>(g, ts[0], ts[1], ts[2], step,
                                                                                      cap, plx, plz, groups, taps);
     SFB_CUDA(cudaGetLastError());
     count_launch();
     const int lo[3] = {0, 0, zlo}, hi[3] = {g.nx, g.ny, zhi};
-    auto blocks = [&](int E) {  // (L chunk, O block) x (groups of kColPlanes E planes)
+    auto blocks = [&](int E) {  // L chunks x groups of kColPlanes E planes x O blocks
         const int L = E == 0 ? 2 : 0, O = 3 - E - L;
         const int64_t tiles = int64_t((hi[L] - lo[L] + 31) / 32) * ((hi[O] - lo[O] + kColK - 1) / kColK);
         return unsigned(tiles * ((hi[E] - lo[E] + kColPlanes - 1) / kColPlanes));
@@ -1031,8 +1199,8 @@ void graded_taps(const sf_grid& level, const double ts[3], double coeff, double 
         SFB_CUDA(cudaGetLastError());
         count_launch();
     }
-    if (pz) SFB_CUDA(cudaFreeAsync(pz, s));
-    SFB_CUDA(cudaFreeAsync(px, s));
+    if (pz && pz_scratch) SFB_CUDA(cudaFreeAsync(pz, s));
+    if (px_scratch) SFB_CUDA(cudaFreeAsync(px, s));
     SFB_CUDA(cudaFreeAsync(taps, s));
     SFB_CUDA(cudaFreeAsync(groups, s));
 }
@@ -1045,13 +1213,16 @@ bool use_taps(const double ts[3]) {
 }  // namespace
 
 void launch_graded(const sf_grid& level, const double ts[3], double coeff, double step, int zlo, int zhi,
-                   float* out, cudaStream_t s, bool fast) {
+                   float* out, cudaStream_t s, bool fast, PadCache* cache) {
     if (zhi <= zlo) return;
-    if (use_taps(ts)) {
+    // the tap kernels address records with 32-bit element offsets
+    const bool fits = pad_layout(level.nx, level.ny, level.nz, 0).count < (int64_t(1) << 31) &&
+                      pad_layout(level.nx, level.ny, level.nz, 2).count < (int64_t(1) << 31);
+    if (use_taps(ts) && fits) {
         if (fast)
-            graded_taps<float, float2>(level, ts, coeff, step, zlo, zhi, out, s);
+            graded_taps<float, float2>(level, ts, coeff, step, zlo, zhi, out, s, cache);
         else
-            graded_taps<double, double2>(level, ts, coeff, step, zlo, zhi, out, s);
+            graded_taps<double, double2>(level, ts, coeff, step, zlo, zhi, out, s, cache);
         return;
     }
     const size_t rows = size_t(level.nx) * level.ny * size_t(zhi - zlo);
@@ -1083,8 +1254,14 @@ void launch_conv3(const sf_grid& in, const float k27[27], int zlo, int zhi, floa
     if (zhi <= zlo) return;
     Kernel27 k;
     for (int i = 0; i < 27; ++i) k.k[i] = k27[i];
-    (fast ? k_conv3<true> : k_conv3<false>)<<<grid_for(size_t(in.nx) * in.ny * size_t(zhi - zlo)), kBlock, 0, s>>>(
-        in.d, in.nx, in.ny, in.nz, k, zlo, zhi, out);
+    static const bool v1 = std::getenv("SF_BUILD_V1") != nullptr;  // A/B: the one-thread-per-voxel kernel
+    if (fast && !v1) {
+        const dim3 grid((in.nx + 31) / 32, (in.ny + 7) / 8, (zhi - zlo + kConvZ - 1) / kConvZ);
+        k_conv3_zwin<<<grid, dim3(32, 8), 0, s>>>(in.d, in.nx, in.ny, in.nz, k, zlo, zhi, out);
+    } else {
+        (fast ? k_conv3<true> : k_conv3<false>)<<<grid_for(size_t(in.nx) * in.ny * size_t(zhi - zlo)), kBlock, 0,
+                                                   s>>>(in.d, in.nx, in.ny, in.nz, k, zlo, zhi, out);
+    }
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
@@ -1109,8 +1286,14 @@ void launch_combine(const std::vector<const sf_grid*>& conv, const std::vector<f
                   (a.nz == 2 * b.nz || (a.nz == 1 && b.nz == 1)) && b.vs == 2.0 * a.vs &&
                   b.origin[0] == a.origin[0] && b.origin[1] == a.origin[1] && b.origin[2] == a.origin[2];
     }
-    (halving ? k_combine<true> : k_combine<false>)<<<grid_for(size_t(base.nx) * base.ny * size_t(zhi - zlo)), kBlock, 0,
-                                                      s>>>(lv, base.dev(), zlo, zhi, out);
+    static const bool v1 = std::getenv("SF_BUILD_V1") != nullptr;
+    if (halving && !v1) {
+        const dim3 grid(((base.nx + 1) / 2 + 31) / 32, ((base.ny + 1) / 2 + 7) / 8, (zhi - zlo + 1) / 2);
+        k_combine_blk<<<grid, dim3(32, 8), 0, s>>>(lv, base.dev(), zlo, zhi, out);
+    } else {
+        (halving ? k_combine<true> : k_combine<false>)<<<grid_for(size_t(base.nx) * base.ny * size_t(zhi - zlo)),
+                                                          kBlock, 0, s>>>(lv, base.dev(), zlo, zhi, out);
+    }
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }

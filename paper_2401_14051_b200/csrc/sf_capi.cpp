@@ -525,6 +525,7 @@ int sf_pyramid_build(const sf_grid* finest, sf_pyramid** out, sf_stream stream) 
                 g->owned = false;
                 off += g->count();
                 p->levels.push_back(g.release());
+                p->pads.push_back(std::make_unique<sfb::PadCache>());
             }
             SFB_CUDA(cudaMemcpyAsync(p->levels[0]->d, finest->d, finest->count() * sizeof(float),
                                      cudaMemcpyDeviceToDevice, stream));
@@ -578,7 +579,8 @@ sf_grid* graded_level(const sf_pyramid* p, int level, const double light[3], dou
     sf_grid* out = scratch ? new_scratch_grid(rho->nx, rho->ny, rho->nz, rho->vs, rho->origin, s)
                            : new_grid(rho->nx, rho->ny, rho->nz, rho->vs, rho->origin);
     try {
-        sfb::launch_graded(*rho, ts, coeff, step, zlo, zhi < 0 ? rho->nz : zhi, out->d, s, fast);
+        sfb::launch_graded(*rho, ts, coeff, step, zlo, zhi < 0 ? rho->nz : zhi, out->d, s, fast,
+                           p->pads.size() > size_t(level) ? p->pads[size_t(level)].get() : nullptr);
     } catch (...) {
         free_grid(out);
         throw;

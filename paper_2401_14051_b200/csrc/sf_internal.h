@@ -6,6 +6,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -69,9 +71,28 @@ struct sf_grid {
     }
 };
 
+namespace sfb {
+// Padded pair records of one pyramid level (the input of the graded-transmittance tap kernels),
+// made on first use and kept with the pyramid (the density is immutable): [FP32, FP64] x
+// [x-fastest, z-fastest]. `ready` orders later users on other streams after the fill.
+struct PadCache {
+    std::mutex mu;
+    void* rec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    cudaEvent_t ready[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    ~PadCache() {
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b) {
+                if (rec[a][b]) cudaFree(rec[a][b]);
+                if (ready[a][b]) cudaEventDestroy(ready[a][b]);
+            }
+    }
+};
+}  // namespace sfb
+
 struct sf_pyramid {
     std::vector<sf_grid*> levels;  // level 0 is a copy of the finest grid
     float* block = nullptr;        // one allocation holding every level (levels are views)
+    std::vector<std::unique_ptr<sfb::PadCache>> pads;  // one per level
 };
 
 struct sf_tvol {
@@ -138,8 +159,9 @@ void launch_pyramid_down(const sf_grid& src, sf_grid& dst, cudaStream_t s);
 // Per-light build kernels over voxel rows z in [zlo, zhi) (the whole grid, or a z-slab of a
 // build sharded over GPUs). launch_combine writes rows [zlo, zhi) to out[0...].
 // fast: FP32 march (production bf16 path; ~1e-6 relative optical depth) instead of the FP64 reference march
+// cache (optional): the level's padded records, kept between calls
 void launch_graded(const sf_grid& level, const double to_source[3], double coeff, double step, int zlo, int zhi,
-                   float* out, cudaStream_t s, bool fast = false);
+                   float* out, cudaStream_t s, bool fast = false, PadCache* cache = nullptr);
 // fast: FP32 accumulation / interpolation (production build), else the reference's FP64.
 void launch_conv3(const sf_grid& in, const float k27[27], int zlo, int zhi, float* out, cudaStream_t s,
                   bool fast = false);
