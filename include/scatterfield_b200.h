@@ -132,9 +132,11 @@ int sf_combine_transmittance(const sf_grid* const* fields, int n, const float* k
 int sf_build_transmittance_volume(const sf_pyramid* p, const double light[3],
                                   const float* kernels, const float* scales, double lambda,
                                   double step_scale, sf_tvol** out, sf_stream stream);
-/* Build flags. SF_BUILD_FP32_MARCH: the graded-transmittance march in FP32 (ray setup still
- * FP64, compensated sum) — the production build feeding the bf16 query path: ~1e-6 relative
- * optical depth against the FP64 reference march, 2-3x faster. 0 = the reference's FP64. */
+/* Build flags. SF_BUILD_FP32_MARCH: the graded transmittance summed in FP32 (ray setup, plane
+ * tap weights and sample positions FP64) — the production build feeding the bf16 query path:
+ * |dT| ~3e-7 against the FP64 reference march, ~2x faster. 0 = FP64 sums, bit-identical to the
+ * reference's march in practice. Both evaluate the midpoint sum of every voxel through the
+ * shared per-plane tap lists (sf_build.cu, k_tap_build / k_graded_cols). */
 enum { SF_BUILD_FP32_MARCH = 1 };
 int sf_build_transmittance_volume_ex(const sf_pyramid* p, const double light[3],
                                      const float* kernels, const float* scales, double lambda,
@@ -142,7 +144,8 @@ int sf_build_transmittance_volume_ex(const sf_pyramid* p, const double light[3],
 /* Rows z in [z0, z1) of build_transmittance_volume's level-0 values, bit-identical to the
  * same rows of the full build: the per-light build sharded by z-slab over GPUs (SURVEY.md
  * §8e). Level 0 is marched only for the slab plus a 2-row halo, coarser levels whole.
- * out h/d [(z1-z0)][ny][nx]; gather the slabs and wrap them with sf_tvol_from_values. */
+ * out h/d [(z1-z0)][ny][nx] (device: asynchronous on `stream`); gather the slabs into
+ * sf_scene_tvol_storage, or wrap them with sf_tvol_from_values. */
 int sf_build_transmittance_slab(const sf_pyramid* p, const double light[3], const float* kernels,
                                 const float* scales, double lambda, double step_scale, int flags, int z0,
                                 int z1, float* out, sf_stream stream);
@@ -216,9 +219,30 @@ int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_templa
                     const sf_template* highlight, const sf_phase_model* model,
                     const sf_phase_table* table, double template_scale, sf_scene** out);
 void sf_scene_destroy(sf_scene* s);
+/* Per-light / per-frame rebuild of a scene's transmittance feature volume:
+ * build_transmittance_volume(pyramid, light, weights, cfg) (feature_pipeline.h:119-122) into the
+ * scene's own volume, then the query records, asynchronously on `stream` (no host sync; one
+ * allocation on the first call). This is render_neural's per-call build
+ * (src/predictor.cpp:593-599) for a renderer that keeps the scene across lights (config C3) or
+ * frames (config C5). `p` must be the pyramid of the scene's density grid; kernels == NULL
+ * selects the identity combiner; flags as sf_build_transmittance_volume_ex. */
+int sf_scene_relight(sf_scene* s, const sf_pyramid* p, const double light[3], const float* kernels,
+                     const float* scales, double lambda, double step_scale, int flags, sf_stream stream);
+/* The scene's own transmittance storage (device, [nz][ny][nx] f32, allocated on first use) for a
+ * volume assembled outside the library — the per-light build sharded by z-slab over GPUs
+ * (sf_build_transmittance_slab on every rank, then an all-gather into this storage);
+ * sf_scene_commit_tvol then makes it the scene's volume (light = its light direction) and
+ * refreshes the query records on `stream`. */
+int sf_scene_tvol_storage(sf_scene* s, float** out);
+int sf_scene_commit_tvol(sf_scene* s, const double light[3], sf_stream stream);
 /* For each query row (p, omega, l): sample_features for both templates,
  * make_config (alpha = angle(omega, l)), backbone forward, decode. queries h/d
- * [n][9]; F_out h/d [n][3] f64; y_out optional h/d [n][3] f32. */
+ * [n][9]; F_out h/d [n][3] f64; y_out optional h/d [n][3] f32.
+ * Errors: a row whose highlight placement is undefined (light entry == p, where the
+ * reference's place_template throws, src/templates.cpp:219-220) makes the call return
+ * SF_ERR_INVALID_ARGUMENT when any argument is host memory (the call synchronizes); with
+ * device queries and outputs the call stays asynchronous and such rows come out as NaN
+ * (y and F, both precisions). */
 int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium,
              int64_t n, const double* queries, int precision, double* F_out, float* y_out,
              sf_stream stream);
@@ -253,9 +277,12 @@ enum sf_stage {
     SF_STAGE_SLICE = 3,              /* per-layer sort + pools */
     SF_STAGE_BACKBONE = 4,           /* network forward + decode */
     SF_STAGE_SAMPLE_SORT = 5,        /* fused features + sort/pool + bf16 operand packing */
-    SF_STAGE_COUNT = 6
+    SF_STAGE_MARCH = 6,              /* graded transmittance, every level (sf_scene_relight) */
+    SF_STAGE_COMBINER = 7,           /* the 3D-CNN combiner: conv3 + combine (sf_scene_relight) */
+    SF_STAGE_RECORDS = 8,            /* query records of the new volume (sf_scene_relight) */
+    SF_STAGE_COUNT = 9
 };
-/* When enabled, sf_query/sf_predict record a CUDA event pair around every stage on
+/* When enabled, sf_query/sf_predict/sf_scene_relight record a CUDA event pair around every stage on
  * the caller's stream (no synchronization). sf_profile_read synchronizes on those
  * events, writes the summed device milliseconds and launch counts per stage, and
  * resets the accumulators. */

@@ -92,6 +92,9 @@ _SIGS = {
     "sf_predict": (I, [P, I64, P, P, I, P, P, P]),
     "sf_scene_create": (I, [P, P, P, P, P, P, D, PP]),
     "sf_scene_destroy": (None, [P]),
+    "sf_scene_relight": (I, [P, P, P, P, P, D, D, I, P]),
+    "sf_scene_tvol_storage": (I, [P, PP]),
+    "sf_scene_commit_tvol": (I, [P, P, P]),
     "sf_query": (I, [P, P, P, I64, P, I, P, P, P]),
     "sf_query_media": (I, [P, P, I64, P, P, I, P, P, P]),
     "sf_bake_field": (I, [P, P, P, P, I, P, P]),
@@ -105,7 +108,8 @@ _SIGS = {
     "sf_probe_l2_read": (I, [C.c_size_t, I, P]),
 }
 
-STAGES = ("config", "features_diffuse", "features_highlight", "slice", "backbone", "sample_sort")
+STAGES = ("config", "features_diffuse", "features_highlight", "slice", "backbone", "sample_sort", "march", "combiner",
+          "records")
 
 
 def profile_read():

@@ -643,6 +643,41 @@ class Scene:
         self._h = h
         self.model = model
 
+    def relight(self, pyramid: DensityPyramid, light, weights: CombinerWeights = None, cfg: FeatureConfig = None,
+                fast: bool = False, stream=None):
+        """Rebuild the scene's transmittance feature volume for `light` (build_transmittance_volume,
+        src/feature_pipeline.cpp:200-211, as render_neural runs it per call, src/predictor.cpp:593-599)
+        into the scene's own storage, asynchronously on `stream`. `pyramid` is the density's."""
+        cfg = cfg or FeatureConfig()
+        weights = weights or CombinerWeights.identity(pyramid.level_count())
+        if weights.level_count() != pyramid.level_count():
+            raise ScatterfieldError(7, "combine_transmittance: weight/level mismatch")
+        k = np.ascontiguousarray(weights.kernels, np.float32)
+        sc = np.ascontiguousarray(weights.scales, np.float32)
+        check(lib.sf_scene_relight(self._h, pyramid._h, dvec(light), ptr(k), ptr(sc), float(cfg.lambda_),
+                                   float(cfg.step_scale), BUILD_FP32_MARCH if fast else 0, stream_ptr(stream)))
+        self._pyramid = pyramid
+        self.light = _normalize(light)
+        return self
+
+    def tvol_storage(self):
+        """The scene's own transmittance storage as a CUDA tensor view [nz, ny, nx] float32 (for a
+        volume assembled outside the library, e.g. gathered z-slabs); then commit_tvol(light)."""
+        import torch
+        p = C.c_void_p()
+        check(lib.sf_scene_tvol_storage(self._h, C.byref(p)))
+        nx, ny, nz = self._keep[0].dims
+
+        class _Cai:
+            __cuda_array_interface__ = {"shape": (nz, ny, nx), "typestr": "<f4", "data": (p.value, False),
+                                        "version": 3, "strides": None}
+        return torch.as_tensor(_Cai(), device="cuda")
+
+    def commit_tvol(self, light, stream=None):
+        check(lib.sf_scene_commit_tvol(self._h, dvec(light), stream_ptr(stream)))
+        self.light = _normalize(light)
+        return self
+
     def __del__(self):
         if getattr(self, "_h", None):
             lib.sf_scene_destroy(self._h)

@@ -147,6 +147,8 @@ void sync(cudaStream_t s) { SFB_CUDA(cudaStreamSynchronize(s)); }
 sf_grid* new_grid(int nx, int ny, int nz, double vs, const double o[3]) {
     if (nx <= 0 || ny <= 0 || nz <= 0) fail(SF_ERR_BAD_DIMS, "density grid: dims must be positive");
     if (!(vs > 0.0)) fail(SF_ERR_BAD_VALUE, "density grid: voxel_size must be positive");
+    // the kernels index voxels with 32-bit integers
+    if (int64_t(nx) * ny * nz >= (int64_t(1) << 31)) fail(SF_ERR_BAD_DIMS, "density grid: more than 2^31 - 1 voxels");
     auto g = std::make_unique<sf_grid>();
     g->nx = nx;
     g->ny = ny;
@@ -606,7 +608,7 @@ void combiner_weights(int L, const float* kernels, const float* scales, std::vec
 // [z0, z1) into out.
 void conv_combine(const std::vector<const sf_grid*>& fields, const std::vector<float>& K,
                   const std::vector<float>& S, int c0, int c1, int z0, int z1, float* out, cudaStream_t s,
-                  bool fast = false) {
+                  bool fast = false, bool sync_end = true) {
     const sf_grid& base = *fields[0];
     std::vector<sf_grid*> conv;
     try {
@@ -618,7 +620,7 @@ void conv_combine(const std::vector<const sf_grid*>& fields, const std::vector<f
         }
         std::vector<const sf_grid*> cv(conv.begin(), conv.end());
         sfb::launch_combine(cv, S, base, z0, z1, out, s, fast);
-        sync(s);
+        if (sync_end) sync(s);  // scratch grids are stream-ordered pool memory: no sync needed to free them
     } catch (...) {
         for (sf_grid* c : conv) free_grid(c);
         throw;
@@ -736,14 +738,14 @@ int sf_build_transmittance_slab(const sf_pyramid* p, const double light[3], cons
             std::vector<float> K, S;
             combiner_weights(int(fields.size()), kernels, scales, K, S);
             std::vector<const sf_grid*> f(fields.begin(), fields.end());
-            conv_combine(f, K, S, c0, c1, z0, z1, o.d, stream, fast);
+            conv_combine(f, K, S, c0, c1, z0, z1, o.d, stream, fast, o.host != nullptr);
         } catch (...) {
             for (sf_grid* g : fields) free_grid(g);
             throw;
         }
         for (sf_grid* g : fields) free_grid(g);
         o.finish();
-        sync(stream);
+        if (o.host) sync(stream);  // device output: asynchronous on `stream`
     });
 }
 
@@ -1021,19 +1023,6 @@ void check_precision(const sf_backbone& b, int precision, cudaStream_t s) {
     sfb::tc_prepare(const_cast<sf_backbone&>(b), s);
 }
 
-// Copy stream for the host-I/O overlap of the bf16 query (one per process; calls serialise on it).
-struct CopyStream {
-    std::mutex mu;
-    cudaStream_t cs = nullptr;
-};
-CopyStream& copy_stream() {
-    static CopyStream* c = [] {
-        auto* p = new CopyStream;
-        SFB_CUDA(cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking));
-        return p;
-    }();
-    return *c;
-}
 
 // Event recorded on `from` and waited on by `to`; `ev` a reusable event (a wait captures the
 // event's state when it is enqueued, so re-recording it later is safe).
@@ -1058,6 +1047,7 @@ struct Workspace {
     cudaEvent_t done = nullptr;        // recorded at the end of the last call's work
     cudaStream_t last = nullptr;
     bool used = false;
+    cudaStream_t copy = nullptr;       // this device's copy stream for the host-I/O overlap
 };
 std::mutex g_ws_mu;
 std::unordered_map<int, Workspace>& workspaces() {
@@ -1144,6 +1134,9 @@ int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_templa
         const sf_grid& tv = *tvol->values;
         if (tv.nx != density->nx || tv.ny != density->ny || tv.nz != density->nz)
             fail(SF_ERR_SHAPE_MISMATCH, "scene: transmittance volume geometry differs");
+        // the production sampler addresses 32-byte xy-quad records with unsigned 32-bit indices
+        if (sfb::xpair_records(density->nx, density->ny, density->nz) / 2 >= (size_t(1) << 32))
+            fail(SF_ERR_BAD_DIMS, "scene: volume too large for the query records (2^32 records)");
         auto s = std::make_unique<sf_scene>();
         s->density = density;
         s->tvol = tvol;
@@ -1160,7 +1153,7 @@ int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_templa
             SFB_CUDA(cudaMalloc(&s->d_planes, size_t(s->n_planes) * table->a * (table->h + 1) * sizeof(float2)));
             SFB_CUDA(cudaMalloc(&s->d_pre, std::max<size_t>(1, size_t(dt->total)) * 2 * sizeof(float4)));
             sfb::launch_interleave(density->d, tv.d, s->d_dt, density->count(), nullptr);
-            sfb::launch_xpair(s->d_dt, density->nx, density->ny, density->nz, s->d_dt4, nullptr);
+            sfb::launch_xpair(density->d, tv.d, density->nx, density->ny, density->nz, s->d_dt4, nullptr);
             sfb::launch_blend_planes(*table, *model, s->d_planes, nullptr);
             SFB_CUDA(cudaDeviceSynchronize());
         } catch (...) {
@@ -1174,8 +1167,78 @@ int sf_scene_create(const sf_grid* density, const sf_tvol* tvol, const sf_templa
     });
 }
 
+// the scene's own transmittance volume (one allocation on first use, kept)
+static sf_tvol* scene_own_tvol(sf_scene* s) {
+    if (!s->own_tvol) {
+        const sf_grid& d = *s->density;
+        auto t = std::make_unique<sf_tvol>();
+        t->values = new_grid(d.nx, d.ny, d.nz, d.vs, d.origin);
+        s->own_tvol = t.release();
+    }
+    return s->own_tvol;
+}
+
+int sf_scene_relight(sf_scene* s, const sf_pyramid* p, const double light[3], const float* kernels,
+                     const float* scales, double lambda, double step_scale, int flags, sf_stream stream) {
+    return guard([&] {
+        if (!s || !p || p->levels.empty()) fail(SF_ERR_INVALID_ARGUMENT, "scene_relight: null scene or pyramid");
+        const sf_grid& g0 = *p->levels[0];
+        const sf_grid& d = *s->density;
+        if (g0.nx != d.nx || g0.ny != d.ny || g0.nz != d.nz || g0.vs != d.vs || g0.origin[0] != d.origin[0] ||
+            g0.origin[1] != d.origin[1] || g0.origin[2] != d.origin[2])
+            fail(SF_ERR_SHAPE_MISMATCH, "scene_relight: pyramid geometry differs from the scene's density");
+        const bool fast = (flags & SF_BUILD_FP32_MARCH) != 0;
+        const int L = int(p->levels.size());
+        sf_tvol* t = scene_own_tvol(s);  // first relight: the scene's own volume (one allocation, kept)
+        normalize3(light, t->light);
+        combiner_weights(L, kernels, scales, t->kernels, t->scales);
+        std::vector<sf_grid*> fields;
+        try {
+            {
+                StageScope st(SF_STAGE_MARCH, stream);
+                for (int i = 0; i < L; ++i) {
+                    const double step = step_scale * p->levels[size_t(i)]->vs;
+                    fields.push_back(graded_level(p, i, light, lambda, step, stream, true, 0, -1, fast));
+                }
+            }
+            std::vector<const sf_grid*> f(fields.begin(), fields.end());
+            StageScope st(SF_STAGE_COMBINER, stream);
+            conv_combine(f, t->kernels, t->scales, 0, d.nz, 0, d.nz, t->values->d, stream, fast, false);
+        } catch (...) {
+            for (sf_grid* g : fields) free_grid(g);
+            throw;
+        }
+        for (sf_grid* g : fields) free_grid(g);
+        s->tvol = t;
+        StageScope st(SF_STAGE_RECORDS, stream);
+        sfb::launch_xpair(d.d, t->values->d, d.nx, d.ny, d.nz, s->d_dt4, stream);
+        s->dt_stale = true;
+    });
+}
+
+int sf_scene_tvol_storage(sf_scene* s, float** out) {
+    return guard([&] {
+        if (!s || !out) fail(SF_ERR_INVALID_ARGUMENT, "scene_tvol_storage: null argument");
+        *out = scene_own_tvol(s)->values->d;
+    });
+}
+
+int sf_scene_commit_tvol(sf_scene* s, const double light[3], sf_stream stream) {
+    return guard([&] {
+        if (!s) fail(SF_ERR_INVALID_ARGUMENT, "scene_commit_tvol: null scene");
+        sf_tvol* t = scene_own_tvol(s);
+        normalize3(light, t->light);
+        s->tvol = t;
+        const sf_grid& d = *s->density;
+        StageScope st(SF_STAGE_RECORDS, stream);
+        sfb::launch_xpair(d.d, t->values->d, d.nx, d.ny, d.nz, s->d_dt4, stream);
+        s->dt_stale = true;
+    });
+}
+
 void sf_scene_destroy(sf_scene* s) {
     if (!s) return;
+    sf_tvol_destroy(s->own_tvol);
     cudaFree(s->d_dt);
     cudaFree(s->d_dt4);
     cudaFree(s->d_planes);
@@ -1184,6 +1247,14 @@ void sf_scene_destroy(sf_scene* s) {
 }
 
 namespace {
+// The interleaved {density, transmittance} volume of the exact (FP32) path after a relight.
+void refresh_dt(const sf_scene* s, cudaStream_t stream) {
+    if (!s->dt_stale) return;
+    sf_scene* m = const_cast<sf_scene*>(s);
+    sfb::launch_interleave(s->density->d, s->tvol->values->d, m->d_dt, s->density->count(), stream);
+    m->dt_stale = false;
+}
+
 // sf_query / sf_query_media: medium is the scene-wide medium, media (nullable) per-query
 // {g, albedo rgb} rows that override it (single-lobe HG per query).
 void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium, const double* media_in,
@@ -1315,6 +1386,7 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             } else if (ws.used && ws.last != stream) {
                 SFB_CUDA(cudaStreamWaitEvent(stream, ws.done, 0));  // the previous call, other stream
             }
+            const bool had_prev = ws.used;
             ws.used = true;
             ws.last = stream;
             struct DoneGuard {  // on every exit path: later calls order after this one
@@ -1350,13 +1422,13 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                                               s->template_scale);
             sc.dt4 = s->d_dt4;
             sfb::TemplateDev dt = sfb::template_dev(*s->dt), ht = sfb::template_dev(*s->ht);
-            CopyStream& cps = copy_stream();
-            std::unique_lock<std::mutex> clk(cps.mu, std::defer_lock);
             cudaStream_t cs = stream;
-            if (h_in || h_out) {
-                clk.lock();
-                cs = cps.cs;
-                stream_wait(cs, stream, next_event());  // earlier uses of the workspace are on `stream`
+            if (h_in || h_out) {  // the device's copy stream (calls on one device hold g_ws_mu)
+                if (!ws.copy) SFB_CUDA(cudaStreamCreateWithFlags(&ws.copy, cudaStreamNonBlocking));
+                cs = ws.copy;
+                // the rows may land as soon as the previous call is done with the workspace, so the
+                // copy overlaps whatever the caller queued on `stream` since (e.g. a relight)
+                if (had_prev) SFB_CUDA(cudaStreamWaitEvent(cs, ws.done, 0));
             }
             // every chunk's rows are queued at once, each followed by its own event
             std::vector<cudaEvent_t> rows_ready;
@@ -1442,6 +1514,7 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             if (herr) fail(SF_ERR_INVALID_ARGUMENT, "place_template: entry coincides with p");
             return;
         }
+        refresh_dt(s, stream);
         In<double> iq(queries, size_t(n) * 9, stream);
         Out<double> oF(F_out, size_t(n) * 3, stream);
         Out<float> oy(y_out, size_t(n) * 3, stream);

@@ -1,12 +1,14 @@
 // sf_fused.cu — production front half of the query: per shading point, sample
 // the 266 template features, sort/pool every (layer, feature type) and emit the
-// tensor-core operands directly (K5 + K6 fused; features never reach HBM).
+// tensor-core operands directly (K5 + K6 fused: the fp32 features stay in shared memory;
+// the sorted bf16 operand blocks go to HBM for k_backbone_tc).
 //
 // Block = 8 consecutive queries (one 8-row group of a 128-row UMMA tile):
 //  phase 1  warp w samples the template points of query q0 + w, point-parallel so a
 //           warp's gathers stay inside one template footprint. Density and
-//           transmittance come from x-pair records {rho, T}(x0), {rho, T}(x0 + 1)
-//           (one 16-byte load per (y, z) corner row); the Eq. 8 phase feature from
+//           transmittance come from xy-quad records {rho, T} at (x0, y), (x0 + 1, y),
+//           (x0, y + 1), (x0 + 1, y + 1) (one 32-byte load per z corner row, k_xpair);
+//           the Eq. 8 phase feature from
 //           phase planes pre-blended at each lobe's g, held in shared memory.
 //  phase 2  thread-per-(query, segment) register bitonic sorts (a 48-point layer is
 //           split over a lane pair), sequential float sum in sorted order
@@ -248,7 +250,7 @@ __device__ __forceinline__ void ld_nc_256(const float4* p, float4& a, float4& b)
 
 // {density, transmittance} at voxel coordinate base + frac: 0 / 1 outside the box
 // (sample_trilinear + TransmittanceFeatureVolume::sample), else trilinear over
-// x-pair records with the clamp-to-edge cell of src/volume_grid.cpp:45-56.
+// xy-quad records with the clamp-to-edge cell of src/volume_grid.cpp:45-56.
 // `box` = per-base {lo, hi} fraction bounds of the closed grid box: inside iff
 // lo_c <= f_c <= hi_c (lo = -0.5 - base, hi = n - 0.5 - base).
 __device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, const float* box, const float* f,
@@ -399,6 +401,8 @@ __global__ void __launch_bounds__(kPrepThreads)
             qc.pad_[0] = qc.pad_[1] = 0;
             s_rec[threadIdx.x] = qc;
             write_cfg8(m, media ? media + 4 * src : nullptr, c, s_cfg + 8 * threadIdx.x);
+            if (!qc.ok)  // highlight placement fails (entry == p; the reference throws, src/templates.cpp:219-220):
+                for (int k = 4; k < 7; ++k) s_cfg[8 * threadIdx.x + k] = __longlong_as_double(0x7ff8000000000000LL);
         }
         __syncthreads();
         const int rows = n - q0 < kPrepThreads ? int(n - q0) : kPrepThreads;
@@ -446,7 +450,8 @@ __global__ void k_morton(GridDev g, int64_t n, const double* __restrict__ querie
 // values, so the sampler has no clamps, and a trilinear cell is two 256-bit loads (z0, z0+1).
 // Four records share a 128-byte line as a 2x1x2 (x, y, z) brick: a cell's two records are in
 // one line when z0 is even. Index ((z/2 * PY + y) * XH + x/2) * 4 + (z&1) * 2 + (x&1).
-__global__ void k_xpair(const float2* __restrict__ v, int nx, int ny, int nz, float4* __restrict__ out) {
+__global__ void k_xpair(const float* __restrict__ rho, const float* __restrict__ tr, int nx, int ny, int nz,
+                        float4* __restrict__ out) {
     const int px = nx + 1, py = ny + 1, pz = nz + 2;
     const size_t n = size_t(px) * py * pz;
     const size_t sx = size_t((px + 1) >> 1) << 2, sz = size_t(py) * sx;
@@ -456,7 +461,10 @@ __global__ void k_xpair(const float2* __restrict__ v, int nx, int ny, int nz, fl
         const int cy0 = min(max(y - 1, 0), ny - 1), cy1 = min(y, ny - 1);
         const int cz = min(max(z - 1, 0), nz - 1);
         const size_t r0 = (size_t(cz) * ny + cy0) * nx, r1 = (size_t(cz) * ny + cy1) * nx;
-        const float2 a = v[r0 + cx0], b = v[r0 + cx1], c = v[r1 + cx0], d = v[r1 + cx1];
+        const float2 a = make_float2(__ldg(rho + r0 + cx0), __ldg(tr + r0 + cx0));
+        const float2 b = make_float2(__ldg(rho + r0 + cx1), __ldg(tr + r0 + cx1));
+        const float2 c = make_float2(__ldg(rho + r1 + cx0), __ldg(tr + r1 + cx0));
+        const float2 d = make_float2(__ldg(rho + r1 + cx1), __ldg(tr + r1 + cx1));
         const size_t rec = size_t(z >> 1) * sz + size_t(y) * sx + (size_t(x >> 1) << 2) + ((z & 1) << 1) + (x & 1);
         out[2 * rec] = make_float4(a.x, a.y, b.x, b.y);
         out[2 * rec + 1] = make_float4(c.x, c.y, d.x, d.y);
@@ -855,9 +863,9 @@ void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float
     count_launch();
 }
 
-void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStream_t s) {
+void launch_xpair(const float* rho, const float* tr, int nx, int ny, int nz, float4* out, cudaStream_t s) {
     const size_t n = size_t(nx + 1) * (ny + 1) * (nz + 2);
-    k_xpair<<<unsigned(std::min<size_t>((n + 255) / 256, size_t(sm_count()) * 32)), 256, 0, s>>>(dt, nx, ny, nz,
+    k_xpair<<<unsigned(std::min<size_t>((n + 255) / 256, size_t(sm_count()) * 32)), 256, 0, s>>>(rho, tr, nx, ny, nz,
                                                                                                  out);
     SFB_CUDA(cudaGetLastError());
     count_launch();
@@ -875,7 +883,11 @@ __global__ void k_l2_probe(const float4* __restrict__ buf, size_t n32, int reps,
     for (int r = 0; r < reps; ++r)
         for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n32; i += stride) {
             float4 a, b;
-            ld_nc_256(buf + 2 * i, a, b);
+            // volatile: the compiler may not merge the repeated loads of the `reps` loop
+            asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                         : "l"(buf + 2 * i)
+                         : "memory");
             acc += a.x + b.w;
         }
     if (acc == 1.2345f) sink[0] = acc;  // never true for the zeroed buffer; keeps the loads live

@@ -150,6 +150,8 @@ struct sf_scene {
     int n_planes = 0;
     float4* d_dt4 = nullptr;    // xy-quad records of the {density, transmittance} volume (k_xpair)
     float4* d_pre = nullptr;    // per diffuse point {offset (voxels), half angle}, {unit axis, light side}
+    sf_tvol* own_tvol = nullptr;  // the volume sf_scene_relight builds into (owned)
+    bool dt_stale = false;        // d_dt not yet refreshed after a relight (the FP32 path refreshes it)
 };
 
 // ---- launchers (defined in the .cu files) --------------------------------------
@@ -263,7 +265,7 @@ void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_mediu
                        const float* planes = nullptr, int n_planes = 0, float4* pre = nullptr);
 // Morton keys of the queries' positions in the grid box + identity indices (for cub sort)
 void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t* keys, int* idx, cudaStream_t s);
-void launch_xpair(const float2* dt, int nx, int ny, int nz, float4* out, cudaStream_t s);
+void launch_xpair(const float* rho, const float* tr, int nx, int ny, int nz, float4* out, cudaStream_t s);
 double probe_l2_read_gbs(size_t bytes, int reps);  // k_l2_probe: 32-byte reads of an L2-resident buffer
 size_t xpair_records(int nx, int ny, int nz);  // float4 units of the padded xy-quad record layout
 // Pre-blended phase planes: for each lobe, the table interpolated at that lobe's g

@@ -26,6 +26,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "sf_internal.h"
@@ -718,12 +720,18 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
     size_t smem = 1024 + 2 * kUmmaM * 32 * 2 + kUmmaM * 64 * 2 + size_t(kSlots) * kSlotBytes;
     static const bool solo = std::getenv("SF_DEBUG_TC") && std::atoi(std::getenv("SF_DEBUG_TC")) == 2;
     if (solo) smem = 200 * 1024;  // one CTA per SM: uncontended chain latency
-    static size_t attr_set = 0;
-    if (attr_set != smem) {
+    // function attributes are per device: remember the size set on each device (a process may
+    // drive several GPUs, from several threads)
+    static std::mutex attr_mu;
+    static std::unordered_map<int, size_t> attr_set;
+    int dev = 0;
+    SFB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(attr_mu);
+    if (attr_set[dev] != smem) {
         SFB_CUDA(cudaFuncSetAttribute(k_backbone_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         SFB_CUDA(cudaFuncSetAttribute(k_backbone_tc, cudaFuncAttributePreferredSharedMemoryCarveout,
                                       int(cudaSharedmemCarveoutMaxShared)));
-        attr_set = smem;
+        attr_set[dev] = smem;
         // two co-resident tiles per SM by design (168 registers x 160 threads, 105 KB smem,
         // 2 x 256 TMEM columns); ncu reports "Block Limit Registers 2 / Shared Mem 2"
         // (profiles/ncu_traffic.json), while cudaOccupancyMaxActiveBlocksPerMultiprocessor

@@ -121,3 +121,39 @@ def build_tvol_sharded(pyramid, light, rank: int, world: int, weights=None, cfg=
     api.build_transmittance_slab(pyramid, light, z0, z1, weights, cfg, out=local, fast=fast)
     full = gather_slabs(local, nz, rank, world, group)
     return api.TransmittanceFeatureVolume.from_values(full.contiguous(), g0.voxel_size(), g0.origin(), light, weights)
+
+
+def relight_sharded(scene, pyramid, light, rank: int, world: int, weights=None, cfg=None, group=None, fast=False,
+                    stream=None):
+    """Scene.relight with the per-light build split by z-slab over the ranks of `group`: every rank
+    builds its slab (sf_build_transmittance_slab, bit-identical rows), one all_gather assembles the
+    volume straight into the scene's own storage, and the query records are refreshed — the
+    result is bit-identical to scene.relight(pyramid, light) on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    from . import api
+
+    g0 = pyramid.level(0)
+    nx, ny, nz = g0.dims
+    slabs = z_slabs(nz, world)
+    pad = max(z1 - z0 for z0, z1 in slabs)
+    z0, z1 = slabs[rank]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    even = all(z1_ - z0_ == pad for z0_, z1_ in slabs)
+    store = scene.tvol_storage()
+    if even:
+        # equal slabs: gather in place, rank r's rows land at [r*pad, (r+1)*pad)
+        local = store[z0:z1]
+        api.build_transmittance_slab(pyramid, light, z0, z1, weights, cfg, out=local, fast=fast, stream=stream)
+        if world > 1:
+            dist.all_gather_into_tensor(store, local, group=group)  # in place: local is store's slice
+    else:
+        buf = torch.empty((pad, ny, nx), dtype=torch.float32, device=dev)
+        api.build_transmittance_slab(pyramid, light, z0, z1, weights, cfg, out=buf[: z1 - z0], fast=fast, stream=stream)
+        full = torch.empty((world * pad, ny, nx), dtype=torch.float32, device=dev)
+        dist.all_gather_into_tensor(full, buf, group=group)
+        for r, (a, b) in enumerate(slabs):
+            store[a:b].copy_(full[r * pad: r * pad + (b - a)])
+    scene.commit_tvol(light, stream=stream)
+    return scene
