@@ -297,6 +297,13 @@ int sf_host_alloc(size_t bytes, void** out);
 int sf_host_free(void* p);
 /* Number of kernels this library has launched since load (all entry points). */
 int64_t sf_launch_count(void);
+/* Diagnostics (parity tests): the production (bf16 path) sampler's fp32 per-layer pools for
+ * query rows h/d [n][9] — slice_layers' {mean, max} per feature type (src/predictor.cpp:153-191)
+ * as k_sample_sort computes them before the bf16 packing: pools h/d [n_layers][n][8] =
+ * {mean density, phase, transmittance, max density, phase, transmittance, 0, 0}, layers
+ * diffuse then highlight in template order. Runs the bf16 query (F discarded). */
+int sf_debug_query_pools(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium, int64_t n,
+                         const double* queries, float* pools, sf_stream stream);
 /* Diagnostics: with SF_DEBUG_TC set in the environment, CTA 0 of the tensor-core
  * backbone accumulates clock64 cycles per phase (0 bundle wait FC-1, 1 attention,
  * 2 FC-1 MMA, 3 FC-1 epilogue, 4 bundle wait FC-2, 5 FC-2 MMA, 6 FC-2 epilogue,

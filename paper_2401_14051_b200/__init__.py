@@ -15,6 +15,6 @@ from .api import (BF16, DIFFUSE, FP32, HIGHLIGHT, Backbone, BackboneConfig, Comb
                   decode_prediction, encode_label, graded_transmittance, light_entry_point, load_template,
                   make_backbone, make_config, place_template, predict, predict_y, query, query_media, sample_features,
                   Camera, RenderOptions, bake_field, render_volume, render_neural, pinned_empty,
-                  save_template)
+                  save_template, debug_query_pools)
 
 __version__ = "0.1.0"

@@ -95,6 +95,7 @@ _SIGS = {
     "sf_scene_relight": (I, [P, P, P, P, P, D, D, I, P]),
     "sf_scene_tvol_storage": (I, [P, PP]),
     "sf_scene_commit_tvol": (I, [P, P, P]),
+    "sf_debug_query_pools": (I, [P, P, P, I64, P, P, P]),
     "sf_query": (I, [P, P, P, I64, P, I, P, P, P]),
     "sf_query_media": (I, [P, P, I64, P, P, I, P, P, P]),
     "sf_bake_field": (I, [P, P, P, P, I, P, P]),

@@ -746,6 +746,18 @@ def query(scene: Scene, net: Backbone, medium: MediumParams, queries, precision=
     return F_out
 
 
+def debug_query_pools(scene: Scene, net: Backbone, medium: MediumParams, queries, stream=None):
+    """The production sampler's fp32 per-layer pools (slice_layers' mean / max per feature type,
+    src/predictor.cpp:153-191) for [n,9] query rows: [n, n_layers, 6] = mean d, p, t, max d, p, t."""
+    q = _arr(queries, np.float64)
+    n = q.shape[0]
+    nl = len(net.config.diffuse_counts) + len(net.config.highlight_counts)
+    out = np.empty((nl, n, 8), np.float32)
+    m = medium.to_c()
+    check(lib.sf_debug_query_pools(scene._h, net._h, C.byref(m), n, ptr(q), ptr(out), stream_ptr(stream)))
+    return np.ascontiguousarray(out[:, :, :6].transpose(1, 0, 2))
+
+
 def query_media(scene: Scene, net: Backbone, queries, media, precision=FP32, F_out=None, y_out=None, stream=None):
     """query() with a per-query medium: media [n, 4] = (g, albedo r, g, b), each query using
     PhaseModel.hg(g) for its phase features and ConfigParams(g=(g,), albedo) (config C4)."""

@@ -1258,7 +1258,8 @@ void refresh_dt(const sf_scene* s, cudaStream_t stream) {
 // sf_query / sf_query_media: medium is the scene-wide medium, media (nullable) per-query
 // {g, albedo rgb} rows that override it (single-lobe HG per query).
 void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium, const double* media_in,
-                int64_t n, const double* queries, int precision, double* F_out, float* y_out, cudaStream_t stream) {
+                int64_t n, const double* queries, int precision, double* F_out, float* y_out, cudaStream_t stream,
+                float* dbg_pools = nullptr) {
         if (n <= 0) return;
         sf_medium_params uniform{};
         if (media_in) {
@@ -1302,8 +1303,8 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             static const int morton_env = std::getenv("SF_MORTON") ? std::atoi(std::getenv("SF_MORTON")) : -1;
             const size_t vol_bytes = sfb::xpair_records(s->density->nx, s->density->ny, s->density->nz) *
                                      sizeof(float4);
-            const bool reorder = morton_env >= 0 ? morton_env > 0 && n > 1
-                                                 : (vol_bytes > (size_t(96) << 20) && n >= 4096);
+            const bool reorder = !dbg_pools && (morton_env >= 0 ? morton_env > 0 && n > 1
+                                                                : (vol_bytes > (size_t(96) << 20) && n >= 4096));
             if (hF0 && !reorder && (reinterpret_cast<uintptr_t>(F_out) & 15) == 0) {
                 z_F = static_cast<double*>(mapped_alias(F_out));
                 zero_copy = z_F != nullptr;
@@ -1486,6 +1487,10 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                         sfb::launch_backbone_tc(*b, m, ops.p, mms.p, cfg8.p, yd ? yd + 3 * c0 : nullptr,
                                                 Fd ? Fd + 3 * c0 : nullptr, stream);
                 }
+                if (dbg_pools)  // the chunk's fp32 pools, [layer][row][8] -> [layer][n][8]
+                    SFB_CUDA(cudaMemcpy2DAsync(dbg_pools + 8 * c0, size_t(n) * 8 * sizeof(float), mms.p,
+                                               size_t(chunk) * 8 * sizeof(float), size_t(m) * 8 * sizeof(float),
+                                               size_t(L.n_layers), cudaMemcpyDeviceToDevice, stream));
                 if (h_out && !reorder) {  // results home: on the copy stream while a next chunk computes
                     const bool last = c0 + chunk >= n;
                     cudaStream_t ds = last ? stream : cs;
@@ -1569,6 +1574,19 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
         if (herr) fail(SF_ERR_INVALID_ARGUMENT, "place_template: entry coincides with p");
 }
 }  // namespace
+
+int sf_debug_query_pools(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium, int64_t n,
+                         const double* queries, float* pools, sf_stream stream) {
+    return guard([&] {
+        if (n <= 0) return;
+        const sfb::SortLayout L = sfb::sort_layout(b->cfg);
+        Out<float> o(pools, size_t(L.n_layers) * size_t(n) * 8, stream);
+        Scratch<double> Fd(size_t(n) * 3, stream);
+        query_impl(s, b, medium, nullptr, n, queries, SF_PRECISION_BF16, Fd.p, nullptr, stream, o.d);
+        o.finish();
+        sync(stream);
+    });
+}
 
 int sf_query(const sf_scene* s, const sf_backbone* b, const sf_medium_params* medium, int64_t n,
              const double* queries, int precision, double* F_out, float* y_out, sf_stream stream) {

@@ -74,9 +74,8 @@ struct SortDesc {
 
 // Bilinear lookup in a pre-blended phase plane pl[a][h] = P(a,h), rows padded to H+1 floats
 // (rows a and a+1 in different banks).
-__device__ __forceinline__ float plane_lookup(const float* pl, int A, int H, float su, float sv, float angle,
-                                              float half) {
-    float u = fminf(fmaxf(angle, 0.0f), float(kPi)) * su;
+__device__ __forceinline__ float plane_lookup(const float* pl, int A, int H, float sv, float ua, float half) {
+    const float u = fminf(fmaxf(ua, 0.0f), float(A - 1));  // angle coordinate, see unit_coord
     int i0 = min(int(u), A - 2);
     float t = u - float(i0);
     float v = fminf(fmaxf(half, 0.0f), float(kPi)) * sv;
@@ -90,42 +89,36 @@ __device__ __forceinline__ float plane_lookup(const float* pl, int A, int H, flo
     return fmaf(t, b - a, a);
 }
 
-// acos on [-1, 1] for the phase-plane coordinate: sqrt(1 - |x|) P7(|x|) (Abramowitz & Stegun
-// 4.4.46, |error| <= 2e-8 rad) and acos(-x) = pi - acos(x) — 16 instructions where acosf
-// compiles to ~32. The lookup is continuous across cells, so the ~1e-7 rad difference
-// moves the phase feature by ~1e-7 relative, far inside the bf16 rounding it then gets.
-__device__ __forceinline__ float acos_fast(float x) {
-    const float ax = fabsf(x);
-    float p = -0.0012624911f;
-    p = fmaf(p, ax, 0.0066700901f);
-    p = fmaf(p, ax, -0.0170881256f);
-    p = fmaf(p, ax, 0.0308918810f);
-    p = fmaf(p, ax, -0.0501743046f);
-    p = fmaf(p, ax, 0.0889789874f);
-    p = fmaf(p, ax, -0.2145988016f);
-    p = fmaf(p, ax, 1.5707963050f);
-    const float s = fmaxf(1.0f - ax, 1e-30f);
-    const float r = s * rsqrtf(s) * p;
-    return x < 0.0f ? float(kPi) - r : r;
+// Angle coordinate of the phase table, u = angle_between(a, b) (A - 1) / pi (inc/math.h:53-56,
+// src/phase.cpp:196-205), for unit vectors a and b, from t = 2 asin(|a -/+ b| / 2): u = t su, or
+// (A - 1) - t su when a . b < 0 (angle = pi - t). Both branches keep the error ~1e-7 rad where
+// acos of an FP32 dot product loses sqrt(eps) ~ 3e-4 rad near 0 and pi, and an FP32 angle near
+// pi rounds to ulp(pi); the phase features stay within ~1e-5 of the reference's FP64 lookup
+// (tests/test_gpu_reference_live.py).
+__device__ __forceinline__ float unit_coord(float ax, float ay, float az, float bx, float by, float bz, float su,
+                                           int A) {
+    const float dot = fmaf(ax, bx, fmaf(ay, by, az * bz));
+    const float sg = dot < 0.0f ? -1.0f : 1.0f;
+    const float dx = fmaf(-sg, bx, ax), dy = fmaf(-sg, by, ay), dz = fmaf(-sg, bz, az);
+    const float t = 2.0f * asinf(fminf(0.5f * sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))), 1.0f));
+    return dot < 0.0f ? fmaf(-t, su, float(A - 1)) : t * su;
 }
 
 // PhaseTable::lookup (src/phase.cpp:221-230) on the pre-blended planes.
-__device__ __forceinline__ float cap_phase(const float* planes, const SortDesc& d, float cosine, float half) {
-    const float angle = acos_fast(fminf(fmaxf(cosine, -1.0f), 1.0f));
-    if (d.n_planes == 1) return d.w[0] * plane_lookup(planes, d.A, d.H, d.su, d.sv, angle, half);  // one lobe / iso
+__device__ __forceinline__ float cap_phase(const float* planes, const SortDesc& d, float ua, float half) {
+    if (d.n_planes == 1) return d.w[0] * plane_lookup(planes, d.A, d.H, d.sv, ua, half);  // one lobe / iso
     float f = 0.0f;
     for (int k = 0; k < d.n_planes; ++k)
-        f = fmaf(d.w[k], plane_lookup(planes + k * d.A * (d.H + 1), d.A, d.H, d.su, d.sv, angle, half), f);
+        f = fmaf(d.w[k], plane_lookup(planes + k * d.A * (d.H + 1), d.A, d.H, d.sv, ua, half), f);
     return f;
 }
 
 // PhaseTable::lookup_hg (src/phase.cpp:191-219) at a per-query g cell (gi, gt) on the full
 // table [G][A][H] in global memory (L1/L2 resident): bilinear in (angle, aperture) on planes
 // gi and gi + 1, then the g lerp. FP32 (bf16 production path only).
-__device__ __forceinline__ float table_phase(const SortDesc& d, int gi, float gt, float cosine, float half) {
-    const float angle = acos_fast(fminf(fmaxf(cosine, -1.0f), 1.0f));
+__device__ __forceinline__ float table_phase(const SortDesc& d, int gi, float gt, float ua, float half) {
     const int A = d.A, H = d.H;
-    const float u = fminf(fmaxf(angle, 0.0f), float(kPi)) * d.su;
+    const float u = fminf(fmaxf(ua, 0.0f), float(A - 1));
     const int i0 = min(int(u), A - 2);
     const float t = u - float(i0);
     const float v = fminf(fmaxf(half, 0.0f), float(kPi)) * d.sv;
@@ -156,7 +149,7 @@ __device__ __forceinline__ void voxel_split(const GridDev& g, const double* s, i
 
 // Per-query context, computed once per query by k_query_prep (one thread per
 // query) instead of redundantly by the 32 lanes of the sampling warp.
-struct __align__(16) QueryCtx {
+struct __align__(16) QueryCtx {  // 240 bytes: copied as 16-byte chunks
     int pb[3];               // query base cell
     float pf[3];             // query base fraction
     int eb[3];               // highlight entry cell
@@ -171,15 +164,19 @@ struct __align__(16) QueryCtx {
     int same_light;          // light and medium equal query 0's (diffuse light side precomputed)
     int gi;                  // per-query g (mixed media): table g cell and weight
     float gt;
-    int pad_[2];
+    int tiny;                // highlight template within half a voxel of its entry (see query_ctx)
+    float eface[6];          // the entry's distances to the box faces (lo x, y, z, hi x, y, z), voxels
+    int pad_[3];
 };
+
+static_assert(sizeof(QueryCtx) % 16 == 0, "QueryCtx is moved in 16-byte chunks");
 
 // Phase feature factor at the query's medium: the scene's pre-blended planes, or the full
 // table at the query's own g (mixed media).
 template <bool kMixed>
-__device__ __forceinline__ float qphase(const float* planes, const SortDesc& d, const QueryCtx& q, float cosine,
+__device__ __forceinline__ float qphase(const float* planes, const SortDesc& d, const QueryCtx& q, float ua,
                                        float half) {
-    return kMixed ? table_phase(d, q.gi, q.gt, cosine, half) : cap_phase(planes, d, cosine, half);
+    return kMixed ? table_phase(d, q.gi, q.gt, ua, half) : cap_phase(planes, d, ua, half);
 }
 
 __device__ __forceinline__ void box_bounds(const GridDev& g, const int* base, float* box) {
@@ -195,12 +192,14 @@ __device__ __forceinline__ void query_ctx(const SceneDev& sc, const TemplateDev&
     const double p[3] = {c[0], c[1], c[2]}, omega[3] = {c[3], c[4], c[5]}, light[3] = {c[6], c[7], c[8]};
     const GridDev& g = sc.grid;
     voxel_split(g, p, q.pb, q.pf);
-    for (int i = 0; i < 3; ++i) {
-        q.wf[i] = float(omega[i]);
-        q.lf[i] = float(light[i]);
+    {  // unit omega and light (normalised in FP64)
+        const double iw = 1.0 / sqrt(dot3(omega, omega)), il = 1.0 / sqrt(dot3(light, light));
+        for (int i = 0; i < 3; ++i) {
+            q.wf[i] = float(omega[i] * iw);
+            q.lf[i] = float(light[i] * il);
+        }
+        q.iw = q.il = 1.0f;
     }
-    q.iw = rsqrtf(q.wf[0] * q.wf[0] + q.wf[1] * q.wf[1] + q.wf[2] * q.wf[2]);
-    q.il = rsqrtf(q.lf[0] * q.lf[0] + q.lf[1] * q.lf[1] + q.lf[2] * q.lf[2]);
     // light entry + highlight frame (src/feature_pipeline.cpp:130-137, src/templates.cpp:220-239)
     const double lo[3] = {g.ox, g.oy, g.oz}, hi[3] = {g.hx, g.hy, g.hz};
     double entry[3];
@@ -229,9 +228,18 @@ __device__ __forceinline__ void query_ctx(const SceneDev& sc, const TemplateDev&
         q.t[i] = float(t[i]);
         q.b[i] = float(b[i]);
         q.a[i] = float(axis[i]);
-        q.dpe[i] = float(q.eb[i] - q.pb[i]) + (q.ef[i] - q.pf[i]);
     }
     q.hs = float(len / ht.gen_distance * ivs);
+    // A highlight template shrunk to within half a voxel of its entry point (p on or next to the
+    // face the light enters through) straddles that face at a scale the entry's FP32 voxel
+    // fraction does not resolve: its points are tested against the box by their offset from the
+    // entry and the entry's own distances to the faces (both accurate relative to themselves).
+    q.tiny = len * ivs < 0.5 ? 1 : 0;
+    for (int i = 0; i < 3; ++i) {
+        q.eface[i] = float((entry[i] - lo[i]) * ivs);
+        q.eface[3 + i] = float((hi[i] - entry[i]) * ivs);
+        q.dpe[i] = float((entry[i] - p[i]) * ivs);  // FP64 difference: no cancellation when len is tiny
+    }
     box_bounds(g, q.pb, q.pbox);
     box_bounds(g, q.eb, q.ebox);
     for (int i = 0; i < 3; ++i) {  // bases in the padded record coordinates (voxel + 1), see k_xpair
@@ -253,12 +261,9 @@ __device__ __forceinline__ void ld_nc_256(const float4* p, float4& a, float4& b)
 // xy-quad records with the clamp-to-edge cell of src/volume_grid.cpp:45-56.
 // `box` = per-base {lo, hi} fraction bounds of the closed grid box: inside iff
 // lo_c <= f_c <= hi_c (lo = -0.5 - base, hi = n - 0.5 - base).
-__device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, const float* box, const float* f,
-                                          float& rho, float& tr) {
+__device__ __forceinline__ void sample_rt_in(const SceneDev& sc, const int* base, bool inside, const float* f,
+                                             float& rho, float& tr) {
     const GridDev& g = sc.grid;
-    // non-short-circuit: one predicate chain instead of six compare-and-branch pairs
-    const bool inside = (f[0] >= box[0]) & (f[0] <= box[1]) & (f[1] >= box[2]) & (f[1] <= box[3]) &
-                        (f[2] >= box[4]) & (f[2] <= box[5]);
     if (!inside) {
         rho = 0.0f;
         tr = 1.0f;
@@ -296,6 +301,14 @@ __device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, c
     tr = fmaf(t[2], e1 - e0, e0);
 }
 
+__device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, const float* box, const float* f,
+                                          float& rho, float& tr) {
+    // non-short-circuit: one predicate chain instead of six compare-and-branch pairs
+    const bool inside = (f[0] >= box[0]) & (f[0] <= box[1]) & (f[1] >= box[2]) & (f[1] <= box[3]) &
+                        (f[2] >= box[4]) & (f[2] <= box[5]);
+    sample_rt_in(sc, base, inside, f, rho, tr);
+}
+
 // Features of template point i (diffuse 0..npts0-1, then highlight).
 template <bool kMixed>
 __device__ __forceinline__ void point_features(const SceneDev& sc, const TemplateDev& ht, const QueryCtx& q, int i,
@@ -310,10 +323,10 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
             ph = 1.0f;  // diffuse centre point (src/feature_pipeline.cpp:163-164)
             return;
         }
-        const float fw = qphase<kMixed>(planes, d, q, (q.wf[0] * p1.x + q.wf[1] * p1.y + q.wf[2] * p1.z) * q.iw, p0.w);
+        const float fw = qphase<kMixed>(planes, d, q, unit_coord(q.wf[0], q.wf[1], q.wf[2], p1.x, p1.y, p1.z, d.su, d.A), p0.w);
         const float fl = same_light
                              ? p1.w
-                             : qphase<kMixed>(planes, d, q, (q.lf[0] * p1.x + q.lf[1] * p1.y + q.lf[2] * p1.z) * q.il, p0.w);
+                             : qphase<kMixed>(planes, d, q, unit_coord(q.lf[0], q.lf[1], q.lf[2], p1.x, p1.y, p1.z, d.su, d.A), p0.w);
         ph = fw * fl;
         return;
     }
@@ -322,7 +335,13 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
 #pragma unroll
     for (int c = 0; c < 3; ++c) h[c] = fmaf(q.a[c], tq.z, fmaf(q.b[c], tq.y, q.t[c] * tq.x)) * q.hs;
     const float f[3] = {q.ef[0] + h[0], q.ef[1] + h[1], q.ef[2] + h[2]};
-    sample_rt(sc, q.eb, q.ebox, f, rho, tr);
+    if (q.tiny) {  // warp-uniform (one query per warp): the box test relative to the entry
+        const bool inside = (h[0] >= -q.eface[0]) & (h[0] <= q.eface[3]) & (h[1] >= -q.eface[1]) &
+                            (h[1] <= q.eface[4]) & (h[2] >= -q.eface[2]) & (h[2] <= q.eface[5]);
+        sample_rt_in(sc, q.eb, inside, f, rho, tr);
+    } else {
+        sample_rt(sc, q.eb, q.ebox, f, rho, tr);
+    }
     const float dx = q.dpe[0] + h[0], dy = q.dpe[1] + h[1], dz = q.dpe[2] + h[2];
     const float dd = dx * dx + dy * dy + dz * dz;
     if (dd <= 0.0f) {
@@ -333,8 +352,8 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
     const float r = tq.w * q.hs * inv;  // cap / dist, both in voxels
     const float half = r >= 1.0f ? float(kPi) : asinf(r);
     const float ax = dx * inv, ay = dy * inv, az = dz * inv;
-    ph = qphase<kMixed>(planes, d, q, (q.wf[0] * ax + q.wf[1] * ay + q.wf[2] * az) * q.iw, half) *
-         qphase<kMixed>(planes, d, q, (q.lf[0] * ax + q.lf[1] * ay + q.lf[2] * az) * q.il, half);
+    ph = qphase<kMixed>(planes, d, q, unit_coord(q.wf[0], q.wf[1], q.wf[2], ax, ay, az, d.su, d.A), half) *
+         qphase<kMixed>(planes, d, q, unit_coord(q.lf[0], q.lf[1], q.lf[2], ax, ay, az, d.su, d.A), half);
 }
 
 // Per-scene diffuse constants: pre[2i] = {offset (voxels), half angle or -1 at the
@@ -355,10 +374,11 @@ __device__ __forceinline__ void diffuse_point(const SceneDev& sc, const Template
     const double dist = sqrt(dd), cap = dt.caps[i] * ts;
     const float half = float(cap >= dist ? kPi : asin(cap / dist));
     const float ax = float(ox / dist), ay = float(oy / dist), az = float(oz / dist);
-    const float lx = float(queries[6]), ly = float(queries[7]), lz = float(queries[8]);
-    const float cl = (lx * ax + ly * ay + lz * az) * rsqrtf(lx * lx + ly * ly + lz * lz);
+    // light side of the cap: angle_between(l, axis) in FP64 (inc/math.h:53-56), once per scene
+    const double axis[3] = {ox / dist, oy / dist, oz / dist};
+    const float ul = float(angle_between(queries + 6, axis) / kPi * (d.A - 1));
     pre[2 * i] = make_float4(float(ox * ivs), float(oy * ivs), float(oz * ivs), half);
-    pre[2 * i + 1] = make_float4(ax, ay, az, cap_phase(planes, d, cl, half));
+    pre[2 * i + 1] = make_float4(ax, ay, az, cap_phase(planes, d, ul, half));
 }
 
 // Per-query preparation for the production path: make_config rows
@@ -398,7 +418,7 @@ __global__ void __launch_bounds__(kPrepThreads)
                 table_coord(media[4 * src], -0.99, 0.99, sc.phase.gr, qc.gi, gt);
                 qc.gt = float(gt);
             }
-            qc.pad_[0] = qc.pad_[1] = 0;
+            qc.pad_[0] = qc.pad_[1] = qc.pad_[2] = 0;
             s_rec[threadIdx.x] = qc;
             write_cfg8(m, media ? media + 4 * src : nullptr, c, s_cfg + 8 * threadIdx.x);
             if (!qc.ok)  // highlight placement fails (entry == p; the reference throws, src/templates.cpp:219-220):
@@ -795,7 +815,7 @@ SortDesc make_desc(const SceneDev* sc, int n_planes, const SortLayout& L, int64_
     if (sc) {
         d.A = sc->phase.ar;
         d.H = sc->phase.hr;
-        d.su = float(d.A - 1) / float(kPi);
+        d.su = float(double(d.A - 1) / kPi);
         d.sv = float(d.H - 1) / float(kPi);
         d.n_planes = n_planes;
         if (sc->phase.kind == SF_PHASE_ISOTROPIC) {

@@ -1,0 +1,57 @@
+"""Debug: production sampler pools vs the reference on an odd non-cubic grid."""
+import os, sys
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+import numpy as np
+import paper_2401_14051_b200 as sf
+from oracle.oracle import Reference, PhaseModel
+from test_gpu_reference_live import slice_pools, DT, HT
+from conftest import LIGHT
+R = Reference(); R.set_threads(os.cpu_count())
+case = sys.argv[1] if len(sys.argv) > 1 else "odd"
+rng = np.random.default_rng(7)
+if case == "odd":
+    nx, ny, nz, vs = 33, 20, 17, 0.0625
+    origin = np.array([-1.0, -0.6, -0.5])
+elif case == "cubic_off":   # cubic, origin offset
+    nx, ny, nz, vs = 32, 32, 32, 0.0625
+    origin = np.array([-1.0, -0.6, -0.5])
+elif case == "odd_std":     # odd dims, standard origin
+    nx, ny, nz, vs = 33, 20, 17, 0.0625
+    origin = np.array([-1.0, -1.0, -1.0])
+else:
+    nx, ny, nz, vs = 32, 32, 32, 0.0625
+    origin = np.array([-1.0, -1.0, -1.0])
+vol = rng.uniform(0.0, 1.0, (nz, ny, nx)).astype(np.float32)
+tvol = rng.uniform(0.05, 1.0, (nz, ny, nx)).astype(np.float32)
+hi = origin + vs * np.array([nx, ny, nz])
+n = 512
+p = origin + rng.uniform(0.0, 1.0, (n, 3)) * (hi - origin)
+faces = "--faces" in sys.argv
+if faces:
+    for k in range(0, 96):
+        a = k % 3
+        p[k, a] = origin[a] if k % 2 else hi[a]
+w = rng.normal(size=(n, 3)); w /= np.linalg.norm(w, axis=1, keepdims=True)
+rows = np.concatenate([p, w, np.broadcast_to(LIGHT, (n, 3))], axis=1)
+tab = R.phase_table(64, 128, 32, 16)
+ctx = R.make_ctx(vol, tvol, vs, origin, DT, HT, PhaseModel.hg(0.7), tab)
+feats = R.features(ctx, rows, 194, 72)
+want = slice_pools(feats)
+g = sf.DensityGrid.from_array(vol, vs, origin)
+tv = sf.TransmittanceFeatureVolume.from_values(tvol, vs, origin, LIGHT)
+d, h = sf.load_template(DT), sf.load_template(HT)
+gt = sf.PhaseTable(64, 128, 32, 16)
+scene = sf.Scene(g, tv, d, h, sf.PhaseModel.hg(0.7), gt)
+net = sf.make_backbone(sf.BackboneConfig(seed=0))
+got = sf.debug_query_pools(scene, net, sf.MediumParams((0.7,), (0.99,) * 3), rows)
+# exact path features
+fd = sf.sample_features(rows, d, g, tv, sf.PhaseModel.hg(0.7), gt)
+fh = sf.sample_features(rows, h, g, tv, sf.PhaseModel.hg(0.7), gt)
+fx = np.concatenate([fd.reshape(n, -1), fh.reshape(n, -1)], axis=1)
+print(case, "faces" if faces else "", "exact-path feature max abs err", np.abs(fx - feats).max())
+names = ["mean_d", "mean_p", "mean_t", "max_d", "max_p", "max_t"]
+for k in range(6):
+    e = np.abs(got[..., k] - want[..., k]) / np.maximum(np.abs(want[..., k]), 1e-6 * np.abs(want[..., k]).max())
+    qi, li = np.unravel_index(np.argmax(e), e.shape)
+    print(f"{names[k]}: max rel {e.max():.3e} at q {qi} layer {li}: got {got[qi, li, k]:.7g} want {want[qi, li, k]:.7g}"
+          f"  frac>1e-5 {np.mean(e > 1e-5):.4f}  p={rows[qi,:3]}")
