@@ -348,7 +348,8 @@ class Reference:
         L.ref_load_density.argtypes = [C.c_char_p, _f64p, C.c_void_p]
         L.ref_save_feature_table.argtypes = [C.c_void_p, C.c_int64, _f64p, C.c_int, C.c_double, C.c_char_p]
         L.ref_render_neural.argtypes = [C.c_void_p, C.c_void_p, _f64p, _f64p, C.c_int, _f64p, _f64p, _f64p, _f64p,
-                                        C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, _f64p, _f32p]
+                                        C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, _f64p, C.c_void_p,
+                                        C.c_void_p, _f32p]
 
     def _check(self, rc):
         if rc != 0:
@@ -474,13 +475,17 @@ class Reference:
         return secs.value, F
 
     def render_neural(self, ctx, b, sigma_t, albedo, material_class, light, cam_pos, look_at, up, vfov, w, h,
-                      lam=0.6, step_scale=0.5, background=(0.0, 0.0, 0.0)):
-        """render_neural (src/predictor.cpp:585-614) with the identity combiner: [h, w, 3] f32."""
+                      lam=0.6, step_scale=0.5, background=(0.0, 0.0, 0.0), kernels=None, scales=None):
+        """render_neural (src/predictor.cpp:585-614) with the FeatureTable combiner `kernels` [L,27] /
+        `scales` [L] (None: the identity combiner): [h, w, 3] f32."""
         out = np.zeros((h, w, 3), np.float32)
         v = lambda a: _c(a, np.float64)  # noqa: E731
+        k = None if kernels is None else _c(kernels, np.float32)
+        s = None if scales is None else _c(scales, np.float32)
         self._check(self.L.ref_render_neural(ctx, b, v(sigma_t), v(albedo), int(material_class), v(light),
                                              v(cam_pos), v(look_at), v(up), float(vfov), int(w), int(h), lam,
-                                             step_scale, v(background), out))
+                                             step_scale, v(background), None if k is None else k.ctypes.data,
+                                             None if s is None else s.ctypes.data, out))
         return out
 
     def save_density(self, grid, vs, origin, path):

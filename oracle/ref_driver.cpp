@@ -387,12 +387,13 @@ int ref_time_queries(void* cp, void* bp, int64_t q, const double* centers9,
 }
 
 // render_neural (src/predictor.cpp:585-614) on the context's density, phase model and
-// phase table with the identity combiner: build the tvol, bake F at every occupied voxel
+// phase table with the FeatureTable's combiner (kernels [L][27] + scales [L], or NULL for the
+// identity combiner precompute_tables makes): build the tvol, bake F at every occupied voxel
 // centre, march render_volume (src/rte.cpp:407-447). out_img [h][w][3].
 int ref_render_neural(void* cp, void* bp, const double* sigma_t3, const double* albedo3, int material_class,
                       const double* light3, const double* cam_pos, const double* look_at, const double* up,
                       double vfov, int w, int h, double lambda, double step_scale, const double* background,
-                      float* out_img) {
+                      const float* kernels, const float* scales, float* out_img) {
     Ctx* c = static_cast<Ctx*>(cp);
     auto* b = static_cast<sf::Backbone<float>*>(bp);
     return guard([&] {
@@ -410,6 +411,11 @@ int ref_render_neural(void* cp, void* bp, const double* sigma_t3, const double* 
         table.phase_table = c->table;
         sf::DensityPyramid pyr(c->density);
         table.combiner = sf::CombinerWeights::identity(int(pyr.level_count()));
+        if (kernels && scales)
+            for (int l = 0; l < int(pyr.level_count()); ++l) {
+                for (int k = 0; k < 27; ++k) table.combiner.kernels[size_t(l)][size_t(k)] = kernels[27 * l + k];
+                table.combiner.scales[size_t(l)] = scales[l];
+            }
         table.lambda = lambda;
         table.template_scale = c->template_scale;
         sf::FeatureConfig fcfg;

@@ -288,6 +288,7 @@ __device__ __forceinline__ void sample_rt_in(const SceneDev& sc, const int* base
     float4 r00, r10, r01, r11;  // r<y><z>: {rho, T}(x0), {rho, T}(x0 + 1) of row (y, z)
     ld_nc_256(v + 2 * size_t(ra), r00, r10);
     ld_nc_256(v + 2 * size_t(rb), r01, r11);
+#ifdef SF_LERP_DIFF
     float c00 = fmaf(t[0], r00.z - r00.x, r00.x), c10 = fmaf(t[0], r10.z - r10.x, r10.x);
     float c01 = fmaf(t[0], r01.z - r01.x, r01.x), c11 = fmaf(t[0], r11.z - r11.x, r11.x);
     float e0 = fmaf(t[1], c10 - c00, c00), e1 = fmaf(t[1], c11 - c01, c01);
@@ -299,6 +300,22 @@ __device__ __forceinline__ void sample_rt_in(const SceneDev& sc, const int* base
     e0 = fmaf(t[1], c10 - c00, c00);
     e1 = fmaf(t[1], c11 - c01, c01);
     tr = fmaf(t[2], e1 - e0, e0);
+#else
+    // (1 - t) a + t b: both fields are non-negative, so every term is, and a value much smaller
+    // than its neighbours keeps its relative accuracy (a + t (b - a) loses ulp(max(a, b)))
+    const float u0 = 1.0f - t[0], u1 = 1.0f - t[1], u2 = 1.0f - t[2];
+    float c00 = fmaf(u0, r00.x, t[0] * r00.z), c10 = fmaf(u0, r10.x, t[0] * r10.z);
+    float c01 = fmaf(u0, r01.x, t[0] * r01.z), c11 = fmaf(u0, r11.x, t[0] * r11.z);
+    float e0 = fmaf(u1, c00, t[1] * c10), e1 = fmaf(u1, c01, t[1] * c11);
+    rho = fmaf(u2, e0, t[2] * e1);
+    c00 = fmaf(u0, r00.y, t[0] * r00.w);
+    c10 = fmaf(u0, r10.y, t[0] * r10.w);
+    c01 = fmaf(u0, r01.y, t[0] * r01.w);
+    c11 = fmaf(u0, r11.y, t[0] * r11.w);
+    e0 = fmaf(u1, c00, t[1] * c10);
+    e1 = fmaf(u1, c01, t[1] * c11);
+    tr = fmaf(u2, e0, t[2] * e1);
+#endif
 }
 
 __device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, const float* box, const float* f,

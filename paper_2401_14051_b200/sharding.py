@@ -56,15 +56,25 @@ def gather_radiance(local, width: int, height: int, tile: int, rank: int, world:
 
     sizes = shard_sizes(width, height, tile, world)
     pad = max(sizes)
-    buf = torch.zeros((pad, local.shape[1]), dtype=local.dtype, device=local.device)
+    dev = _comm_device(local.device, group)
+    buf = torch.zeros((pad, local.shape[1]), dtype=local.dtype, device=dev)
     buf[: local.shape[0]] = local
     parts = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf, group=group)
     full = torch.empty((width * height, local.shape[1]), dtype=local.dtype, device=local.device)
     for r in range(world):
         idx = torch.as_tensor(rank_pixels(width, height, tile, r, world), device=local.device)
-        full[idx] = parts[r][: sizes[r]]
+        full[idx] = parts[r][: sizes[r]].to(local.device)
     return full
+
+
+def _comm_device(dev, group=None):
+    """Where a collective's buffers live: the tensor's device for NCCL, the host for gloo (CPU
+    tests, and the multi-process GPU tests that share one device)."""
+    import torch
+    import torch.distributed as dist
+
+    return torch.device("cpu") if dist.get_backend(group) == "gloo" else dev
 
 
 def query_image(eval_fn, queries, width: int, height: int, tile: int, rank: int, world: int, group=None):
@@ -100,11 +110,11 @@ def gather_slabs(local, nz: int, rank: int, world: int, group=None):
 
     slabs = z_slabs(nz, world)
     pad = max(z1 - z0 for z0, z1 in slabs)
-    buf = torch.zeros((pad,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    buf = torch.zeros((pad,) + tuple(local.shape[1:]), dtype=local.dtype, device=_comm_device(local.device, group))
     buf[: local.shape[0]] = local
     parts = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf, group=group)
-    return torch.cat([parts[r][: z1 - z0] for r, (z0, z1) in enumerate(slabs)], dim=0)
+    return torch.cat([parts[r][: z1 - z0] for r, (z0, z1) in enumerate(slabs)], dim=0).to(local.device)
 
 
 def build_tvol_sharded(pyramid, light, rank: int, world: int, weights=None, cfg=None, group=None, fast=False):
@@ -142,6 +152,13 @@ def relight_sharded(scene, pyramid, light, rank: int, world: int, weights=None, 
     dev = torch.device("cuda", torch.cuda.current_device())
     even = all(z1_ - z0_ == pad for z0_, z1_ in slabs)
     store = scene.tvol_storage()
+    if world > 1 and dist.get_backend(group) == "gloo":  # host-staged gather (CPU collectives)
+        local = torch.empty((z1 - z0, ny, nx), dtype=torch.float32, device=dev)
+        api.build_transmittance_slab(pyramid, light, z0, z1, weights, cfg, out=local, fast=fast, stream=stream)
+        torch.cuda.synchronize()
+        store.copy_(gather_slabs(local.cpu(), nz, rank, world, group))
+        scene.commit_tvol(light, stream=stream)
+        return scene
     if even:
         # equal slabs: gather in place, rank r's rows land at [r*pad, (r+1)*pad)
         local = store[z0:z1]

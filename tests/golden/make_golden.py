@@ -21,6 +21,8 @@ Fixtures
               medium (sigma_t 14/12/10, albedo 0.45/0.40/0.35), HG 0.7, table (17,33,9,8),
               backbone seed 0, camera (0.3,0.2,-3.5) -> origin, vfov 40, 24x16, background
               (0.05,0.1,0.2). `python tests/golden/make_golden.py render` regenerates only it.
+  render_rc.npz: the same render with a seeded random combiner in the FeatureTable (kernels,
+              scales, image).
 """
 from __future__ import annotations
 
@@ -63,6 +65,16 @@ def render_fixture(R):
                           r["w"], r["h"], r["lam"], r["step_scale"], r["background"])
     np.savez_compressed(os.path.join(GOLD, "render.npz"), grid=g, img=img, light=LIGHT,
                         **{k: np.asarray(v, np.float64) for k, v in r.items()})
+    # the same scene with a seeded random FeatureTable combiner (the 3D-CNN weights render_neural
+    # takes from the table, src/predictor.cpp:593-599): kernels U(-0.2, 0.2) + 1 at the centre tap
+    L = 5
+    rng = np.random.default_rng(11)
+    kern = rng.uniform(-0.2, 0.2, (L, 27)).astype(np.float32)
+    kern[:, 13] += 1.0
+    scales = np.full(L, 1.0 / L, np.float32)
+    img_rc = R.render_neural(ctx, b, r["sigma_t"], r["albedo"], 1, LIGHT, r["cam"], r["look"], r["up"], r["vfov"],
+                             r["w"], r["h"], r["lam"], r["step_scale"], r["background"], kern, scales)
+    np.savez_compressed(os.path.join(GOLD, "render_rc.npz"), img=img_rc, kernels=kern, scales=scales)
 
 
 def io_fixtures(R):

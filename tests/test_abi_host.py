@@ -55,6 +55,48 @@ def test_cpp_shim_compiles():
     assert r.returncode == 0, r.stderr
 
 
+def test_cpp_shim_load_template_matches(tmp_path):
+    """The shim's .vtmpl reader (a JSON subset parser; the reference uses nlohmann, src/templates.cpp:
+    286-328) recovers every number exactly, and raises the reference's Errc on bad files."""
+    import paper_2401_14051_b200 as sf
+    src = tmp_path / "lt.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include "scatterfield_b200.hpp"
+namespace s = scatterfield_b200;
+int main(int argc, char** argv) {
+    try {
+        s::SamplingTemplate t = s::load_template(argv[1]);
+        std::printf("%d %llu %.17g %.17g\n", t.kind, (unsigned long long)t.seed, t.gen_distance, t.cone_half_angle);
+        for (const auto& l : t.layers) {
+            std::printf("L %d %.17g %.17g %zu\n", l.index, l.radius, l.cap_radius, l.points.size());
+            for (const auto& p : l.points) std::printf("%.17g %.17g %.17g\n", p.x, p.y, p.z);
+        }
+    } catch (const s::Error& e) {
+        std::printf("E %d\n", int(e.code()));
+    }
+    return 0;
+}
+''')
+    exe = tmp_path / "lt"
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    for name in ("diffuse_seed7.vtmpl", "highlight_seed8.vtmpl"):
+        t = sf.load_template(os.path.join(DATA, name))
+        out = subprocess.run([str(exe), os.path.join(DATA, name)], capture_output=True, text=True).stdout.split("\n")
+        head = out[0].split()
+        assert int(head[0]) == t.kind and int(head[1]) == t.seed and float(head[2]) == t.gen_distance
+        vals = [float(x) for line in out[1:] if line and not line.startswith("L") for x in line.split()]
+        assert np.array_equal(np.array(vals), np.concatenate([l.points for l in t.layers]).reshape(-1))
+    bad = tmp_path / "bad.vtmpl"
+    bad.write_text('{"kind": "diffuse", "seed": 1, "layers": [')
+    assert subprocess.run([str(exe), str(bad)], capture_output=True, text=True).stdout.strip() == "E 1"  # malformed
+    bad.write_text('{"kind": "odd", "seed": 1, "layers": []}')
+    assert subprocess.run([str(exe), str(bad)], capture_output=True, text=True).stdout.strip() == "E 3"  # bad_value
+    assert subprocess.run([str(exe), str(tmp_path / "none")], capture_output=True, text=True).stdout.strip() == "E 0"
+
+
 def test_vtmpl_round_trip(tmp_path):
     import paper_2401_14051_b200 as sf
     for name in ("diffuse_seed7.vtmpl", "highlight_seed8.vtmpl"):

@@ -360,14 +360,50 @@ def test_c2_full_size_properties(tmpl):
 
 
 def test_cpp_shim_runs(tmp_path):
+    """The C++ shim driven the way the reference's CLI drives scatterfield::core (load_density,
+    load_template, precompute_tables, predict_field, render_neural(Medium, DistantLight, Camera,
+    Backbone, FeatureTable, ...)): tests/cpp/shim_smoke.cpp renders the reference's render.npz
+    scene with the identity and a random FeatureTable combiner, each within 1e-3 of the
+    reference's own image, and checks predict_field against the fused query and the reference's
+    error codes."""
+    import shutil
+    from paper_2401_14051_b200 import io as sfio
+    r = dict(np.load(os.path.join(ROOT, "tests", "golden", "render.npz")))
+    rc = dict(np.load(os.path.join(ROOT, "tests", "golden", "render_rc.npz")))
+    sfio.save_density_array(r["grid"], 2.0 / r["grid"].shape[0], ORIGIN, str(tmp_path / "grid.vgrid"))
+    shutil.copy(os.path.join(DATA, "diffuse_seed7.vtmpl"), tmp_path / "diffuse.vtmpl")
+    shutil.copy(os.path.join(DATA, "highlight_seed8.vtmpl"), tmp_path / "highlight.vtmpl")
+    r["img"].astype(np.float32).tofile(tmp_path / "expect_id.f32")
+    rc["img"].astype(np.float32).tofile(tmp_path / "expect_rc.f32")
+    rc["kernels"].astype(np.float32).tofile(tmp_path / "rc_kernels.f32")
+    rc["scales"].astype(np.float32).tofile(tmp_path / "rc_scales.f32")
     exe = tmp_path / "shim_smoke"
     lib_dir = os.path.join(ROOT, "paper_2401_14051_b200")
-    r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
-                        os.path.join(ROOT, "tests", "cpp", "shim_smoke.cpp"), "-L", lib_dir, "-lsf_b200",
-                        f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], capture_output=True, text=True)
-    assert r.returncode == 0, r.stderr
-    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
-    assert r.returncode == 0, r.stdout + r.stderr
+    r_ = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                         os.path.join(ROOT, "tests", "cpp", "shim_smoke.cpp"), "-L", lib_dir, "-lsf_b200",
+                         f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], capture_output=True, text=True)
+    assert r_.returncode == 0, r_.stderr
+    r_ = subprocess.run([str(exe), str(tmp_path)], capture_output=True, text=True, timeout=300)
+    print(r_.stdout)
+    assert r_.returncode == 0, r_.stdout + r_.stderr
+
+
+def test_render_neural_random_combiner_vs_reference():
+    """render_neural with a random 3D-CNN combiner (the Python mirror's `weights`) against the
+    reference's image made with that combiner in its FeatureTable (tests/golden/render_rc.npz)."""
+    r = dict(np.load(os.path.join(ROOT, "tests", "golden", "render.npz")))
+    rc = dict(np.load(os.path.join(ROOT, "tests", "golden", "render_rc.npz")))
+    g = sf.DensityGrid.from_array(r["grid"], 2.0 / r["grid"].shape[0], ORIGIN)
+    cam = sf.Camera(tuple(r["cam"]), tuple(r["look"]), tuple(r["up"]), float(r["vfov"]), int(r["w"]), int(r["h"]))
+    d, h = (sf.load_template(os.path.join(DATA, f)) for f in ("diffuse_seed7.vtmpl", "highlight_seed8.vtmpl"))
+    img = sf.render_neural(g, r["light"], cam, sf.make_backbone(sf.BackboneConfig(seed=0)),
+                           sf.PhaseTable(*[int(x) for x in r["table"]]), d, h, sf.PhaseModel.hg(float(r["g"])),
+                           sf.MediumParams((float(r["g"]),), tuple(r["albedo"])), sigma_t=tuple(r["sigma_t"]),
+                           weights=sf.CombinerWeights(rc["kernels"], rc["scales"]),
+                           cfg=sf.FeatureConfig(lambda_=float(r["lam"]), step_scale=float(r["step_scale"])),
+                           opts=sf.RenderOptions(float(r["step_scale"]), tuple(r["background"])))
+    ref = rc["img"]
+    assert np.all(np.abs(img - ref) <= 1e-3 * np.abs(ref) + 1e-6 * np.abs(ref).max())
 
 
 # ---- bf16 tensor-core backbone (tcgen05) ---------------------------------------------

@@ -11,8 +11,8 @@ reference core compiled from its sources (it ships to the GPU box with the snaps
     the frame's rows through Scene.relight + query, production pair and exact pair.
   * The production sampler's fp32 per-layer pools (sf_debug_query_pools: slice_layers' mean /
     max per feature type before the bf16 packing) against pools made from the reference's own
-    features (src/feature_pipeline.cpp:139-172, src/predictor.cpp:153-191): 1e-5 relative
-    (floor 1e-6 x max) for >= 99.9% of them and 3e-5 for all (check_pools), on C2 rows and on an
+    features (src/feature_pipeline.cpp:139-172, src/predictor.cpp:153-191): 1e-5 relative with an
+    absolute floor of 1e-7 x the type's max (check_pools), on C2 rows and on an
     odd, non-cubic 33 x 20 x 17 grid with points on the box faces (the record strides differ per
     axis there; a point on the face the light enters through shrinks its highlight template to
     ~1e-9, straddling that face).
@@ -165,15 +165,15 @@ def slice_pools(feats, counts_d=(6, 8, 12, 16, 24, 32, 48, 48), counts_h=(32, 16
 
 def check_pools(got, want):
     """Stated bound of the production (FP32) sampler, which feeds bf16 operands (2^-9 relative):
-    every pool within 3e-5 relative (floor 1e-6 x max of its type) and at most 0.1% of them above
-    1e-5 (measured: max 2.1e-5, 0.02% above 1e-5; FP32 lerps of small values next to large ones
-    and FP32 cap geometry near tangency). The parity path's features are bit-identical to the
-    reference (test_gpu_parity.py)."""
+    |got - want| <= 1e-5 |want| + 1e-7 max|want| for every pool (per type). The absolute floor is
+    1e-7 of the field's maximum where 1e-6 x max was asked for the feature tensors: a tiny value
+    from a trilinear weight near 0 carries the FP32 weight's absolute error (~1e-9 measured;
+    relative 5e-5 at a density feature of 1.1e-5). The parity path's features are bit-identical
+    to the reference (test_gpu_parity.py, test_gpu_reference_live.py::test_c1_*)."""
     for k in range(6):
-        w, gk = want[..., k], got[..., k]
-        err = rel_err(gk, w, 1e-6 * max(1e-30, np.abs(w).max()))
-        assert err.max() <= 3e-5, (k, err.max())
-        assert np.mean(err > 1e-5) <= 1e-3, (k, np.mean(err > 1e-5))
+        w, gk = want[..., k].astype(np.float64), got[..., k].astype(np.float64)
+        bound = 1e-5 * np.abs(w) + 1e-7 * np.abs(w).max()
+        assert np.all(np.abs(gk - w) <= bound), (k, float((np.abs(gk - w) / bound).max()))
 
 
 def test_sampler_pools_c2(c2, tables, templates):
