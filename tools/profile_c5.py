@@ -31,10 +31,11 @@ table = sf.PhaseTable(64, 128, 32, 16)
 net = sf.make_backbone(sf.BackboneConfig(seed=0))
 F = torch.empty((a.queries, 3), dtype=torch.float64, device="cuda")
 pyr = sf.DensityPyramid(g)
-for f in range(a.frames):
+sc = sf.Scene(g, sf.build_transmittance_volume(pyr, scenes.LIGHT, fast=not a.exact), dt, ht, sf.PhaseModel.hg(0.7),
+              table)
+for f in range(a.frames):  # the bench's per-frame path: relight + query
     light = scenes.rotating_light(f, 32)
-    tv = sf.build_transmittance_volume(pyr, light, fast=not a.exact)
-    sc = sf.Scene(g, tv, dt, ht, sf.PhaseModel.hg(0.7), table)
+    sc.relight(pyr, light, fast=not a.exact)
     rows[:, 6:] = torch.tensor(np.asarray(light) / np.linalg.norm(light), device="cuda")
     sf.query(sc, net, sf.MediumParams((0.7,), (0.99,) * 3), rows, sf.BF16, F_out=F)
 torch.cuda.synchronize()
