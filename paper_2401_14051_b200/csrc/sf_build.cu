@@ -358,11 +358,26 @@ __device__ __forceinline__ double axis_lo(const GridDev& g, int a) { return a ==
 __device__ __forceinline__ double axis_hi(const GridDev& g, int a) { return a == 0 ? g.hx : (a == 1 ? g.hy : g.hz); }
 __device__ __forceinline__ int axis_n(const GridDev& g, int a) { return a == 0 ? g.nx : (a == 1 ? g.ny : g.nz); }
 
-// intersect_box's far-plane distance for axis a (inc/math.h:85-107: inv = 1 / d, ta, tb, swap)
-__device__ __forceinline__ double face_exit(const GridDev& g, const double ts[3], int a, double pa) {
-    if (ts[a] == 0.0) return 1e300;
-    const double inv = 1.0 / ts[a];
-    const double ta = (axis_lo(g, a) - pa) * inv, tb = (axis_hi(g, a) - pa) * inv;
+// Light direction toward the source and its per-axis reciprocals (intersect_box's inv = 1 / d,
+// inc/math.h:85-107, made once on the host: IEEE division gives the same value there).
+struct LightDev {
+    double ts[3];
+    double inv[3];
+};
+
+inline LightDev light_dev(const double ts[3]) {
+    LightDev l;
+    for (int a = 0; a < 3; ++a) {
+        l.ts[a] = ts[a];
+        l.inv[a] = ts[a] != 0.0 ? 1.0 / ts[a] : 0.0;
+    }
+    return l;
+}
+
+// intersect_box's far-plane distance for axis a (ta, tb, swap)
+__device__ __forceinline__ double face_exit(const GridDev& g, const LightDev& l, int a, double pa) {
+    if (l.ts[a] == 0.0) return 1e300;
+    const double ta = (axis_lo(g, a) - pa) * l.inv[a], tb = (axis_hi(g, a) - pa) * l.inv[a];
     return ta > tb ? ta : tb;
 }
 
@@ -398,8 +413,8 @@ __device__ __forceinline__ int group_index(const GridDev& g, int E, int c) {
 // emitting them (no duplicate columns at chunk seams). Pass 0 counts, pass 1 writes after a
 // warp prefix sum.
 template <typename W>
-__global__ void __launch_bounds__(kTapWarps * 32) k_tap_build(GridDev g, double tsx, double tsy, double tsz,
-                                                               double step, int cap, PadLayout plx, PadLayout plz,
+__global__ void __launch_bounds__(kTapWarps * 32) k_tap_build(GridDev g, LightDev lt, double step, int cap,
+                                                               PadLayout plx, PadLayout plz,
                                                                TapGroup* __restrict__ groups,
                                                                ColTap<W>* __restrict__ taps) {
     const int gi = blockIdx.x * kTapWarps + threadIdx.x / 32;
@@ -408,14 +423,14 @@ __global__ void __launch_bounds__(kTapWarps * 32) k_tap_build(GridDev g, double 
     TapGroup& G = groups[gi];
     const int E = gi < g.ny ? 1 : (gi < g.ny + g.nz ? 2 : 0);
     const int c = gi - (E == 1 ? 0 : (E == 2 ? g.ny : g.ny + g.nz));
-    const double ts[3] = {tsx, tsy, tsz};
+    const double* ts = lt.ts;
     if (ts[E] == 0.0) {
         if (lane == 0) G.n = 0;
         return;
     }
     // plane geometry: exit through E's far face, len, n, h, dir (as optical_depth computes them)
     const double pE = axis_lo(g, E) + (c + 0.5) * g.vs;
-    const double texit = face_exit(g, ts, E, pE);
+    const double texit = face_exit(g, lt, E, pE);
     double d[3] = {ts[0] * texit, ts[1] * texit, ts[2] * texit};
     const double len = sqrt(dot3(d, d));
     int ns = int(ceil(len / step));
@@ -641,8 +656,8 @@ constexpr int kColPlanes = 8;  // E planes (warps) per block
 
 template <typename W, typename Rec, int E>
 __global__ void __launch_bounds__(256, 3) k_graded_cols(GridDev g, const Rec* __restrict__ rec, PadLayout pl,
-                                                        const Rec* __restrict__ recx, PadLayout plx, double tsx,
-                                                        double tsy, double tsz, double coeff, double step, int zlo,
+                                                        const Rec* __restrict__ recx, PadLayout plx, LightDev lt,
+                                                        double coeff, double step, int zlo,
                                                         int zhi, const TapGroup* __restrict__ groups,
                                                         const ColTap<W>* __restrict__ taps, float* __restrict__ out) {
     constexpr int L = E == 0 ? 2 : 0, O = 3 - E - L, K = kColK;
@@ -660,12 +675,12 @@ __global__ void __launch_bounds__(256, 3) k_graded_cols(GridDev g, const Rec* __
     v[L] = lo[L] + ch * 32 + lane;
     v[E] = e;
     const int o0 = lo[O] + ob * K;
-    const double ts[3] = {tsx, tsy, tsz};
+    const double* ts = lt.ts;
     const bool lane_in = e < hi[E] && v[L] < hi[L];
     double p[3];
     p[L] = axis_lo(g, L) + (v[L] + 0.5) * g.vs;
     p[E] = axis_lo(g, E) + (v[E] + 0.5) * g.vs;
-    const double tE = face_exit(g, ts, E, p[E]), tL = face_exit(g, ts, L, p[L]);
+    const double tE = face_exit(g, lt, E, p[E]), tL = face_exit(g, lt, L, p[L]);
     TapGroup G;
     G.n = 0;
     G.tap0 = 0;
@@ -679,7 +694,7 @@ __global__ void __launch_bounds__(256, 3) k_graded_cols(GridDev g, const Rec* __
     for (int j = 0; j < K; ++j) {
         const int o = o0 + j;
         p[O] = axis_lo(g, O) + (o + 0.5) * g.vs;
-        const double tO = face_exit(g, ts, O, p[O]);
+        const double tO = face_exit(g, lt, O, p[O]);
         double t3[3];
         t3[L] = tL;
         t3[E] = tE;
@@ -1171,8 +1186,9 @@ void graded_taps(const sf_grid& level, const double ts[3], double coeff, double 
     SFB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&taps), size_t(n_groups) * cap * sizeof(ColTap<W>), s));
     px = padded_records<Rec>(level, plx, cache, s, px_scratch);
     if (face_x) pz = padded_records<Rec>(level, plz, cache, s, pz_scratch);
-    k_tap_build<W><<<(n_groups + kTapWarps - 1) / kTapWarps, kTapWarps * 32, 0, s>>>(g, ts[0], ts[1], ts[2], step,
-                                                                                     cap, plx, plz, groups, taps);
+    const LightDev lt = light_dev(ts);
+    k_tap_build<W><<<(n_groups + kTapWarps - 1) / kTapWarps, kTapWarps * 32, 0, s>>>(g, lt, step, cap, plx, plz, groups,
+                                                                                     taps);
     SFB_CUDA(cudaGetLastError());
     count_launch();
     const int lo[3] = {0, 0, zlo}, hi[3] = {g.nx, g.ny, zhi};
@@ -1183,19 +1199,19 @@ void graded_taps(const sf_grid& level, const double ts[3], double coeff, double 
     };
     if (ts[1] != 0.0) {
         k_graded_cols<W, Rec, 1><<<blocks(1), 256, 0, s>>>(
-            g, px, plx, px, plx, ts[0], ts[1], ts[2], coeff, step, zlo, zhi, groups, taps, out);
+            g, px, plx, px, plx, lt, coeff, step, zlo, zhi, groups, taps, out);
         SFB_CUDA(cudaGetLastError());
         count_launch();
     }
     if (ts[2] != 0.0) {
         k_graded_cols<W, Rec, 2><<<blocks(2), 256, 0, s>>>(
-            g, px, plx, px, plx, ts[0], ts[1], ts[2], coeff, step, zlo, zhi, groups, taps, out);
+            g, px, plx, px, plx, lt, coeff, step, zlo, zhi, groups, taps, out);
         SFB_CUDA(cudaGetLastError());
         count_launch();
     }
     if (face_x) {
         k_graded_cols<W, Rec, 0><<<blocks(0), 256, 0, s>>>(
-            g, pz, plz, px, plx, ts[0], ts[1], ts[2], coeff, step, zlo, zhi, groups, taps, out);
+            g, pz, plz, px, plx, lt, coeff, step, zlo, zhi, groups, taps, out);
         SFB_CUDA(cudaGetLastError());
         count_launch();
     }
