@@ -304,7 +304,10 @@ struct TapGroup {
 };
 
 constexpr int kTapWarps = 4;
-constexpr int kColK = 4;  // voxels per lane along O
+#ifndef SF_COLK
+#define SF_COLK 8
+#endif
+constexpr int kColK = SF_COLK;  // voxels per lane along O: K + 1 row gathers per tap serve K voxels
 
 // Padded pair layout of one lane axis. L = 0: x-fastest, index (x+1) + (y+1) sy + (z+1) sz over
 // x in [-1, nx-1], y in [-1, ny], z in [-1, nz]; L = 2: z-fastest, (z+1) + (y+1) sy + (x+1) sx.
@@ -748,7 +751,7 @@ __global__ void __launch_bounds__(256, 3) k_graded_cols(GridDev g, const Rec* __
             for (int i = lane; i < nt; i += 32) tile[warp][i] = tp[t0 + i];
             __syncthreads();
             if (warp_taps) {
-                constexpr int U = sizeof(W) == 4 ? 2 : 1;  // taps in flight (FP64: registers)
+                constexpr int U = (sizeof(W) == 4 && kColK <= 4) ? 2 : 1;  // taps in flight (registers)
                 int k = 0;
                 for (; k + U <= nt; k += U) {
                     ColTap<W> t[U];
