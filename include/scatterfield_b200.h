@@ -50,7 +50,10 @@ enum sf_status {
     SF_ERR_CUDA = 100
 };
 
-enum sf_precision { SF_PRECISION_FP32 = 0, SF_PRECISION_BF16 = 1 };
+/* FP32: the reference's arithmetic (parity path). BF16 / FP16: the production path — tcgen05
+ * tensor-core network with 16-bit operands (bfloat16 or IEEE half) and fp32 accumulation, same
+ * rate; fp16 rounds 8x finer (10-bit mantissa) for the feature and activation ranges here. */
+enum sf_precision { SF_PRECISION_FP32 = 0, SF_PRECISION_BF16 = 1, SF_PRECISION_FP16 = 2 };
 enum sf_template_kind { SF_TEMPLATE_DIFFUSE = 0, SF_TEMPLATE_HIGHLIGHT = 1 };
 enum sf_phase_kind { SF_PHASE_ISOTROPIC = 0, SF_PHASE_HG = 1, SF_PHASE_MULTI_HG = 2 };
 

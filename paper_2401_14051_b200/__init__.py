@@ -8,7 +8,7 @@ missing — there is no CPU fallback.
 """
 from ._lib import EXPORTS, LIB_PATH, ScatterfieldError, lib  # noqa: F401
 from .api import *  # noqa: F401,F403
-from .api import (BF16, DIFFUSE, FP32, HIGHLIGHT, Backbone, BackboneConfig, CombinerWeights, ConfigParams,  # noqa
+from .api import (BF16, DIFFUSE, FP16, FP32, HIGHLIGHT, Backbone, BackboneConfig, CombinerWeights, ConfigParams,  # noqa
                   DensityGrid, DensityPyramid, FeatureConfig, MediumParams, PhaseModel, PhaseTable,
                   SamplingTemplate, Scene, TransmittanceFeatureVolume, angle_between, build_pyramid,
                   build_transmittance_slab, build_transmittance_volume, combine_transmittance, config_rows, conv3_replicate,

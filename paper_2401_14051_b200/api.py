@@ -22,7 +22,7 @@ from ._lib import (SfBackboneConfig, SfMediumParams, SfPhaseModel, ScatterfieldE
                    ptr, stream_ptr)
 
 DIFFUSE, HIGHLIGHT = 0, 1
-FP32, BF16 = 0, 1
+FP32, BF16, FP16 = 0, 1, 2
 
 
 def _arr(a, dtype):

@@ -1015,12 +1015,13 @@ std::mutex g_tc_mu;
 
 void check_precision(const sf_backbone& b, int precision, cudaStream_t s) {
     if (precision == SF_PRECISION_FP32) return;
-    if (precision != SF_PRECISION_BF16) fail(SF_ERR_INVALID_ARGUMENT, "unknown precision");
+    if (precision != SF_PRECISION_BF16 && precision != SF_PRECISION_FP16)
+        fail(SF_ERR_INVALID_ARGUMENT, "unknown precision");
     if (!sfb::tc_supported(b.cfg))
         fail(SF_ERR_INVALID_ARGUMENT,
              "bf16 tensor-core backbone needs widths 32/64/64 and layers of at most 62 points");
     std::lock_guard<std::mutex> lk(g_tc_mu);
-    sfb::tc_prepare(const_cast<sf_backbone&>(b), s);
+    sfb::tc_prepare(const_cast<sf_backbone&>(b), s, precision == SF_PRECISION_FP16);
 }
 
 
@@ -1072,14 +1073,15 @@ struct Carve {
 void run_bf16_chunk(const sf_backbone& b, const sfb::SortLayout& L, const sfb::SceneDev* sc,
                     const sfb::TemplateDev* dt, const sfb::TemplateDev* ht, const float* planes, int n_planes,
                     const float4* pre, int64_t m, const void* recs, const float* feats, const double* cfg8,
-                    uint8_t* ops, float* mms, int* err, float* y, double* F, cudaStream_t s) {
+                    uint8_t* ops, float* mms, int* err, float* y, double* F, cudaStream_t s, bool f16) {
     {
         StageScope st(SF_STAGE_SAMPLE_SORT, s);
-        sfb::launch_sample_sort(sc, dt, ht, planes, n_planes, pre, L, m, recs, feats, ops, mms, err, s);
+        sfb::launch_sample_sort(sc, dt, ht, planes, n_planes, pre, L, m, recs, feats, ops, mms, err, s, false, 0, 0,
+                                f16);
     }
     {
         StageScope st(SF_STAGE_BACKBONE, s);
-        sfb::launch_backbone_tc(b, m, ops, mms, cfg8, y, F, s);
+        sfb::launch_backbone_tc(b, m, ops, mms, cfg8, y, F, s, nullptr, f16);
     }
 }
 }  // namespace
@@ -1115,7 +1117,7 @@ int sf_predict(const sf_backbone* b, int64_t n, const float* features, const dou
             Scratch<uint8_t> ops(size_t(tiles) * L.tile_bytes, stream);
             Scratch<float> mms(size_t(L.n_layers) * tiles * sfb::kUmmaM * 8, stream);
             run_bf16_chunk(*b, L, nullptr, nullptr, nullptr, nullptr, 0, nullptr, n, nullptr, f.d, cf.d, ops.p,
-                           mms.p, nullptr, oy.d, oF.d, stream);
+                           mms.p, nullptr, oy.d, oF.d, stream, precision == SF_PRECISION_FP16);
         }
         oy.finish();
         oF.finish();
@@ -1282,7 +1284,8 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
         if (nd != s->dt->total || nh != s->ht->total)
             fail(SF_ERR_SHAPE_MISMATCH, "feature block does not match template counts");
         check_precision(*b, precision, stream);
-        if (precision == SF_PRECISION_BF16) {
+        if (precision == SF_PRECISION_BF16 || precision == SF_PRECISION_FP16) {
+            const bool f16 = precision == SF_PRECISION_FP16;
             // production path: query_prep -> fused sample+sort -> tcgen05 backbone per chunk of
             // up to 4096 tiles, all on the caller's stream. With host query rows the chunk's rows
             // arrive on a copy stream in two windows: the first (~1/5 of the rows, a whole number
@@ -1476,16 +1479,16 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                         StageScope st(SF_STAGE_SAMPLE_SORT, stream);
                         sfb::launch_sample_sort(&sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, L, w.m, recs.p,
                                                 nullptr, ops.p, mms.p, err.p, stream, media != nullptr,
-                                                (w.r0 - c0) / sfb::kUmmaM, layout_tiles);
+                                                (w.r0 - c0) / sfb::kUmmaM, layout_tiles, f16);
                     }
                 }
                 {
                     StageScope st(SF_STAGE_BACKBONE, stream);
                     if (reorder)
-                        sfb::launch_backbone_tc(*b, m, ops.p, mms.p, cfg8.p, yd, Fd, stream, perm.p + c0);
+                        sfb::launch_backbone_tc(*b, m, ops.p, mms.p, cfg8.p, yd, Fd, stream, perm.p + c0, f16);
                     else
                         sfb::launch_backbone_tc(*b, m, ops.p, mms.p, cfg8.p, yd ? yd + 3 * c0 : nullptr,
-                                                Fd ? Fd + 3 * c0 : nullptr, stream);
+                                                Fd ? Fd + 3 * c0 : nullptr, stream, nullptr, f16);
                 }
                 if (dbg_pools)  // the chunk's fp32 pools, [layer][row][8] -> [layer][n][8]
                     SFB_CUDA(cudaMemcpy2DAsync(dbg_pools + 8 * c0, size_t(n) * 8 * sizeof(float), mms.p,

@@ -234,12 +234,14 @@ SortLayout sort_layout(const sf_backbone_config& c);
 
 // Tensor-core (tcgen05, bf16 operands / fp32 accumulation) backbone.
 bool tc_supported(const sf_backbone_config& c);
-void tc_prepare(sf_backbone& b, cudaStream_t s);
+// f16: pack the weights as fp16 (SF_PRECISION_FP16), else bf16; both packs are kept
+void tc_prepare(sf_backbone& b, cudaStream_t s, bool f16 = false);
 void tc_release(sf_backbone& b);
 void tc_read_prof(unsigned long long* out);
 // perm (optional): processing row q writes the caller's row perm[q] of y / F
 void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, const float* mms,
-                        const double* cfg8, float* y, double* F, cudaStream_t s, const int* perm = nullptr);
+                        const double* cfg8, float* y, double* F, cudaStream_t s, const int* perm = nullptr,
+                        bool f16 = false);
 
 // Fused feature sampling + per-layer sort/pool + bf16 operand packing (K5+K6).
 // Samples the scene when `feats` is null, else sorts the given feature rows.
@@ -247,7 +249,7 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
                         const float* planes, int n_planes, const float4* pre, const SortLayout& L,
                         int64_t n, const void* recs, const float* feats, uint8_t* ops, float* mms,
                         int* err, cudaStream_t s, bool mixed = false, int64_t tile0 = 0,
-                        int64_t layout_tiles = 0);
+                        int64_t layout_tiles = 0, bool f16 = false);
 // layout_tiles > 0: this launch fills tiles [tile0, tile0 + ceil(n / 128)) of an operand /
 // pool layout of layout_tiles tiles (one backbone launch over several sampling launches).
 // Queries the persistent sampling grid processes per round (one per warp, every SM full):

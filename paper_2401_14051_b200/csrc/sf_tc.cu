@@ -186,8 +186,9 @@ __device__ __forceinline__ void mma_wait(Ring& r) {
 }
 
 // D[128 x n] (+)= A[128 x k] * W[n x k]^T, both K-major canonical; one UMMA per 16 K.
+template <bool kH>
 __device__ __forceinline__ void issue_gemm(uint32_t tmem_d, int n, uint32_t a, int k, uint32_t w, bool accumulate) {
-    const uint32_t id = idesc_bf16(n);
+    const uint32_t id = idesc16(n, kH);
     const uint64_t da = smem_desc(a, 128, k * 16), dw = smem_desc(w, 128, k * 16);
     for (int s = 0; s < k / 16; ++s)  // +256 B per K step = +16 in the start-address field
         umma_bf16(tmem_d, da + 16u * s, dw + 16u * s, id, (accumulate || s > 0) ? 1u : 0u);
@@ -248,11 +249,14 @@ __device__ __forceinline__ void stack_start(const uint8_t* slot, int tau, const 
     }
 }
 
+template <bool kH>
 __device__ __forceinline__ void store_row32(uint8_t* a, const float* v) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) store_chunk(a, threadIdx.x, c, 32, v + 8 * c);
+    for (int c = 0; c < 4; ++c) store_chunk<kH>(a, threadIdx.x, c, 32, v + 8 * c);
 }
 
+// kH: fp16 GEMM operands (SF_PRECISION_FP16), else bf16; fp32 accumulation either way
+template <bool kH>
 __global__ void __launch_bounds__(kThreads, 2)
     k_backbone_tc(const TcDesc d, const uint8_t* __restrict__ wpk, const uint8_t* __restrict__ ops,
                   const uint8_t* __restrict__ mms, int n_tiles, int64_t n, const double* __restrict__ cfg8,
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     float oa[32];  // o_att of the current layer (fp32 residual); its bf16 copy is a_att
     // step 0: payload of the first FC-1 step
     stack_start(wait_full(r, 0), 0, rc, oa);
-    store_row32(a_att, oa);
+    store_row32<kH>(a_att, oa);
     int j = 1;
     for (int tau = 0; tau < 3; ++tau) {
         for (int kind = 0; kind < 2; ++kind) {
@@ -350,8 +354,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 mma_sync();
                 if (tid == 0) {
                     const uint32_t b1s = smem_u32(s1);
-                    issue_gemm(tmem + 0, 32, s_att, 32, b1s + kSlotW1a, false);
-                    issue_gemm(tmem + 0, 32, b1s + kSlotFeat, s_kf[kind][i], b1s + kSlotW1b, true);
+                    issue_gemm<kH>(tmem + 0, 32, s_att, 32, b1s + kSlotW1a, false);
+                    issue_gemm<kH>(tmem + 0, 32, b1s + kSlotFeat, s_kf[kind][i], b1s + kSlotW1b, true);
                     umma_commit(r.mma);
                     release(r, j - 1);
                 }
@@ -364,14 +368,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                     tmem_ld32(tmem + lane + 0, acc);
 #pragma unroll
                     for (int e = 0; e < 32; ++e) acc[e] = relu(acc[e] + b1[e]);
-                    store_row32(a2, acc);
+                    store_row32<kH>(a2, acc);
                 }
                 PROF(2);
                 const uint8_t* s2 = wait_full(r, j + 1);
                 PROF(3);
                 mma_sync();
                 if (tid == 0) {
-                    issue_gemm(tmem + 32, 32, s_a2, 32, smem_u32(s2), false);
+                    issue_gemm<kH>(tmem + 32, 32, s_a2, 32, smem_u32(s2), false);
                     umma_commit(r.mma);
                     release(r, j);
                 }
@@ -396,14 +400,14 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                     for (int e = 0; e < 32; ++e) oa[e] = o[e] * w_next;
                     PROF(10);
-                    store_row32(a_att, oa);
+                    store_row32<kH>(a_att, oa);
                     PROF(11);
                 } else if (kind == 0) {  // od: K 0-31 of the merge input
-                    store_row32(a_od, o);
+                    store_row32<kH>(a_od, o);
                     stack_start(s2, tau, rc, oa);  // highlight stack (once per type: not overlapped)
-                    store_row32(a_att, oa);
+                    store_row32<kH>(a_att, oa);
                 } else {  // oh: K 32-63 of the merge input
-                    store_row32(a2, o);
+                    store_row32<kH>(a2, o);
                 }
                 j += 2;
             }
@@ -413,8 +417,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint8_t* sm = wait_full(r, j);
             mma_sync();
             if (tid == 0) {
-                issue_gemm(tmem + 64, 64, s_od, 32, smem_u32(sm), false);
-                issue_gemm(tmem + 64, 64, s_a2, 32, smem_u32(sm) + kSlotWmHi, true);
+                issue_gemm<kH>(tmem + 64, 64, s_od, 32, smem_u32(sm), false);
+                issue_gemm<kH>(tmem + 64, 64, s_a2, 32, smem_u32(sm) + kSlotWmHi, true);
                 umma_commit(r.mma);
                 release(r, j - 1);
             }
@@ -426,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                 for (int e = 0; e < 32; ++e) acc[e] = relu(acc[e] + bm[32 * half + e]);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) store_chunk(a2, tid, half * 4 + c, 64, acc + 8 * c);
+                for (int c = 0; c < 4; ++c) store_chunk<kH>(a2, tid, half * 4 + c, 64, acc + 8 * c);
             }
             ++j;
         }
@@ -435,13 +439,13 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint8_t* sc = wait_full(r, j);
             mma_sync();
             if (tid == 0) {
-                issue_gemm(tmem + 128, 64, s_a2, 64, smem_u32(sc), tau > 0);
+                issue_gemm<kH>(tmem + 128, 64, s_a2, 64, smem_u32(sc), tau > 0);
                 umma_commit(r.mma);
                 release(r, j - 1);
             }
             if (tau < 2) {  // next type's first diffuse layer, while the cross MMA runs
                 stack_start(sc, tau + 1, rc, oa);
-                store_row32(a_att, oa);
+                store_row32<kH>(a_att, oa);
             }
             mma_wait(r);
             if (tau == 2) {  // the last cross bundle carries the cross bias
@@ -452,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                     for (int e = 0; e < 32; ++e) h[e] = relu(h[e] + bc[32 * half + e]);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) store_chunk(a2, tid, half * 4 + c, 64, h + 8 * c);
+                    for (int c = 0; c < 4; ++c) store_chunk<kH>(a2, tid, half * 4 + c, 64, h + 8 * c);
                 }
             }
             ++j;
@@ -463,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint8_t* sh = wait_full(r, j);
         mma_sync();
         if (tid == 0) {
-            issue_gemm(tmem + 64, 64, s_a2, 64, smem_u32(sh), false);
+            issue_gemm<kH>(tmem + 64, 64, s_a2, 64, smem_u32(sh), false);
             umma_commit(r.mma);
             release(r, j - 1);
         }
@@ -476,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int e = 0; e < 64; ++e) h[e] = relu(h[e] + bh[e]);
         if (l == 0) {
 #pragma unroll
-            for (int c = 0; c < 8; ++c) store_chunk(a2, tid, c, 64, h + 8 * c);
+            for (int c = 0; c < 8; ++c) store_chunk<kH>(a2, tid, c, 64, h + 8 * c);
         } else {
             const float* h2 = reinterpret_cast<const float*>(sh + kSlotHead2);
             float y[3];
@@ -521,15 +525,21 @@ __global__ void __launch_bounds__(kThreads, 2)
 // ---- host-side packing ------------------------------------------------------------
 
 // B operand of one GEMM: rows = N outputs, cols [col0, col0+cols) of W (leading dim ld), zero padded to Kp.
-uint32_t pack_blob(std::vector<uint8_t>& buf, const float* W, int rows, int cols, int ld, int col0, int Kp) {
+uint32_t pack_blob(std::vector<uint8_t>& buf, const float* W, int rows, int cols, int ld, int col0, int Kp,
+                   bool f16) {
     size_t off = (buf.size() + 127) & ~size_t(127);
     size_t bytes = size_t(rows) * Kp * 2;
     buf.resize(off + bytes, 0);
     for (int r = 0; r < rows; ++r)
         for (int k = 0; k < Kp; ++k) {
             float v = k < cols ? W[size_t(r) * ld + col0 + k] : 0.0f;
-            __nv_bfloat16 h = __float2bfloat16_rn(v);
-            std::memcpy(&buf[off + canon_off(r, k, Kp)], &h, 2);
+            if (f16) {
+                __half h = __float2half_rn(v);
+                std::memcpy(&buf[off + canon_off(r, k, Kp)], &h, 2);
+            } else {
+                __nv_bfloat16 h = __float2bfloat16_rn(v);
+                std::memcpy(&buf[off + canon_off(r, k, Kp)], &h, 2);
+            }
         }
     return uint32_t(off);
 }
@@ -590,8 +600,18 @@ SortLayout sort_layout(const sf_backbone_config& c) {
     return L;
 }
 
-void tc_prepare(sf_backbone& b, cudaStream_t s) {
-    if (b.tc) return;
+// The packed operands of one backbone: [0] bf16, [1] fp16 (each made on first use).
+struct TcPacks {
+    std::unique_ptr<TcPack> p[2];
+};
+
+void tc_prepare(sf_backbone& b, cudaStream_t s, bool f16) {
+    if (!b.tc) b.tc = new TcPacks;
+    auto* packs = static_cast<TcPacks*>(b.tc);
+    if (packs->p[f16 ? 1 : 0]) return;
+    auto pack_blob_ = [&](std::vector<uint8_t>& bf, const float* W, int rows, int cols, int ld, int col0, int Kp) {
+        return pack_blob(bf, W, rows, cols, ld, col0, Kp, f16);
+    };
     const sf_backbone_config& c = b.cfg;
     const BackboneLayout& L = b.layout;
     const SortLayout S = sort_layout(c);
@@ -634,8 +654,8 @@ void tc_prepare(sf_backbone& b, cudaStream_t s) {
                 const int K = W + cnt + 2, kf = S.kf[kind][i];
                 Step st{};
                 st.k2 = kf;
-                st.c[0] = pcopy(pack_blob(buf, P.data() + off, W, W, K, 0, W), W * W * 2, kSlotW1a);
-                st.c[1] = pcopy(pack_blob(buf, P.data() + off, W, cnt + 2, K, W, kf), uint32_t(W * kf * 2), kSlotW1b);
+                st.c[0] = pcopy(pack_blob_(buf, P.data() + off, W, W, K, 0, W), W * W * 2, kSlotW1a);
+                st.c[1] = pcopy(pack_blob_(buf, P.data() + off, W, cnt + 2, K, W, kf), uint32_t(W * kf * 2), kSlotW1b);
                 st.c[2] = Copy{1, uint32_t(kSlotFeat), uint32_t(kUmmaM * kf * 2), 0, S.seg_prefix[kind][i][tau],
                                int64_t(kUmmaM) * kf * 2};
                 st.c[3] = pcopy(pack_f32(buf, slice(P, off + int64_t(W) * K, W)), f32_bytes(W), kSlotB1);
@@ -644,7 +664,7 @@ void tc_prepare(sf_backbone& b, cudaStream_t s) {
                 off += int64_t(W) * K + W;
                 Step s2{};
                 s2.k2 = W;
-                s2.c[0] = pcopy(pack_blob(buf, P.data() + off, W, W, W, 0, W), W * W * 2, 0);
+                s2.c[0] = pcopy(pack_blob_(buf, P.data() + off, W, W, W, 0, W), W * W * 2, 0);
                 s2.c[1] = pcopy(pack_f32(buf, slice(P, off + W * W, W)), f32_bytes(W), kSlotB2);
                 s2.ncopy = 2;
                 push(s2);
@@ -654,14 +674,14 @@ void tc_prepare(sf_backbone& b, cudaStream_t s) {
         const int64_t mo = L.merge_off + int64_t(tau) * (64 * 64 + 64);
         Step sm{};
         sm.k2 = 64;
-        sm.c[0] = pcopy(pack_blob(buf, P.data() + mo, 64, 32, 64, 0, 32), 4096, 0);
-        sm.c[1] = pcopy(pack_blob(buf, P.data() + mo, 64, 32, 64, 32, 32), 4096, kSlotWmHi);
+        sm.c[0] = pcopy(pack_blob_(buf, P.data() + mo, 64, 32, 64, 0, 32), 4096, 0);
+        sm.c[1] = pcopy(pack_blob_(buf, P.data() + mo, 64, 32, 64, 32, 32), 4096, kSlotWmHi);
         sm.c[2] = pcopy(pack_f32(buf, slice(P, mo + 64 * 64, 64)), f32_bytes(64), kSlotBias);
         sm.ncopy = 3;
         push(sm);
         Step sc{};
         sc.k2 = 64;
-        sc.c[0] = pcopy(pack_blob(buf, P.data() + L.cross_off, 64, 64, 192, 64 * tau, 64), 8192, 0);
+        sc.c[0] = pcopy(pack_blob_(buf, P.data() + L.cross_off, 64, 64, 192, 64 * tau, 64), 8192, 0);
         sc.ncopy = 1;
         if (tau == 2) {
             sc.c[1] = pcopy(pack_f32(buf, slice(P, L.cross_off + 64 * 192, 64)), f32_bytes(64), kSlotBias);
@@ -672,7 +692,7 @@ void tc_prepare(sf_backbone& b, cudaStream_t s) {
     for (int l = 0; l < 2; ++l) {
         Step sh{};
         sh.k2 = 64;
-        sh.c[0] = pcopy(pack_blob(buf, P.data() + L.head_off[l], 64, 64, 64, 0, 64), 8192, 0);
+        sh.c[0] = pcopy(pack_blob_(buf, P.data() + L.head_off[l], 64, 64, 64, 0, 64), 8192, 0);
         sh.c[1] = pcopy(pack_f32(buf, slice(P, L.head_off[l] + 64 * 64, 64)), f32_bytes(64), kSlotBias);
         sh.ncopy = 2;
         if (l == 1) {
@@ -702,45 +722,52 @@ void tc_prepare(sf_backbone& b, cudaStream_t s) {
     SFB_CUDA(cudaMalloc(&pk->d_blobs, buf.size()));
     SFB_CUDA(cudaMemcpy(pk->d_blobs, buf.data(), buf.size(), cudaMemcpyHostToDevice));
     d.steps = reinterpret_cast<const Step*>(pk->d_blobs + blob_bytes);
-    b.tc = pk.release();
+    packs->p[f16 ? 1 : 0] = std::move(pk);
 }
 
 void tc_release(sf_backbone& b) {
-    auto pk = static_cast<TcPack*>(b.tc);
-    if (!pk) return;
-    cudaFree(pk->d_blobs);
-    delete pk;
+    auto packs = static_cast<TcPacks*>(b.tc);
+    if (!packs) return;
+    for (auto& pk : packs->p)
+        if (pk) cudaFree(pk->d_blobs);
+    delete packs;
     b.tc = nullptr;
 }
 
 void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, const float* mms, const double* cfg8,
-                        float* y, double* F, cudaStream_t s, const int* perm) {
+                        float* y, double* F, cudaStream_t s, const int* perm, bool f16) {
     if (n <= 0) return;
-    auto pk = static_cast<const TcPack*>(b.tc);
+    auto packs = static_cast<const TcPacks*>(b.tc);
+    const TcPack* pk = packs ? packs->p[f16 ? 1 : 0].get() : nullptr;
+    if (!pk) fail(SF_ERR_INVALID_ARGUMENT, "tc backbone: operands not prepared for this precision");
     size_t smem = 1024 + 2 * kUmmaM * 32 * 2 + kUmmaM * 64 * 2 + size_t(kSlots) * kSlotBytes;
     static const bool solo = std::getenv("SF_DEBUG_TC") && std::atoi(std::getenv("SF_DEBUG_TC")) == 2;
     if (solo) smem = 200 * 1024;  // one CTA per SM: uncontended chain latency
-    // function attributes are per device: remember the size set on each device (a process may
-    // drive several GPUs, from several threads)
+    auto kern = f16 ? k_backbone_tc<true> : k_backbone_tc<false>;
+    // function attributes are per device: remember the size set on each device and variant (a
+    // process may drive several GPUs, from several threads)
     static std::mutex attr_mu;
     static std::unordered_map<int, size_t> attr_set;
     int dev = 0;
     SFB_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(attr_mu);
-    if (attr_set[dev] != smem) {
-        SFB_CUDA(cudaFuncSetAttribute(k_backbone_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        SFB_CUDA(cudaFuncSetAttribute(k_backbone_tc, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                      int(cudaSharedmemCarveoutMaxShared)));
-        attr_set[dev] = smem;
-        // two co-resident tiles per SM by design (168 registers x 160 threads, 105 KB smem,
-        // 2 x 256 TMEM columns); ncu reports "Block Limit Registers 2 / Shared Mem 2"
-        // (profiles/ncu_traffic.json), while cudaOccupancyMaxActiveBlocksPerMultiprocessor
-        // answers 1 for this kernel, so no runtime check here.
+    {
+        std::lock_guard<std::mutex> lk(attr_mu);
+        const int key = 2 * dev + (f16 ? 1 : 0);
+        if (attr_set[key] != smem) {
+            SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          int(cudaSharedmemCarveoutMaxShared)));
+            attr_set[key] = smem;
+            // two co-resident tiles per SM by design (168 registers x 160 threads, 105 KB smem,
+            // 2 x 256 TMEM columns); ncu reports "Block Limit Registers 2 / Shared Mem 2"
+            // (profiles/ncu_traffic.json), while cudaOccupancyMaxActiveBlocksPerMultiprocessor
+            // answers 1 for this kernel, so no runtime check here.
+        }
     }
     const int n_tiles = int((n + kUmmaM - 1) / kUmmaM);
     const int f_stage = F && !perm && (reinterpret_cast<uintptr_t>(F) & 15) == 0 ? 1 : 0;
-    k_backbone_tc<<<n_tiles, kThreads, smem, s>>>(pk->desc, pk->d_blobs, ops, reinterpret_cast<const uint8_t*>(mms),
-                                                  n_tiles, n, cfg8, y, F, perm, f_stage);
+    kern<<<n_tiles, kThreads, smem, s>>>(pk->desc, pk->d_blobs, ops, reinterpret_cast<const uint8_t*>(mms), n_tiles, n,
+                                        cfg8, y, F, perm, f_stage);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cstdint>
 
 namespace sfb {
@@ -19,11 +20,13 @@ __host__ __device__ constexpr uint32_t canon_off(int r, int k, int K) {
     return uint32_t((r >> 3) * (K * 16) + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
 }
 
-// kind::f16 instruction descriptor: D f32 (bits 4-5 = 1), A/B bf16 (bits 7-9,
-// 10-12 = 1), both K-major (bits 15, 16 = 0), N>>3 at bits 17-22, M>>4 at 24-28.
-__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(kUmmaM >> 4) << 24);
+// kind::f16 instruction descriptor: D f32 (bits 4-5 = 1), A/B bf16 (bits 7-9, 10-12 = 1) or
+// f16 (= 0), both K-major (bits 15, 16 = 0), N>>3 at bits 17-22, M>>4 at 24-28.
+__host__ __device__ constexpr uint32_t idesc16(int n, bool f16) {
+    return (1u << 4) | (f16 ? 0u : ((1u << 7) | (1u << 10))) | (uint32_t(n >> 3) << 17) |
+           (uint32_t(kUmmaM >> 4) << 24);
 }
+__host__ __device__ constexpr uint32_t idesc_bf16(int n) { return idesc16(n, false); }
 
 #if defined(__CUDACC__)
 
@@ -130,29 +133,38 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+// Two floats as a pair of 16-bit GEMM operands: bf16 (kH false) or fp16 (kH true), round to nearest.
+template <bool kH = false>
+__device__ __forceinline__ uint32_t pack16(float a, float b) {
+    if (kH) {
+        __half2 h = __floats2half2_rn(a, b);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
 }
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) { return pack16<false>(a, b); }
 
 // Streaming variant for operand blocks written to global memory and read back by a later
 // kernel: evict-first in L2, so the stream does not push out what the writer gathers from.
+template <bool kH = false>
 __device__ __forceinline__ void store_chunk_stream(uint8_t* base, int row, int kchunk, int K, const float* v8) {
     uint4 u;
-    u.x = pack_bf16(v8[0], v8[1]);
-    u.y = pack_bf16(v8[2], v8[3]);
-    u.z = pack_bf16(v8[4], v8[5]);
-    u.w = pack_bf16(v8[6], v8[7]);
+    u.x = pack16<kH>(v8[0], v8[1]);
+    u.y = pack16<kH>(v8[2], v8[3]);
+    u.z = pack16<kH>(v8[4], v8[5]);
+    u.w = pack16<kH>(v8[6], v8[7]);
     __stcs(reinterpret_cast<uint4*>(base + canon_off(row, kchunk * 8, K)), u);
 }
 
 // Chunk `kchunk` (8 consecutive K elements, 16 B) of row `row` of a K-wide operand.
+template <bool kH = false>
 __device__ __forceinline__ void store_chunk(uint8_t* base, int row, int kchunk, int K, const float* v8) {
     uint4 u;
-    u.x = pack_bf16(v8[0], v8[1]);
-    u.y = pack_bf16(v8[2], v8[3]);
-    u.z = pack_bf16(v8[4], v8[5]);
-    u.w = pack_bf16(v8[6], v8[7]);
+    u.x = pack16<kH>(v8[0], v8[1]);
+    u.y = pack16<kH>(v8[2], v8[3]);
+    u.z = pack16<kH>(v8[4], v8[5]);
+    u.w = pack16<kH>(v8[6], v8[7]);
     *reinterpret_cast<uint4*>(base + canon_off(row, kchunk * 8, K)) = u;
 }
 

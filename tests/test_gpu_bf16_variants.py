@@ -1,10 +1,11 @@
-"""The bf16 production path (fused sample/sort + tcgen05 backbone) against the FP32 exact path
+"""The production path (fused sample/sort + tcgen05 backbone, bf16 and fp16 operands) against the FP32 exact path
 across the configuration space the reference supports: phase models (isotropic, HG, 2- and
 3-lobe HG), literal attention, template scale, per-query lights (the diffuse light side is not
 the precomputed one), ragged batch sizes and queries on the box boundary. Tolerance: the
 stated bf16 bound of tests/test_gpu_parity.py in its scale-aware form: bf16 rounding through the
 network grows with the output, so |dy| <= 0.03 max(1, |y|) and, through decode's Jacobian,
-|dF| <= 0.03 max(1, |y|) (|F| + eta^gamma) (literal attention drives y to ~6 on these scenes)."""
+|dF| <= 0.03 max(1, |y|) (|F| + eta^gamma) (literal attention drives y to ~6 on these scenes);
+fp16 operands (10-bit mantissa) the same with 0.01."""
 import os
 
 import numpy as np
@@ -29,18 +30,22 @@ def base():
 
 
 def _check(scene, net, med, rows, albedo):
+    """Both 16-bit operand types: bf16 within 0.03 (scale-aware), fp16 within 0.01."""
     n = len(rows)
     y32 = np.empty((n, 3), np.float32)
-    y16 = np.empty((n, 3), np.float32)
     F32 = sf.query(scene, net, med, rows, sf.FP32, y_out=y32)
-    F16 = sf.query(scene, net, med, rows, sf.BF16, y_out=y16)
-    assert np.all(np.isfinite(F16))
-    dy = np.abs(y16 - y32)
     scale = np.maximum(1.0, np.abs(y32))
-    assert np.all(dy <= 0.03 * scale), (dy / scale).max()
     eg = np.power(np.asarray(albedo), 4.0)
-    assert np.all(np.abs(F16 - F32) <= 0.03 * scale * (np.abs(F32) + eg))
-    return dy
+    out = None
+    for prec, bound in ((sf.BF16, 0.03), (sf.FP16, 0.01)):
+        y16 = np.empty((n, 3), np.float32)
+        F16 = sf.query(scene, net, med, rows, prec, y_out=y16)
+        assert np.all(np.isfinite(F16))
+        dy = np.abs(y16 - y32)
+        assert np.all(dy <= bound * scale), (prec, (dy / scale).max())
+        assert np.all(np.abs(F16 - F32) <= bound * scale * (np.abs(F32) + eg))
+        out = dy if out is None else out
+    return out
 
 
 MODELS = {
@@ -122,3 +127,5 @@ def test_bf16_predict_nondefault_counts(small):
     y32, F32 = sf.predict(net, feats, cfg8, sf.FP32)
     y16, F16 = sf.predict(net, feats, cfg8, sf.BF16)
     assert np.all(np.abs(y16 - y32) <= 0.03 * np.maximum(1.0, np.abs(y32)))
+    yh, Fh = sf.predict(net, feats, cfg8, sf.FP16)
+    assert np.all(np.abs(yh - y32) <= 0.01 * np.maximum(1.0, np.abs(y32)))

@@ -19,6 +19,7 @@ ap.add_argument("--frames", type=int, default=1)
 ap.add_argument("--grid", type=int, default=256)
 ap.add_argument("--queries", type=int, default=1280 * 720)
 ap.add_argument("--exact", action="store_true")
+ap.add_argument("--profile-last", action="store_true", help="cudaProfilerStart/Stop around the last frame only")
 a = ap.parse_args()
 N = a.grid
 vol = scenes.noise_volume(N, 5)
@@ -34,9 +35,14 @@ pyr = sf.DensityPyramid(g)
 sc = sf.Scene(g, sf.build_transmittance_volume(pyr, scenes.LIGHT, fast=not a.exact), dt, ht, sf.PhaseModel.hg(0.7),
               table)
 for f in range(a.frames):  # the bench's per-frame path: relight + query
+    if a.profile_last and f == a.frames - 1:
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
     light = scenes.rotating_light(f, 32)
     sc.relight(pyr, light, fast=not a.exact)
     rows[:, 6:] = torch.tensor(np.asarray(light) / np.linalg.norm(light), device="cuda")
     sf.query(sc, net, sf.MediumParams((0.7,), (0.99,) * 3), rows, sf.BF16, F_out=F)
 torch.cuda.synchronize()
+if a.profile_last:
+    torch.cuda.profiler.stop()
 print("ok", float(F.mean()))
