@@ -661,7 +661,7 @@ __device__ __forceinline__ void sort_emit(const float* seg, int cnt, const SegOu
         if (j < cnt) acc += v[j];
     const float mean = acc / float(cnt), mx = v[0];
     if (!store) return;
-    emit_chunks<P>(v, 0, 0, o.kf / 8, cnt, mean, mx, o);
+    emit_chunks<P>(v, 0, 0, o.kf / 8, cnt, 0.0f, 0.0f, o);  // operand row: sorted values, zero padding
     emit_pools(o, mean, mx);
 }
 
@@ -709,9 +709,9 @@ __device__ __forceinline__ void sort_emit_pair(const float* seg, int cnt, bool u
     }
     if (!store) return;
     if (!upper) {
-        emit_chunks<32>(v, 0, 0, 4, cnt, mean, mx, o);
+        emit_chunks<32>(v, 0, 0, 4, cnt, 0.0f, 0.0f, o);
     } else {
-        emit_chunks<32>(v, 32, 4, o.kf / 8, cnt, mean, mx, o);
+        emit_chunks<32>(v, 32, 4, o.kf / 8, cnt, 0.0f, 0.0f, o);
         emit_pools(o, mean, mx);
     }
 }

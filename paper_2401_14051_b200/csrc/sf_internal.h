@@ -216,8 +216,8 @@ void launch_make_cfg8(const sf_medium_params& m, int64_t n, const double* querie
 
 // Layout of the sorted-feature operand blocks produced by k_sample_sort and
 // consumed by the tensor-core backbone: for every (kind, layer, tau) segment a
-// [n_tiles][128 x kf] bf16 block in UMMA canonical layout (kf = pad16(n + 2):
-// sorted values, mean, max, zeros), and for every (kind, layer) a
+// [n_tiles][128 x kf] bf16 block in UMMA canonical layout (kf = pad16(n):
+// sorted values, zeros; the pools enter FC-1 in fp32 from the block below), and for every (kind, layer) a
 // [n_tiles*128][8] fp32 block {mean d,p,t, max d,p,t, 0, 0} for the attention.
 struct SortLayout {
     int nl[2];

@@ -7,7 +7,9 @@
 //
 //   FC-1  = [o_att | sorted_tau, mean, max] W1^T as two MMAs into one accumulator:
 //           A_att (K=32, written by the threads) x W1[:, :32]  +
-//           F     (K=pad16(n+2), bulk-copied, produced by k_sample_sort) x W1[:, 32:]
+//           F     (K=pad16(n), bulk-copied, produced by k_sample_sort) x W1[:, 32:32+n]
+//           and the layer's (mean, max) x W1's last two columns as an fp32 rank-2
+//           update in the epilogue (keeps K small and the pools unrounded)
 //   FC-2  (N=32, K=32), per-type merge (N=64, K=64), cross merge accumulated
 //   chunk by chunk as each merged_tau appears (3 x K=64), head 0/1 (N=64, K=64).
 //
@@ -51,7 +53,7 @@ constexpr int kSlotWmHi = 4096;  // merge bundle: W_m[:, 0:32] at 0, W_m[:, 32:6
 // the attention weight is computed while that step's MMA runs: the tile's mean/max block,
 // [52] attention W1 b1 W2 b2 (+pad), [224 + 32] conditioning W/b (first layer of a stack).
 constexpr int kPayMM = 9728, kPayAtt = 13824, kPayInit = 14080;
-static_assert(kPayInit + 1024 <= kSlotB1 && kSlotB1 + 128 <= kSlotBytes, "slot layout");
+static_assert(kPayInit + 1024 <= kSlotB1 && kSlotB1 + 384 <= kSlotBytes, "slot layout");
 constexpr int kMaxSteps = 96;
 constexpr int kMaxCopies = 6;
 
@@ -215,10 +217,12 @@ struct RowCtx {
 };
 
 // Channel attention weight of type tau (src/neural.cpp:473-491) from a bundle's payload.
-__device__ __forceinline__ float attention(const uint8_t* slot, int tau, const RowCtx& rc) {
+// Also returns the layer's pools of type tau (mean, max: the fp32 part of its FC-1).
+__device__ __forceinline__ float attention(const uint8_t* slot, int tau, const RowCtx& rc, float2& pool) {
     const float4* mm = reinterpret_cast<const float4*>(slot + kPayMM) + threadIdx.x * 2;
     const float4 m0 = mm[0], m1 = mm[1];
     const float v[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, rc.g_mean, rc.alpha};
+    pool = tau == 0 ? make_float2(m0.x, m0.w) : (tau == 1 ? make_float2(m0.y, m1.x) : make_float2(m0.z, m1.y));
     if (rc.literal) {
         float acc = 0.0f;
 #pragma unroll
@@ -236,9 +240,9 @@ __device__ __forceinline__ float attention(const uint8_t* slot, int tau, const R
 }
 
 // First layer of a stack: o = relu(W_init cfg + b) (src/predictor.cpp:206-212), o_att = w o.
-__device__ __forceinline__ void stack_start(const uint8_t* slot, int tau, const RowCtx& rc, float* oa) {
+__device__ __forceinline__ void stack_start(const uint8_t* slot, int tau, const RowCtx& rc, float* oa, float2& pool) {
     const float* ini = reinterpret_cast<const float*>(slot + kPayInit);
-    const float w = attention(slot, tau, rc);
+    const float w = attention(slot, tau, rc, pool);
 #pragma unroll
     for (int g = 0; g < 4; ++g) {  // 8 outputs at a time: bounds the loads the compiler hoists
         float o[8];
@@ -297,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int s = 0; s < 2 * kSlots + 1; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < 32) s_kf[tid >> 4][tid & 15] = (d.counts[tid >> 4][tid & 15] + 2 + 15) / 16 * 16;
+    if (tid < 32) s_kf[tid >> 4][tid & 15] = (d.counts[tid >> 4][tid & 15] + 15) / 16 * 16;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -339,8 +343,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 
     float oa[32];  // o_att of the current layer (fp32 residual); its bf16 copy is a_att
+    float2 pool;   // the current layer's (mean, max) of its feature type
     // step 0: payload of the first FC-1 step
-    stack_start(wait_full(r, 0), 0, rc, oa);
+    stack_start(wait_full(r, 0), 0, rc, oa, pool);
     store_row32<kH>(a_att, oa);
     int j = 1;
     for (int tau = 0; tau < 3; ++tau) {
@@ -363,11 +368,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                 PROF(1);
                 // FC-1 epilogue: u = relu(acc + b1) -> bf16 operand of FC-2
                 {
-                    const float* b1 = reinterpret_cast<const float*>(s1 + kSlotB1);
+                    const float* b1 = reinterpret_cast<const float*>(s1 + kSlotB1);  // b1, W1 mean / max cols
                     float acc[32];
                     tmem_ld32(tmem + lane + 0, acc);
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) acc[e] = relu(acc[e] + b1[e]);
+                    for (int e = 0; e < 32; ++e)
+                        acc[e] = relu(acc[e] + fmaf(pool.x, b1[32 + e], fmaf(pool.y, b1[64 + e], b1[e])));
                     store_row32<kH>(a2, acc);
                 }
                 PROF(2);
@@ -383,7 +389,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 // while FC-2 runs: the next FC-1's attention weight (payload of this bundle)
                 const bool last = i == nl - 1;
                 float w_next = 0.0f;
-                if (!last) w_next = attention(s2, tau, rc);
+                float2 pool_next = pool;
+                if (!last) w_next = attention(s2, tau, rc, pool_next);
                 PROF(5);
                 mma_wait(r);
                 PROF(6);
@@ -396,6 +403,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                     for (int e = 0; e < 32; ++e) o[e] = relu(o[e] + b2[e]) + oa[e];
                 }
+                pool = pool_next;
                 if (!last) {
 #pragma unroll
                     for (int e = 0; e < 32; ++e) oa[e] = o[e] * w_next;
@@ -404,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     PROF(11);
                 } else if (kind == 0) {  // od: K 0-31 of the merge input
                     store_row32<kH>(a_od, o);
-                    stack_start(s2, tau, rc, oa);  // highlight stack (once per type: not overlapped)
+                    stack_start(s2, tau, rc, oa, pool);  // highlight stack (once per type: not overlapped)
                     store_row32<kH>(a_att, oa);
                 } else {  // oh: K 32-63 of the merge input
                     store_row32<kH>(a2, o);
@@ -444,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 release(r, j - 1);
             }
             if (tau < 2) {  // next type's first diffuse layer, while the cross MMA runs
-                stack_start(sc, tau + 1, rc, oa);
+                stack_start(sc, tau + 1, rc, oa, pool);
                 store_row32<kH>(a_att, oa);
             }
             mma_wait(r);
@@ -567,9 +575,9 @@ bool tc_supported(const sf_backbone_config& c) {
     if (c.width != 32 || c.merge_width != 64 || c.head_width != 64) return false;
     if (c.n_diffuse_layers * 6 + c.n_highlight_layers * 6 + 3 * 2 + 2 + 1 > kMaxSteps) return false;
     for (int i = 0; i < c.n_diffuse_layers; ++i)
-        if (c.diffuse_counts[i] + 2 > 64) return false;
+        if (c.diffuse_counts[i] > 64) return false;
     for (int i = 0; i < c.n_highlight_layers; ++i)
-        if (c.highlight_counts[i] + 2 > 64) return false;
+        if (c.highlight_counts[i] > 64) return false;
     return true;
 }
 
@@ -585,7 +593,7 @@ SortLayout sort_layout(const sf_backbone_config& c) {
         for (int i = 0; i < L.nl[k]; ++i) {
             L.counts[k][i] = counts[i];
             L.start[k][i] = start;
-            L.kf[k][i] = (counts[i] + 2 + 15) / 16 * 16;
+            L.kf[k][i] = (counts[i] + 15) / 16 * 16;  // sorted values only (mean / max: fp32 in the epilogue)
             L.mm_layer[k][i] = layer++;
             start += counts[i];
             for (int t = 0; t < 3; ++t) {
@@ -655,10 +663,14 @@ void tc_prepare(sf_backbone& b, cudaStream_t s, bool f16) {
                 Step st{};
                 st.k2 = kf;
                 st.c[0] = pcopy(pack_blob_(buf, P.data() + off, W, W, K, 0, W), W * W * 2, kSlotW1a);
-                st.c[1] = pcopy(pack_blob_(buf, P.data() + off, W, cnt + 2, K, W, kf), uint32_t(W * kf * 2), kSlotW1b);
+                st.c[1] = pcopy(pack_blob_(buf, P.data() + off, W, cnt, K, W, kf), uint32_t(W * kf * 2), kSlotW1b);
                 st.c[2] = Copy{1, uint32_t(kSlotFeat), uint32_t(kUmmaM * kf * 2), 0, S.seg_prefix[kind][i][tau],
                                int64_t(kUmmaM) * kf * 2};
-                st.c[3] = pcopy(pack_f32(buf, slice(P, off + int64_t(W) * K, W)), f32_bytes(W), kSlotB1);
+                // b1 [32], then the mean and max columns of W1 [32] + [32] (fp32 rank-2 update)
+                std::vector<float> bmx = slice(P, off + int64_t(W) * K, W);
+                for (int r = 0; r < W; ++r) bmx.push_back(P[size_t(off + int64_t(r) * K + W + cnt)]);
+                for (int r = 0; r < W; ++r) bmx.push_back(P[size_t(off + int64_t(r) * K + W + cnt + 1)]);
+                st.c[3] = pcopy(pack_f32(buf, bmx), f32_bytes(bmx.size()), kSlotB1);
                 st.ncopy = 4;
                 push(st);
                 off += int64_t(W) * K + W;

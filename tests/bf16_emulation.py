@@ -3,8 +3,8 @@
 Same network as the reference forward (src/predictor.cpp:206-235, 352-387), with
 the tcgen05 kernel's precision recipe: every GEMM operand (weights and
 activations) rounded to bf16, fp32 accumulation, fp32 bias / activation /
-residual; the SIMT parts (conditioning layer, attention, 64->3 output layer) in
-fp32. The kernel must match this to fp32 accumulation-order noise; the
+residual; the SIMT parts (conditioning layer, attention, the FC-1 mean / max
+columns, 64->3 output layer) in fp32. The kernel must match this to fp32 accumulation-order noise; the
 difference between this emulation and the FP32 reference is the bf16 error
 budget stated in tests/test_gpu_parity.py.
 """
@@ -83,8 +83,11 @@ def forward(params, feats, cfg8, counts_d=(6, 8, 12, 16, 24, 32, 48, 48), counts
                 f1W, f1b = take(W * K).reshape(W, K), take(W)
                 f2W, f2b = take(W * W).reshape(W, W), take(W)
                 s, mean, mx = sl[(kind, i, tau)]
-                x = np.concatenate([oa, s, mean[:, None], mx[:, None]], 1)
-                u = relu(bf16(x) @ bf16(f1W).T + f1b)
+                # the sorted features and o_att are 16-bit GEMM operands; the layer's mean / max
+                # columns are an fp32 rank-2 update in the epilogue
+                x = np.concatenate([oa, s], 1)
+                u = relu(bf16(x) @ bf16(f1W[:, :W + n]).T + (mean[:, None] * f1W[None, :, W + n]
+                                                             + mx[:, None] * f1W[None, :, W + n + 1]) + f1b)
                 o = (relu(bf16(u) @ bf16(f2W).T + f2b) + oa).astype(np.float32)
             stacks[(kind, tau)] = o
     merged = []

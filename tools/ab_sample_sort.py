@@ -7,17 +7,19 @@ import numpy as np, torch
 import paper_2401_14051_b200 as sf
 from paper_2401_14051_b200 import scenes
 from paper_2401_14051_b200._lib import profile_read
-vol = scenes.fractal_ellipsoid(128, 1)
-c = torch.from_numpy(scenes.draw_centers(vol, 65536, 11, scenes.LIGHT)).cuda()
-g = sf.DensityGrid.from_array(vol, 2.0 / 128, (-1.0, -1.0, -1.0))
+C5 = os.environ.get("AB_C5") is not None
+N = 256 if C5 else 128
+vol = scenes.noise_volume(256, 5) if C5 else scenes.fractal_ellipsoid(128, 1)
+c = torch.from_numpy(scenes.draw_centers(vol, 921600 if C5 else 65536, 21 if C5 else 11, scenes.LIGHT)).cuda()
+g = sf.DensityGrid.from_array(vol, 2.0 / N, (-1.0, -1.0, -1.0))
 tv = sf.build_transmittance_volume(sf.DensityPyramid(g), scenes.LIGHT)
 data = os.path.join(os.path.dirname(sf.__file__), "data")
 sc = sf.Scene(g, tv, sf.load_template(os.path.join(data, "diffuse_seed7.vtmpl")), sf.load_template(os.path.join(data, "highlight_seed8.vtmpl")), sf.PhaseModel.hg(0.85), sf.PhaseTable(64, 128, 32, 16))
 net = sf.make_backbone(sf.BackboneConfig(seed=0)); med = sf.MediumParams((0.85,), (0.999,) * 3)
-F = torch.empty((65536, 3), dtype=torch.float64, device="cuda")
-for _ in range(3): sf.query(sc, net, med, c, sf.BF16, F_out=F)
+F = torch.empty((len(c), 3), dtype=torch.float64, device="cuda")
+for _ in range(3): sf.query(sc, net, med, c, sf.FP16, F_out=F)
 torch.cuda.synchronize(); sf.lib.sf_profile_enable(1); profile_read()
-for _ in range(10): sf.query(sc, net, med, c, sf.BF16, F_out=F)
+for _ in range(10): sf.query(sc, net, med, c, sf.FP16, F_out=F)
 torch.cuda.synchronize(); st = profile_read()
 print(json.dumps({k: v[0] / 10 for k, v in st.items() if v[1]}))
 '''
