@@ -1314,7 +1314,11 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             }
             const bool h_out = (hF0 && !zero_copy) || (y_out && !is_device_ptr(y_out));
             const bool overlap = overlap_on && !reorder && h_in && n_tiles >= 64;
-            const int64_t chunk_tiles = std::min<int64_t>(n_tiles, 1 << 12);  // operand blocks <= ~1.3 GB
+            // SF_CHUNK_TILES (A/B): chunks small enough that the sampler's operand blocks are still
+            // in L2 when the backbone reads them (plain stores instead of evict-first)
+            static const int64_t chunk_env = std::getenv("SF_CHUNK_TILES") ? std::atoll(std::getenv("SF_CHUNK_TILES")) : 0;
+            const int64_t chunk_tiles = std::min<int64_t>(n_tiles, chunk_env > 0 ? chunk_env : 1 << 12);  // operands <= ~1 GB
+            const bool l2_keep = chunk_env > 0;
             const int64_t chunk = chunk_tiles * sfb::kUmmaM;
             // sampling windows {first row, rows, chunk's first row}
             struct Win {
@@ -1479,7 +1483,7 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                         StageScope st(SF_STAGE_SAMPLE_SORT, stream);
                         sfb::launch_sample_sort(&sc, &dt, &ht, s->d_planes, s->n_planes, s->d_pre, L, w.m, recs.p,
                                                 nullptr, ops.p, mms.p, err.p, stream, media != nullptr,
-                                                (w.r0 - c0) / sfb::kUmmaM, layout_tiles, f16);
+                                                (w.r0 - c0) / sfb::kUmmaM, layout_tiles, f16, l2_keep);
                     }
                 }
                 {

@@ -70,7 +70,8 @@ struct SortDesc {
     int G;                           // table g resolution
     const float* table;              // [G][A][H] (mixed only)
     int nbuf;                        // scratch buffers (2: one block barrier per group, if 3 blocks/SM still fit)
-    int f16;                         // operand blocks in fp16 (SF_PRECISION_FP16) instead of bf16
+    int f16;  // bit 0: operand blocks in fp16 (SF_PRECISION_FP16) instead of bf16; bit 1: plain
+              // stores (the chunk's operands stay in L2 for the backbone) instead of evict-first
 };
 
 // Bilinear lookup in a pre-blended phase plane pl[a][h] = P(a,h), rows padded to H+1 floats
@@ -575,7 +576,7 @@ struct SegOut {
     uint8_t* blk;
     int row, kf, tau;
     float* mm;  // 8 floats
-    int f16;    // operand type: fp16 (1) or bf16 (0), uniform per launch
+    int f16;    // SortDesc::f16 bits, uniform per launch
 };
 
 // Value idx of the operand row [sorted (cnt), mean, max, 0...] from the registers of
@@ -610,10 +611,12 @@ __device__ __forceinline__ void emit_chunks(const float* v, int off, int j0, int
 #pragma unroll
             for (int e = 0; e < 8; ++e) v8[e] = row_value<P>(v, off, 8 * jj + e, cnt, mean, mx);
         }
-        if (o.f16)
-            store_chunk_stream<true>(o.blk, o.row, jj, o.kf, v8);
-        else
-            store_chunk_stream<false>(o.blk, o.row, jj, o.kf, v8);
+        switch (o.f16) {
+            case 0: store_chunk_stream<false>(o.blk, o.row, jj, o.kf, v8); break;
+            case 1: store_chunk_stream<true>(o.blk, o.row, jj, o.kf, v8); break;
+            case 2: store_chunk<false>(o.blk, o.row, jj, o.kf, v8); break;
+            default: store_chunk<true>(o.blk, o.row, jj, o.kf, v8); break;
+        }
     }
 }
 
@@ -1016,11 +1019,11 @@ void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_mediu
 void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const TemplateDev* ht, const float* planes,
                         int n_planes, const float4* pre, const SortLayout& L, int64_t n, const void* recs,
                         const float* feats, uint8_t* ops, float* mms, int* err, cudaStream_t s, bool mixed,
-                        int64_t tile0, int64_t layout_tiles, bool f16) {
+                        int64_t tile0, int64_t layout_tiles, bool f16, bool l2_keep) {
     (void)dt;  // diffuse placement comes from `pre` (k_query_prep's diffuse blocks)
     if (n <= 0) return;
     SortDesc d = make_desc(sc, n_planes, L, n);
-    d.f16 = f16 ? 1 : 0;
+    d.f16 = (f16 ? 1 : 0) | (l2_keep ? 2 : 0);
     if (layout_tiles > 0) {  // a window of a larger operand layout
         if (tile0 < 0 || tile0 + d.n_tiles > layout_tiles) fail(SF_ERR_INVALID_ARGUMENT, "sample_sort: tile window");
         d.tile0 = int(tile0);

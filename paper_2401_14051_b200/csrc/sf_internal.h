@@ -249,7 +249,7 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
                         const float* planes, int n_planes, const float4* pre, const SortLayout& L,
                         int64_t n, const void* recs, const float* feats, uint8_t* ops, float* mms,
                         int* err, cudaStream_t s, bool mixed = false, int64_t tile0 = 0,
-                        int64_t layout_tiles = 0, bool f16 = false);
+                        int64_t layout_tiles = 0, bool f16 = false, bool l2_keep = false);
 // layout_tiles > 0: this launch fills tiles [tile0, tile0 + ceil(n / 128)) of an operand /
 // pool layout of layout_tiles tiles (one backbone launch over several sampling launches).
 // Queries the persistent sampling grid processes per round (one per warp, every SM full):
