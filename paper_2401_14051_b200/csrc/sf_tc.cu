@@ -364,16 +364,21 @@ __global__ void __launch_bounds__(kThreads, 2)
                     umma_commit(r.mma);
                     release(r, j - 1);
                 }
+                // while the MMA runs: the FC-1 bias with the layer's fp32 mean / max columns
+                float be[32];
+                {
+                    const float* b1 = reinterpret_cast<const float*>(s1 + kSlotB1);  // b1, W1 mean / max cols
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) be[e] = fmaf(pool.x, b1[32 + e], fmaf(pool.y, b1[64 + e], b1[e]));
+                }
                 mma_wait(r);
                 PROF(1);
                 // FC-1 epilogue: u = relu(acc + b1) -> bf16 operand of FC-2
                 {
-                    const float* b1 = reinterpret_cast<const float*>(s1 + kSlotB1);  // b1, W1 mean / max cols
                     float acc[32];
                     tmem_ld32(tmem + lane + 0, acc);
 #pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        acc[e] = relu(acc[e] + fmaf(pool.x, b1[32 + e], fmaf(pool.y, b1[64 + e], b1[e])));
+                    for (int e = 0; e < 32; ++e) acc[e] = relu(acc[e] + be[e]);
                     store_row32<kH>(a2, acc);
                 }
                 PROF(2);
@@ -391,17 +396,28 @@ __global__ void __launch_bounds__(kThreads, 2)
                 float w_next = 0.0f;
                 float2 pool_next = pool;
                 if (!last) w_next = attention(s2, tau, rc, pool_next);
+                float b2r[32];  // FC-2 bias into registers while the MMA runs
+                {
+                    const float4* b2 = reinterpret_cast<const float4*>(s2 + kSlotB2);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const float4 v = b2[e];
+                        b2r[4 * e] = v.x;
+                        b2r[4 * e + 1] = v.y;
+                        b2r[4 * e + 2] = v.z;
+                        b2r[4 * e + 3] = v.w;
+                    }
+                }
                 PROF(5);
                 mma_wait(r);
                 PROF(6);
                 // FC-2 epilogue + residual: o = relu(acc + b2) + o_att (fp32)
                 float o[32];
                 {
-                    const float* b2 = reinterpret_cast<const float*>(s2 + kSlotB2);
                     tmem_ld32(tmem + lane + 32, o);
                     PROF(9);
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] = relu(o[e] + b2[e]) + oa[e];
+                    for (int e = 0; e < 32; ++e) o[e] = relu(o[e] + b2r[e]) + oa[e];
                 }
                 pool = pool_next;
                 if (!last) {
