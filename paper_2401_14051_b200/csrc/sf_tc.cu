@@ -24,6 +24,7 @@
 //
 // Precision: bf16 GEMM operands (weights, o_att, features, u, merges), fp32
 // accumulation, fp32 bias / activation / residual / attention (tests/bf16_emulation.py).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -42,10 +43,19 @@ namespace {
 constexpr int kConsumers = 128;             // one thread per query row / TMEM lane
 constexpr int kThreads = kConsumers + 32;    // + one producer warp issuing the bundle copies
 constexpr int kTmemCols = 256;  // fc1 [0,32) fc2 [32,64) merge/head [64,128) cross [128,192)
-constexpr int kSlots = 3;
-constexpr int kSlotBytes = 23552;
+// Ring geometry (compile-time, so every bundle read has a constant offset): slots of the
+// network's largest FC-1 bundle. Layers of up to 48 points: 4 slots of 17,792 B (three
+// bundles in flight while a step runs); up to 64 points: 3 slots of 23,552 B. Either way
+// ~105 KB of shared memory: two CTAs per SM.
+struct RingNarrow {
+    static constexpr int NS = 4, SB = 17792, OF = 5120, OB = 17408, KF = 48;
+};
+struct RingWide {
+    static constexpr int NS = 3, SB = 23552, OF = 6144, OB = 22528, KF = 64;
+};
 // FC-1 bundle: W1[:, :32], W1[:, 32:], the tile's sorted-feature block, FC-1 bias
-constexpr int kSlotW1a = 0, kSlotW1b = 2048, kSlotFeat = 6144, kSlotB1 = 22528;
+// (the sorted-feature block at RC::OF, b1 + W1's mean / max columns at RC::OB)
+constexpr int kSlotW1a = 0, kSlotW1b = 2048;
 // FC-2 bundle: W2, bias. 64-wide bundles: weights, bias, head2 W/b (head-1 bundle)
 constexpr int kSlotB2 = 2048, kSlotBias = 8192, kSlotHead2 = 8448;
 constexpr int kSlotWmHi = 4096;  // merge bundle: W_m[:, 0:32] at 0, W_m[:, 32:64] here
@@ -53,7 +63,16 @@ constexpr int kSlotWmHi = 4096;  // merge bundle: W_m[:, 0:32] at 0, W_m[:, 32:6
 // the attention weight is computed while that step's MMA runs: the tile's mean/max block,
 // [52] attention W1 b1 W2 b2 (+pad), [224 + 32] conditioning W/b (first layer of a stack).
 constexpr int kPayMM = 9728, kPayAtt = 13824, kPayInit = 14080;
-static_assert(kPayInit + 1024 <= kSlotB1 && kSlotB1 + 384 <= kSlotBytes, "slot layout");
+template <class RC>
+constexpr bool ring_ok() {
+    return kSlotW1b + 32 * RC::KF * 2 <= RC::OF && RC::OF + kUmmaM * RC::KF * 2 <= RC::OB && RC::OB + 384 <= RC::SB &&
+           kPayInit + 1024 <= RC::SB && RC::OF % 128 == 0 && RC::SB % 128 == 0;
+}
+static_assert(ring_ok<RingNarrow>() && ring_ok<RingWide>(), "slot layout");
+template <class RC>
+constexpr size_t ring_smem() {
+    return 1024 + 2 * kUmmaM * 32 * 2 + kUmmaM * 64 * 2 + size_t(RC::NS) * RC::SB;
+}
 constexpr int kMaxSteps = 96;
 constexpr int kMaxCopies = 6;
 
@@ -91,17 +110,18 @@ __device__ unsigned long long g_tc_prof[16];
 struct TcPack {
     uint8_t* d_blobs = nullptr;
     TcDesc desc{};
+    bool narrow = false;  // RingNarrow (every layer <= 48 points) else RingWide
 };
 
 struct Ring {
     uint8_t* base;
-    uint64_t* full;   // [kSlots] bundle landed (producer expect_tx + bulk copies)
-    uint64_t* empty;  // [kSlots] bundle consumed (consumer thread 0)
+    uint64_t* full;   // [NS] bundle landed (producer expect_tx + bulk copies)
+    uint64_t* empty;  // [NS] bundle consumed (consumer thread 0)
     uint64_t* mma;    // MMA completion (tcgen05.commit)
     uint32_t mpar;
 };
 
-// Producer: the copies of one step into ring slot j % kSlots. The step program is in
+// Producer: the copies of one step into ring slot j % NS. The step program is in
 // global memory; the whole descriptor is fetched with independent loads (one L2 round
 // trip) before the producer waits for the slot, so only the copies remain to issue.
 struct StepRegs {
@@ -114,9 +134,10 @@ __device__ __forceinline__ void load_step(const TcDesc& d, int j, StepRegs& sr) 
     for (int k = 0; k < 1 + 2 * kMaxCopies; ++k) sr.w[k] = __ldg(p + k);
 }
 
+template <class RC>
 __device__ __forceinline__ void issue_step(const Ring& r, const StepRegs& sr, int j, const uint8_t* wpk,
                                            const uint8_t* ops, const uint8_t* mms, int tile, int n_tiles) {
-    const int slot = j % kSlots;
+    const int slot = j % RC::NS;
     uint64_t* bar = &r.full[slot];
     mbar_expect_tx(bar, uint32_t(sr.w[0].y));
 #pragma unroll
@@ -134,7 +155,7 @@ __device__ __forceinline__ void issue_step(const Ring& r, const StepRegs& sr, in
             src = ops + a * n_tiles + int64_t(tile) * stride;
         else
             src = mms + a * int64_t(n_tiles) * 4096 + int64_t(tile) * 4096;
-        bulk_g2s(r.base + slot * kSlotBytes + dst, src, bytes, bar);
+        bulk_g2s(r.base + slot * RC::SB + dst, src, bytes, bar);
     }
 }
 
@@ -162,15 +183,17 @@ __device__ void wd_wait(uint64_t* bar, uint32_t parity, int code, int j) {
 #define SF_WAIT(bar, par, code, j) mbar_wait(bar, par)
 #endif
 
+template <class RC>
 __device__ __forceinline__ uint8_t* wait_full(const Ring& r, int j) {
-    const int slot = j % kSlots;
-    SF_WAIT(&r.full[slot], uint32_t(j / kSlots) & 1u, 1, j);
-    return r.base + slot * kSlotBytes;
+    const int slot = j % RC::NS;
+    SF_WAIT(&r.full[slot], uint32_t(j / RC::NS) & 1u, 1, j);
+    return r.base + slot * RC::SB;
 }
 
 // Consumer thread 0: step j's bundle is no longer read (its MMA completed, epilogue done).
+template <class RC>
 __device__ __forceinline__ void release(const Ring& r, int j) {
-    if (j >= 0) mbar_arrive(&r.empty[j % kSlots]);
+    if (j >= 0) mbar_arrive(&r.empty[j % RC::NS]);
 }
 
 // Operands written by the consumer threads -> visible to the tensor core; then thread 0 issues.
@@ -260,14 +283,14 @@ __device__ __forceinline__ void store_row32(uint8_t* a, const float* v) {
 }
 
 // kH: fp16 GEMM operands (SF_PRECISION_FP16), else bf16; fp32 accumulation either way
-template <bool kH>
+template <bool kH, class RC>
 __global__ void __launch_bounds__(kThreads, 2)
     k_backbone_tc(const TcDesc d, const uint8_t* __restrict__ wpk, const uint8_t* __restrict__ ops,
                   const uint8_t* __restrict__ mms, int n_tiles, int64_t n, const double* __restrict__ cfg8,
                   float* __restrict__ y_out, double* __restrict__ F_out, const int* __restrict__ perm,
                   int f_stage) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    __shared__ uint64_t bars[2 * kSlots + 1];
+    __shared__ uint64_t bars[2 * RC::NS + 1];
     __shared__ uint32_t tmem_slot;
     __shared__ int s_kf[2][16];
 
@@ -292,13 +315,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     Ring r;
     r.base = a2 + kUmmaM * 64 * 2;
     r.full = bars;
-    r.empty = bars + kSlots;
-    r.mma = bars + 2 * kSlots;
+    r.empty = bars + RC::NS;
+    r.mma = bars + 2 * RC::NS;
     r.mpar = 0;
 
     if (warp == 0) tmem_alloc(&tmem_slot, kTmemCols);
     if (tid == 0) {
-        for (int s = 0; s < 2 * kSlots + 1; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < 2 * RC::NS + 1; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid < 32) s_kf[tid >> 4][tid & 15] = (d.counts[tid >> 4][tid & 15] + 15) / 16 * 16;
@@ -312,8 +335,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             load_step(d, 0, cur);
             for (int j = 0; j < d.n_steps; ++j) {
                 if (j + 1 < d.n_steps) load_step(d, j + 1, nxt);  // in flight across the slot wait
-                if (j >= kSlots) SF_WAIT(&r.empty[j % kSlots], uint32_t(j / kSlots - 1) & 1u, 2, j);
-                issue_step(r, cur, j, wpk, ops, mms, tile, n_tiles);
+                if (j >= RC::NS) SF_WAIT(&r.empty[j % RC::NS], uint32_t(j / RC::NS - 1) & 1u, 2, j);
+                issue_step<RC>(r, cur, j, wpk, ops, mms, tile, n_tiles);
                 cur = nxt;
             }
         }
@@ -345,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     float oa[32];  // o_att of the current layer (fp32 residual); its bf16 copy is a_att
     float2 pool;   // the current layer's (mean, max) of its feature type
     // step 0: payload of the first FC-1 step
-    stack_start(wait_full(r, 0), 0, rc, oa, pool);
+    stack_start(wait_full<RC>(r, 0), 0, rc, oa, pool);
     store_row32<kH>(a_att, oa);
     int j = 1;
     for (int tau = 0; tau < 3; ++tau) {
@@ -354,20 +377,20 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int i = 0; i < nl; ++i) {
                 // FC-1 = [o_att | sorted_tau, mean, max] W1^T
                 PROF(7);
-                const uint8_t* s1 = wait_full(r, j);
+                const uint8_t* s1 = wait_full<RC>(r, j);
                 PROF(0);
                 mma_sync();
                 if (tid == 0) {
                     const uint32_t b1s = smem_u32(s1);
                     issue_gemm<kH>(tmem + 0, 32, s_att, 32, b1s + kSlotW1a, false);
-                    issue_gemm<kH>(tmem + 0, 32, b1s + kSlotFeat, s_kf[kind][i], b1s + kSlotW1b, true);
+                    issue_gemm<kH>(tmem + 0, 32, b1s + RC::OF, s_kf[kind][i], b1s + kSlotW1b, true);
                     umma_commit(r.mma);
-                    release(r, j - 1);
+                    release<RC>(r, j - 1);
                 }
                 // while the MMA runs: the FC-1 bias with the layer's fp32 mean / max columns
                 float be[32];
                 {
-                    const float* b1 = reinterpret_cast<const float*>(s1 + kSlotB1);  // b1, W1 mean / max cols
+                    const float* b1 = reinterpret_cast<const float*>(s1 + RC::OB);  // b1, W1 mean / max cols
 #pragma unroll
                     for (int e = 0; e < 32; ++e) be[e] = fmaf(pool.x, b1[32 + e], fmaf(pool.y, b1[64 + e], b1[e]));
                 }
@@ -382,13 +405,13 @@ __global__ void __launch_bounds__(kThreads, 2)
                     store_row32<kH>(a2, acc);
                 }
                 PROF(2);
-                const uint8_t* s2 = wait_full(r, j + 1);
+                const uint8_t* s2 = wait_full<RC>(r, j + 1);
                 PROF(3);
                 mma_sync();
                 if (tid == 0) {
                     issue_gemm<kH>(tmem + 32, 32, s_a2, 32, smem_u32(s2), false);
                     umma_commit(r.mma);
-                    release(r, j);
+                    release<RC>(r, j);
                 }
                 PROF(4);
                 // while FC-2 runs: the next FC-1's attention weight (payload of this bundle)
@@ -438,13 +461,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         // merged_tau = relu(W_m [od; oh] + b)
         {
-            const uint8_t* sm = wait_full(r, j);
+            const uint8_t* sm = wait_full<RC>(r, j);
             mma_sync();
             if (tid == 0) {
                 issue_gemm<kH>(tmem + 64, 64, s_od, 32, smem_u32(sm), false);
                 issue_gemm<kH>(tmem + 64, 64, s_a2, 32, smem_u32(sm) + kSlotWmHi, true);
                 umma_commit(r.mma);
-                release(r, j - 1);
+                release<RC>(r, j - 1);
             }
             mma_wait(r);
             const float* bm = reinterpret_cast<const float*>(sm + kSlotBias);
@@ -460,12 +483,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         // cross += W_c[:, 64 tau : 64 tau + 64] merged_tau (accumulated in TMEM)
         {
-            const uint8_t* sc = wait_full(r, j);
+            const uint8_t* sc = wait_full<RC>(r, j);
             mma_sync();
             if (tid == 0) {
                 issue_gemm<kH>(tmem + 128, 64, s_a2, 64, smem_u32(sc), tau > 0);
                 umma_commit(r.mma);
-                release(r, j - 1);
+                release<RC>(r, j - 1);
             }
             if (tau < 2) {  // next type's first diffuse layer, while the cross MMA runs
                 stack_start(sc, tau + 1, rc, oa, pool);
@@ -488,12 +511,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     // head 0 / 1 (64 -> 64, relu); head 2 (64 -> 3) SIMT from the head-1 bundle
     for (int l = 0; l < 2; ++l) {
-        const uint8_t* sh = wait_full(r, j);
+        const uint8_t* sh = wait_full<RC>(r, j);
         mma_sync();
         if (tid == 0) {
             issue_gemm<kH>(tmem + 64, 64, s_a2, 64, smem_u32(sh), false);
             umma_commit(r.mma);
-            release(r, j - 1);
+            release<RC>(r, j - 1);
         }
         mma_wait(r);
         const float* bh = reinterpret_cast<const float*>(sh + kSlotBias);
@@ -639,10 +662,16 @@ void tc_prepare(sf_backbone& b, cudaStream_t s, bool f16) {
     const sf_backbone_config& c = b.cfg;
     const BackboneLayout& L = b.layout;
     const SortLayout S = sort_layout(c);
+    int kf_max = 0;
+    for (int k = 0; k < 2; ++k)
+        for (int i = 0; i < S.nl[k]; ++i) kf_max = std::max(kf_max, S.kf[k][i]);
+    static const bool force_wide = std::getenv("SF_TC_WIDE") != nullptr;  // A/B
+    const bool narrow = kf_max <= RingNarrow::KF && !force_wide;
     std::vector<float> P(size_t(L.total));
     SFB_CUDA(cudaMemcpyAsync(P.data(), b.d_params, P.size() * sizeof(float), cudaMemcpyDeviceToHost, s));
     SFB_CUDA(cudaStreamSynchronize(s));
     auto pk = std::make_unique<TcPack>();
+    pk->narrow = narrow;
     std::vector<uint8_t> buf;
     std::vector<Step> steps;
     const int W = 32;
@@ -680,13 +709,13 @@ void tc_prepare(sf_backbone& b, cudaStream_t s, bool f16) {
                 st.k2 = kf;
                 st.c[0] = pcopy(pack_blob_(buf, P.data() + off, W, W, K, 0, W), W * W * 2, kSlotW1a);
                 st.c[1] = pcopy(pack_blob_(buf, P.data() + off, W, cnt, K, W, kf), uint32_t(W * kf * 2), kSlotW1b);
-                st.c[2] = Copy{1, uint32_t(kSlotFeat), uint32_t(kUmmaM * kf * 2), 0, S.seg_prefix[kind][i][tau],
+                st.c[2] = Copy{1, uint32_t(narrow ? RingNarrow::OF : RingWide::OF), uint32_t(kUmmaM * kf * 2), 0, S.seg_prefix[kind][i][tau],
                                int64_t(kUmmaM) * kf * 2};
                 // b1 [32], then the mean and max columns of W1 [32] + [32] (fp32 rank-2 update)
                 std::vector<float> bmx = slice(P, off + int64_t(W) * K, W);
                 for (int r = 0; r < W; ++r) bmx.push_back(P[size_t(off + int64_t(r) * K + W + cnt)]);
                 for (int r = 0; r < W; ++r) bmx.push_back(P[size_t(off + int64_t(r) * K + W + cnt + 1)]);
-                st.c[3] = pcopy(pack_f32(buf, bmx), f32_bytes(bmx.size()), kSlotB1);
+                st.c[3] = pcopy(pack_f32(buf, bmx), f32_bytes(bmx.size()), narrow ? RingNarrow::OB : RingWide::OB);
                 st.ncopy = 4;
                 push(st);
                 off += int64_t(W) * K + W;
@@ -768,10 +797,11 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
     auto packs = static_cast<const TcPacks*>(b.tc);
     const TcPack* pk = packs ? packs->p[f16 ? 1 : 0].get() : nullptr;
     if (!pk) fail(SF_ERR_INVALID_ARGUMENT, "tc backbone: operands not prepared for this precision");
-    size_t smem = 1024 + 2 * kUmmaM * 32 * 2 + kUmmaM * 64 * 2 + size_t(kSlots) * kSlotBytes;
+    size_t smem = pk->narrow ? ring_smem<RingNarrow>() : ring_smem<RingWide>();
     static const bool solo = std::getenv("SF_DEBUG_TC") && std::atoi(std::getenv("SF_DEBUG_TC")) == 2;
     if (solo) smem = 200 * 1024;  // one CTA per SM: uncontended chain latency
-    auto kern = f16 ? k_backbone_tc<true> : k_backbone_tc<false>;
+    auto kern = pk->narrow ? (f16 ? k_backbone_tc<true, RingNarrow> : k_backbone_tc<false, RingNarrow>)
+                           : (f16 ? k_backbone_tc<true, RingWide> : k_backbone_tc<false, RingWide>);
     // function attributes are per device: remember the size set on each device and variant (a
     // process may drive several GPUs, from several threads)
     static std::mutex attr_mu;
@@ -780,7 +810,7 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
     SFB_CUDA(cudaGetDevice(&dev));
     {
         std::lock_guard<std::mutex> lk(attr_mu);
-        const int key = 2 * dev + (f16 ? 1 : 0);
+        const int key = 4 * dev + (f16 ? 1 : 0) + (pk->narrow ? 2 : 0);
         if (attr_set[key] != smem) {
             SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
