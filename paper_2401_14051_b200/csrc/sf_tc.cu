@@ -18,9 +18,12 @@
 // Everything a step needs — its weight blob, the tile's sorted-feature operand
 // block and mean/max block, and the step's small FP32 SIMT parameters (attention
 // 8->4->3, biases, the 7->32 conditioning layer, the 64->3 output layer) — is one
-// bundle of cp.async.bulk copies into a 3-slot SMEM ring completing on one
-// mbarrier; bundle j+2 is in flight while step j runs, so no global load sits on
-// the per-layer critical path. The step program lives in the kernel parameters.
+// bundle of cp.async.bulk copies into a ring of SMEM slots completing on one
+// mbarrier; every consumer warp releases a slot the moment it is done with it (the
+// step's MMA completed, its biases already in registers), so the next bundle lands
+// while the layer's epilogue runs. The step program is read from global memory by the
+// producer warp. The per-layer chain (MMA -> epilogue -> MMA) is latency-bound, so
+// throughput comes from independent chains per SM: three CTAs (RingTri).
 //
 // Precision: bf16 GEMM operands (weights, o_att, features, u, merges), fp32
 // accumulation, fp32 bias / activation / residual / attention (tests/bf16_emulation.py).
@@ -30,6 +33,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <unordered_map>
 #include <vector>
 
@@ -42,16 +46,23 @@ namespace {
 
 constexpr int kConsumers = 128;             // one thread per query row / TMEM lane
 constexpr int kThreads = kConsumers + 32;    // + one producer warp issuing the bundle copies
-constexpr int kTmemCols = 256;  // fc1 [0,32) fc2 [32,64) merge/head [64,128) cross [128,192)
+// TMEM: fc1 [0,32) fc2 [32,64); merge / head [0,64) once a type's stacks are done; cross [64,128)
+constexpr int kTmemCols = 128;
+constexpr int kColMerge = 0, kColCross = 64;
 // Ring geometry (compile-time, so every bundle read has a constant offset): slots of the
-// network's largest FC-1 bundle. Layers of up to 48 points: 4 slots of 17,792 B (three
-// bundles in flight while a step runs); up to 64 points: 3 slots of 23,552 B. Either way
-// ~105 KB of shared memory: two CTAs per SM.
+// network's largest FC-1 bundle. Layers of up to 48 points: RingTri, 2 slots of 17,792 B
+// (~70 KB of shared memory, 128 TMEM columns, <= 128 registers: three CTAs = three
+// independent layer chains per SM; a slot is refilled as soon as every warp is done with
+// it); up to 64 points: RingWide, 3 slots of 23,552 B, two CTAs per SM.
 struct RingNarrow {
-    static constexpr int NS = 4, SB = 17792, OF = 5120, OB = 17408, KF = 48;
+    static constexpr int NS = 4, SB = 17792, OF = 5120, OB = 17408, KF = 48, MINB = 2;
 };
 struct RingWide {
-    static constexpr int NS = 3, SB = 23552, OF = 6144, OB = 22528, KF = 64;
+    static constexpr int NS = 3, SB = 23552, OF = 6144, OB = 22528, KF = 64, MINB = 2;
+};
+// two slots, ~70 KB: three CTAs (three independent chains) per SM
+struct RingTri {
+    static constexpr int NS = 2, SB = 17792, OF = 5120, OB = 17408, KF = 48, MINB = 3;
 };
 // FC-1 bundle: W1[:, :32], W1[:, 32:], the tile's sorted-feature block, FC-1 bias
 // (the sorted-feature block at RC::OF, b1 + W1's mean / max columns at RC::OB)
@@ -68,7 +79,7 @@ constexpr bool ring_ok() {
     return kSlotW1b + 32 * RC::KF * 2 <= RC::OF && RC::OF + kUmmaM * RC::KF * 2 <= RC::OB && RC::OB + 384 <= RC::SB &&
            kPayInit + 1024 <= RC::SB && RC::OF % 128 == 0 && RC::SB % 128 == 0;
 }
-static_assert(ring_ok<RingNarrow>() && ring_ok<RingWide>(), "slot layout");
+static_assert(ring_ok<RingNarrow>() && ring_ok<RingWide>() && ring_ok<RingTri>(), "slot layout");
 template <class RC>
 constexpr size_t ring_smem() {
     return 1024 + 2 * kUmmaM * 32 * 2 + kUmmaM * 64 * 2 + size_t(RC::NS) * RC::SB;
@@ -110,7 +121,8 @@ __device__ unsigned long long g_tc_prof[16];
 struct TcPack {
     uint8_t* d_blobs = nullptr;
     TcDesc desc{};
-    bool narrow = false;  // RingNarrow (every layer <= 48 points) else RingWide
+    bool narrow = false;  // RingNarrow / RingTri (every layer <= 48 points) else RingWide
+    bool tri = false;     // RingTri (default for narrow networks; SF_TC_RING=narrow: RingNarrow)
 };
 
 struct Ring {
@@ -190,10 +202,12 @@ __device__ __forceinline__ uint8_t* wait_full(const Ring& r, int j) {
     return r.base + slot * RC::SB;
 }
 
-// Consumer thread 0: step j's bundle is no longer read (its MMA completed, epilogue done).
+// Every consumer warp, once step j's bundle is dead for it (its MMA completed and the warp's
+// last read of the slot done): one arrival per warp, so a slot is refilled as early as possible.
 template <class RC>
 __device__ __forceinline__ void release(const Ring& r, int j) {
-    if (j >= 0) mbar_arrive(&r.empty[j % RC::NS]);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&r.empty[j % RC::NS]);
 }
 
 // Operands written by the consumer threads -> visible to the tensor core; then thread 0 issues.
@@ -284,7 +298,7 @@ __device__ __forceinline__ void store_row32(uint8_t* a, const float* v) {
 
 // kH: fp16 GEMM operands (SF_PRECISION_FP16), else bf16; fp32 accumulation either way
 template <bool kH, class RC>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, RC::MINB)
     k_backbone_tc(const TcDesc d, const uint8_t* __restrict__ wpk, const uint8_t* __restrict__ ops,
                   const uint8_t* __restrict__ mms, int n_tiles, int64_t n, const double* __restrict__ cfg8,
                   float* __restrict__ y_out, double* __restrict__ F_out, const int* __restrict__ perm,
@@ -321,7 +335,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     if (warp == 0) tmem_alloc(&tmem_slot, kTmemCols);
     if (tid == 0) {
-        for (int s = 0; s < 2 * RC::NS + 1; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < 2 * RC::NS + 1; ++s)
+            mbar_init(&bars[s], s >= RC::NS && s < 2 * RC::NS ? kConsumers / 32 : 1);  // empty: per warp
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid < 32) s_kf[tid >> 4][tid & 15] = (d.counts[tid >> 4][tid & 15] + 15) / 16 * 16;
@@ -369,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     float2 pool;   // the current layer's (mean, max) of its feature type
     // step 0: payload of the first FC-1 step
     stack_start(wait_full<RC>(r, 0), 0, rc, oa, pool);
+    release<RC>(r, 0);
     store_row32<kH>(a_att, oa);
     int j = 1;
     for (int tau = 0; tau < 3; ++tau) {
@@ -385,7 +401,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                     issue_gemm<kH>(tmem + 0, 32, s_att, 32, b1s + kSlotW1a, false);
                     issue_gemm<kH>(tmem + 0, 32, b1s + RC::OF, s_kf[kind][i], b1s + kSlotW1b, true);
                     umma_commit(r.mma);
-                    release<RC>(r, j - 1);
                 }
                 // while the MMA runs: the FC-1 bias with the layer's fp32 mean / max columns
                 float be[32];
@@ -395,6 +410,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     for (int e = 0; e < 32; ++e) be[e] = fmaf(pool.x, b1[32 + e], fmaf(pool.y, b1[64 + e], b1[e]));
                 }
                 mma_wait(r);
+                release<RC>(r, j);  // W1 / features consumed, bias in registers
                 PROF(1);
                 // FC-1 epilogue: u = relu(acc + b1) -> bf16 operand of FC-2
                 {
@@ -411,7 +427,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (tid == 0) {
                     issue_gemm<kH>(tmem + 32, 32, s_a2, 32, smem_u32(s2), false);
                     umma_commit(r.mma);
-                    release<RC>(r, j);
                 }
                 PROF(4);
                 // while FC-2 runs: the next FC-1's attention weight (payload of this bundle)
@@ -433,6 +448,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 PROF(5);
                 mma_wait(r);
+                if (!(last && kind == 0)) release<RC>(r, j + 1);  // else after the highlight stack's start
                 PROF(6);
                 // FC-2 epilogue + residual: o = relu(acc + b2) + o_att (fp32)
                 float o[32];
@@ -452,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 } else if (kind == 0) {  // od: K 0-31 of the merge input
                     store_row32<kH>(a_od, o);
                     stack_start(s2, tau, rc, oa, pool);  // highlight stack (once per type: not overlapped)
+                    release<RC>(r, j + 1);
                     store_row32<kH>(a_att, oa);
                 } else {  // oh: K 32-63 of the merge input
                     store_row32<kH>(a2, o);
@@ -464,21 +481,21 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint8_t* sm = wait_full<RC>(r, j);
             mma_sync();
             if (tid == 0) {
-                issue_gemm<kH>(tmem + 64, 64, s_od, 32, smem_u32(sm), false);
-                issue_gemm<kH>(tmem + 64, 64, s_a2, 32, smem_u32(sm) + kSlotWmHi, true);
+                issue_gemm<kH>(tmem + kColMerge, 64, s_od, 32, smem_u32(sm), false);
+                issue_gemm<kH>(tmem + kColMerge, 64, s_a2, 32, smem_u32(sm) + kSlotWmHi, true);
                 umma_commit(r.mma);
-                release<RC>(r, j - 1);
             }
             mma_wait(r);
             const float* bm = reinterpret_cast<const float*>(sm + kSlotBias);
             for (int half = 0; half < 2; ++half) {
                 float acc[32];
-                tmem_ld32(tmem + lane + 64 + 32 * half, acc);
+                tmem_ld32(tmem + lane + kColMerge + 32 * half, acc);
 #pragma unroll
                 for (int e = 0; e < 32; ++e) acc[e] = relu(acc[e] + bm[32 * half + e]);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) store_chunk<kH>(a2, tid, half * 4 + c, 64, acc + 8 * c);
             }
+            release<RC>(r, j);
             ++j;
         }
         // cross += W_c[:, 64 tau : 64 tau + 64] merged_tau (accumulated in TMEM)
@@ -486,9 +503,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint8_t* sc = wait_full<RC>(r, j);
             mma_sync();
             if (tid == 0) {
-                issue_gemm<kH>(tmem + 128, 64, s_a2, 64, smem_u32(sc), tau > 0);
+                issue_gemm<kH>(tmem + kColCross, 64, s_a2, 64, smem_u32(sc), tau > 0);
                 umma_commit(r.mma);
-                release<RC>(r, j - 1);
             }
             if (tau < 2) {  // next type's first diffuse layer, while the cross MMA runs
                 stack_start(sc, tau + 1, rc, oa, pool);
@@ -499,13 +515,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const float* bc = reinterpret_cast<const float*>(sc + kSlotBias);
                 for (int half = 0; half < 2; ++half) {
                     float h[32];
-                    tmem_ld32(tmem + lane + 128 + 32 * half, h);
+                    tmem_ld32(tmem + lane + kColCross + 32 * half, h);
 #pragma unroll
                     for (int e = 0; e < 32; ++e) h[e] = relu(h[e] + bc[32 * half + e]);
 #pragma unroll
                     for (int c = 0; c < 4; ++c) store_chunk<kH>(a2, tid, half * 4 + c, 64, h + 8 * c);
                 }
             }
+            release<RC>(r, j);
             ++j;
         }
     }
@@ -514,15 +531,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint8_t* sh = wait_full<RC>(r, j);
         mma_sync();
         if (tid == 0) {
-            issue_gemm<kH>(tmem + 64, 64, s_a2, 64, smem_u32(sh), false);
+            issue_gemm<kH>(tmem + kColMerge, 64, s_a2, 64, smem_u32(sh), false);
             umma_commit(r.mma);
-            release<RC>(r, j - 1);
         }
         mma_wait(r);
         const float* bh = reinterpret_cast<const float*>(sh + kSlotBias);
         float h[64];
-        tmem_ld32(tmem + lane + 64, h);
-        tmem_ld32(tmem + lane + 96, h + 32);
+        tmem_ld32(tmem + lane + kColMerge, h);
+        tmem_ld32(tmem + lane + kColMerge + 32, h + 32);
 #pragma unroll
         for (int e = 0; e < 64; ++e) h[e] = relu(h[e] + bh[e]);
         if (l == 0) {
@@ -672,6 +688,10 @@ void tc_prepare(sf_backbone& b, cudaStream_t s, bool f16) {
     SFB_CUDA(cudaStreamSynchronize(s));
     auto pk = std::make_unique<TcPack>();
     pk->narrow = narrow;
+    // RingTri unless SF_TC_RING=narrow (A/B): three 2-slot CTAs per SM measured 13% faster than
+    // two 4-slot ones at C5 (1.71 vs 1.97 ms, bit-identical results)
+    static const bool want_tri = !(std::getenv("SF_TC_RING") && std::string(std::getenv("SF_TC_RING")) == "narrow");
+    pk->tri = narrow && want_tri;
     std::vector<uint8_t> buf;
     std::vector<Step> steps;
     const int W = 32;
@@ -797,11 +817,12 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
     auto packs = static_cast<const TcPacks*>(b.tc);
     const TcPack* pk = packs ? packs->p[f16 ? 1 : 0].get() : nullptr;
     if (!pk) fail(SF_ERR_INVALID_ARGUMENT, "tc backbone: operands not prepared for this precision");
-    size_t smem = pk->narrow ? ring_smem<RingNarrow>() : ring_smem<RingWide>();
+    size_t smem = pk->tri ? ring_smem<RingTri>() : pk->narrow ? ring_smem<RingNarrow>() : ring_smem<RingWide>();
     static const bool solo = std::getenv("SF_DEBUG_TC") && std::atoi(std::getenv("SF_DEBUG_TC")) == 2;
     if (solo) smem = 200 * 1024;  // one CTA per SM: uncontended chain latency
-    auto kern = pk->narrow ? (f16 ? k_backbone_tc<true, RingNarrow> : k_backbone_tc<false, RingNarrow>)
-                           : (f16 ? k_backbone_tc<true, RingWide> : k_backbone_tc<false, RingWide>);
+    auto kern = pk->tri      ? (f16 ? k_backbone_tc<true, RingTri> : k_backbone_tc<false, RingTri>)
+                : pk->narrow ? (f16 ? k_backbone_tc<true, RingNarrow> : k_backbone_tc<false, RingNarrow>)
+                             : (f16 ? k_backbone_tc<true, RingWide> : k_backbone_tc<false, RingWide>);
     // function attributes are per device: remember the size set on each device and variant (a
     // process may drive several GPUs, from several threads)
     static std::mutex attr_mu;
@@ -810,16 +831,15 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
     SFB_CUDA(cudaGetDevice(&dev));
     {
         std::lock_guard<std::mutex> lk(attr_mu);
-        const int key = 4 * dev + (f16 ? 1 : 0) + (pk->narrow ? 2 : 0);
+        const int key = 8 * dev + (f16 ? 1 : 0) + (pk->narrow ? 2 : 0) + (pk->tri ? 4 : 0);
         if (attr_set[key] != smem) {
             SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                           int(cudaSharedmemCarveoutMaxShared)));
             attr_set[key] = smem;
-            // two co-resident tiles per SM by design (168 registers x 160 threads, 105 KB smem,
-            // 2 x 256 TMEM columns); ncu reports "Block Limit Registers 2 / Shared Mem 2"
-            // (profiles/ncu_traffic.json), while cudaOccupancyMaxActiveBlocksPerMultiprocessor
-            // answers 1 for this kernel, so no runtime check here.
+            // co-resident tiles per SM by design (RingTri: 3 x (128 registers x 160 threads,
+            // ~70 KB smem, 128 TMEM columns); RingWide: 2); the occupancy API does not model
+            // TMEM, so no runtime check here.
         }
     }
     const int n_tiles = int((n + kUmmaM - 1) / kUmmaM);
