@@ -557,6 +557,15 @@ def run_b200(args):
     return 0
 
 
+def binding(k):
+    """What binds a gather kernel whose logical bytes mostly hit L1/L2 (so frac vs HBM can exceed 1):
+    the ncu-measured L1 data-pipe utilisation and the real DRAM bytes per launch."""
+    if not k:
+        return "L1 data pipe (no ncu summary for this workload)"
+    return (f"L1 data pipe {k.get('l1_data_pipe_pct', 0):.0f}% busy, issue {k.get('issue_active_pct', 0):.0f}% "
+            f"(ncu); real DRAM {k.get('dram_bytes', 0) / 1e6:.0f} MB per launch")
+
+
 def roofline(sf, w, stage_ms, n, precision):
     """Dominant kernel's roofline from the live per-stage events, plus rows for the other kernels.
     Algorithmic work per unit: sampling 33,984 B/query of logical gathers (266
@@ -573,7 +582,8 @@ def roofline(sf, w, stage_ms, n, precision):
         rows["k_sample_sort"] = {"bound": "hbm", "achieved": bytes_q * n / t / 1e9, "peak": hbm, "unit": "GB/s",
                                  "frac": bytes_q * n / t / 1e9 / hbm, "traffic": k.get("dram_bytes"),
                                  "l1_data_pipe_pct": k.get("l1_data_pipe_pct"), "ms": stage_ms["sample_sort"],
-                                 "algorithmic": f"{bytes_q} B/query logical gathers x {n} queries per launch"}
+                                 "algorithmic": f"{bytes_q} B/query logical gathers x {n} queries per launch",
+                                 "binding": binding(k)}
     if "backbone" in stage_ms:
         t = stage_ms["backbone"] * 1e-3
         k = ncu.get("k_backbone_tc", {})
@@ -581,7 +591,9 @@ def roofline(sf, w, stage_ms, n, precision):
         rows["k_backbone_tc"] = {"bound": "tensor", "achieved": ach, "peak": bf16_sus, "unit": "TFLOP/s",
                                  "frac": ach / bf16_sus, "traffic": k.get("dram_bytes"),
                                  "tensor_pipe_pct": k.get("tensor_pipe_active_pct"), "ms": stage_ms["backbone"],
-                                 "algorithmic": f"{flop_q} FLOP/query x {n} queries per launch"}
+                                 "algorithmic": f"{flop_q} FLOP/query x {n} queries per launch",
+                                 "binding": "latency of the per-layer MMA -> epilogue chain (36 layers per tile); "
+                                            "three independent chains (CTAs) per SM, limited by shared memory"}
     if "march" in stage_ms and w.name != "c2":
         smp = samples_per_light(w.grid, w.step_lights(0)[0][0])
         t = stage_ms["march"] / w.per_step * 1e-3
@@ -589,7 +601,8 @@ def roofline(sf, w, stage_ms, n, precision):
         rows["k_graded_cols"] = {"bound": "hbm", "achieved": 32 * smp / t / 1e9, "peak": hbm, "unit": "GB/s",
                                  "frac": 32 * smp / t / 1e9 / hbm, "traffic": k.get("dram_bytes"),
                                  "l1_data_pipe_pct": k.get("l1_data_pipe_pct"), "ms": stage_ms["march"] / w.per_step,
-                                 "algorithmic": f"32 B per trilinear sample x {smp} samples per light (all levels)"}
+                                 "algorithmic": f"32 B per trilinear sample x {smp} samples per light (all levels)",
+                                 "binding": binding(k)}
     if "combiner" in stage_ms and w.name != "c2":
         nv = w.grid ** 3
         levels = int(math.log2(w.grid)) + 1

@@ -297,6 +297,9 @@ __device__ __forceinline__ void store_row32(uint8_t* a, const float* v) {
 }
 
 // kH: fp16 GEMM operands (SF_PRECISION_FP16), else bf16; fp32 accumulation either way
+#ifndef SF_TC_EARLY_B2
+#define SF_TC_EARLY_B2 1
+#endif
 template <bool kH, class RC>
 __global__ void __launch_bounds__(kThreads, RC::MINB)
     k_backbone_tc(const TcDesc d, const uint8_t* __restrict__ wpk, const uint8_t* __restrict__ ops,
@@ -435,6 +438,7 @@ __global__ void __launch_bounds__(kThreads, RC::MINB)
                 float2 pool_next = pool;
                 if (!last) w_next = attention(s2, tau, rc, pool_next);
                 float b2r[32];  // FC-2 bias into registers while the MMA runs
+#if SF_TC_EARLY_B2
                 {
                     const float4* b2 = reinterpret_cast<const float4*>(s2 + kSlotB2);
 #pragma unroll
@@ -446,14 +450,18 @@ __global__ void __launch_bounds__(kThreads, RC::MINB)
                         b2r[4 * e + 3] = v.w;
                     }
                 }
+#endif
                 PROF(5);
                 mma_wait(r);
-                if (!(last && kind == 0)) release<RC>(r, j + 1);  // else after the highlight stack's start
+                if (!(last && kind == 0) && SF_TC_EARLY_B2) release<RC>(r, j + 1);  // else after the stack start
                 PROF(6);
                 // FC-2 epilogue + residual: o = relu(acc + b2) + o_att (fp32)
                 float o[32];
                 {
                     tmem_ld32(tmem + lane + 32, o);
+#if !SF_TC_EARLY_B2
+                    for (int e = 0; e < 32; ++e) b2r[e] = reinterpret_cast<const float*>(s2 + kSlotB2)[e];
+#endif
                     PROF(9);
 #pragma unroll
                     for (int e = 0; e < 32; ++e) o[e] = relu(o[e] + b2r[e]) + oa[e];
@@ -468,11 +476,12 @@ __global__ void __launch_bounds__(kThreads, RC::MINB)
                 } else if (kind == 0) {  // od: K 0-31 of the merge input
                     store_row32<kH>(a_od, o);
                     stack_start(s2, tau, rc, oa, pool);  // highlight stack (once per type: not overlapped)
-                    release<RC>(r, j + 1);
+                    if (SF_TC_EARLY_B2) release<RC>(r, j + 1);
                     store_row32<kH>(a_att, oa);
                 } else {  // oh: K 32-63 of the merge input
                     store_row32<kH>(a2, o);
                 }
+                if (!SF_TC_EARLY_B2) release<RC>(r, j + 1);
                 j += 2;
             }
         }

@@ -35,7 +35,7 @@ def main():
     kernels = {}
     for r in rows[2:]:
         d = dict(zip(head, r))
-        name = d["Kernel Name"].split("(")[0].split("::")[-1].split("<")[0]  # template args dropped
+        name = d["Kernel Name"].split("(")[0].split("<")[0].split("::")[-1]  # template args dropped
         if name in kernels:
             continue
         e = {}

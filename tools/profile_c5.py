@@ -1,5 +1,5 @@
 """One (or a few) C5 frames for ncu captures: pyramid once, then per frame the FP32-march
-transmittance build, scene records and the bf16 query of 921,600 shading points.
+transmittance build, scene records and the fp16 (default) or bf16 query of 921,600 shading points.
 
 usage: python tools/profile_c5.py [--frames 1] [--grid 256] [--queries 921600]
 """
@@ -19,6 +19,7 @@ ap.add_argument("--frames", type=int, default=1)
 ap.add_argument("--grid", type=int, default=256)
 ap.add_argument("--queries", type=int, default=1280 * 720)
 ap.add_argument("--exact", action="store_true")
+ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16"])
 ap.add_argument("--profile-last", action="store_true", help="cudaProfilerStart/Stop around the last frame only")
 a = ap.parse_args()
 N = a.grid
@@ -41,7 +42,7 @@ for f in range(a.frames):  # the bench's per-frame path: relight + query
     light = scenes.rotating_light(f, 32)
     sc.relight(pyr, light, fast=not a.exact)
     rows[:, 6:] = torch.tensor(np.asarray(light) / np.linalg.norm(light), device="cuda")
-    sf.query(sc, net, sf.MediumParams((0.7,), (0.99,) * 3), rows, sf.BF16, F_out=F)
+    sf.query(sc, net, sf.MediumParams((0.7,), (0.99,) * 3), rows, sf.FP16 if a.precision == "fp16" else sf.BF16, F_out=F)
 torch.cuda.synchronize()
 if a.profile_last:
     torch.cuda.profiler.stop()
