@@ -657,7 +657,7 @@ def cpu_baseline_and_parity(sf, w, scene, net, pyr, query, args, precision, dev,
     dy = np.abs(y - y_ref)
     floor = 1e-2 * np.abs(F_ref).max()
     frel = np.abs(F - F_ref) / np.maximum(np.abs(F_ref), floor)
-    ybound = 0.01 if precision == sf.FP16 else 0.03  # DESIGN.md §5 stated tolerances
+    ybound = 0.01 if precision == sf.FP16 else 0.04  # DESIGN.md §5 stated tolerances
     bound = ybound * (np.abs(F_ref) + eta)  # |dy| <= ybound through dF/dy = eta^gamma e^y
     parity = {"rows": n, "vs": "reference (oracle/_ref) F on the same rows, its own FP64 build",
               "path": (f"FP32-sum tap build + {'fp16' if precision == sf.FP16 else 'bf16'} tcgen05 network" if fast

@@ -122,7 +122,7 @@ struct TcPack {
     uint8_t* d_blobs = nullptr;
     TcDesc desc{};
     bool narrow = false;  // RingNarrow / RingTri (every layer <= 48 points) else RingWide
-    bool tri = false;     // RingTri (default for narrow networks; SF_TC_RING=narrow: RingNarrow)
+    bool tri = false;     // RingTri may run it (same layout as RingNarrow; chosen per launch)
 };
 
 struct Ring {
@@ -697,10 +697,7 @@ void tc_prepare(sf_backbone& b, cudaStream_t s, bool f16) {
     SFB_CUDA(cudaStreamSynchronize(s));
     auto pk = std::make_unique<TcPack>();
     pk->narrow = narrow;
-    // RingTri unless SF_TC_RING=narrow (A/B): three 2-slot CTAs per SM measured 13% faster than
-    // two 4-slot ones at C5 (1.71 vs 1.97 ms, bit-identical results)
-    static const bool want_tri = !(std::getenv("SF_TC_RING") && std::string(std::getenv("SF_TC_RING")) == "narrow");
-    pk->tri = narrow && want_tri;
+    pk->tri = narrow;  // RingNarrow and RingTri share the bundle layout: chosen per launch
     std::vector<uint8_t> buf;
     std::vector<Step> steps;
     const int W = 32;
@@ -826,10 +823,23 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
     auto packs = static_cast<const TcPacks*>(b.tc);
     const TcPack* pk = packs ? packs->p[f16 ? 1 : 0].get() : nullptr;
     if (!pk) fail(SF_ERR_INVALID_ARGUMENT, "tc backbone: operands not prepared for this precision");
-    size_t smem = pk->tri ? ring_smem<RingTri>() : pk->narrow ? ring_smem<RingNarrow>() : ring_smem<RingWide>();
+    // RingTri (three chains per SM, each ~1.3x slower under the heavier sharing) or RingNarrow (two)
+    // by whole waves: at C5 (7,200 tiles) RingTri measured 1.71 vs 1.97 ms (bit-identical), while a
+    // 512-tile C2 batch is two waves either way and RingNarrow's faster chains win.
+    // SF_TC_RING=tri|narrow forces one (A/B).
+    const int64_t n_tiles64 = (n + kUmmaM - 1) / kUmmaM;
+    bool tri = false;
+    if (pk->tri) {
+        static const char* force = std::getenv("SF_TC_RING");
+        const int64_t S = sm_count();
+        const double t_tri = 1.3 * double((n_tiles64 + 3 * S - 1) / (3 * S));
+        const double t_nar = double((n_tiles64 + 2 * S - 1) / (2 * S));
+        tri = force ? std::string(force) == "tri" : t_tri < t_nar;
+    }
+    size_t smem = tri ? ring_smem<RingTri>() : pk->narrow ? ring_smem<RingNarrow>() : ring_smem<RingWide>();
     static const bool solo = std::getenv("SF_DEBUG_TC") && std::atoi(std::getenv("SF_DEBUG_TC")) == 2;
     if (solo) smem = 200 * 1024;  // one CTA per SM: uncontended chain latency
-    auto kern = pk->tri      ? (f16 ? k_backbone_tc<true, RingTri> : k_backbone_tc<false, RingTri>)
+    auto kern = tri          ? (f16 ? k_backbone_tc<true, RingTri> : k_backbone_tc<false, RingTri>)
                 : pk->narrow ? (f16 ? k_backbone_tc<true, RingNarrow> : k_backbone_tc<false, RingNarrow>)
                              : (f16 ? k_backbone_tc<true, RingWide> : k_backbone_tc<false, RingWide>);
     // function attributes are per device: remember the size set on each device and variant (a
@@ -840,7 +850,7 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
     SFB_CUDA(cudaGetDevice(&dev));
     {
         std::lock_guard<std::mutex> lk(attr_mu);
-        const int key = 8 * dev + (f16 ? 1 : 0) + (pk->narrow ? 2 : 0) + (pk->tri ? 4 : 0);
+        const int key = 8 * dev + (f16 ? 1 : 0) + (pk->narrow ? 2 : 0) + (tri ? 4 : 0);
         if (attr_set[key] != smem) {
             SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
