@@ -122,6 +122,26 @@ __device__ __forceinline__ float unit_coord(float ax, float ay, float az, float 
     return dot < 0.0f ? fmaf(-t, su, float(A - 1)) : t * su;
 }
 
+#ifndef SF_PLANE_PAIRS
+#define SF_PLANE_PAIRS 1
+#endif
+// k_sample_sort's shared-memory copy of the planes as (aperture) pairs: entry (i, j) of a row
+// of H + 1 float2 = {p[i][j], p[i][j + 1]}, so a bilinear lookup is two 8-byte loads instead of
+// four scalar ones (the odd row stride spreads the rows over the banks). Same values, same
+// arithmetic as plane_lookup.
+__device__ __forceinline__ float plane_lookup_pairs(const float2* pl, int A, int H, float sv, float ua, float half) {
+    const float u = fminf(fmaxf(ua, 0.0f), float(A - 1));
+    int i0 = min(int(u), A - 2);
+    float t = u - float(i0);
+    float v = fminf(fmaxf(half, 0.0f), float(kPi)) * sv;
+    int j0 = min(int(v), H - 2);
+    float s = v - float(j0);
+    const float2 q0 = pl[i0 * (H + 1) + j0], q1 = pl[(i0 + 1) * (H + 1) + j0];
+    float a = fmaf(s, q0.y - q0.x, q0.x);
+    float b = fmaf(s, q1.y - q1.x, q1.x);
+    return fmaf(t, b - a, a);
+}
+
 // PhaseTable::lookup (src/phase.cpp:221-230) on the pre-blended planes.
 __device__ __forceinline__ float cap_phase(const float* planes, const SortDesc& d, float ua, float half) {
     if (d.n_planes == 1) return d.w[0] * plane_lookup(planes, d.A, d.H, d.sv, ua, half);  // one lobe / iso
@@ -194,7 +214,17 @@ static_assert(sizeof(QueryCtx) % 16 == 0, "QueryCtx is moved in 16-byte chunks")
 template <bool kMixed>
 __device__ __forceinline__ float qphase(const float* planes, const SortDesc& d, const QueryCtx& q, float ua,
                                        float half) {
+#if SF_PLANE_PAIRS
+    if (kMixed) return table_phase(d, q.gi, q.gt, ua, half);
+    const float2* pp = reinterpret_cast<const float2*>(planes);
+    if (d.n_planes == 1) return d.w[0] * plane_lookup_pairs(pp, d.A, d.H, d.sv, ua, half);
+    float f = 0.0f;
+    for (int k = 0; k < d.n_planes; ++k)
+        f = fmaf(d.w[k], plane_lookup_pairs(pp + k * d.A * (d.H + 1), d.A, d.H, d.sv, ua, half), f);
+    return f;
+#else
     return kMixed ? table_phase(d, q.gi, q.gt, ua, half) : cap_phase(planes, d, ua, half);
+#endif
 }
 
 __device__ __forceinline__ void box_bounds(const GridDev& g, const int* base, float* box) {
@@ -725,9 +755,18 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
                   const float4* __restrict__ pre, int64_t n, const QueryCtx* __restrict__ recs,
                   const float* __restrict__ feats, uint8_t* __restrict__ ops, float* __restrict__ mms, int* err) {
     extern __shared__ __align__(16) float sm[];
+#if SF_PLANE_PAIRS
+    const int plane_floats = 2 * d.n_planes * d.A * (d.H + 1);  // float2 pairs (plane_lookup_pairs)
+    float* planes = sm;
+    for (int i = threadIdx.x; i < plane_floats / 2; i += blockDim.x) {
+        const bool last = i % (d.H + 1) == d.H;  // the row's last entry has no right neighbour (unused)
+        reinterpret_cast<float2*>(planes)[i] = make_float2(planes_g[i], last ? 0.0f : planes_g[i + 1]);
+    }
+#else
     const int plane_floats = d.n_planes * d.A * (d.H + 1);
     float* planes = sm;
     for (int i = threadIdx.x; i < plane_floats; i += blockDim.x) planes[i] = planes_g[i];
+#endif
     __shared__ int s_scr[kMaxSegs], s_n[kMaxSegs], s_kf[kMaxSegs];
     __shared__ int s_prefix[kMaxSegs];  // bytes per tile before the segment's block (< 2^31)
     __shared__ uint8_t s_task[2 * kMaxSegs];
@@ -1036,7 +1075,8 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
         d.w[0] = 1.0f;  // PhaseModel::hg(g): one lobe of weight 1
     }
     auto smem_for = [&](int w, int nbuf) {
-        return size_t(d.n_planes * d.A * (d.H + 1) + size_t(nbuf) * w * d.scr_floats) * sizeof(float) +
+        return size_t(d.n_planes * d.A * (d.H + 1) * (SF_PLANE_PAIRS ? 2 : 1) + size_t(nbuf) * w * d.scr_floats) *
+                   sizeof(float) +
                2 * size_t(w) * sizeof(QueryCtx) + 16;
     };
     static const size_t static_smem = [] {
