@@ -99,8 +99,8 @@ struct Copy {
 struct Step {
     int32_t ncopy;
     uint32_t total;
-    int32_t k2;  // K of the (second) GEMM operand
-    int32_t pad;
+    int32_t k2;   // K of the (second) GEMM operand
+    int32_t cls;  // k_backbone_rr: 0 big ring (FC-1 bundles), 1 small ring
     Copy c[kMaxCopies];
 };
 
@@ -123,6 +123,8 @@ struct TcPack {
     TcDesc desc{};
     bool narrow = false;  // RingNarrow / RingTri (every layer <= 48 points) else RingWide
     bool tri = false;     // RingTri may run it (same layout as RingNarrow; chosen per launch)
+    bool rr = false;      // k_backbone_rr's program (desc_rr) was built
+    TcDesc desc_rr{};
 };
 
 struct Ring {
@@ -255,8 +257,9 @@ struct RowCtx {
 
 // Channel attention weight of type tau (src/neural.cpp:473-491) from a bundle's payload.
 // Also returns the layer's pools of type tau (mean, max: the fp32 part of its FC-1).
+template <int kMM = kPayMM, int kAtt = kPayAtt>
 __device__ __forceinline__ float attention(const uint8_t* slot, int tau, const RowCtx& rc, float2& pool) {
-    const float4* mm = reinterpret_cast<const float4*>(slot + kPayMM) + threadIdx.x * 2;
+    const float4* mm = reinterpret_cast<const float4*>(slot + kMM) + threadIdx.x * 2;
     const float4 m0 = mm[0], m1 = mm[1];
     const float v[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, rc.g_mean, rc.alpha};
     pool = tau == 0 ? make_float2(m0.x, m0.w) : (tau == 1 ? make_float2(m0.y, m1.x) : make_float2(m0.z, m1.y));
@@ -266,7 +269,7 @@ __device__ __forceinline__ float attention(const uint8_t* slot, int tau, const R
         for (int j = 0; j < 8; ++j) acc += relu(v[j]);
         return 1.0f / (1.0f + __expf(-(acc / 8.0f)));
     }
-    const float* prm = reinterpret_cast<const float*>(slot + kPayAtt);
+    const float* prm = reinterpret_cast<const float*>(slot + kAtt);
     float h[4], w3[3];
     dense_s<4, 8>(prm, prm + 32, v, h);
 #pragma unroll
@@ -277,9 +280,10 @@ __device__ __forceinline__ float attention(const uint8_t* slot, int tau, const R
 }
 
 // First layer of a stack: o = relu(W_init cfg + b) (src/predictor.cpp:206-212), o_att = w o.
+template <int kMM = kPayMM, int kAtt = kPayAtt, int kInit = kPayInit>
 __device__ __forceinline__ void stack_start(const uint8_t* slot, int tau, const RowCtx& rc, float* oa, float2& pool) {
-    const float* ini = reinterpret_cast<const float*>(slot + kPayInit);
-    const float w = attention(slot, tau, rc, pool);
+    const float* ini = reinterpret_cast<const float*>(slot + kInit);
+    const float w = attention<kMM, kAtt>(slot, tau, rc, pool);
 #pragma unroll
     for (int g = 0; g < 4; ++g) {  // 8 outputs at a time: bounds the loads the compiler hoists
         float o[8];
@@ -594,6 +598,446 @@ __global__ void __launch_bounds__(kThreads, RC::MINB)
 #undef PROF
 }
 
+// ---- round-robin backbone: a tile's three feature-type chains interleaved ------------
+//
+// The six stacks of the network (src/predictor.cpp:352-387) are independent until the per-type
+// merges, and a stack is a chain of 2 x 12 small GEMMs whose cost is the tcgen05 round trip
+// (issue -> commit -> mbarrier -> tcgen05.ld, ~800 cycles measured) rather than the MMA work.
+// Here one CTA runs the three chains tau = 0, 1, 2 of its tile round robin — chain tau is the
+// diffuse stack of type tau followed by the highlight stack of type tau — so while one chain's
+// MMA is in flight the consumer warps do the other two chains' epilogues; every GEMM is the
+// same operation on the same operands as in k_backbone_tc (bit-identical results). The
+// diffuse output of a chain waits in TMEM (fp32) for its merge. Two CTAs per SM (two tiles,
+// six chains), ~106 KB of shared memory each:
+//   A[3]    the chains' [128 x 32] 16-bit operands (o_att, then u, then the next o_att)
+//   big[3]  FC-1 bundles: W1[:, :32], W1[:, 32:], the tile's sorted-feature block, b1 + W1's
+//           mean / max columns (the three chains' FC-1 of one layer in flight together)
+//   small[3] FC-2 bundles (W2, b2 + the payload of the chain's next FC-1: the layer's mean/max
+//           block, attention parameters, conditioning layer), then merge / cross / head bundles
+// TMEM (256 columns): [32 tau, +32) chain accumulators, [96 + 32 tau, +32) the chains' fp32
+// residuals o_att, [192 + 16 tau, +16) diffuse outputs as 16-bit pairs (the merge operand, rounded
+// as k_backbone_tc rounds it); the cross accumulator [192, 256) once those are read.
+namespace rr {
+constexpr int NSB = 3, NSS = 3;
+constexpr int SBB = 17792, OF = 5120, OB = 17408, KF = 48;  // big slot (FC-1)
+constexpr int SBS = 9344;                                   // small slot
+constexpr int PMM = 2304, PATT = 6400, PINIT = 6656;        // FC-2 payload offsets
+constexpr int kA = kUmmaM * 32 * 2;
+constexpr size_t kSmem = 128 + 3 * kA + size_t(NSB) * SBB + size_t(NSS) * SBS;
+constexpr int kCols = 256, kColRes = 96, kColOd = 192, kColX = 192;
+constexpr int kThreadsRR = kConsumers + 64;  // + producer warp + MMA-issuer warp
+static_assert(kSlotW1b + 32 * KF * 2 <= OF && OF + kUmmaM * KF * 2 <= OB && OB + 384 <= SBB, "rr big slot");
+static_assert(kSlotB2 + 128 <= PMM && PMM + kUmmaM * 32 <= PATT && PATT + 256 <= PINIT && PINIT + 1024 <= SBS &&
+                  kSlotHead2 + 784 <= SBS && SBS % 128 == 0 && SBB % 128 == 0 && kA % 128 == 0,
+              "rr small slot");
+}  // namespace rr
+
+// One step's copies into `dst` (a ring slot), completing on `bar`.
+__device__ __forceinline__ void issue_bundle(uint8_t* dst, uint64_t* bar, const StepRegs& sr, const uint8_t* wpk,
+                                             const uint8_t* ops, const uint8_t* mms, int tile, int n_tiles) {
+    mbar_expect_tx(bar, uint32_t(sr.w[0].y));
+#pragma unroll
+    for (int c = 0; c < kMaxCopies; ++c) {
+        if (c >= sr.w[0].x) break;
+        const int4 c0 = sr.w[1 + 2 * c], c1 = sr.w[2 + 2 * c];
+        const int kind = c0.x;
+        const uint32_t off = uint32_t(c0.y), bytes = uint32_t(c0.z);
+        const int64_t a = (int64_t(uint32_t(c1.y)) << 32) | uint32_t(c1.x);
+        const int64_t stride = (int64_t(uint32_t(c1.w)) << 32) | uint32_t(c1.z);
+        const uint8_t* src;
+        if (kind == 0)
+            src = wpk + a;
+        else if (kind == 1)
+            src = ops + a * n_tiles + int64_t(tile) * stride;
+        else
+            src = mms + a * int64_t(n_tiles) * 4096 + int64_t(tile) * 4096;
+        bulk_g2s(dst + off, src, bytes, bar);
+    }
+}
+
+template <bool kH>
+__global__ void __launch_bounds__(rr::kThreadsRR, 2)
+    k_backbone_rr(const TcDesc d, const uint8_t* __restrict__ wpk, const uint8_t* __restrict__ ops,
+                  const uint8_t* __restrict__ mms, int n_tiles, int64_t n, const double* __restrict__ cfg8,
+                  float* __restrict__ y_out, double* __restrict__ F_out, const int* __restrict__ perm,
+                  int f_stage) {
+    using namespace rr;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // full / empty of the big and small rings; per chain: MMA done (commit), operand ready
+    // (one arrival per consumer warp, awaited by the MMA warp)
+    __shared__ uint64_t bars[2 * NSB + 2 * NSS + 6];
+    __shared__ uint32_t tmem_slot;
+    __shared__ int s_kf[2][16];
+    uint64_t* full_b = bars;
+    uint64_t* empty_b = bars + NSB;
+    uint64_t* full_s = bars + 2 * NSB;
+    uint64_t* empty_s = bars + 2 * NSB + NSS;
+    uint64_t* mbar = bars + 2 * NSB + 2 * NSS;
+    uint64_t* ready = mbar + 3;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int tile = blockIdx.x;
+    const bool prof = d.prof && blockIdx.x == 0 && tid == 0;
+    long long t_last = clock64();
+    const long long t_start = t_last;
+#define RPROF(k)                                                            \
+    if (prof) {                                                             \
+        long long t_now = clock64();                                        \
+        atomicAdd(&g_tc_prof[k], (unsigned long long)(t_now - t_last));     \
+        t_last = t_now;                                                     \
+    }
+    uint8_t* abuf = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    uint8_t* big = abuf + 3 * kA;
+    uint8_t* small = big + NSB * SBB;
+    uint8_t* D[3] = {big, big + SBB, big + 2 * SBB};  // merge staging in the idle big slots (tail)
+    auto A = [&](int t) { return abuf + t * kA; };
+
+    if (warp == 0) tmem_alloc(&tmem_slot, kCols);
+    if (tid == 0) {
+        for (int s = 0; s < 2 * NSB + 2 * NSS + 6; ++s) {
+            const bool per_warp = (s >= NSB && s < 2 * NSB) || (s >= 2 * NSB + NSS && s < 2 * NSB + 2 * NSS) ||
+                                  s >= 2 * NSB + 2 * NSS + 3;
+            mbar_init(&bars[s], per_warp ? kConsumers / 32 : 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < 32) s_kf[tid >> 4][tid & 15] = (d.counts[tid >> 4][tid & 15] + 15) / 16 * 16;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    const int nl0 = d.nl[0], L = d.nl[0] + d.nl[1];
+
+    if (warp == kConsumers / 32) {  // producer: both rings, in program order
+        if ((tid & 31) == 0) {
+            StepRegs cur, nxt;
+            load_step(d, 0, cur);
+            int cnt[2] = {0, 0};
+            for (int j = 0; j < d.n_steps; ++j) {
+                if (j + 1 < d.n_steps) load_step(d, j + 1, nxt);
+                const int cls = cur.w[0].w;  // 0 big (FC-1), 1 small
+                const int c = cnt[cls]++;
+                const int slot = c % 3;
+                if (c >= 3) SF_WAIT(&(cls ? empty_s : empty_b)[slot], uint32_t(c / 3 - 1) & 1u, 2, j);
+                issue_bundle(cls ? small + slot * SBS : big + slot * SBB, &(cls ? full_s : full_b)[slot], cur, wpk,
+                             ops, mms, tile, n_tiles);
+                cur = nxt;
+            }
+        }
+        return;
+    }
+    if (warp == kConsumers / 32 + 1) {  // MMA issuer: every GEMM of the tile, in consumer order
+        if ((tid & 31) == 0) {
+            uint32_t rpar = 0;
+            auto wready = [&](int t) {
+                SF_WAIT(&ready[t], (rpar >> t) & 1u, 5, t);
+                rpar ^= 1u << t;
+                tc_fence_after();
+            };
+            int nb = 0, nsm = 3;  // bundles taken (the chain-start payloads are the consumers')
+            auto fc1 = [&](int t, int kind, int i) {
+                wready(t);
+                SF_WAIT(&full_b[t], uint32_t(nb / 3) & 1u, 6, nb);
+                ++nb;
+                const uint32_t b1s = smem_u32(big + t * SBB);
+                issue_gemm<kH>(tmem + 32 * t, 32, smem_u32(A(t)), 32, b1s + kSlotW1a, false);
+                issue_gemm<kH>(tmem + 32 * t, 32, b1s + OF, s_kf[kind][i], b1s + kSlotW1b, true);
+                umma_commit(&mbar[t]);
+            };
+            auto small_wait = [&](int t) {
+                SF_WAIT(&full_s[t], uint32_t(nsm / 3) & 1u, 7, nsm);
+                ++nsm;
+            };
+            for (int t = 0; t < 3; ++t) fc1(t, 0, 0);
+            for (int l = 0; l < L; ++l) {
+                for (int t = 0; t < 3; ++t) {
+                    wready(t);
+                    small_wait(t);
+                    issue_gemm<kH>(tmem + 32 * t, 32, smem_u32(A(t)), 32, smem_u32(small + t * SBS), false);
+                    umma_commit(&mbar[t]);
+                }
+                if (l + 1 < L)
+                    for (int t = 0; t < 3; ++t) fc1(t, l + 1 < nl0 ? 0 : 1, l + 1 < nl0 ? l + 1 : l + 1 - nl0);
+            }
+            // merges (ready[0] = the consumers staged od and oh of every chain)
+            wready(0);
+            for (int t = 0; t < 3; ++t) small_wait(t);
+            for (int t = 0; t < 3; ++t) {
+                const uint32_t sm = smem_u32(small + t * SBS);
+                issue_gemm<kH>(tmem + 64 * t, 64, smem_u32(D[t]), 32, sm, false);
+                issue_gemm<kH>(tmem + 64 * t, 64, smem_u32(A(t)), 32, sm + kSlotWmHi, true);
+            }
+            umma_commit(&mbar[0]);
+            // cross
+            wready(0);
+            for (int t = 0; t < 3; ++t) small_wait(t);
+            for (int t = 0; t < 3; ++t) {
+                const uint32_t sc = smem_u32(small + t * SBS);
+                issue_gemm<kH>(tmem + kColX, 64, smem_u32(D[t]), 32, sc, t > 0);
+                issue_gemm<kH>(tmem + kColX, 64, smem_u32(A(t)), 32, sc + kSlotWmHi, true);
+            }
+            umma_commit(&mbar[0]);
+            // heads
+            for (int hl = 0; hl < 2; ++hl) {
+                wready(0);
+                const int sh = nsm % 3;
+                small_wait(sh);
+                const uint32_t shp = smem_u32(small + sh * SBS);
+                issue_gemm<kH>(tmem, 64, smem_u32(D[0]), 32, shp, false);
+                issue_gemm<kH>(tmem, 64, smem_u32(A(0)), 32, shp + kSlotWmHi, true);
+                umma_commit(&mbar[0]);
+            }
+        }
+        return;
+    }
+
+    // ---- consumer warps: thread = query row = TMEM lane
+    const int64_t q = int64_t(tile) * kUmmaM + tid;
+    const bool live = q < n;
+    const uint32_t lane = uint32_t(warp * 32) << 16;
+
+    RowCtx rc;
+    for (int i = 0; i < 7; ++i) rc.cfgv[i] = 0.0f;
+    rc.g_mean = 0.0f;
+    rc.alpha = 0.0f;
+    rc.literal = d.literal;
+    if (live) {
+        const double* c8 = cfg8 + 8 * q;
+        int ng = int(c8[0]);
+        for (int i = 0; i < ng; ++i) rc.g_mean += float(c8[1 + i]);
+        if (ng > 0) rc.g_mean /= float(double(ng));
+        rc.alpha = float(c8[7]);
+        for (int i = 0; i < ng && i < 3; ++i) rc.cfgv[i] = float(c8[1 + i]);
+        for (int i = 0; i < 4; ++i) rc.cfgv[3 + i] = float(c8[4 + i]);
+    }
+
+    int nb = 0, nsm = 0;  // bundles taken from each ring (program order); chain t always uses slot t
+    auto acq_big = [&]() {
+        RPROF(6);
+        SF_WAIT(&full_b[nb % NSB], uint32_t(nb / NSB) & 1u, 1, nb);
+        RPROF(1);
+        ++nb;
+    };
+    auto acq_small = [&]() {
+        RPROF(6);
+        SF_WAIT(&full_s[nsm % NSS], uint32_t(nsm / NSS) & 1u, 4, nsm);
+        RPROF(2);
+        ++nsm;
+    };
+    auto rel = [&](uint64_t* bar) {
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(bar);
+    };
+    // operands written by this warp -> visible to the tensor core; one arrival per warp
+    auto signal = [&](int t) {
+        fence_proxy_async();
+        tc_fence_before();
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&ready[t]);
+        RPROF(3);
+    };
+    uint32_t mpar = 0;
+    auto wait_mma = [&](int t) {
+        RPROF(7);
+        SF_WAIT(&mbar[t], (mpar >> t) & 1u, 3, t);
+        RPROF(0);
+        mpar ^= 1u << t;
+        tc_fence_after();
+    };
+
+    // each chain's current layer (mean, max) of its type, kept in registers; the chain loops stay
+    // rolled (one copy of the code: the unrolled kernel missed in the instruction cache)
+    float2 pool0 = make_float2(0.0f, 0.0f), pool1 = pool0, pool2 = pool0;
+    auto get_pool = [&](int t) { return t == 0 ? pool0 : (t == 1 ? pool1 : pool2); };
+    auto set_pool = [&](int t, float2 v) {
+        if (t == 0)
+            pool0 = v;
+        else if (t == 1)
+            pool1 = v;
+        else
+            pool2 = v;
+    };
+
+    // chain starts: the first diffuse layer's conditioning + attention (one payload bundle each)
+#pragma unroll 1
+    for (int t = 0; t < 3; ++t) {
+        acq_small();
+        float oa[32];
+        float2 pl;
+        stack_start<PMM, PATT, PINIT>(small + t * SBS, t, rc, oa, pl);
+        set_pool(t, pl);
+        rel(&empty_s[t]);
+        tmem_st32(tmem + lane + kColRes + 32 * t, oa);
+        store_row32<kH>(A(t), oa);
+        signal(t);
+    }
+    for (int l = 0; l < L; ++l) {
+        // FC-1 epilogues: u = relu(acc + b1 + mean W1[:, mean] + max W1[:, max])
+#pragma unroll 1
+        for (int t = 0; t < 3; ++t) {
+            acq_big();
+            wait_mma(t);
+            const float* b1 = reinterpret_cast<const float*>(big + t * SBB + OB);
+            const float2 pl = get_pool(t);
+            float acc[32];
+            tmem_ld32(tmem + lane + 32 * t, acc);
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+                acc[e] = relu(acc[e] + fmaf(pl.x, b1[32 + e], fmaf(pl.y, b1[64 + e], b1[e])));
+            rel(&empty_b[t]);
+            store_row32<kH>(A(t), acc);
+            RPROF(4);
+            signal(t);
+        }
+        // FC-2 epilogues: o = relu(acc + b2) + o_att -> the next layer's o_att
+        const bool last = l == L - 1, sw = l + 1 == nl0;
+#pragma unroll 1
+        for (int t = 0; t < 3; ++t) {
+            acq_small();
+            wait_mma(t);
+            const uint8_t* s2 = small + t * SBS;
+            float o[32];
+            {
+                float res[32];
+                tmem_ld32(tmem + lane + 32 * t, o);
+                tmem_ld32(tmem + lane + kColRes + 32 * t, res);
+                const float4* b2 = reinterpret_cast<const float4*>(s2 + kSlotB2);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float4 v = b2[e];
+                    o[4 * e] = relu(o[4 * e] + v.x) + res[4 * e];
+                    o[4 * e + 1] = relu(o[4 * e + 1] + v.y) + res[4 * e + 1];
+                    o[4 * e + 2] = relu(o[4 * e + 2] + v.z) + res[4 * e + 2];
+                    o[4 * e + 3] = relu(o[4 * e + 3] + v.w) + res[4 * e + 3];
+                }
+            }
+            if (last) {  // the highlight output: K 32-63 of the merge input
+                rel(&empty_s[t]);
+                store_row32<kH>(A(t), o);
+                continue;
+            }
+            float2 pn;
+            if (sw) {  // diffuse output (16-bit, as the merge reads it) parked in TMEM; highlight stack starts
+                uint32_t pk16[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) pk16[e] = pack16<kH>(o[2 * e], o[2 * e + 1]);
+                tmem_st16(tmem + lane + kColOd + 16 * t, pk16);
+                stack_start<PMM, PATT, PINIT>(s2, t, rc, o, pn);
+            } else {
+                const float w = attention<PMM, PATT>(s2, t, rc, pn);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) o[e] = o[e] * w;
+            }
+            set_pool(t, pn);
+            rel(&empty_s[t]);
+            tmem_st32(tmem + lane + kColRes + 32 * t, o);  // the next layer's o_att
+            store_row32<kH>(A(t), o);
+            RPROF(5);
+            signal(t);
+        }
+    }
+    RPROF(9);
+
+    // merges: merged_tau = relu(W_m [od; oh] + b), od (TMEM, 16-bit) staged in the idle big slots
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        uint32_t od[16];
+        tmem_ld16(tmem + lane + kColOd + 16 * t, od);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<uint4*>(D[t] + canon_off(tid, 8 * c, 32)) =
+                make_uint4(od[4 * c], od[4 * c + 1], od[4 * c + 2], od[4 * c + 3]);
+    }
+    signal(0);
+    for (int t = 0; t < 3; ++t) acq_small();
+    wait_mma(0);
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        const float* bm = reinterpret_cast<const float*>(small + t * SBS + kSlotBias);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            float acc[32];
+            tmem_ld32(tmem + lane + 64 * t + 32 * half, acc);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) acc[e] = relu(acc[e] + bm[32 * half + e]);
+            store_row32<kH>(half ? A(t) : D[t], acc);
+        }
+        rel(&empty_s[t]);
+    }
+    signal(0);
+    // cross = sum_tau W_c[:, 64 tau : 64 tau + 64] merged_tau (one accumulator)
+    for (int t = 0; t < 3; ++t) acq_small();
+    wait_mma(0);
+    {
+        const float* bc = reinterpret_cast<const float*>(small + 2 * SBS + kSlotBias);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            float h[32];
+            tmem_ld32(tmem + lane + kColX + 32 * half, h);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) h[e] = relu(h[e] + bc[32 * half + e]);
+            store_row32<kH>(half ? A(0) : D[0], h);
+        }
+    }
+    for (int t = 0; t < 3; ++t) rel(&empty_s[t]);
+    signal(0);
+    // head 0 / 1 (64 -> 64, relu); head 2 (64 -> 3) SIMT from the head-1 bundle
+    for (int hl = 0; hl < 2; ++hl) {
+        const int sh = nsm % NSS;
+        acq_small();
+        const uint8_t* shp = small + sh * SBS;
+        wait_mma(0);
+        const float* bh = reinterpret_cast<const float*>(shp + kSlotBias);
+        float h[64];
+        tmem_ld32(tmem + lane, h);
+        tmem_ld32(tmem + lane + 32, h + 32);
+#pragma unroll
+        for (int e = 0; e < 64; ++e) h[e] = relu(h[e] + bh[e]);
+        if (hl == 0) {
+            store_row32<kH>(D[0], h);
+            store_row32<kH>(A(0), h + 32);
+            rel(&empty_s[sh]);
+            signal(0);
+            continue;
+        }
+        const float* h2 = reinterpret_cast<const float*>(shp + kSlotHead2);
+        float y[3];
+        dense_s<3, 64>(h2, h2 + 192, h, y);
+        double* fs = reinterpret_cast<double*>(D[1]);  // F staging (see k_backbone_tc)
+        if (live) {
+            for (int c = 0; c < 3; ++c) {
+                const float yc = fabsf(y[c]);
+                const int64_t oq = perm ? int64_t(perm[q]) : q;
+                if (y_out) y_out[3 * oq + c] = yc;
+                if (F_out) {
+                    const double f = pow(cfg8[8 * q + 4 + c], d.gamma) * expm1(double(yc));  // decode_prediction
+                    if (f_stage)
+                        fs[3 * tid + c] = f;
+                    else
+                        F_out[3 * oq + c] = f;
+                }
+            }
+        }
+        if (f_stage && F_out) {
+            consumer_bar_sync();
+            const int64_t rem = n - int64_t(tile) * kUmmaM, rows = rem < kUmmaM ? rem : kUmmaM;
+            const int chunks = int(rows * 3 / 2);
+            double* dst = F_out + int64_t(tile) * kUmmaM * 3;
+            for (int k = tid; k < chunks; k += kConsumers)
+                reinterpret_cast<double2*>(dst)[k] = reinterpret_cast<const double2*>(fs)[k];
+            if ((rows & 1) && tid == 0) dst[rows * 3 - 1] = fs[rows * 3 - 1];
+        }
+        rel(&empty_s[sh]);
+    }
+    RPROF(10);
+    tc_fence_before();
+    consumer_bar_sync();
+    if (warp == 0) tmem_dealloc(tmem, kCols);
+    if (prof) atomicAdd(&g_tc_prof[8], (unsigned long long)(clock64() - t_start));
+#undef RPROF
+}
+
 // ---- host-side packing ------------------------------------------------------------
 
 // B operand of one GEMM: rows = N outputs, cols [col0, col0+cols) of W (leading dim ld), zero padded to Kp.
@@ -790,6 +1234,107 @@ void tc_prepare(sf_backbone& b, cudaStream_t s, bool f16) {
         st.total = 0;
         for (int k = 0; k < st.ncopy; ++k) st.total += st.c[k].bytes;
     }
+    // k_backbone_rr's program: the three chains' steps interleaved in the order the consumers
+    // take them (chain starts; per layer three FC-1 (big ring) then three FC-2 (small ring, each
+    // carrying the payload of its chain's next FC-1); merges, cross chunks, heads).
+    std::vector<Step> rsteps;
+    const int Lr = S.nl[0] + S.nl[1];
+    pk->rr = narrow && S.nl[0] >= 1 && S.nl[1] >= 1 && 3 + 6 * Lr + 8 <= kMaxSteps;
+    if (pk->rr) {
+        int64_t att_o[2][3][16], w1_o[2][3][16], w2_o[2][3][16];
+        for (int kind = 0; kind < 2; ++kind)
+            for (int tau = 0; tau < 3; ++tau) {
+                int64_t off = L.stack_off[kind][tau] + W * 7 + W;
+                for (int i = 0; i < S.nl[kind]; ++i) {
+                    att_o[kind][tau][i] = off;
+                    if (!c.literal_attention) off += 51;
+                    w1_o[kind][tau][i] = off;
+                    off += int64_t(W) * (W + S.counts[kind][i] + 2) + W;
+                    w2_o[kind][tau][i] = off;
+                    off += W * W + W;
+                }
+            }
+        auto payload = [&](Step& st, int kind, int tau, int i) {
+            st.c[st.ncopy++] = Copy{2, uint32_t(rr::PMM), uint32_t(kUmmaM * 8 * 4), 0, S.mm_layer[kind][i], 4096};
+            std::vector<float> att(52, 0.0f);
+            if (!c.literal_attention)
+                for (int k = 0; k < 51; ++k) att[size_t(k)] = P[size_t(att_o[kind][tau][i] + k)];
+            st.c[st.ncopy++] = pcopy(pack_f32(buf, att), f32_bytes(att.size()), rr::PATT);
+            if (i == 0) {
+                std::vector<float> ini = slice(P, L.stack_off[kind][tau], size_t(W * 7 + W));
+                st.c[st.ncopy++] = pcopy(pack_f32(buf, ini), f32_bytes(ini.size()), rr::PINIT);
+            }
+        };
+        for (int tau = 0; tau < 3; ++tau) {
+            Step st{};
+            st.cls = 1;
+            payload(st, 0, tau, 0);
+            rsteps.push_back(st);
+        }
+        for (int l = 0; l < Lr; ++l) {
+            const int kind = l < S.nl[0] ? 0 : 1, i = kind ? l - S.nl[0] : l;
+            const int cnt = S.counts[kind][i], K = W + cnt + 2, kf = S.kf[kind][i];
+            for (int tau = 0; tau < 3; ++tau) {
+                const int64_t off = w1_o[kind][tau][i];
+                Step st{};
+                st.cls = 0;
+                st.k2 = kf;
+                st.c[0] = pcopy(pack_blob_(buf, P.data() + off, W, W, K, 0, W), W * W * 2, kSlotW1a);
+                st.c[1] = pcopy(pack_blob_(buf, P.data() + off, W, cnt, K, W, kf), uint32_t(W * kf * 2), kSlotW1b);
+                st.c[2] = Copy{1, uint32_t(rr::OF), uint32_t(kUmmaM * kf * 2), 0, S.seg_prefix[kind][i][tau],
+                               int64_t(kUmmaM) * kf * 2};
+                std::vector<float> bmx = slice(P, off + int64_t(W) * K, W);
+                for (int r = 0; r < W; ++r) bmx.push_back(P[size_t(off + int64_t(r) * K + W + cnt)]);
+                for (int r = 0; r < W; ++r) bmx.push_back(P[size_t(off + int64_t(r) * K + W + cnt + 1)]);
+                st.c[3] = pcopy(pack_f32(buf, bmx), f32_bytes(bmx.size()), rr::OB);
+                st.ncopy = 4;
+                rsteps.push_back(st);
+            }
+            for (int tau = 0; tau < 3; ++tau) {
+                const int64_t off = w2_o[kind][tau][i];
+                Step st{};
+                st.cls = 1;
+                st.k2 = W;
+                st.c[0] = pcopy(pack_blob_(buf, P.data() + off, W, W, W, 0, W), W * W * 2, 0);
+                st.c[1] = pcopy(pack_f32(buf, slice(P, off + W * W, W)), f32_bytes(W), kSlotB2);
+                st.ncopy = 2;
+                if (l + 1 < Lr) {
+                    const int kn = l + 1 < S.nl[0] ? 0 : 1, inx = kn ? l + 1 - S.nl[0] : l + 1;
+                    payload(st, kn, tau, inx);
+                }
+                rsteps.push_back(st);
+            }
+        }
+        // 64-wide bundles: W[:, 0:32] at 0, W[:, 32:64] at kSlotWmHi, bias at kSlotBias
+        auto wide = [&](int64_t w_off, int ld, int col0, int64_t b_off) {
+            Step st{};
+            st.cls = 1;
+            st.k2 = 64;
+            st.c[0] = pcopy(pack_blob_(buf, P.data() + w_off, 64, 32, ld, col0, 32), 4096, 0);
+            st.c[1] = pcopy(pack_blob_(buf, P.data() + w_off, 64, 32, ld, col0 + 32, 32), 4096, kSlotWmHi);
+            st.ncopy = 2;
+            if (b_off >= 0) st.c[st.ncopy++] = pcopy(pack_f32(buf, slice(P, b_off, 64)), f32_bytes(64), kSlotBias);
+            return st;
+        };
+        for (int tau = 0; tau < 3; ++tau) {
+            const int64_t mo = L.merge_off + int64_t(tau) * (64 * 64 + 64);
+            rsteps.push_back(wide(mo, 64, 0, mo + 64 * 64));
+        }
+        for (int tau = 0; tau < 3; ++tau)
+            rsteps.push_back(wide(L.cross_off, 192, 64 * tau, tau == 2 ? L.cross_off + 64 * 192 : -1));
+        for (int l = 0; l < 2; ++l) {
+            Step st = wide(L.head_off[l], 64, 0, L.head_off[l] + 64 * 64);
+            if (l == 1) {
+                std::vector<float> h2 = slice(P, L.head_off[2], 3 * 64 + 3);
+                st.c[st.ncopy++] = pcopy(pack_f32(buf, h2), f32_bytes(h2.size()), kSlotHead2);
+            }
+            rsteps.push_back(st);
+        }
+        for (Step& st : rsteps) {
+            st.total = 0;
+            for (int k = 0; k < st.ncopy; ++k) st.total += st.c[k].bytes;
+        }
+    }
     TcDesc& d = pk->desc;
     d.nl[0] = S.nl[0];
     d.nl[1] = S.nl[1];
@@ -800,11 +1345,16 @@ void tc_prepare(sf_backbone& b, cudaStream_t s, bool f16) {
     d.n_steps = int(steps.size());
     d.prof = std::getenv("SF_DEBUG_TC") != nullptr;
     const size_t blob_bytes = (buf.size() + 255) & ~size_t(255);
-    buf.resize(blob_bytes + steps.size() * sizeof(Step));
+    buf.resize(blob_bytes + (steps.size() + rsteps.size()) * sizeof(Step));
     std::memcpy(buf.data() + blob_bytes, steps.data(), steps.size() * sizeof(Step));
+    if (!rsteps.empty())
+        std::memcpy(buf.data() + blob_bytes + steps.size() * sizeof(Step), rsteps.data(), rsteps.size() * sizeof(Step));
     SFB_CUDA(cudaMalloc(&pk->d_blobs, buf.size()));
     SFB_CUDA(cudaMemcpy(pk->d_blobs, buf.data(), buf.size(), cudaMemcpyHostToDevice));
     d.steps = reinterpret_cast<const Step*>(pk->d_blobs + blob_bytes);
+    pk->desc_rr = d;
+    pk->desc_rr.n_steps = int(rsteps.size());
+    pk->desc_rr.steps = d.steps + steps.size();
     packs->p[f16 ? 1 : 0] = std::move(pk);
 }
 
@@ -828,6 +1378,34 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
     // 512-tile C2 batch is two waves either way and RingNarrow's faster chains win.
     // SF_TC_RING=tri|narrow forces one (A/B).
     const int64_t n_tiles64 = (n + kUmmaM - 1) / kUmmaM;
+    // k_backbone_rr (the three chains of a tile interleaved, two CTAs per SM) with SF_TC_RR=1:
+    // bit-identical, measured slower at C5 (2.04 vs 1.86 ms: its consumer warps are latency-bound
+    // and two CTAs per SM give 8 of them where the one-chain kernel's three give 12)
+    static const char* rr_env = std::getenv("SF_TC_RR");
+    if (pk->rr && rr_env && rr_env[0] == '1') {
+        auto kern = f16 ? k_backbone_rr<true> : k_backbone_rr<false>;
+        static std::mutex rr_mu;
+        static std::unordered_map<int, bool> rr_set;
+        int dev = 0;
+        SFB_CUDA(cudaGetDevice(&dev));
+        {
+            std::lock_guard<std::mutex> lk(rr_mu);
+            const int key = 2 * dev + (f16 ? 1 : 0);
+            if (!rr_set[key]) {
+                SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rr::kSmem)));
+                SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                              int(cudaSharedmemCarveoutMaxShared)));
+                rr_set[key] = true;
+            }
+        }
+        const int n_tiles = int(n_tiles64);
+        const int f_stage = F && !perm && (reinterpret_cast<uintptr_t>(F) & 15) == 0 ? 1 : 0;
+        kern<<<n_tiles, rr::kThreadsRR, rr::kSmem, s>>>(pk->desc_rr, pk->d_blobs, ops, reinterpret_cast<const uint8_t*>(mms),
+                                                 n_tiles, n, cfg8, y, F, perm, f_stage);
+        SFB_CUDA(cudaGetLastError());
+        count_launch();
+        return;
+    }
     bool tri = false;
     if (pk->tri) {
         static const char* force = std::getenv("SF_TC_RING");
