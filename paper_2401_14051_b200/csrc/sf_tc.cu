@@ -112,7 +112,7 @@ struct TcDesc {
     int literal;
     double gamma;
     int n_steps;
-    int prof;  // SF_DEBUG_TC: CTA 0 / thread 0 accumulates clock64 per phase into g_tc_prof
+    int prof;  // SF_DEBUG_TC (builds with -DSF_TC_PROFILE): CTA 0 / thread 0 accumulates clock64 per phase
     const Step* steps;  // step program in global memory (read through the L1 by the issuing thread)
 };
 
@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, RC::MINB)
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int tile = blockIdx.x;
+#ifdef SF_TC_PROFILE
     const bool prof = d.prof && blockIdx.x == 0 && tid == 0;
     long long t_last = clock64();
     const long long t_start = t_last;
@@ -327,6 +328,9 @@ __global__ void __launch_bounds__(kThreads, RC::MINB)
         atomicAdd(&g_tc_prof[k], (unsigned long long)(t_now - t_last));     \
         t_last = t_now;                                                     \
     }
+#else
+#define PROF(k)
+#endif
 
     // 1024-byte aligned in the shared window; derived from smem_raw by pointer arithmetic so the
     // compiler keeps the shared address space (LDS/STS, not generic LD/ST, for every ring read)
@@ -594,7 +598,9 @@ __global__ void __launch_bounds__(kThreads, RC::MINB)
     tc_fence_before();
     consumer_bar_sync();
     if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+#ifdef SF_TC_PROFILE
     if (prof) atomicAdd(&g_tc_prof[8], (unsigned long long)(clock64() - t_start));
+#endif
 #undef PROF
 }
 
@@ -678,6 +684,7 @@ __global__ void __launch_bounds__(rr::kThreadsRR, 2)
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int tile = blockIdx.x;
+#ifdef SF_TC_PROFILE
     const bool prof = d.prof && blockIdx.x == 0 && tid == 0;
     long long t_last = clock64();
     const long long t_start = t_last;
@@ -687,6 +694,9 @@ __global__ void __launch_bounds__(rr::kThreadsRR, 2)
         atomicAdd(&g_tc_prof[k], (unsigned long long)(t_now - t_last));     \
         t_last = t_now;                                                     \
     }
+#else
+#define RPROF(k)
+#endif
     uint8_t* abuf = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     uint8_t* big = abuf + 3 * kA;
     uint8_t* small = big + NSB * SBB;
@@ -1034,7 +1044,9 @@ __global__ void __launch_bounds__(rr::kThreadsRR, 2)
     tc_fence_before();
     consumer_bar_sync();
     if (warp == 0) tmem_dealloc(tmem, kCols);
+#ifdef SF_TC_PROFILE
     if (prof) atomicAdd(&g_tc_prof[8], (unsigned long long)(clock64() - t_start));
+#endif
 #undef RPROF
 }
 

@@ -1,4 +1,5 @@
-"""Per-phase cycle breakdown of tensor-core backbone CTA 0 (SF_DEBUG_TC=1)."""
+"""Per-phase cycle breakdown of tensor-core backbone CTA 0 (SF_DEBUG_TC=1; needs a library built with
+SF_NVCC_EXTRA=-DSF_TC_PROFILE, e.g. tools/build_variant.py variants/prof.so -DSF_TC_PROFILE + SF_B200_LIB)."""
 import ctypes, os, sys
 os.environ["SF_DEBUG_TC"] = sys.argv[1] if len(sys.argv) > 1 else "1"
 sys.path.insert(0, os.getcwd())

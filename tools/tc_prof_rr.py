@@ -1,6 +1,6 @@
 """Per-phase cycle breakdown of k_backbone_rr, CTA 0 / thread 0 (SF_DEBUG_TC=1), on the C5 frame query
 (tools/ab_c5.py's workload). Phases: wait_mma, wait_big, wait_small, barrier+issue, FC-1 epilogue,
-FC-2 epilogue (+attention), misc, tail."""
+FC-2 epilogue (+attention), misc, tail. Needs a -DSF_TC_PROFILE build (see tools/tc_prof.py)."""
 import ctypes, os, sys
 os.environ.setdefault("SF_DEBUG_TC", "1")
 sys.path.insert(0, os.getcwd())
