@@ -65,7 +65,7 @@ struct SortDesc {
     uint8_t chunk_seg[kMaxChunks];
     uint8_t chunk_j[kMaxChunks];
     uint8_t task_seg[2 * kMaxSegs];  // sort tasks by network size; bit 7 = upper half of a 64-wide pair
-    int debug;                       // SF_DEBUG_SAMPLE_SORT: 1 skip sampling, 2 skip sort, 4 skip stores
+    int debug;  // SF_DEBUG_SAMPLE_SORT (-DSF_SAMPLE_SORT_DEBUG builds): 1 skip sampling, 2 skip sort, 4 skip stores
     int mixed;                       // per-query g (C4): phase from the full table at the query's g
     int G;                           // table g resolution
     const float* table;              // [G][A][H] (mixed only)
@@ -210,14 +210,17 @@ struct __align__(16) QueryCtx {  // 240 bytes: copied as 16-byte chunks
 static_assert(sizeof(QueryCtx) % 16 == 0, "QueryCtx is moved in 16-byte chunks");
 
 // Phase feature factor at the query's medium: the scene's pre-blended planes, or the full
-// table at the query's own g (mixed media).
-template <bool kMixed>
+// table at the query's own g (mixed media). kPh: kPhPlanes (any number of lobes), kPhMixed (per-query
+// g, full table), kPhOne (one pre-blended plane: no per-lookup lobe loop).
+constexpr int kPhPlanes = 0, kPhMixed = 1, kPhOne = 2;
+template <int kPh>
 __device__ __forceinline__ float qphase(const float* planes, const SortDesc& d, const QueryCtx& q, float ua,
                                        float half) {
+    constexpr bool kMixed = kPh == kPhMixed;
 #if SF_PLANE_PAIRS
     if (kMixed) return table_phase(d, q.gi, q.gt, ua, half);
     const float2* pp = reinterpret_cast<const float2*>(planes);
-    if (d.n_planes == 1) return d.w[0] * plane_lookup_pairs(pp, d.A, d.H, d.sv, ua, half);
+    if (kPh == kPhOne || d.n_planes == 1) return d.w[0] * plane_lookup_pairs(pp, d.A, d.H, d.sv, ua, half);
     float f = 0.0f;
     for (int k = 0; k < d.n_planes; ++k)
         f = fmaf(d.w[k], plane_lookup_pairs(pp + k * d.A * (d.H + 1), d.A, d.H, d.sv, ua, half), f);
@@ -375,7 +378,7 @@ __device__ __forceinline__ void sample_rt(const SceneDev& sc, const int* base, c
 }
 
 // Features of template point i (diffuse 0..npts0-1, then highlight).
-template <bool kMixed>
+template <int kPh>
 __device__ __forceinline__ void point_features(const SceneDev& sc, const TemplateDev& ht, const QueryCtx& q, int i,
                                                const SortDesc& d, const float* planes, const float4* __restrict__ pre,
                                                bool same_light, float& rho, float& tr, float& ph) {
@@ -388,10 +391,10 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
             ph = 1.0f;  // diffuse centre point (src/feature_pipeline.cpp:163-164)
             return;
         }
-        const float fw = qphase<kMixed>(planes, d, q, unit_coord(q.wf[0], q.wf[1], q.wf[2], p1.x, p1.y, p1.z, d.su, d.A), p0.w);
+        const float fw = qphase<kPh>(planes, d, q, unit_coord(q.wf[0], q.wf[1], q.wf[2], p1.x, p1.y, p1.z, d.su, d.A), p0.w);
         const float fl = same_light
                              ? p1.w
-                             : qphase<kMixed>(planes, d, q, unit_coord(q.lf[0], q.lf[1], q.lf[2], p1.x, p1.y, p1.z, d.su, d.A), p0.w);
+                             : qphase<kPh>(planes, d, q, unit_coord(q.lf[0], q.lf[1], q.lf[2], p1.x, p1.y, p1.z, d.su, d.A), p0.w);
         ph = fw * fl;
         return;
     }
@@ -417,8 +420,8 @@ __device__ __forceinline__ void point_features(const SceneDev& sc, const Templat
     const float r = tq.w * q.hs * inv;  // cap / dist, both in voxels
     const float half = r >= 1.0f ? float(kPi) : asinf(r);
     const float ax = dx * inv, ay = dy * inv, az = dz * inv;
-    ph = qphase<kMixed>(planes, d, q, unit_coord(q.wf[0], q.wf[1], q.wf[2], ax, ay, az, d.su, d.A), half) *
-         qphase<kMixed>(planes, d, q, unit_coord(q.lf[0], q.lf[1], q.lf[2], ax, ay, az, d.su, d.A), half);
+    ph = qphase<kPh>(planes, d, q, unit_coord(q.wf[0], q.wf[1], q.wf[2], ax, ay, az, d.su, d.A), half) *
+         qphase<kPh>(planes, d, q, unit_coord(q.lf[0], q.lf[1], q.lf[2], ax, ay, az, d.su, d.A), half);
 }
 
 // Per-scene diffuse constants: pre[2i] = {offset (voxels), half angle or -1 at the
@@ -749,7 +752,13 @@ __device__ __forceinline__ void sort_emit_pair(const float* seg, int cnt, bool u
     }
 }
 
-template <bool kMixed, int kWarps, int kMinB>  // kMixed: per-query g (C4), phase from the full table
+// kPh: phase lookups (kPhMixed: per-query g (C4), phase from the full table; kPhOne: one plane)
+#ifdef SF_SAMPLE_SORT_DEBUG
+#define SS_DEBUG(d) ((d).debug)
+#else
+#define SS_DEBUG(d) 0  // SF_DEBUG_SAMPLE_SORT needs a -DSF_SAMPLE_SORT_DEBUG build
+#endif
+template <int kPh, int kWarps, int kMinB>
 __global__ void __launch_bounds__(kWarps * 32, kMinB)
     k_sample_sort(SceneDev sc, TemplateDev ht, SortDesc d, const float* __restrict__ planes_g,
                   const float4* __restrict__ pre, int64_t n, const QueryCtx* __restrict__ recs,
@@ -812,14 +821,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
             __syncwarp();
             const QueryCtx& qc = s_qc[(it & 1) * kWarps + warp];
             prefetch_ctx(grp + gridDim.x, (it + 1) & 1);  // next group's context lands during this one
-            if (q >= n || (d.debug & 1)) {
+            if (q >= n || (SS_DEBUG(d) & 1)) {
                 for (int i = lane; i < 3 * d.ntot; i += 32) scr[i] = 0.0f;
             } else if (recs != nullptr) {
                 if (!qc.ok && lane == 0) atomicExch(err, 1);
                 const bool same_light = qc.same_light != 0;
                 for (int i = lane; i < d.ntot; i += 32) {
                     float rho, tr, ph;
-                    point_features<kMixed>(sc, ht, qc, i, d, planes, pre, same_light, rho, tr, ph);
+                    point_features<kPh>(sc, ht, qc, i, d, planes, pre, same_light, rho, tr, ph);
                     scr[i] = rho;
                     scr[d.ntot + i] = tr;
                     scr[2 * d.ntot + i] = ph;
@@ -838,8 +847,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
         // and pools straight from registers
         const int64_t tile = d.tile0 + q0 / kUmmaM;
         const int row0 = int(q0 % kUmmaM);
-        const bool store = !(d.debug & 4);
-        for (int t = threadIdx.x; t < ((d.debug & 2) ? 0 : d.n_tasks * kWarps); t += blockDim.x) {
+        const bool store = !(SS_DEBUG(d) & 4);
+        for (int t = threadIdx.x; t < ((SS_DEBUG(d) & 2) ? 0 : d.n_tasks * kWarps); t += blockDim.x) {
             const int task = s_task[t / kWarps];
             const int sg = task & 0x7f;
             const int cnt = s_n[sg];
@@ -1081,7 +1090,7 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
     };
     static const size_t static_smem = [] {
         cudaFuncAttributes fa{};
-        SFB_CUDA(cudaFuncGetAttributes(&fa, k_sample_sort<true, kWBig, kMinBBig>));
+        SFB_CUDA(cudaFuncGetAttributes(&fa, k_sample_sort<kPhMixed, kWBig, kMinBBig>));
         return fa.sharedSizeBytes;
     }();
     // Block shape: 32 warps (one block per SM) when its shared memory fits, else 8 warps x 4.
@@ -1097,8 +1106,13 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
         if (std::atoi(e) == 2 && minb * (smem_for(w, 2) + static_smem + 1024) <= 228 * 1024) d.nbuf = 2;
     const size_t smem = smem_for(w, d.nbuf);
     if (smem + static_smem > budget) fail(SF_ERR_INVALID_ARGUMENT, "sample_sort: templates too large for shared memory");
-    auto kern = big ? (d.mixed ? k_sample_sort<true, kWBig, kMinBBig> : k_sample_sort<false, kWBig, kMinBBig>)
-                    : (d.mixed ? k_sample_sort<true, kWSmall, kMinBSmall> : k_sample_sort<false, kWSmall, kMinBSmall>);
+    const int ph = d.mixed ? kPhMixed : (d.n_planes == 1 ? kPhOne : kPhPlanes);
+    auto kern = big ? (ph == kPhMixed ? k_sample_sort<kPhMixed, kWBig, kMinBBig>
+                                      : (ph == kPhOne ? k_sample_sort<kPhOne, kWBig, kMinBBig>
+                                                      : k_sample_sort<kPhPlanes, kWBig, kMinBBig>))
+                    : (ph == kPhMixed ? k_sample_sort<kPhMixed, kWSmall, kMinBSmall>
+                                      : (ph == kPhOne ? k_sample_sort<kPhOne, kWSmall, kMinBSmall>
+                                                      : k_sample_sort<kPhPlanes, kWSmall, kMinBSmall>));
     if (smem > 48 * 1024)
         // (no carveout preference: the driver's choice from the occupancy need is the fastest)
         SFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

@@ -1,4 +1,5 @@
-"""Time the bf16 query stages under SF_DEBUG_SAMPLE_SORT variants (one process per variant)."""
+"""Time the bf16 query stages under SF_DEBUG_SAMPLE_SORT variants (one process per variant; the library
+must be built with SF_NVCC_EXTRA=-DSF_SAMPLE_SORT_DEBUG, else the switches are compiled out)."""
 import os, subprocess, sys, json
 code = r'''
 import os, sys, json
