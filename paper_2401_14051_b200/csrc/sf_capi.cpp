@@ -875,6 +875,7 @@ int sf_phase_table_lookup_hg(const sf_phase_table* t, int64_t n, const double* g
 void sf_phase_table_destroy(sf_phase_table* t) {
     if (!t) return;
     cudaFree(t->d);
+    cudaFree(t->d_quad);
     delete t;
 }
 
@@ -1429,6 +1430,7 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             sfb::SceneDev sc = sfb::scene_dev(*s->density, *s->tvol->values, s->d_dt, s->model, *s->table,
                                               s->template_scale);
             sc.dt4 = s->d_dt4;
+            if (media) sc.phase.quad = sfb::phase_quad(*s->table, stream);
             sfb::TemplateDev dt = sfb::template_dev(*s->dt), ht = sfb::template_dev(*s->ht);
             cudaStream_t cs = stream;
             if (h_in || h_out) {  // the device's copy stream (calls on one device hold g_ws_mu)

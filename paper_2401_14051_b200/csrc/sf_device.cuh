@@ -37,6 +37,7 @@ struct PhaseDev {
     double g[3];
     const float* table;
     int gr, ar, hr;
+    const float4* quad;  // sf_phase_table::d_quad (mixed-media production sampler), or null
 };
 
 #if defined(__CUDACC__)

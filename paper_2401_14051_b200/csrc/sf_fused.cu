@@ -69,6 +69,7 @@ struct SortDesc {
     int mixed;                       // per-query g (C4): phase from the full table at the query's g
     int G;                           // table g resolution
     const float* table;              // [G][A][H] (mixed only)
+    const float4* quad;              // the table's quad records (mixed only, see table_phase)
     int nbuf;                        // scratch buffers (2: one block barrier per group, if 3 blocks/SM still fit)
     int f16;  // bit 0: operand blocks in fp16 (SF_PRECISION_FP16) instead of bf16; bit 1: plain
               // stores (the chunk's operands stay in L2 for the backbone) instead of evict-first
@@ -152,8 +153,10 @@ __device__ __forceinline__ float cap_phase(const float* planes, const SortDesc& 
 }
 
 // PhaseTable::lookup_hg (src/phase.cpp:191-219) at a per-query g cell (gi, gt) on the full
-// table [G][A][H] in global memory (L1/L2 resident): bilinear in (angle, aperture) on planes
-// gi and gi + 1, then the g lerp. FP32 (bf16 production path only).
+// table [G][A][H] (L1/L2 resident): bilinear in (angle, aperture) on planes gi and gi + 1, then
+// the g lerp. FP32 (production path only). The eight corners come from two 16-byte quad records
+// (rows a and a + 1, each {P(gi, a, h), P(gi, a, h + 1), P(gi + 1, a, h), P(gi + 1, a, h + 1)})
+// instead of eight scalar loads: same values, same arithmetic.
 __device__ __forceinline__ float table_phase(const SortDesc& d, int gi, float gt, float ua, float half) {
     const int A = d.A, H = d.H;
     const float u = fminf(fmaxf(ua, 0.0f), float(A - 1));
@@ -162,12 +165,13 @@ __device__ __forceinline__ float table_phase(const SortDesc& d, int gi, float gt
     const float v = fminf(fmaxf(half, 0.0f), float(kPi)) * d.sv;
     const int j0 = min(int(v), H - 2);
     const float s = v - float(j0);
+    const float4* qb = d.quad + (size_t(gi) * A + i0) * H + j0;
+    const float4 q0 = __ldg(qb), q1 = __ldg(qb + H);
+    const float r00[2] = {q0.x, q0.z}, r01[2] = {q0.y, q0.w}, r10[2] = {q1.x, q1.z}, r11[2] = {q1.y, q1.w};
     float pg[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const float* b = d.table + (size_t(gi + k) * A + i0) * H + j0;
-        const float r00 = __ldg(b), r01 = __ldg(b + 1), r10 = __ldg(b + H), r11 = __ldg(b + H + 1);
-        const float a = fmaf(s, r01 - r00, r00), c = fmaf(s, r11 - r10, r10);
+        const float a = fmaf(s, r01[k] - r00[k], r00[k]), c = fmaf(s, r11[k] - r10[k], r10[k]);
         pg[k] = fmaf(t, c - a, a);
     }
     return d.w[0] * fmaf(gt, pg[1] - pg[0], pg[0]);
@@ -1081,6 +1085,8 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
         d.mixed = 1;
         d.G = sc->phase.gr;
         d.table = sc->phase.table;
+        d.quad = sc->phase.quad;
+        if (!d.quad) fail(SF_ERR_INVALID_ARGUMENT, "sample_sort: mixed media need the table's quad records");
         d.w[0] = 1.0f;  // PhaseModel::hg(g): one lobe of weight 1
     }
     auto smem_for = [&](int w, int nbuf) {
@@ -1127,6 +1133,29 @@ void launch_sample_sort(const SceneDev* sc, const TemplateDev* dt, const Templat
                                                 ops, mms, err);
     SFB_CUDA(cudaGetLastError());
     count_launch();
+}
+
+__global__ void k_phase_quad(const float* __restrict__ t, int G, int A, int H, float4* __restrict__ q) {
+    const int64_t n = int64_t(G) * A * H;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int h = int(i % H), a = int((i / H) % A), g = int(i / (int64_t(A) * H));
+        const int h1 = min(h + 1, H - 1), g1 = min(g + 1, G - 1);
+        const float* p0 = t + (int64_t(g) * A + a) * H;
+        const float* p1 = t + (int64_t(g1) * A + a) * H;
+        q[i] = make_float4(p0[h], p0[h1], p1[h], p1[h1]);
+    }
+}
+
+const float4* phase_quad(const sf_phase_table& t, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(t.quad_mu);
+    if (!t.d_quad) {
+        const size_t n = size_t(t.g) * t.a * t.h;
+        SFB_CUDA(cudaMalloc(&t.d_quad, n * sizeof(float4)));
+        k_phase_quad<<<unsigned(std::min<size_t>((n + 255) / 256, 65535)), 256, 0, s>>>(t.d, t.g, t.a, t.h, t.d_quad);
+        SFB_CUDA(cudaGetLastError());
+        count_launch();
+    }
+    return t.d_quad;
 }
 
 }  // namespace sfb

@@ -104,6 +104,10 @@ struct sf_tvol {
 struct sf_phase_table {
     int g = 0, a = 0, h = 0;
     float* d = nullptr;
+    // [G][A][H] float4 {P(g, a, h), P(g, a, h + 1), P(g + 1, a, h), P(g + 1, a, h + 1)}: the per-query-g
+    // lookup's two bilinear cells as 16-byte records (made on the first mixed-media query)
+    mutable float4* d_quad = nullptr;
+    mutable std::mutex quad_mu;
 };
 
 struct sf_template {
@@ -173,6 +177,8 @@ void launch_interleave(const float* density, const float* tvol, float2* out, siz
                        cudaStream_t s);
 void launch_phase_table(int gr, int ar, int hr, const std::vector<double>& nodes,
                         const std::vector<double>& weights, float* out, cudaStream_t s);
+// The table's quad records (sf_phase_table::d_quad), made once.
+const float4* phase_quad(const sf_phase_table& t, cudaStream_t s);
 void launch_lookup_hg(const sf_phase_table& t, int64_t n, const double* g, const double* a,
                       const double* h, double* out, cudaStream_t s);
 void launch_sample_trilinear(const sf_grid& g, int64_t n, const double* pts, double* out,

@@ -498,6 +498,7 @@ SceneDev scene_dev(const sf_grid& density, const sf_grid& tvol, const float2* dt
     s.phase.gr = t.g;
     s.phase.ar = t.a;
     s.phase.hr = t.h;
+    s.phase.quad = t.d_quad;
     s.template_scale = ts;
     return s;
 }
