@@ -105,6 +105,32 @@ def test_c4_bf16_vs_fp32(tm):
     assert np.all(np.abs(F16 - F32) <= 0.03 * (np.abs(F32) + eg))
 
 
+@pytest.mark.parametrize("table", [(64, 128, 32, 16), (9, 17, 5, 8), (4, 6, 3, 8)])
+def test_c4_fp16_table_quads(tm, table):
+    """The production mixed-media sampler reads the phase table through 16-byte quad records
+    (two rows of {P(g, a, h), P(g, a, h + 1), P(g + 1, a, h), P(g + 1, a, h + 1)}); small and odd
+    table shapes (and g at the ends of the range) against the FP32 path at the fp16 bound."""
+    from conftest import LIGHT
+    dens, alb, gg = scenes.mixed_medium(64, 9)
+    rows = scenes.draw_centers(dens, 3000, 5, LIGHT)
+    media = scenes.sample_media(alb, gg, rows)
+    media[:64, 0] = -0.98  # g cells at both ends of the table's g axis
+    media[64:128, 0] = 0.98
+    g = sf.DensityGrid.from_array(dens, 2.0 / 64, ORIGIN)
+    tv = sf.build_transmittance_volume(sf.DensityPyramid(g), LIGHT)
+    scene = sf.Scene(g, tv, tm[0], tm[1], sf.PhaseModel.hg(0.5), sf.PhaseTable(*table))
+    net = sf.make_backbone(sf.BackboneConfig(seed=0))
+    y32 = np.empty((len(rows), 3), np.float32)
+    y16 = np.empty((len(rows), 3), np.float32)
+    F32 = sf.query_media(scene, net, rows, media, sf.FP32, y_out=y32)
+    F16 = sf.query_media(scene, net, rows, media, sf.FP16, y_out=y16)
+    assert np.all(np.isfinite(F16))
+    scale = np.maximum(1.0, np.abs(y32))
+    assert (np.abs(y16 - y32) / scale).max() <= 0.01
+    eg = media[:, 1:] ** 4
+    assert np.all(np.abs(F16 - F32) <= 0.01 * scale * (np.abs(F32) + eg))
+
+
 def test_c5_animated_frames_vs_oracle(oracle, templates, otab, tm):
     vol = scenes.noise_volume(16, 5)
     rows = scenes.draw_centers(vol, 64, 2, scenes.LIGHT)
