@@ -173,3 +173,31 @@ def test_two_lights_across_windows(det):
     sf.query(scene, net, med, rows[19000:21000], sf.BF16, y_out=y16[:2000])
     sf.query(scene, net, med, rows[19000:21000], sf.FP32, y_out=y32[:2000])
     assert np.all(np.abs(y16[:2000] - y32[:2000]) <= 0.03 * np.maximum(1.0, np.abs(y32[:2000])))
+
+
+def test_morton_chunks_host_vs_device():
+    """A volume beyond L2 (256^3: queries processed in Morton order, results scattered back to
+    the caller's rows) and a batch of two chunks: F and y are bit-identical with device buffers,
+    pageable and pinned host buffers."""
+    import torch
+    vol = scenes.noise_volume(256, 5)
+    g = sf.DensityGrid.from_array(vol, 2.0 / 256, ORIGIN)
+    tv = sf.build_transmittance_volume(sf.DensityPyramid(g), scenes.LIGHT, fast=True)
+    tm = (sf.load_template(os.path.join(DATA, "diffuse_seed7.vtmpl")),
+          sf.load_template(os.path.join(DATA, "highlight_seed8.vtmpl")))
+    sc = sf.Scene(g, tv, tm[0], tm[1], sf.PhaseModel.hg(0.7), sf.PhaseTable(64, 128, 32, 16))
+    net = sf.make_backbone(sf.BackboneConfig(seed=0))
+    med = sf.MediumParams((0.7,), (0.99,) * 3)
+    n = 600_000  # > one 524,288-query chunk
+    rows = scenes.draw_centers(vol, n, 3, scenes.LIGHT)
+    Fd = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    yd = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    sf.query(sc, net, med, torch.from_numpy(rows).cuda(), sf.FP16, F_out=Fd, y_out=yd)
+    torch.cuda.synchronize()
+    yh = np.empty((n, 3), np.float32)
+    Fh = sf.query(sc, net, med, rows, sf.FP16, y_out=yh)
+    assert np.array_equal(Fh, Fd.cpu().numpy())
+    assert np.array_equal(yh, yd.cpu().numpy())
+    Fp = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    sf.query(sc, net, med, torch.from_numpy(rows).pin_memory(), sf.FP16, F_out=Fp)
+    assert np.array_equal(Fp.numpy(), Fh)
