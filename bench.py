@@ -566,6 +566,19 @@ def binding(k):
             f"(ncu); real DRAM {k.get('dram_bytes', 0) / 1e6:.0f} MB per launch")
 
 
+def l2_read_peak(sf):
+    """L2 read bandwidth (GB/s) of 32-byte loads over a 32 MiB L2-resident buffer (sf_probe_l2_read),
+    best of 3; None if the probe fails."""
+    import ctypes
+    best = 0.0
+    for _ in range(3):
+        v = ctypes.c_double(0.0)
+        if sf.lib.sf_probe_l2_read(32 << 20, 200, ctypes.byref(v)) != 0:
+            return None
+        best = max(best, v.value)
+    return best or None
+
+
 def roofline(sf, w, stage_ms, n, precision):
     """Dominant kernel's roofline from the live per-stage events, plus rows for the other kernels.
     Algorithmic work per unit: sampling 33,984 B/query of logical gathers (266
@@ -584,6 +597,16 @@ def roofline(sf, w, stage_ms, n, precision):
                                  "l1_data_pipe_pct": k.get("l1_data_pipe_pct"), "ms": stage_ms["sample_sort"],
                                  "algorithmic": f"{bytes_q} B/query logical gathers x {n} queries per launch",
                                  "binding": binding(k)}
+        # cross-checks: the same logical bytes against the L2 read bandwidth measured
+        # live on this GPU with the sampler's 32-byte loads, and the real DRAM rate of the ncu launch
+        l2 = l2_read_peak(sf)
+        if l2:
+            rows["k_sample_sort"]["l2_read_peak_GBs"] = l2
+            rows["k_sample_sort"]["frac_vs_l2"] = bytes_q * n / t / 1e9 / l2
+        if k.get("dram_bytes") and k.get("duration_us"):
+            dr = k["dram_bytes"] / (k["duration_us"] * 1e-6) / 1e9
+            rows["k_sample_sort"]["dram_GBs_ncu"] = dr
+            rows["k_sample_sort"]["dram_frac_ncu"] = dr / hbm
     if "backbone" in stage_ms:
         t = stage_ms["backbone"] * 1e-3
         k = ncu.get("k_backbone_tc", {})
