@@ -30,13 +30,18 @@ def with_light(rows, light):
 
 def multi_light_query(grid, pyramid, lights, intensities, rows, dt, ht, model, table, medium, net,
                       precision=api.FP32, weights=None, cfg=None, template_scale=1.0):
-    """C3: F = sum_l I_l F_l over `lights`; returns (F [n,3], [F_l]). The transmittance volume
-    of each light is built on the device and dropped after its queries."""
+    """C3: F = sum_l I_l F_l over `lights`; returns (F [n,3], [F_l]). One scene: its
+    transmittance volume is rebuilt in place for each light (Scene.relight: no per-light
+    allocation or host synchronisation) before that light's queries."""
     total = np.zeros((len(rows), 3))
     per = []
+    scene = None
     for light, inten in zip(lights, intensities):
-        tvol = api.build_transmittance_volume(pyramid, light, weights, cfg)
-        scene = api.Scene(grid, tvol, dt, ht, model, table, template_scale)
+        if scene is None:
+            tvol = api.build_transmittance_volume(pyramid, light, weights, cfg)
+            scene = api.Scene(grid, tvol, dt, ht, model, table, template_scale)
+        else:
+            scene.relight(pyramid, light, weights, cfg)
         F = api.query(scene, net, medium, with_light(rows, light), precision)
         per.append(F)
         total += inten * F
@@ -52,12 +57,16 @@ def animated_sequence(grid, n_frames, rows, dt, ht, model, table, medium, net, p
     the list of per-frame F."""
     pyramid = api.DensityPyramid(grid, stream=stream)
     out = []
+    scene = None
     for f in (range(n_frames) if frames is None else frames):
         light = scenes.rotating_light(f, n_frames)
         if timer:
             timer("transmittance")
-        tvol = api.build_transmittance_volume(pyramid, light, stream=stream)
-        scene = api.Scene(grid, tvol, dt, ht, model, table)
+        if scene is None:  # the first frame's volume makes the scene; later frames rebuild it in place
+            tvol = api.build_transmittance_volume(pyramid, light, stream=stream)
+            scene = api.Scene(grid, tvol, dt, ht, model, table)
+        else:
+            scene.relight(pyramid, light, stream=stream)
         if timer:
             timer("query")
         out.append(api.query(scene, net, medium, with_light(rows, light), precision, stream=stream))
