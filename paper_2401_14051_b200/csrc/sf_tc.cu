@@ -1391,7 +1391,7 @@ void launch_backbone_tc(const sf_backbone& b, int64_t n, const uint8_t* ops, con
     // SF_TC_RING=tri|narrow forces one (A/B).
     const int64_t n_tiles64 = (n + kUmmaM - 1) / kUmmaM;
     // k_backbone_rr (the three chains of a tile interleaved, two CTAs per SM) with SF_TC_RR=1:
-    // bit-identical, measured slower at C5 (2.04 vs 1.86 ms: its consumer warps are latency-bound
+    // bit-identical, measured slower at C5 (2.05 vs 1.53 ms: its consumer warps are latency-bound
     // and two CTAs per SM give 8 of them where the one-chain kernel's three give 12)
     static const char* rr_env = std::getenv("SF_TC_RR");
     if (pk->rr && rr_env && rr_env[0] == '1') {
