@@ -1181,6 +1181,29 @@ static sf_tvol* scene_own_tvol(sf_scene* s) {
     return s->own_tvol;
 }
 
+namespace {
+// Per device: a second stream and a fork / join event pair for the per-light build, whose coarse
+// mip levels (a tail of small launches that cannot fill the GPU) run beside level 0's passes.
+struct BuildSide {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+std::mutex g_side_mu;
+BuildSide& build_side() {
+    static auto* m = new std::unordered_map<int, BuildSide>;
+    int dev = 0;
+    SFB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_side_mu);
+    BuildSide& b = (*m)[dev];
+    if (!b.side) {
+        SFB_CUDA(cudaStreamCreateWithFlags(&b.side, cudaStreamNonBlocking));
+        SFB_CUDA(cudaEventCreateWithFlags(&b.fork, cudaEventDisableTiming));
+        SFB_CUDA(cudaEventCreateWithFlags(&b.join, cudaEventDisableTiming));
+    }
+    return b;
+}
+}  // namespace
+
 int sf_scene_relight(sf_scene* s, const sf_pyramid* p, const double light[3], const float* kernels,
                      const float* scales, double lambda, double step_scale, int flags, sf_stream stream) {
     return guard([&] {
@@ -1195,22 +1218,46 @@ int sf_scene_relight(sf_scene* s, const sf_pyramid* p, const double light[3], co
         sf_tvol* t = scene_own_tvol(s);  // first relight: the scene's own volume (one allocation, kept)
         normalize3(light, t->light);
         combiner_weights(L, kernels, scales, t->kernels, t->scales);
-        std::vector<sf_grid*> fields;
+        std::vector<sf_grid*> fields, conv;
         try {
+            // levels 1.. (graded field and 3D-CNN convolution) on the side stream while level 0 runs
+            // on `stream` (the same kernels and operands: bit-identical); the combine waits for both.
+            // Side-stream scratch is freed on `stream` after the join.
+            static const bool side_on = !std::getenv("SF_BUILD_SERIAL");
+            BuildSide* bs = side_on && L > 1 ? &build_side() : nullptr;
+            if (bs) {
+                SFB_CUDA(cudaEventRecord(bs->fork, stream));
+                SFB_CUDA(cudaStreamWaitEvent(bs->side, bs->fork, 0));
+            }
+            auto level_stream = [&](int i) { return bs && i > 0 ? bs->side : stream; };
             {
                 StageScope st(SF_STAGE_MARCH, stream);
                 for (int i = 0; i < L; ++i) {
                     const double step = step_scale * p->levels[size_t(i)]->vs;
-                    fields.push_back(graded_level(p, i, light, lambda, step, stream, true, 0, -1, fast));
+                    fields.push_back(graded_level(p, i, light, lambda, step, level_stream(i), true, 0, -1, fast));
                 }
             }
-            std::vector<const sf_grid*> f(fields.begin(), fields.end());
             StageScope st(SF_STAGE_COMBINER, stream);
-            conv_combine(f, t->kernels, t->scales, 0, d.nz, 0, d.nz, t->values->d, stream, fast, false);
+            for (int i = L - 1; i >= 0; --i) {  // the side stream's convolutions are queued first
+                const sf_grid& f = *fields[size_t(i)];
+                sf_grid* c = new_scratch_grid(f.nx, f.ny, f.nz, f.vs, f.origin, level_stream(i));
+                conv.insert(conv.begin(), c);
+                sfb::launch_conv3(f, &t->kernels[size_t(i) * 27], 0, f.nz, c->d, level_stream(i), fast);
+            }
+            if (bs) {
+                SFB_CUDA(cudaEventRecord(bs->join, bs->side));
+                SFB_CUDA(cudaStreamWaitEvent(stream, bs->join, 0));
+                for (sf_grid* g : fields) g->pool_stream = stream;
+                for (sf_grid* g : conv) g->pool_stream = stream;
+            }
+            std::vector<const sf_grid*> cv(conv.begin(), conv.end());
+            sfb::launch_combine(cv, t->scales, *fields[0], 0, d.nz, t->values->d, stream, fast);
         } catch (...) {
             for (sf_grid* g : fields) free_grid(g);
+            for (sf_grid* g : conv) free_grid(g);
             throw;
         }
+        for (sf_grid* g : conv) free_grid(g);
         for (sf_grid* g : fields) free_grid(g);
         s->tvol = t;
         StageScope st(SF_STAGE_RECORDS, stream);
