@@ -687,6 +687,61 @@ int sf_combine_transmittance(const sf_grid* const* fields, int n, const float* k
     });
 }
 
+namespace {
+// Per device: a second stream and a fork / join event pair for the per-light build, whose coarse
+// mip levels (a tail of small launches that cannot fill the GPU) run beside level 0's passes.
+struct BuildSide {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+std::mutex g_side_mu;
+BuildSide& build_side() {
+    static auto* m = new std::unordered_map<int, BuildSide>;
+    int dev = 0;
+    SFB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_side_mu);
+    BuildSide& b = (*m)[dev];
+    if (!b.side) {
+        SFB_CUDA(cudaStreamCreateWithFlags(&b.side, cudaStreamNonBlocking));
+        SFB_CUDA(cudaEventCreateWithFlags(&b.fork, cudaEventDisableTiming));
+        SFB_CUDA(cudaEventCreateWithFlags(&b.join, cudaEventDisableTiming));
+    }
+    return b;
+}
+
+// Graded fields of every level (level 0 over rows [m0, m1), m1 < 0: all). With `fork`, levels 1..
+// run on the side stream beside level 0 (bit-identical) and are joined before returning; all
+// scratch is then freed on `stream`. The per-frame builds fork (relight, z-slab); the one-shot
+// build_transmittance_volume, which allocates its output volume per call, does not (no gain there).
+std::vector<sf_grid*> graded_fields(const sf_pyramid* p, const double light[3], double lambda, double step_scale,
+                                    bool fast, cudaStream_t stream, int m0 = 0, int m1 = -1, bool fork = false) {
+    static const bool side_on = !std::getenv("SF_BUILD_SERIAL");
+    const int L = int(p->levels.size());
+    BuildSide* bs = fork && side_on && L > 1 ? &build_side() : nullptr;
+    if (bs) {
+        SFB_CUDA(cudaEventRecord(bs->fork, stream));
+        SFB_CUDA(cudaStreamWaitEvent(bs->side, bs->fork, 0));
+    }
+    std::vector<sf_grid*> fields;
+    try {
+        for (int i = 0; i < L; ++i) {
+            const double step = step_scale * p->levels[size_t(i)]->vs;
+            fields.push_back(graded_level(p, i, light, lambda, step, bs && i > 0 ? bs->side : stream, true,
+                                          i == 0 ? m0 : 0, i == 0 ? m1 : -1, fast));
+        }
+    } catch (...) {
+        for (sf_grid* g : fields) free_grid(g);
+        throw;
+    }
+    if (bs) {
+        SFB_CUDA(cudaEventRecord(bs->join, bs->side));
+        SFB_CUDA(cudaStreamWaitEvent(stream, bs->join, 0));
+        for (sf_grid* g : fields) g->pool_stream = stream;
+    }
+    return fields;
+}
+}  // namespace
+
 int sf_build_transmittance_volume_ex(const sf_pyramid* p, const double light[3], const float* kernels,
                                      const float* scales, double lambda, double step_scale, int flags,
                                      sf_tvol** out, sf_stream stream) {
@@ -694,10 +749,7 @@ int sf_build_transmittance_volume_ex(const sf_pyramid* p, const double light[3],
         const bool fast = (flags & SF_BUILD_FP32_MARCH) != 0;
         std::vector<sf_grid*> fields;
         try {
-            for (int i = 0; i < int(p->levels.size()); ++i) {
-                double step = step_scale * p->levels[size_t(i)]->vs;
-                fields.push_back(graded_level(p, i, light, lambda, step, stream, true, 0, -1, fast));
-            }
+            fields = graded_fields(p, light, lambda, step_scale, fast, stream);
             std::vector<const sf_grid*> f(fields.begin(), fields.end());
             *out = combine(f, kernels, scales, light, stream, fast);
         } catch (...) {
@@ -730,11 +782,7 @@ int sf_build_transmittance_slab(const sf_pyramid* p, const double light[3], cons
             // levels whole (<= 1/8 of the work, computed by every shard)
             const int c0 = std::max(z0 - 1, 0), c1 = std::min(z1 + 1, g0.nz);
             const int m0 = std::max(z0 - 2, 0), m1 = std::min(z1 + 2, g0.nz);
-            for (int i = 0; i < int(p->levels.size()); ++i) {
-                const double step = step_scale * p->levels[size_t(i)]->vs;
-                fields.push_back(
-                    graded_level(p, i, light, lambda, step, stream, true, i == 0 ? m0 : 0, i == 0 ? m1 : -1, fast));
-            }
+            fields = graded_fields(p, light, lambda, step_scale, fast, stream, m0, m1, true);
             std::vector<float> K, S;
             combiner_weights(int(fields.size()), kernels, scales, K, S);
             std::vector<const sf_grid*> f(fields.begin(), fields.end());
@@ -1181,28 +1229,6 @@ static sf_tvol* scene_own_tvol(sf_scene* s) {
     return s->own_tvol;
 }
 
-namespace {
-// Per device: a second stream and a fork / join event pair for the per-light build, whose coarse
-// mip levels (a tail of small launches that cannot fill the GPU) run beside level 0's passes.
-struct BuildSide {
-    cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-};
-std::mutex g_side_mu;
-BuildSide& build_side() {
-    static auto* m = new std::unordered_map<int, BuildSide>;
-    int dev = 0;
-    SFB_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(g_side_mu);
-    BuildSide& b = (*m)[dev];
-    if (!b.side) {
-        SFB_CUDA(cudaStreamCreateWithFlags(&b.side, cudaStreamNonBlocking));
-        SFB_CUDA(cudaEventCreateWithFlags(&b.fork, cudaEventDisableTiming));
-        SFB_CUDA(cudaEventCreateWithFlags(&b.join, cudaEventDisableTiming));
-    }
-    return b;
-}
-}  // namespace
 
 int sf_scene_relight(sf_scene* s, const sf_pyramid* p, const double light[3], const float* kernels,
                      const float* scales, double lambda, double step_scale, int flags, sf_stream stream) {
