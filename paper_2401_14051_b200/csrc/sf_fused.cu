@@ -1154,6 +1154,8 @@ const float4* phase_quad(const sf_phase_table& t, cudaStream_t s) {
         k_phase_quad<<<unsigned(std::min<size_t>((n + 255) / 256, 65535)), 256, 0, s>>>(t.d, t.g, t.a, t.h, t.d_quad);
         SFB_CUDA(cudaGetLastError());
         count_launch();
+        // once per table: complete before any stream (not only `s`) may read the records
+        SFB_CUDA(cudaStreamSynchronize(s));
     }
     return t.d_quad;
 }
