@@ -1374,9 +1374,10 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             const bool hF0 = F_out && !is_device_ptr(F_out);
             bool zero_copy = false;
             static const bool overlap_on = !std::getenv("SF_NO_HOST_OVERLAP");
-            // Volumes beyond L2 (x-pair records of a 256^3 grid are 268 MB): process the queries in
-            // Morton order of p so concurrently sampled queries share the volume's cache lines;
-            // results are written back to the caller's rows.
+            // Volumes beyond L2 (x-pair records of a 256^3 grid are 268 MB): process the queries
+            // grouped by the Morton order of their 64^3 cell (a counting sort, launch_cell_order) so
+            // concurrently sampled queries share the volume's cache lines; results are written back
+            // to the caller's rows.
             static const int morton_env = std::getenv("SF_MORTON") ? std::atoi(std::getenv("SF_MORTON")) : -1;
             const size_t vol_bytes = sfb::xpair_records(s->density->nx, s->density->ny, s->density->nz) *
                                      sizeof(float4);
@@ -1439,14 +1440,13 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                 b.F = cv.take<double>(hF ? size_t(n) * 3 : 0);
                 b.y = cv.take<float>(hy ? size_t(n) * 3 : 0);
                 b.perm = cv.take<int>(reorder ? size_t(n) : 0);
-                b.keys = cv.take<uint32_t>(reorder ? size_t(n) * 2 : 0);
-                b.idx = cv.take<int>(reorder ? size_t(n) : 0);
+                b.keys = cv.take<uint32_t>(reorder ? size_t(n) : 0);  // cell keys (launch_cell_order)
+                b.idx = nullptr;
                 return b;
             };
             Carve probe{nullptr};
             carve_all(nullptr, probe);
-            size_t sort_tmp = 0;
-            if (reorder) sfb::launch_sort_keys(nullptr, nullptr, nullptr, nullptr, int(n), 30, nullptr, sort_tmp, stream);
+            const size_t sort_tmp = reorder ? size_t(sfb::kOrderCells + 1024) * sizeof(int) : 0;  // cell counts
             const size_t need = probe.off + sort_tmp + 256;
             std::unique_lock<std::mutex> wlk(g_ws_mu);
             int dev = 0;
@@ -1532,10 +1532,8 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
                 }
             if (reorder) {
                 for (cudaEvent_t e : rows_ready) SFB_CUDA(cudaStreamWaitEvent(stream, e, 0));  // every row
-                sfb::launch_morton(s->density->dev(), n, rows, bufs.keys, bufs.idx, stream);
-                size_t tmp_bytes = sort_tmp;
-                sfb::launch_sort_keys(bufs.keys, bufs.keys + n, bufs.idx, perm.p, int(n), 30, sort_tmp_p, tmp_bytes,
-                                      stream);
+                sfb::launch_cell_order(s->density->dev(), n, rows, bufs.keys, reinterpret_cast<int*>(sort_tmp_p), perm.p,
+                                       stream);
             }
             size_t wi = 0;
             for (int64_t c0 = 0; c0 < n; c0 += chunk) {

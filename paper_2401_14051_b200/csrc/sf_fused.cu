@@ -508,9 +508,7 @@ __global__ void __launch_bounds__(kPrepThreads)
     }
 }
 
-// 30-bit Morton key of each query's voxel (10 bits per axis of the voxel coordinate scaled
-// to 1024 cells), index = row: sorting by key makes concurrently sampled queries share cache
-// lines of the volume when it does not fit in L2.
+// Morton interleave of a 10-bit coordinate (the query cell order below uses 6 bits per axis).
 __device__ __forceinline__ uint32_t spread10(uint32_t v) {
     v &= 1023u;
     v = (v | (v << 16)) & 0x030000FFu;
@@ -520,18 +518,71 @@ __device__ __forceinline__ uint32_t spread10(uint32_t v) {
     return v;
 }
 
-__global__ void k_morton(GridDev g, int64_t n, const double* __restrict__ queries, uint32_t* __restrict__ keys,
-                         int* __restrict__ idx) {
+// Counting sort of the queries by the Morton code of their 64^3 cell (launch_cell_order).
+__global__ void k_cell_key(GridDev g, int64_t n, const double* __restrict__ queries, uint32_t* __restrict__ cells,
+                           int* __restrict__ counts) {
     const double ext[3] = {g.hx - g.ox, g.hy - g.oy, g.hz - g.oz};
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
         uint32_t c[3];
         for (int k = 0; k < 3; ++k) {
             const double o = k == 0 ? g.ox : (k == 1 ? g.oy : g.oz);
-            const double u = (queries[9 * q + k] - o) / ext[k] * 1024.0;
-            c[k] = uint32_t(fmin(fmax(u, 0.0), 1023.0));
+            const double u = (queries[9 * q + k] - o) / ext[k] * 64.0;
+            c[k] = uint32_t(fmin(fmax(u, 0.0), 63.0));
         }
-        keys[q] = spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);
-        idx[q] = int(q);
+        const uint32_t key = spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);  // 18 bits
+        cells[q] = key;
+        atomicAdd(&counts[key], 1);
+    }
+}
+
+// Exclusive scan of the cell counts in two levels: every 1024-cell tile in place (warp shuffles +
+// one shared-memory pass), the tile totals into counts[kOrderCells ...] and scanned by one block.
+__device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int ws = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, ws, off);
+            if (lane >= off) ws += y;
+        }
+        if (lane < nw) warp_sums[lane] = ws;  // inclusive over warps
+    }
+    __syncthreads();
+    total = warp_sums[nw - 1];
+    return x - v + (w > 0 ? warp_sums[w - 1] : 0);
+}
+
+__global__ void __launch_bounds__(1024) k_cell_tile_scan(int* __restrict__ counts) {
+    __shared__ int warp_sums[32];
+    const int i = blockIdx.x * 1024 + threadIdx.x;
+    int total;
+    const int ex = block_exclusive_scan(counts[i], warp_sums, total);
+    counts[i] = ex;
+    if (threadIdx.x == 0) counts[kOrderCells + blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kOrderCells / 1024) k_cell_sum_scan(int* __restrict__ counts) {
+    __shared__ int warp_sums[32];
+    int* sums = counts + kOrderCells;
+    int total;
+    sums[threadIdx.x] = block_exclusive_scan(sums[threadIdx.x], warp_sums, total);
+}
+
+__global__ void k_cell_scatter(int64_t n, const uint32_t* __restrict__ cells, int* __restrict__ offsets,
+                               int* __restrict__ perm) {
+    const int* tile_off = offsets + kOrderCells;
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
+        const uint32_t c = cells[q];
+        perm[atomicAdd(&offsets[c], 1) + tile_off[c >> 10]] = int(q);
     }
 }
 
@@ -985,6 +1036,26 @@ void launch_xpair(const float* rho, const float* tr, int nx, int ny, int nz, flo
     count_launch();
 }
 
+void launch_cell_order(const GridDev& g, int64_t n, const double* queries, uint32_t* cells, int* counts, int* perm,
+                       cudaStream_t s) {
+    if (n <= 0) return;
+    if (n >= (int64_t(1) << 31)) fail(SF_ERR_INVALID_ARGUMENT, "cell order: batch too large");
+    const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, int64_t(sm_count()) * 16));
+    SFB_CUDA(cudaMemsetAsync(counts, 0, size_t(kOrderCells) * sizeof(int), s));
+    k_cell_key<<<blocks, 256, 0, s>>>(g, n, queries, cells, counts);
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+    k_cell_tile_scan<<<kOrderCells / 1024, 1024, 0, s>>>(counts);
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+    k_cell_sum_scan<<<1, kOrderCells / 1024, 0, s>>>(counts);
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+    k_cell_scatter<<<blocks, 256, 0, s>>>(n, cells, counts, perm);
+    SFB_CUDA(cudaGetLastError());
+    count_launch();
+}
+
 size_t query_rec_bytes() { return sizeof(QueryCtx); }
 
 int64_t sample_sort_round_queries() { return int64_t(sm_count()) * (kSortThreadsPerSM / 32); }
@@ -1038,14 +1109,6 @@ double probe_l2_read_gbs(size_t bytes, int reps) {
 // bricks, two float4 per record
 size_t xpair_records(int nx, int ny, int nz) {
     return size_t((nx + 2) / 2) * size_t(ny + 1) * ((nz + 3) / 2) * 4 * 2;
-}
-
-void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t* keys, int* idx, cudaStream_t s) {
-    if (n <= 0) return;
-    const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(sm_count()) * 16);
-    k_morton<<<unsigned(blocks), 256, 0, s>>>(g, n, queries, keys, idx);
-    SFB_CUDA(cudaGetLastError());
-    count_launch();
 }
 
 void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_medium_params& m, int64_t n,

@@ -272,7 +272,12 @@ void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_mediu
                        const int* perm = nullptr, const double* row0 = nullptr, const TemplateDev* dt = nullptr,
                        const float* planes = nullptr, int n_planes = 0, float4* pre = nullptr);
 // Morton keys of the queries' positions in the grid box + identity indices (for cub sort)
-void launch_morton(const GridDev& g, int64_t n, const double* queries, uint32_t* keys, int* idx, cudaStream_t s);
+// Processing order for locality: perm = the query rows grouped by the Morton code of their cell in a
+// 64^3 partition of the box (a counting sort: histogram, scan, scatter; order within a cell is
+// arbitrary, which no result depends on). cells: n keys of scratch; counts: kOrderCells + 1024 ints.
+constexpr int kOrderCells = 1 << 18;
+void launch_cell_order(const GridDev& g, int64_t n, const double* queries, uint32_t* cells, int* counts, int* perm,
+                       cudaStream_t s);
 void launch_xpair(const float* rho, const float* tr, int nx, int ny, int nz, float4* out, cudaStream_t s);
 double probe_l2_read_gbs(size_t bytes, int reps);  // k_l2_probe: 32-byte reads of an L2-resident buffer
 size_t xpair_records(int nx, int ny, int nz);  // float4 units of the padded xy-quad record layout
