@@ -241,4 +241,32 @@ __device__ __forceinline__ void write_cfg8(const sf_medium_params& m, const doub
 
 #endif  // __CUDACC__
 
+#if defined(__CUDACC__)
+// Exclusive scan of one int per thread across the block (warp shuffles + one shared-memory pass
+// over the warp totals; blockDim.x a multiple of 32, <= 1024); `total` = the block's sum.
+__device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int ws = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, ws, off);
+            if (lane >= off) ws += y;
+        }
+        if (lane < nw) warp_sums[lane] = ws;  // inclusive over warps
+    }
+    __syncthreads();
+    total = warp_sums[nw - 1];
+    return x - v + (w > 0 ? warp_sums[w - 1] : 0);
+}
+#endif
+
 }  // namespace sfb

@@ -537,30 +537,6 @@ __global__ void k_cell_key(GridDev g, int64_t n, const double* __restrict__ quer
 
 // Exclusive scan of the cell counts in two levels: every 1024-cell tile in place (warp shuffles +
 // one shared-memory pass), the tile totals into counts[kOrderCells ...] and scanned by one block.
-__device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int& total) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    int x = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, off);
-        if (lane >= off) x += y;
-    }
-    if (lane == 31) warp_sums[w] = x;
-    __syncthreads();
-    if (w == 0) {
-        int ws = lane < nw ? warp_sums[lane] : 0;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, ws, off);
-            if (lane >= off) ws += y;
-        }
-        if (lane < nw) warp_sums[lane] = ws;  // inclusive over warps
-    }
-    __syncthreads();
-    total = warp_sums[nw - 1];
-    return x - v + (w > 0 ? warp_sums[w - 1] : 0);
-}
-
 __global__ void __launch_bounds__(1024) k_cell_tile_scan(int* __restrict__ counts) {
     __shared__ int warp_sums[32];
     const int i = blockIdx.x * 1024 + threadIdx.x;

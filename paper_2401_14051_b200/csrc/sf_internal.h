@@ -36,9 +36,6 @@ inline void cuda_check(cudaError_t e, const char* what) {
 int sm_count();
 void count_launch();  // every kernel launch of the library increments sf_launch_count()
 
-// cub radix sort of (key, index) pairs; tmp == nullptr only sizes tmp_bytes
-void launch_sort_keys(const uint32_t* keys_in, uint32_t* keys_out, const int* idx_in, int* idx_out, int n,
-                      int end_bit, void* tmp, size_t& tmp_bytes, cudaStream_t s);
 // Image entry point (sf_render.cu): occupied-voxel compaction, bake rows, field scatter, march.
 int64_t launch_occupied(const sf_grid& g, int* idx, int* count, void* tmp, size_t& tmp_bytes, cudaStream_t s);
 void launch_bake_rows(const sf_grid& g, const int* idx, const int* count, int64_t max_rows, const double cam[3],
@@ -271,7 +268,6 @@ void launch_query_prep(const SceneDev& sc, const TemplateDev& ht, const sf_mediu
                        const double* queries, const double* media, double* cfg8, void* recs, cudaStream_t s,
                        const int* perm = nullptr, const double* row0 = nullptr, const TemplateDev* dt = nullptr,
                        const float* planes = nullptr, int n_planes = 0, float4* pre = nullptr);
-// Morton keys of the queries' positions in the grid box + identity indices (for cub sort)
 // Processing order for locality: perm = the query rows grouped by the Morton code of their cell in a
 // 64^3 partition of the box (a counting sort: histogram, scan, scatter; order within a cell is
 // arbitrary, which no result depends on). cells: n keys of scratch; counts: kOrderCells + 1024 ints.
@@ -286,9 +282,6 @@ size_t xpair_records(int nx, int ny, int nz);  // float4 units of the padded xy-
 void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float* planes,
                          cudaStream_t s);
 
-// cub radix sort of (key, index) pairs; tmp == nullptr only sizes tmp_bytes
-void launch_sort_keys(const uint32_t* keys_in, uint32_t* keys_out, const int* idx_in, int* idx_out, int n,
-                      int end_bit, void* tmp, size_t& tmp_bytes, cudaStream_t s);
 // Image entry point (sf_render.cu): occupied-voxel compaction, bake rows, field scatter, march.
 int64_t launch_occupied(const sf_grid& g, int* idx, int* count, void* tmp, size_t& tmp_bytes, cudaStream_t s);
 void launch_bake_rows(const sf_grid& g, const int* idx, const int* count, int64_t max_rows, const double cam[3],

@@ -2,15 +2,12 @@
 // 549-581) and render_volume (src/rte.cpp:407-447), the two loops render_neural
 // (src/predictor.cpp:585-614) runs around the per-shading-point query.
 //
-// Bake: the occupied voxels (density > 0) are compacted on the device (cub select), one
+// Bake: the occupied voxels (density > 0) are compacted on the device (ordered, k_occ_*), one
 // query row (p = voxel centre, omega = normalize(p - camera), l) is written per voxel,
 // the fused query runs over the rows, and F is scattered into three float grids (zero
 // elsewhere). Render: one thread per pixel marches the camera ray through the box in
 // FP64 with the reference's operation order (second-order midpoint attenuation), the
 // in-scatter provider being the FP64 trilinear of the baked grids.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_select.cuh>
-#include <cub/iterator/counting_input_iterator.cuh>
 
 #include "sf_internal.h"
 
@@ -25,10 +22,44 @@ inline unsigned grid_for(size_t n, int block = kBlock) {
     return unsigned(g > 0x7fffffff ? 0x7fffffff : (g == 0 ? 1 : g));
 }
 
-struct Occupied {
-    const float* v;
-    __device__ __forceinline__ bool operator()(const int& i) const { return v[i] > 0.0f; }
-};
+// Ordered compaction of the occupied voxels (density > 0) into their indices: per-block counts,
+// a two-level exclusive scan of the counts, then every block writes its voxels in order.
+constexpr int kOccBlock = 1024;
+
+__global__ void __launch_bounds__(kOccBlock) k_occ_count(const float* __restrict__ v, int n, int* __restrict__ cnts) {
+    const int i = blockIdx.x * kOccBlock + threadIdx.x;
+    const int c = __syncthreads_count(i < n && v[i] > 0.0f);
+    if (threadIdx.x == 0) cnts[blockIdx.x] = c;
+}
+
+// In-place exclusive scan of cnts[0, m) in tiles of 1024; tile totals to tsum[]
+__global__ void __launch_bounds__(1024) k_occ_tile_scan(int* __restrict__ cnts, int m, int* __restrict__ tsum) {
+    __shared__ int ws[32];
+    const int i = blockIdx.x * 1024 + threadIdx.x;
+    int total;
+    const int ex = block_exclusive_scan(i < m ? cnts[i] : 0, ws, total);
+    if (i < m) cnts[i] = ex;
+    if (threadIdx.x == 0) tsum[blockIdx.x] = total;
+}
+
+// Exclusive scan of the tile totals (at most 1024 tiles); the grand total -> *count
+__global__ void __launch_bounds__(1024) k_occ_sum_scan(int* __restrict__ tsum, int tiles, int* __restrict__ count) {
+    __shared__ int ws[32];
+    int total;
+    const int ex = block_exclusive_scan(int(threadIdx.x) < tiles ? tsum[threadIdx.x] : 0, ws, total);
+    if (int(threadIdx.x) < tiles) tsum[threadIdx.x] = ex;
+    if (threadIdx.x == 0) *count = total;
+}
+
+__global__ void __launch_bounds__(kOccBlock) k_occ_write(const float* __restrict__ v, int n, const int* __restrict__ cnts,
+                                                       const int* __restrict__ tsum, int* __restrict__ idx) {
+    __shared__ int ws[32];
+    const int i = blockIdx.x * kOccBlock + threadIdx.x;
+    const bool occ = i < n && v[i] > 0.0f;
+    int total;
+    const int ex = block_exclusive_scan(occ ? 1 : 0, ws, total);
+    if (occ) idx[cnts[blockIdx.x] + tsum[blockIdx.x >> 10] + ex] = i;
+}
 
 // One query row per occupied voxel (bake_field's body, src/predictor.cpp:566-575).
 __global__ void k_bake_rows(GridDev g, const int* __restrict__ idx, const int* __restrict__ count, double cx,
@@ -140,21 +171,26 @@ void cross_h(const double* a, const double* b, double* o) {
 }  // namespace
 
 int64_t launch_occupied(const sf_grid& g, int* idx, int* count, void* tmp, size_t& tmp_bytes, cudaStream_t s) {
-    const int n = int(g.count());
-    cub::CountingInputIterator<int> it(0);
-    if (!tmp) {
-        SFB_CUDA(cub::DeviceSelect::If(nullptr, tmp_bytes, it, idx, count, n, Occupied{g.d}, s));
+    const size_t n64 = g.count();
+    if (n64 >= (size_t(1) << 30)) fail(SF_ERR_BAD_DIMS, "occupied voxels: grid too large");
+    const int n = int(n64), nb = (n + kOccBlock - 1) / kOccBlock, tiles = (nb + 1023) / 1024;
+    if (!tmp) {  // size query: block counts + tile totals
+        tmp_bytes = (size_t(nb) + 1024) * sizeof(int);
         return 0;
     }
-    SFB_CUDA(cub::DeviceSelect::If(tmp, tmp_bytes, it, idx, count, n, Occupied{g.d}, s));
-    count_launch();
+    int* cnts = static_cast<int*>(tmp);
+    int* tsum = cnts + nb;
+    if (n == 0) {
+        SFB_CUDA(cudaMemsetAsync(count, 0, sizeof(int), s));
+        return 0;
+    }
+    k_occ_count<<<nb, kOccBlock, 0, s>>>(g.d, n, cnts);
+    k_occ_tile_scan<<<tiles, 1024, 0, s>>>(cnts, nb, tsum);
+    k_occ_sum_scan<<<1, 1024, 0, s>>>(tsum, tiles, count);
+    k_occ_write<<<nb, kOccBlock, 0, s>>>(g.d, n, cnts, tsum, idx);
+    SFB_CUDA(cudaGetLastError());
+    for (int k = 0; k < 4; ++k) count_launch();
     return 0;
-}
-
-void launch_sort_keys(const uint32_t* keys_in, uint32_t* keys_out, const int* idx_in, int* idx_out, int n,
-                      int end_bit, void* tmp, size_t& tmp_bytes, cudaStream_t s) {
-    SFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, idx_in, idx_out, n, 0, end_bit, s));
-    if (tmp) count_launch();
 }
 
 void launch_bake_rows(const sf_grid& g, const int* idx, const int* count, int64_t max_rows, const double cam[3],
