@@ -361,9 +361,16 @@ def run_b200(args):
     import torch.distributed as dist
 
     ws, rank, local = dist_env()
+    # SF_BENCH_BACKEND=gloo runs the multi-rank arm with host-staged collectives, several ranks per
+    # GPU allowed (a functional check of the sharded path on a one-GPU box, not a scaling number)
+    backend = os.environ.get("SF_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend == "gloo" else local
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2401_14051_b200 as sf
     from paper_2401_14051_b200 import scenes, sharding
     from paper_2401_14051_b200._lib import profile_read
@@ -464,7 +471,8 @@ def run_b200(args):
     clocks.active = False
     clocks.stop()
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    red_dev = "cpu" if backend == "gloo" else dev  # gloo reduces host tensors
+    ms_t = torch.tensor([ms], device=red_dev, dtype=torch.float64)
     if ws > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_per_step = float(ms_t.item()) / args.steps
@@ -502,7 +510,7 @@ def run_b200(args):
         e2e_step(i)
     e1.record(stream)
     torch.cuda.synchronize()
-    e_ms = torch.tensor([e0.elapsed_time(e1) / e_steps], device=dev, dtype=torch.float64)
+    e_ms = torch.tensor([e0.elapsed_time(e1) / e_steps], device=red_dev, dtype=torch.float64)
     if ws > 1:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
     e2e_value = q_step / (float(e_ms.item()) * 1e-3)
