@@ -88,7 +88,7 @@ class Workload:
             self.per_step = 1  # lights per step
             self.desc = ("C5: 256^3 seeded 5-octave noise volume (static), 32-frame animated light rotating 360 deg "
                          "about +Y, 1280x720 = 921,600 shading points per frame, transmittance volume rebuilt every "
-                         "frame, HG g=0.7, albedo 0.99, SPEC backbone 32/64/64 (bf16, FP32 accumulate)")
+                         "frame, HG g=0.7, albedo 0.99, SPEC backbone 32/64/64 (operand precision: config.network)")
         elif name == "c3":
             self.grid, self.width, self.height = 256, 512, 512
             self.g, self.albedo = 0.5, 0.95
@@ -96,7 +96,7 @@ class Workload:
             self.n_frames, self.per_step = 1, 4
             self.desc = ("C3: 256^3 curl-noise smoke plume (70% empty), 4 directional lights with the transmittance "
                          "volume rebuilt per light, 512x512 = 262,144 shading points per light, F = sum_l I_l F_l, "
-                         "HG g=0.5, albedo 0.95, SPEC backbone (bf16)")
+                         "HG g=0.5, albedo 0.95, SPEC backbone (operand precision: config.network)")
         elif name == "c4":
             self.grid, self.width, self.height = 512, 1920, 1080
             self.g, self.albedo = 0.6, 0.95
@@ -104,14 +104,14 @@ class Workload:
             self.n_frames, self.per_step = 1, 1
             self.desc = ("C4: 512^3 mixed medium (per-voxel albedo in [0.9,0.999], HG g in [0.3,0.9] sampled at each "
                          "shading point), 1920x1080 = 2,073,600 shading points, one light, frame = transmittance "
-                         "build + queries, SPEC backbone (bf16)")
+                         "build + queries, SPEC backbone (operand precision: config.network)")
         elif name == "c2":
             self.grid, self.width, self.height = 128, 256, 256
             self.g, self.albedo = 0.85, 0.999
             self.lights, self.intensities = [scenes.LIGHT], [1.0]
             self.n_frames, self.per_step = 1, 1
             self.desc = ("C2: 128^3 fractal-noise+ellipsoid cloud, albedo 0.999, HG g=0.85, 65,536 shading points, "
-                         "8 diffuse + 4 highlight layers (266 points) over all 8 mip levels, SPEC backbone (bf16); "
+                         "8 diffuse + 4 highlight layers (266 points) over all 8 mip levels, SPEC backbone (operand precision: config.network); "
                          "query only (the per-light build is reported separately)")
         else:
             raise SystemExit(f"unknown --config {name}")

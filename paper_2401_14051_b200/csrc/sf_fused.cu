@@ -569,25 +569,48 @@ __global__ void k_cell_scatter(int64_t n, const uint32_t* __restrict__ cells, in
 // values, so the sampler has no clamps, and a trilinear cell is two 256-bit loads (z0, z0+1).
 // Four records share a 128-byte line as a 2x1x2 (x, y, z) brick: a cell's two records are in
 // one line when z0 is even. Index ((z/2 * PY + y) * XH + x/2) * 4 + (z&1) * 2 + (x&1).
-__global__ void k_xpair(const float* __restrict__ rho, const float* __restrict__ tr, int nx, int ny, int nz,
-                        float4* __restrict__ out) {
-    const int px = nx + 1, py = ny + 1, pz = nz + 2;
-    const size_t n = size_t(px) * py * pz;
-    const size_t sx = size_t((px + 1) >> 1) << 2, sz = size_t(py) * sx;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
-        const int x = int(i % px), y = int((i / px) % py), z = int(i / (size_t(px) * py));
-        const int cx0 = min(max(x - 1, 0), nx - 1), cx1 = min(x, nx - 1);
-        const int cy0 = min(max(y - 1, 0), ny - 1), cy1 = min(y, ny - 1);
-        const int cz = min(max(z - 1, 0), nz - 1);
-        const size_t r0 = (size_t(cz) * ny + cy0) * nx, r1 = (size_t(cz) * ny + cy1) * nx;
-        const float2 a = make_float2(__ldg(rho + r0 + cx0), __ldg(tr + r0 + cx0));
-        const float2 b = make_float2(__ldg(rho + r0 + cx1), __ldg(tr + r0 + cx1));
-        const float2 c = make_float2(__ldg(rho + r1 + cx0), __ldg(tr + r1 + cx0));
-        const float2 d = make_float2(__ldg(rho + r1 + cx1), __ldg(tr + r1 + cx1));
-        const size_t rec = size_t(z >> 1) * sz + size_t(y) * sx + (size_t(x >> 1) << 2) + ((z & 1) << 1) + (x & 1);
-        out[2 * rec] = make_float4(a.x, a.y, b.x, b.y);
-        out[2 * rec + 1] = make_float4(c.x, c.y, d.x, d.y);
+// One thread per 128-byte brick (x pair 2xh, 2xh + 1; z pair 2zh, 2zh + 1; one y): its four
+// records read three clamped x columns of two y rows at two z slices (24 loads), are staged in
+// shared memory and leave as whole contiguous lines (a warp stores 512 contiguous bytes per
+// instruction). 32-bit index math; every brick of the layout is written (padding bricks hold
+// clamped values no lookup reads).
+constexpr int kXpairThreads = 256;
+__global__ void __launch_bounds__(kXpairThreads) k_xpair(const float* __restrict__ rho, const float* __restrict__ tr,
+                                                         int nx, int ny, int nz, float4* __restrict__ out) {
+    __shared__ float4 st[kXpairThreads * 8];
+    const int XH = (nx + 2) >> 1, py = ny + 1;
+    const int per_slab = XH * py;  // bricks of one z pair
+    const int zh = blockIdx.y;
+    const int m0 = blockIdx.x * kXpairThreads;
+    const int m = m0 + threadIdx.x;
+    if (m < per_slab) {
+        const int y = m / XH, xh = m - y * XH;
+        const int xa = min(max(2 * xh - 1, 0), nx - 1), xb = min(2 * xh, nx - 1), xc = min(2 * xh + 1, nx - 1);
+        const int y0 = min(max(y - 1, 0), ny - 1), y1 = min(y, ny - 1);
+        // brick: rec (dz, dx) at float4 2 (2 dz + dx), each 2 float4; slots XOR-swizzled by the
+        // brick's index so the stores of a warp spread over the banks
+        float4* b = st + threadIdx.x * 8;
+        const int sw = threadIdx.x & 7;
+#pragma unroll
+        for (int dz = 0; dz < 2; ++dz) {
+            const int cz = min(max(2 * zh + dz - 1, 0), nz - 1);
+            const size_t r0 = (size_t(cz) * ny + y0) * nx, r1 = (size_t(cz) * ny + y1) * nx;
+            const float ra0 = __ldg(rho + r0 + xa), rb0 = __ldg(rho + r0 + xb), rc0 = __ldg(rho + r0 + xc);
+            const float ta0 = __ldg(tr + r0 + xa), tb0 = __ldg(tr + r0 + xb), tc0 = __ldg(tr + r0 + xc);
+            const float ra1 = __ldg(rho + r1 + xa), rb1 = __ldg(rho + r1 + xb), rc1 = __ldg(rho + r1 + xc);
+            const float ta1 = __ldg(tr + r1 + xa), tb1 = __ldg(tr + r1 + xb), tc1 = __ldg(tr + r1 + xc);
+            // x = 2xh: corners (xa, xb); x = 2xh + 1: corners (xb, xc)
+            b[(4 * dz + 0) ^ sw] = make_float4(ra0, ta0, rb0, tb0);
+            b[(4 * dz + 1) ^ sw] = make_float4(ra1, ta1, rb1, tb1);
+            b[(4 * dz + 2) ^ sw] = make_float4(rb0, tb0, rc0, tc0);
+            b[(4 * dz + 3) ^ sw] = make_float4(rb1, tb1, rc1, tc1);
+        }
     }
+    __syncthreads();
+    // the block's bricks are consecutive lines of one z-pair slab
+    const int nb = min(kXpairThreads, per_slab - m0);
+    float4* dst = out + (size_t(zh) * per_slab + m0) * 8;
+    for (int k = threadIdx.x; k < nb * 8; k += kXpairThreads) __stcg(dst + k, st[(k & ~7) | ((k ^ (k >> 3)) & 7)]);
 }
 
 // Compile-time bitonic sort of P register values, descending if `desc`.
@@ -1005,9 +1028,9 @@ void launch_blend_planes(const sf_phase_table& t, const sf_phase_model& m, float
 }
 
 void launch_xpair(const float* rho, const float* tr, int nx, int ny, int nz, float4* out, cudaStream_t s) {
-    const size_t n = size_t(nx + 1) * (ny + 1) * (nz + 2);
-    k_xpair<<<unsigned(std::min<size_t>((n + 255) / 256, size_t(sm_count()) * 32)), 256, 0, s>>>(rho, tr, nx, ny, nz,
-                                                                                                 out);
+    const int per_slab = ((nx + 2) >> 1) * (ny + 1);
+    const dim3 grid(unsigned((per_slab + kXpairThreads - 1) / kXpairThreads), unsigned((nz + 3) >> 1));
+    k_xpair<<<grid, kXpairThreads, 0, s>>>(rho, tr, nx, ny, nz, out);
     SFB_CUDA(cudaGetLastError());
     count_launch();
 }
