@@ -657,8 +657,11 @@ __device__ double march_padded(const GridDev& g, const Rec* __restrict__ px, con
 constexpr int kColTile = 64;   // taps per warp per tile
 constexpr int kColPlanes = 8;  // E planes (warps) per block
 
+#ifndef SF_GRADED_MINB
+#define SF_GRADED_MINB 3
+#endif
 template <typename W, typename Rec, int E>
-__global__ void __launch_bounds__(256, 3) k_graded_cols(GridDev g, const Rec* __restrict__ rec, PadLayout pl,
+__global__ void __launch_bounds__(256, SF_GRADED_MINB) k_graded_cols(GridDev g, const Rec* __restrict__ rec, PadLayout pl,
                                                         const Rec* __restrict__ recx, PadLayout plx, LightDev lt,
                                                         double coeff, double step, int zlo,
                                                         int zhi, const TapGroup* __restrict__ groups,
@@ -957,7 +960,10 @@ __global__ void __launch_bounds__(256) k_conv3_zwin(const float* __restrict__ in
 // fine centres of an axis fall in the same or in adjacent coarse cells), loaded once: 27 loads
 // per level for eight voxels instead of 64. Each voxel's lerps are the FP32 operations of
 // k_combine<true> in the same order (bit-identical).
-__global__ void __launch_bounds__(256) k_combine_blk(Levels lv, GridDev base, int zlo, int zhi,
+#ifndef SF_COMBINE_MINB
+#define SF_COMBINE_MINB 1
+#endif
+__global__ void __launch_bounds__(256, SF_COMBINE_MINB) k_combine_blk(Levels lv, GridDev base, int zlo, int zhi,
                                                      float* __restrict__ out) {
     const int bx = blockIdx.x * 32 + threadIdx.x, by = blockIdx.y * 8 + threadIdx.y;
     const int x0 = 2 * bx, y0 = 2 * by, z0 = zlo + 2 * int(blockIdx.z);
