@@ -702,7 +702,13 @@ BuildSide& build_side() {
     std::lock_guard<std::mutex> lk(g_side_mu);
     BuildSide& b = (*m)[dev];
     if (!b.side) {
-        SFB_CUDA(cudaStreamCreateWithFlags(&b.side, cudaStreamNonBlocking));
+        // High priority: the block scheduler then dispatches the coarse levels' blocks into the
+        // slots level 0's large grids free, instead of after those grids' last blocks are issued
+        // (SF_SIDE_PRIO=0: default priority)
+        static const bool high = !std::getenv("SF_SIDE_PRIO") || std::atoi(std::getenv("SF_SIDE_PRIO")) != 0;
+        int least = 0, greatest = 0;
+        SFB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        SFB_CUDA(cudaStreamCreateWithPriority(&b.side, cudaStreamNonBlocking, high ? greatest : least));
         SFB_CUDA(cudaEventCreateWithFlags(&b.fork, cudaEventDisableTiming));
         SFB_CUDA(cudaEventCreateWithFlags(&b.join, cudaEventDisableTiming));
     }
