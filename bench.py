@@ -465,7 +465,7 @@ def run_b200(args):
         step(i)
         ends[i].record(stream)
     torch.cuda.synchronize()
-    launches = (sf.lib.sf_launch_count() - l0) / args.steps
+    launches = int(sf.lib.sf_launch_count() - l0)  # this library's kernels inside the timed region
     if ws > 1:
         dist.barrier()
     clocks.active = False
@@ -552,6 +552,7 @@ def run_b200(args):
                     "h2d_bytes_per_step": int(n_mine * 72 * w.per_step),
                     "d2h_bytes_per_step": int(n_mine * 24 * w.per_step)},
             "gpu_launches": launches,
+            "gpu_launches_per_step": launches / args.steps,
             "roofline": roof,
             "cpu_baseline": cpu,
             "parity": parity,
