@@ -621,11 +621,12 @@ def roofline(sf, w, stage_ms, n, precision):
                                                f"HBM: the {rec_bytes >> 20} MB of records exceed L2",
                                  "l1_data_pipe_pct": k.get("l1_data_pipe_pct"), "ms": stage_ms["sample_sort"],
                                  "algorithmic": (f"{gather_q} B/query of global {{rho, T}} corner gathers x {n} queries "
-                                                 f"per launch (the other {bytes_q - gather_q} B/query of SURVEY 8d's "
+                                                 f"per step (the stage's launches together; the other {bytes_q - gather_q} B/query of SURVEY 8d's "
                                                  f"{bytes_q} are shared-memory phase lookups)"),
                                  "achieved_survey_formula": bytes_q * n / t / 1e9,
                                  "frac_survey_formula": bytes_q * n / t / 1e9 / hbm,
-                                 "binding": binding(k)}
+                                 "binding": binding(k),
+                                 "traffic_launch": "ncu: the stage's first launch (profiles/ncu_*.json names its size)"}
         # cross-checks: the global gathers against the L2 read bandwidth measured
         # live on this GPU with the sampler's 32-byte loads, and the real DRAM rate of the ncu launch
         if l2:
@@ -673,6 +674,15 @@ def roofline(sf, w, stage_ms, n, precision):
                                                       "level reuse neighbours' loads through shared memory / L1, so frac "
                                                       "against HBM can exceed 1; the stage also waits for the side "
                                                       "stream's coarse levels (DESIGN.md 6)"}
+    if "records" in stage_ms and w.name != "c2":
+        # query records (k_xpair): reads rho and T (4 B each) and writes one 32-byte xy-quad record per
+        # (padded) voxel -- a streaming kernel, HBM-bound by design
+        k = ncu.get("k_xpair", {})
+        b = 40 * w.grid ** 3
+        t = stage_ms["records"] / w.per_step * 1e-3
+        rows["k_xpair"] = {"bound": "hbm", "achieved": b / t / 1e9, "peak": hbm, "unit": "GB/s", "frac": b / t / 1e9 / hbm,
+                           "traffic": k.get("dram_bytes"), "ms": stage_ms["records"] / w.per_step,
+                           "algorithmic": f"(2 x 4 B read + 32 B record written) x {w.grid}^3 voxels per light"}
     dom = max(rows, key=lambda k: rows[k]["ms"]) if rows else None
     out = dict(rows[dom]) if dom else {}
     out["kernel"] = dom

@@ -154,6 +154,19 @@ def test_rows_independent_of_batch_and_buffers(det, precision):
     assert np.array_equal(sf.query(scene, net, med, rows[perm], prec), ref[perm])
 
 
+@pytest.mark.parametrize("precision", ["fp16", "bf16", "fp32"])
+def test_empty_batch(det, precision):
+    """No queries: an empty F and no error on every precision (the reference's predict_field over
+    an empty table returns an empty vector, src/predictor.cpp:531-543), and the next call is
+    unaffected."""
+    scene, net, med, rows = det
+    prec = {"fp16": sf.FP16, "bf16": sf.BF16, "fp32": sf.FP32}[precision]
+    F = sf.query(scene, net, med, np.empty((0, 9)), prec)
+    assert F.shape == (0, 3)
+    one = sf.query(scene, net, med, rows[:1], prec)
+    assert one.shape == (1, 3) and np.array_equal(one, sf.query(scene, net, med, rows[:3], prec)[:1])
+
+
 def test_two_lights_across_windows(det):
     """Rows lit by two lights, the second starting inside the host path's second window:
     every window compares its rows' lights with the batch's row 0 (whose light the diffuse
