@@ -1398,7 +1398,16 @@ void query_impl(const sf_scene* s, const sf_backbone* b, const sf_medium_params*
             // SF_CHUNK_TILES (A/B): chunks small enough that the sampler's operand blocks are still
             // in L2 when the backbone reads them (plain stores instead of evict-first)
             static const int64_t chunk_env = std::getenv("SF_CHUNK_TILES") ? std::atoll(std::getenv("SF_CHUNK_TILES")) : 0;
-            const int64_t chunk_tiles = std::min<int64_t>(n_tiles, chunk_env > 0 ? chunk_env : 1 << 12);  // operands <= ~1 GB
+            // Queries go through the sampler and the backbone in chunks of up to 2^14 tiles (2,097,152
+            // queries; ~0.28 MB of operands per tile, so <= ~4.7 GB of workspace operands): one chunk
+            // for a C5 frame, two for C4 -- every backbone launch ends in a tail of partly idle SMs,
+            // so fewer, larger chunks are faster (C5 query 5.86 -> 5.79 ms, C4 22.8 -> 22.4 ms against
+            // 2^12-tile chunks, bit-identical). SF_CHUNK_CAP overrides the cap (A/B, small-memory runs).
+            // (read per call, not cached: tests switch it within one process)
+            const char* cap_s = std::getenv("SF_CHUNK_CAP");
+            const int64_t cap_env = cap_s ? std::atoll(cap_s) : 0;
+            const int64_t chunk_tiles =
+                std::min<int64_t>(n_tiles, chunk_env > 0 ? chunk_env : (cap_env > 0 ? cap_env : 1 << 14));
             const bool l2_keep = chunk_env > 0;
             const int64_t chunk = chunk_tiles * sfb::kUmmaM;
             // sampling windows {first row, rows, chunk's first row}

@@ -188,11 +188,13 @@ def test_two_lights_across_windows(det):
     assert np.all(np.abs(y16[:2000] - y32[:2000]) <= 0.03 * np.maximum(1.0, np.abs(y32[:2000])))
 
 
-def test_morton_chunks_host_vs_device():
+def test_morton_chunks_host_vs_device(monkeypatch):
     """A volume beyond L2 (256^3: queries processed in Morton order, results scattered back to
-    the caller's rows) and a batch of two chunks: F and y are bit-identical with device buffers,
-    pageable and pinned host buffers."""
+    the caller's rows) and a batch of two chunks (SF_CHUNK_CAP = 4096 tiles): F and y are
+    bit-identical with device buffers, pageable and pinned host buffers, and with the same
+    batch processed as one chunk (the default cap)."""
     import torch
+    monkeypatch.setenv("SF_CHUNK_CAP", "4096")
     vol = scenes.noise_volume(256, 5)
     g = sf.DensityGrid.from_array(vol, 2.0 / 256, ORIGIN)
     tv = sf.build_transmittance_volume(sf.DensityPyramid(g), scenes.LIGHT, fast=True)
@@ -201,7 +203,7 @@ def test_morton_chunks_host_vs_device():
     sc = sf.Scene(g, tv, tm[0], tm[1], sf.PhaseModel.hg(0.7), sf.PhaseTable(64, 128, 32, 16))
     net = sf.make_backbone(sf.BackboneConfig(seed=0))
     med = sf.MediumParams((0.7,), (0.99,) * 3)
-    n = 600_000  # > one 524,288-query chunk
+    n = 600_000  # > one 4096-tile (524,288-query) chunk
     rows = scenes.draw_centers(vol, n, 3, scenes.LIGHT)
     Fd = torch.empty((n, 3), dtype=torch.float64, device="cuda")
     yd = torch.empty((n, 3), dtype=torch.float32, device="cuda")
@@ -214,3 +216,8 @@ def test_morton_chunks_host_vs_device():
     Fp = torch.empty((n, 3), dtype=torch.float64).pin_memory()
     sf.query(sc, net, med, torch.from_numpy(rows).pin_memory(), sf.FP16, F_out=Fp)
     assert np.array_equal(Fp.numpy(), Fh)
+    monkeypatch.delenv("SF_CHUNK_CAP")  # one chunk
+    F1 = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    sf.query(sc, net, med, torch.from_numpy(rows).cuda(), sf.FP16, F_out=F1)
+    assert np.array_equal(F1.cpu().numpy(), Fh)
+    assert np.array_equal(sf.query(sc, net, med, rows, sf.FP16), Fh)
