@@ -131,6 +131,35 @@ def test_c4_fp16_table_quads(tm, table):
     assert np.all(np.abs(F16 - F32) <= 0.01 * scale * (np.abs(F32) + eg))
 
 
+@pytest.mark.parametrize("precision", ["fp16", "bf16"])
+def test_chunking_invariance_small_chunks(tm, monkeypatch, precision):
+    """F does not depend on how the batch is split into sampler / backbone chunks (the reference's
+    contract that results do not depend on how work is split, inc/parallel.h:16-17): 5,000 queries
+    as one chunk, as 8-tile chunks (a ragged last chunk) and as 1-tile chunks, fixed-medium and
+    per-query-media paths, host and device buffers."""
+    import torch
+    from conftest import LIGHT
+    prec = sf.FP16 if precision == "fp16" else sf.BF16
+    dens, alb, gg = scenes.mixed_medium(64, 6)
+    rows = scenes.draw_centers(dens, 5000, 11, LIGHT)
+    media = scenes.sample_media(alb, gg, rows)
+    g = sf.DensityGrid.from_array(dens, 2.0 / 64, ORIGIN)
+    tv = sf.build_transmittance_volume(sf.DensityPyramid(g), LIGHT, fast=True)
+    scene = sf.Scene(g, tv, tm[0], tm[1], sf.PhaseModel.hg(0.5), sf.PhaseTable(*TABLE))
+    net = sf.make_backbone(sf.BackboneConfig(seed=0))
+    med = sf.MediumParams((0.5,), (0.97,) * 3)
+    one = sf.query(scene, net, med, rows, prec)
+    one_m = sf.query_media(scene, net, rows, media, prec)
+    for cap in ("8", "1"):
+        monkeypatch.setenv("SF_CHUNK_CAP", cap)
+        assert np.array_equal(sf.query(scene, net, med, rows, prec), one)
+        assert np.array_equal(sf.query_media(scene, net, rows, media, prec), one_m)
+        Fd = torch.empty((len(rows), 3), dtype=torch.float64, device="cuda")
+        sf.query(scene, net, med, torch.from_numpy(rows).cuda(), prec, F_out=Fd)
+        assert np.array_equal(Fd.cpu().numpy(), one)
+    monkeypatch.delenv("SF_CHUNK_CAP")
+
+
 def test_c5_animated_frames_vs_oracle(oracle, templates, otab, tm):
     vol = scenes.noise_volume(16, 5)
     rows = scenes.draw_centers(vol, 64, 2, scenes.LIGHT)
